@@ -1,0 +1,164 @@
+/*
+ * cparls.h -- C ABI of the B200-native CP-ARLS-LEV hot path
+ * (Larsen & Kolda, "Practical Leverage-Based Sampling for Low-Rank Tensor
+ * Decomposition", arXiv 2006.16438).  "P:L" cites /root/reference/PAPER.md
+ * line L; "AMB-n" cites the reading listed in DESIGN.md.
+ *
+ * Library: paper_2006_16438_b200/libcparls.so (sm_100a).  Plain C types only.
+ *
+ * Conventions (apply to every call):
+ *  - Status: every call returns cparls_status; nothing aborts or throws across
+ *    the ABI.  cparls_last_error(ctx) returns the message of the last failure.
+ *    CPARLS_EINVAL / ERANGE / ESAMPLE / ENUMERIC / ESTATE leave the context
+ *    usable; CPARLS_ECUDA / ENCCL poison it (only cparls_destroy is valid).
+ *  - Ownership: the context owns ALL device memory it allocates (the per-mode
+ *    sorted nonzero copies, factors, sampler state).  Input buffers of
+ *    cparls_create / cparls_set_factor may be host or device pointers (detected
+ *    with cudaPointerGetAttributes) and may be freed on return.  Output
+ *    buffers are caller-owned HOST pointers unless stated otherwise.
+ *  - Stream: all device work is issued on opts.stream (a cudaStream_t, e.g.
+ *    torch.cuda.current_stream().cuda_stream); NULL = legacy default stream.
+ *  - Modes are 0-based; "other modes" of mode k are m_1 < ... < m_d (d = D-1).
+ *  - Row-major factors: A_k is n_k x r, element (i,c) at A[i*r + c].
+ *  - Multi-GPU is SPMD (world_size > 1): every rank passes its own chunk of the
+ *    COO and calls the same sequence with the same seed; samples are
+ *    replicated, B rows are owned by the rank holding their nonzeros.
+ */
+#ifndef CPARLS_H
+#define CPARLS_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct cparls_ctx cparls_ctx; /* opaque */
+
+typedef enum {
+  CPARLS_OK = 0,
+  CPARLS_EINVAL = 1,   /* bad argument (mode out of range, r > 64, nnz < 0, ...)   */
+  CPARLS_EOOM = 2,     /* device allocation failed                                  */
+  CPARLS_ECUDA = 3,    /* CUDA runtime error (context poisoned)                     */
+  CPARLS_ENCCL = 4,    /* NCCL error (context poisoned)                             */
+  CPARLS_ENUMERIC = 5, /* non-finite factor / solve failure after fallback          */
+  CPARLS_ESAMPLE = 6,  /* DIDX candidate cap or rejection-attempt cap exceeded      */
+  CPARLS_ERANGE = 7,   /* key width: prod_{m!=k} n_m >= 2^63, or coord >= n_k       */
+  CPARLS_ESTATE = 8    /* call order violated (e.g. solve_mode without sample)      */
+} cparls_status;
+
+typedef struct {
+  int32_t rank;            /* r, 1 <= r <= 64                                         */
+  double tau;              /* deterministic threshold tau: > 0 literal; 1 =
+                              pure random; < 0 = 1/s at sample time  */
+  int32_t value_dtype;     /* vals of cparls_create: 0 fp64, 1 fp32 (stored as given;
+                              accumulation is always fp64)                           */
+  int32_t index_dtype;     /* coords of cparls_create: 0 int32, 1 int64              */
+  void *stream;            /* cudaStream_t                                            */
+  int32_t world_size;      /* 1 = single GPU                                          */
+  int32_t world_rank;
+  void *nccl_comm;         /* ncclComm_t when world_size > 1, else NULL               */
+  int64_t didx_cap;        /* max DIDX list length per level (0 -> default 1<<22)     */
+  int64_t attempt_cap;     /* max SIDX attempts (0 -> 1024*s_rnd + 65536, AMB-7)      */
+} cparls_opts;
+
+typedef struct {
+  int64_t s_det;     /* |DetSet|                                          */
+  int64_t s_rnd;     /* s - s_det                                             */
+  int64_t s_bar;     /* rows after combining                                  */
+  int64_t attempts;  /* SIDX attempts consumed (index of last accepted + 1)           */
+  double p_det;      /* sum_{i in DetSet} p_i                                 */
+  int32_t skipped_random; /* AMB-7: random phase skipped (every drawable row is det) */
+} cparls_sample_info;
+
+typedef struct {
+  int64_t matched_nnz;  /* nonzeros in the sampled fibers (m_k)                      */
+  int64_t touched_rows; /* output rows receiving at least one matched nonzero         */
+  int32_t rank_used;    /* rank of the sampled Gram kept by the solve                 */
+  int32_t chol_fallback;/* 1 if Cholesky failed and the eigen pseudo-inverse was used */
+} cparls_solve_info;
+
+/* Per-phase device times (ms, accumulated since create or the last reset) and
+ * counters of the algorithmic bytes each phase touched (DESIGN.md byte model). */
+typedef struct {
+  double ms_leverage, ms_sample, ms_gram, ms_lookup, ms_rhs, ms_solve, ms_fit;
+  double bytes_leverage, bytes_sample, bytes_gram, bytes_lookup, bytes_rhs, bytes_solve, bytes_fit;
+  int64_t mode_steps, fits, kernel_launches;
+  int64_t last_matched_nnz, last_s_bar, last_attempts;
+} cparls_stats;
+
+/* Build the context: validates sizes (ERANGE if some prod_{m!=k} n_m >= 2^63 or
+ * a coordinate is out of range), copies the COO to the device, builds for every
+ * mode k the sorted-key copy of the nonzeros (per-mode linearized
+ * "other-mode" indices; key = eq:bijection P:220-222, AMB-1), ||X||^2, and
+ * initial factors U[0,1) from init_seed (AMB-21) with their leverage scores.
+ * coords: nnz_local x nmodes row-major, 0-based; vals: nnz_local values. */
+cparls_status cparls_create(cparls_ctx **out, int32_t nmodes, const int64_t *dims,
+                            int64_t nnz_local, const void *coords, const void *vals,
+                            const cparls_opts *opts, uint64_t init_seed);
+cparls_status cparls_destroy(cparls_ctx *ctx);
+
+/* Replace factor k (n_k x r row-major fp64, host or device) and recompute its
+ * leverage scores / CDF.  lambda is reset to ones. */
+cparls_status cparls_set_factor(cparls_ctx *ctx, int32_t mode, const double *A);
+/* Copy factor k (n_k x r) and the model weights lambda (r, may be NULL). */
+cparls_status cparls_get_factor(cparls_ctx *ctx, int32_t mode, double *A, double *lambda);
+
+/* Leverage scores of A_k (Def. leverages_scores P:319-331 as l_i =
+ * a_i (A^T A)^+ a_i^T), refreshing p~_k = l/rank (AMB-11) and the integer CDF
+ * (AMB-9).  scores: n_k host doubles or NULL.  rank_out may be NULL. */
+cparls_status cparls_leverage(cparls_ctx *ctx, int32_t mode, double *scores, int32_t *rank_out);
+/* Copy p~_k (n_k host doubles); set p~_k from given bits (lockstep parity). */
+cparls_status cparls_get_ptilde(cparls_ctx *ctx, int32_t mode, double *pt);
+cparls_status cparls_set_ptilde(cparls_ctx *ctx, int32_t mode, const double *pt);
+
+/* SkrpLev (Alg. 1) for solving mode k: DIDX (exact {p_i > tau},
+ * P:688-735) -> SIDX (Alg. 2, Philox4x32-10 key=seed, counter=(attempt, step,
+ * lane), AMB-8/10) -> CIDX (combine repeats, w^2 = c(1-p_det)/(s_rnd p),
+ * P:526-542, AMB-3).  tau is opts.tau unless cparls_set_tau was called. */
+cparls_status cparls_sample(cparls_ctx *ctx, int32_t mode, int64_t s, uint64_t seed,
+                            uint64_t step, cparls_sample_info *info);
+cparls_status cparls_set_tau(cparls_ctx *ctx, double tau);
+/* Copy the current sample in canonical order: deterministic block (key asc)
+ * then random block (key asc).  Returns s_bar in *n_out; copies min(cap,s_bar). */
+cparls_status cparls_get_sample(cparls_ctx *ctx, int64_t cap, uint64_t *keys, int32_t *counts,
+                                double *w2, double *p, uint8_t *is_det, int64_t *n_out);
+/* Sampled fibers of the current sample (TnsrSamp) in canonical
+ * sample order: len[j] per sample, then the matched (out, value) pairs, each
+ * fiber sorted by out.  Copies min(cap, m_k) pairs; *m_out = m_k. */
+cparls_status cparls_get_fibers(cparls_ctx *ctx, int64_t cap, int64_t *len, int64_t *out,
+                                double *val, int64_t *m_out);
+
+/* One sketched mode update (Alg. 3): KrpSamp + sampled Gram,
+ * TnsrSamp lookup, RHS M = Xs^T diag(w^2) Z_S (AMB-14), r x r Cholesky solve
+ * with eigen pseudo-inverse fallback (AMB-12), column normalization (lambda,
+ * AMB-13), leverage refresh.  Requires a current sample of this mode (ESTATE). */
+cparls_status cparls_solve_mode(cparls_ctx *ctx, int32_t mode, cparls_solve_info *info);
+/* Debug/parity: sampled Gram G (r*r) and unnormalized solution B (n_k*r) of the
+ * last solve (either may be NULL). */
+cparls_status cparls_get_last_solve(cparls_ctx *ctx, double *G, double *B);
+
+/* Exact fit 1 - ||X - M||/||X|| (eq:fit P:871-875) via ||X||^2 - 2<X,M> +
+ * ||M||^2 (AMB-16) with the model [[lambda; A_1..A_D]] (AMB-31). */
+cparls_status cparls_fit(cparls_ctx *ctx, double *fit);
+
+/* Alg. 3: iters outer iterations, each cycling all modes with
+ * step = (iter0 + t)*D + k; fit after every fit_every-th iteration (0 = never).
+ * fit_trace: iters host doubles (NaN where no fit) or NULL.  iter0 lets a run
+ * be resumed exactly (counter-based RNG). */
+cparls_status cparls_run(cparls_ctx *ctx, int32_t iters, int64_t s, uint64_t seed, int32_t iter0,
+                         int32_t fit_every, double *fit_trace);
+
+cparls_status cparls_get_stats(cparls_ctx *ctx, cparls_stats *stats);
+cparls_status cparls_reset_stats(cparls_ctx *ctx);
+/* Record per-phase CUDA events (adds small overhead). 0 off, 1 on. */
+cparls_status cparls_set_profiling(cparls_ctx *ctx, int32_t on);
+const char *cparls_last_error(const cparls_ctx *ctx);
+/* Library/device description string (static). */
+const char *cparls_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CPARLS_H */

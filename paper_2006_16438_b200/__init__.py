@@ -1,0 +1,6 @@
+"""B200-native CP-ARLS-LEV hot path (arXiv 2006.16438).
+
+The product is libcparls.so (csrc/, C ABI in include/cparls.h); this package
+is its ctypes binding.  There is no CPU fallback.
+"""
+from .cparls import (Cparls, CparlsError, EXPORTED, LIB_PATH, lib, version)  # noqa: F401

@@ -1,0 +1,263 @@
+"""Thin ctypes binding of libcparls.so (include/cparls.h).
+
+Argument marshalling only: every step of CP-ARLS-LEV runs in the CUDA kernels
+of csrc/.  There is no CPU fallback -- if the shared library is missing or
+cannot be loaded, or no CUDA device is present, the calls raise.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from typing import Optional
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libcparls.so")
+
+OK, EINVAL, EOOM, ECUDA, ENCCL, ENUMERIC, ESAMPLE, ERANGE, ESTATE = range(9)
+_NAMES = ["OK", "EINVAL", "EOOM", "ECUDA", "ENCCL", "ENUMERIC", "ESAMPLE", "ERANGE", "ESTATE"]
+
+
+class CparlsError(RuntimeError):
+    def __init__(self, status, msg):
+        super().__init__(f"cparls {_NAMES[status] if 0 <= status < 9 else status}: {msg}")
+        self.status = status
+
+
+class Opts(C.Structure):
+    _fields_ = [("rank", C.c_int32), ("tau", C.c_double), ("value_dtype", C.c_int32),
+                ("index_dtype", C.c_int32), ("stream", C.c_void_p), ("world_size", C.c_int32),
+                ("world_rank", C.c_int32), ("nccl_comm", C.c_void_p), ("didx_cap", C.c_int64),
+                ("attempt_cap", C.c_int64)]
+
+
+class SampleInfo(C.Structure):
+    _fields_ = [("s_det", C.c_int64), ("s_rnd", C.c_int64), ("s_bar", C.c_int64),
+                ("attempts", C.c_int64), ("p_det", C.c_double), ("skipped_random", C.c_int32)]
+
+
+class SolveInfo(C.Structure):
+    _fields_ = [("matched_nnz", C.c_int64), ("touched_rows", C.c_int64),
+                ("rank_used", C.c_int32), ("chol_fallback", C.c_int32)]
+
+
+class Stats(C.Structure):
+    _fields_ = [(n, C.c_double) for n in (
+        "ms_leverage", "ms_sample", "ms_gram", "ms_lookup", "ms_rhs", "ms_solve", "ms_fit",
+        "bytes_leverage", "bytes_sample", "bytes_gram", "bytes_lookup", "bytes_rhs", "bytes_solve",
+        "bytes_fit")] + [(n, C.c_int64) for n in (
+        "mode_steps", "fits", "kernel_launches", "last_matched_nnz", "last_s_bar", "last_attempts")]
+
+    def as_dict(self):
+        return {n: getattr(self, n) for n, _ in self._fields_}
+
+
+_lib = None
+
+
+def lib():
+    """Load libcparls.so (raises if it is missing: no fallback)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} missing: run __graft_entry__.build() (nvcc, sm_100a)")
+        L = C.CDLL(LIB_PATH)
+        P, I32, I64, U64, D = C.c_void_p, C.c_int32, C.c_int64, C.c_uint64, C.c_double
+        sig = {
+            "cparls_create": [C.POINTER(P), I32, P, I64, P, P, C.POINTER(Opts), U64],
+            "cparls_destroy": [P],
+            "cparls_set_factor": [P, I32, P],
+            "cparls_get_factor": [P, I32, P, P],
+            "cparls_leverage": [P, I32, P, P],
+            "cparls_get_ptilde": [P, I32, P],
+            "cparls_set_ptilde": [P, I32, P],
+            "cparls_sample": [P, I32, I64, U64, U64, C.POINTER(SampleInfo)],
+            "cparls_set_tau": [P, D],
+            "cparls_get_sample": [P, I64, P, P, P, P, P, P],
+            "cparls_get_fibers": [P, I64, P, P, P, P],
+            "cparls_solve_mode": [P, I32, C.POINTER(SolveInfo)],
+            "cparls_get_last_solve": [P, P, P],
+            "cparls_fit": [P, P],
+            "cparls_run": [P, I32, I64, U64, I32, I32, P],
+            "cparls_get_stats": [P, C.POINTER(Stats)],
+            "cparls_reset_stats": [P],
+            "cparls_set_profiling": [P, I32],
+        }
+        for name, args in sig.items():
+            f = getattr(L, name)
+            f.argtypes = args
+            f.restype = C.c_int
+        L.cparls_last_error.argtypes = [P]
+        L.cparls_last_error.restype = C.c_char_p
+        L.cparls_version.argtypes = []
+        L.cparls_version.restype = C.c_char_p
+        _lib = L
+    return _lib
+
+
+EXPORTED = ["cparls_create", "cparls_destroy", "cparls_set_factor", "cparls_get_factor",
+            "cparls_leverage", "cparls_get_ptilde", "cparls_set_ptilde", "cparls_sample",
+            "cparls_set_tau", "cparls_get_sample", "cparls_get_fibers", "cparls_solve_mode",
+            "cparls_get_last_solve", "cparls_fit", "cparls_run", "cparls_get_stats",
+            "cparls_reset_stats", "cparls_set_profiling", "cparls_last_error", "cparls_version"]
+
+
+def _ptr(x):
+    """Raw pointer of a numpy array or torch tensor (host or device)."""
+    if x is None:
+        return None
+    if isinstance(x, np.ndarray):
+        assert x.flags["C_CONTIGUOUS"]
+        return x.ctypes.data
+    return x.data_ptr()   # torch.Tensor (contiguous, checked by caller)
+
+
+class Cparls:
+    """One CP-ARLS-LEV context (the C ABI's cparls_ctx)."""
+
+    def __init__(self, dims, coords, vals, rank, tau=-1.0, init_seed=2, stream=None,
+                 didx_cap=0, attempt_cap=0):
+        import torch
+        if not torch.cuda.is_available():
+            raise RuntimeError("cparls needs a CUDA device (B200); no CPU fallback exists")
+        L = lib()
+        self.dims = tuple(int(d) for d in dims)
+        self.D = len(self.dims)
+        self.r = int(rank)
+        self._keep = []
+        if isinstance(coords, np.ndarray):
+            coords = np.ascontiguousarray(coords)
+            vals = np.ascontiguousarray(vals)
+            idt = 1 if coords.dtype == np.int64 else 0
+            vdt = 1 if vals.dtype == np.float32 else 0
+            assert coords.dtype in (np.int32, np.int64) and vals.dtype in (np.float32, np.float64)
+        else:
+            coords = coords.contiguous()
+            vals = vals.contiguous()
+            idt = 1 if coords.dtype == torch.int64 else 0
+            vdt = 1 if vals.dtype == torch.float32 else 0
+            assert coords.dtype in (torch.int32, torch.int64) and vals.dtype in (torch.float32, torch.float64)
+        nnz = int(coords.shape[0]) if coords.ndim else 0
+        if stream is None:
+            stream = torch.cuda.current_stream().cuda_stream
+        self.stream = stream
+        o = Opts(rank=self.r, tau=float(tau), value_dtype=vdt, index_dtype=idt,
+                 stream=C.c_void_p(stream), world_size=1, world_rank=0, nccl_comm=None,
+                 didx_cap=int(didx_cap), attempt_cap=int(attempt_cap))
+        d = np.array(self.dims, dtype=np.int64)
+        h = C.c_void_p()
+        st = L.cparls_create(C.byref(h), self.D, d.ctypes.data, nnz, _ptr(coords), _ptr(vals),
+                             C.byref(o), int(init_seed))
+        if st != OK:
+            raise CparlsError(st, L.cparls_last_error(None).decode())
+        self._h = h
+
+    # ------------------------------------------------------------------
+    def _check(self, st):
+        if st != OK:
+            raise CparlsError(st, lib().cparls_last_error(self._h).decode())
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().cparls_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def set_factor(self, k, A):
+        A = np.ascontiguousarray(A, dtype=np.float64)
+        assert A.shape == (self.dims[k], self.r)
+        self._check(lib().cparls_set_factor(self._h, k, A.ctypes.data))
+
+    def get_factor(self, k):
+        A = np.zeros((self.dims[k], self.r))
+        lam = np.zeros(self.r)
+        self._check(lib().cparls_get_factor(self._h, k, A.ctypes.data, lam.ctypes.data))
+        return A, lam
+
+    def leverage(self, k):
+        ell = np.zeros(self.dims[k])
+        rank = C.c_int32()
+        self._check(lib().cparls_leverage(self._h, k, ell.ctypes.data, C.byref(rank)))
+        return ell, rank.value
+
+    def get_ptilde(self, k):
+        pt = np.zeros(self.dims[k])
+        self._check(lib().cparls_get_ptilde(self._h, k, pt.ctypes.data))
+        return pt
+
+    def set_ptilde(self, k, pt):
+        pt = np.ascontiguousarray(pt, dtype=np.float64)
+        self._check(lib().cparls_set_ptilde(self._h, k, pt.ctypes.data))
+
+    def set_tau(self, tau):
+        self._check(lib().cparls_set_tau(self._h, float(tau)))
+
+    def sample(self, k, s, seed, step):
+        info = SampleInfo()
+        self._check(lib().cparls_sample(self._h, k, int(s), int(seed), int(step), C.byref(info)))
+        return info
+
+    def get_sample(self):
+        n = C.c_int64()
+        self._check(lib().cparls_get_sample(self._h, 0, None, None, None, None, None, C.byref(n)))
+        n = n.value
+        keys = np.zeros(n, dtype=np.uint64); cnt = np.zeros(n, dtype=np.int32)
+        w2 = np.zeros(n); p = np.zeros(n); isdet = np.zeros(n, dtype=np.uint8)
+        m = C.c_int64()
+        self._check(lib().cparls_get_sample(self._h, n, keys.ctypes.data, cnt.ctypes.data,
+                                            w2.ctypes.data, p.ctypes.data, isdet.ctypes.data,
+                                            C.byref(m)))
+        return dict(keys=keys, counts=cnt, w2=w2, p=p, is_det=isdet.astype(bool))
+
+    def get_fibers(self):
+        n = C.c_int64()
+        self._check(lib().cparls_get_sample(self._h, 0, None, None, None, None, None, C.byref(n)))
+        lens = np.zeros(n.value, dtype=np.int64)
+        mk = C.c_int64()
+        self._check(lib().cparls_get_fibers(self._h, 0, lens.ctypes.data, None, None, C.byref(mk)))
+        out = np.zeros(mk.value, dtype=np.int64); val = np.zeros(mk.value)
+        self._check(lib().cparls_get_fibers(self._h, mk.value, lens.ctypes.data, out.ctypes.data,
+                                            val.ctypes.data, C.byref(mk)))
+        return lens, out, val
+
+    def solve_mode(self, k):
+        info = SolveInfo()
+        self._check(lib().cparls_solve_mode(self._h, k, C.byref(info)))
+        return info
+
+    def last_solve(self, k):
+        G = np.zeros((self.r, self.r)); B = np.zeros((self.dims[k], self.r))
+        self._check(lib().cparls_get_last_solve(self._h, G.ctypes.data, B.ctypes.data))
+        return G, B
+
+    def fit(self):
+        f = C.c_double()
+        self._check(lib().cparls_fit(self._h, C.byref(f)))
+        return f.value
+
+    def run(self, iters, s, seed, iter0=0, fit_every=1):
+        trace = np.full(max(iters, 1), np.nan)
+        self._check(lib().cparls_run(self._h, int(iters), int(s), int(seed), int(iter0),
+                                     int(fit_every), trace.ctypes.data))
+        return trace[:iters]
+
+    def stats(self):
+        s = Stats()
+        self._check(lib().cparls_get_stats(self._h, C.byref(s)))
+        return s.as_dict()
+
+    def reset_stats(self):
+        self._check(lib().cparls_reset_stats(self._h))
+
+    def set_profiling(self, on=True):
+        self._check(lib().cparls_set_profiling(self._h, 1 if on else 0))
+
+
+def version():
+    return lib().cparls_version().decode()

@@ -1,0 +1,109 @@
+// common.cuh -- device helpers shared by the cparls kernels (sm_100a).
+// Part of the product path; shares nothing with oracle/.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <stdexcept>
+#include <string>
+
+namespace cparls {
+
+constexpr int kMaxModes = 8;
+constexpr int kMaxRank = 64;
+constexpr unsigned long long kEmptyKey = 0xFFFFFFFFFFFFFFFFull;
+constexpr double kTwo62 = 4611686018427387904.0;  // 2^62
+
+struct CudaError : std::runtime_error {
+  cudaError_t code;
+  CudaError(cudaError_t c, const std::string &m) : std::runtime_error(m), code(c) {}
+};
+struct ApiError : std::runtime_error {
+  int status;
+  ApiError(int s, const std::string &m) : std::runtime_error(m), status(s) {}
+};
+
+#define CK(x)                                                                              \
+  do {                                                                                     \
+    cudaError_t e_ = (x);                                                                  \
+    if (e_ != cudaSuccess)                                                                 \
+      throw ::cparls::CudaError(e_, std::string(#x) + ": " + cudaGetErrorString(e_) + " @" + \
+                                          __FILE__ + ":" + std::to_string(__LINE__));      \
+  } while (0)
+
+#define CK_LAUNCH() CK(cudaGetLastError())
+
+__host__ __device__ inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+// ---------------------------------------------------------------- Philox4x32-10
+struct u32x4 { uint32_t x, y, z, w; };
+
+__device__ __forceinline__ u32x4 philox4x32_10(u32x4 c, uint32_t k0, uint32_t k1) {
+#pragma unroll
+  for (int round = 0; round < 10; ++round) {
+    if (round > 0) { k0 += 0x9E3779B9u; k1 += 0xBB67AE85u; }
+    uint32_t hi0 = __umulhi(0xD2511F53u, c.x), lo0 = 0xD2511F53u * c.x;
+    uint32_t hi1 = __umulhi(0xCD9E8D57u, c.z), lo1 = 0xCD9E8D57u * c.z;
+    u32x4 n;
+    n.x = hi1 ^ c.y ^ k0; n.y = lo1; n.z = hi0 ^ c.w ^ k1; n.w = lo0;
+    c = n;
+  }
+  return c;
+}
+
+// ---------------------------------------------------------------- double-double
+struct dd { double hi, lo; };
+__device__ __forceinline__ dd dd_two_sum(double a, double b) {
+  double s = __dadd_rn(a, b);
+  double bb = __dsub_rn(s, a);
+  double err = __dadd_rn(__dsub_rn(a, __dsub_rn(s, bb)), __dsub_rn(b, bb));
+  return {s, err};
+}
+__device__ __forceinline__ dd dd_add(dd a, dd b) {
+  dd s = dd_two_sum(a.hi, b.hi);
+  double lo = __dadd_rn(__dadd_rn(s.lo, a.lo), b.lo);
+  return dd_two_sum(s.hi, lo);
+}
+__device__ __forceinline__ dd dd_add_d(dd a, double b) {
+  dd s = dd_two_sum(a.hi, b);
+  return dd_two_sum(s.hi, __dadd_rn(s.lo, a.lo));
+}
+__device__ __forceinline__ dd dd_shfl_xor(dd v, int m) {
+  return {__shfl_xor_sync(0xffffffffu, v.hi, m), __shfl_xor_sync(0xffffffffu, v.lo, m)};
+}
+__device__ __forceinline__ dd warp_sum_dd(dd v) {
+#pragma unroll
+  for (int m = 16; m >= 1; m >>= 1) v = dd_add(v, dd_shfl_xor(v, m));
+  return v;
+}
+
+template <typename T>
+__device__ __forceinline__ T warp_sum(T v) {
+#pragma unroll
+  for (int m = 16; m >= 1; m >>= 1) v += __shfl_xor_sync(0xffffffffu, v, m);
+  return v;
+}
+
+// atomic max for non-negative doubles (bit pattern order == value order)
+__device__ __forceinline__ void atomic_max_nonneg(double *addr, double v) {
+  atomicMax(reinterpret_cast<unsigned long long *>(addr), (unsigned long long)__double_as_longlong(v));
+}
+
+__device__ __forceinline__ unsigned lanemask_lt() {
+  unsigned m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
+// first index i in [0,n) with C[i] > t (upper_bound); C non-decreasing
+__device__ __forceinline__ int64_t upper_bound_u64(const uint64_t *__restrict__ C, int64_t n, uint64_t t) {
+  int64_t lo = 0, len = n;
+  while (len > 0) {
+    int64_t half = len >> 1;
+    if (__ldg(C + lo + half) <= t) { lo += half + 1; len -= half + 1; }
+    else len = half;
+  }
+  return lo;
+}
+
+}  // namespace cparls

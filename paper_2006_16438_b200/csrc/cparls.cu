@@ -1,0 +1,1249 @@
+// cparls.cu -- host orchestrator and C ABI (include/cparls.h) of the B200-native
+// CP-ARLS-LEV hot path.  All arithmetic of the method runs in the kernels of
+// kernels.cuh; this file only sequences them, owns device memory and moves
+// results across the ABI.  "P:L" cites /root/reference/PAPER.md line L.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <cub/device/device_radix_sort.cuh>
+#include <new>
+#include <numeric>
+#include <string>
+#include <vector>
+
+#include "../../include/cparls.h"
+#include "kernels.cuh"
+
+using namespace cparls;
+
+namespace {
+
+struct ModeIndex {
+  uint64_t *key = nullptr;   // sorted eq:bijection keys over the other modes
+  int32_t *out = nullptr;    // mode-k coordinate (row of B it updates)
+  void *val = nullptr;       // value (fp32 or fp64)
+  int64_t *dir = nullptr;    // dir[b] = first position with key >> shift >= b
+  int shift = 0;
+  int64_t nbkt = 0;
+};
+
+struct DevScalars {
+  double pdet;
+  int64_t total;
+  unsigned long long last_attempt;
+  unsigned long long counter;
+  unsigned long long bad;
+  int64_t mk;
+  unsigned long long touched;
+  unsigned long long det_drawable;
+  double fit[3];
+  double normX2;
+};
+
+}  // namespace
+
+struct cparls_ctx {
+  int D = 0, r = 0, ld = 0;
+  int64_t dims[kMaxModes] = {0};
+  int64_t nnz = 0;
+  int vf32 = 0;
+  cudaStream_t st = nullptr;
+  cparls_opts opts{};
+  double tau = -1.0;
+  bool poisoned = false;
+  std::string err;
+  double normX2 = 0.0;
+  int64_t nmax = 0;
+  ModeIndex idx[kMaxModes];
+  double *A[kMaxModes] = {nullptr};
+  double *pt[kMaxModes] = {nullptr};
+  uint64_t *C[kMaxModes] = {nullptr};
+  ModeDev *md[kMaxModes] = {nullptr};
+  SolveDev *sd = nullptr;
+  double *lam_model = nullptr;   // lambda of the model (AMB-31)
+  DevScalars *dv = nullptr;
+  // scratch
+  double *M = nullptr;
+  uint8_t *touched = nullptr;
+  double *gpart = nullptr;
+  int64_t gpart_blocks = 0;
+  double *Gtmp = nullptr;
+  uint64_t *tile_u64 = nullptr;
+  int64_t *i64part = nullptr;    // scan partials
+  dd *ddpart = nullptr;
+  // sample state
+  int64_t scap = 0;
+  int smode = -1;
+  bool have_sample = false;
+  int64_t sbar = 0, sdet = 0, s_rnd = 0, attempts = 0;
+  double p_det = 0.0;
+  int skipped = 0;
+  uint64_t *skey = nullptr;
+  double *sw2 = nullptr, *sp = nullptr;
+  int32_t *scnt = nullptr;
+  uint8_t *sisdet = nullptr;
+  double *Z = nullptr;
+  int64_t *lo = nullptr, *len = nullptr, *off = nullptr;
+  int64_t mk = 0;
+  bool have_lookup = false;
+  // DIDX
+  int64_t ccap = 0;
+  uint64_t *ckey[kMaxModes] = {nullptr};
+  uint32_t *cidx[kMaxModes] = {nullptr};
+  uint64_t *ckey_tmp = nullptr;
+  uint32_t *cidx_tmp = nullptr;
+  uint32_t *rhist = nullptr;
+  int64_t lcap = 0;
+  uint64_t *lkey[2] = {nullptr, nullptr};
+  double *lpp[2] = {nullptr, nullptr};
+  int64_t *lcnt = nullptr, *loff = nullptr;
+  // SIDX / CIDX
+  int64_t acap = 0;
+  uint64_t *akey = nullptr;
+  double *ap = nullptr;
+  uint64_t *rkey = nullptr;
+  double *rp = nullptr;
+  unsigned long long *hkey = nullptr;
+  uint32_t *hcnt = nullptr;
+  double *hp = nullptr;
+  uint64_t hsize = 0;
+  // bookkeeping
+  std::vector<void *> allocs;
+  cparls_stats stats{};
+  bool profiling = false;
+  int fit_mode = 0;
+  int smode_last_solved = -1;
+};
+
+namespace {
+
+void *dalloc(cparls_ctx *c, size_t bytes) {
+  void *p = nullptr;
+  if (bytes == 0) bytes = 16;
+  cudaError_t e = cudaMalloc(&p, bytes);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    throw ApiError(CPARLS_EOOM, "cudaMalloc(" + std::to_string(bytes) + ") failed: " + cudaGetErrorString(e));
+  }
+  c->allocs.push_back(p);
+  return p;
+}
+void dfree(cparls_ctx *c, void *p) {
+  if (!p) return;
+  auto it = std::find(c->allocs.begin(), c->allocs.end(), p);
+  if (it != c->allocs.end()) c->allocs.erase(it);
+  cudaFree(p);
+}
+
+template <typename T>
+T *dalloc_t(cparls_ctx *c, int64_t n) {
+  return static_cast<T *>(dalloc(c, sizeof(T) * (size_t)std::max<int64_t>(n, 1)));
+}
+
+bool is_device_ptr(const void *p) {
+  cudaPointerAttributes a;
+  cudaError_t e = cudaPointerGetAttributes(&a, p);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+void sync(cparls_ctx *c) { CK(cudaStreamSynchronize(c->st)); }
+
+template <typename T>
+T read_dev(cparls_ctx *c, const T *p) {
+  T v;
+  CK(cudaMemcpyAsync(&v, p, sizeof(T), cudaMemcpyDeviceToHost, c->st));
+  sync(c);
+  return v;
+}
+
+struct Phase {
+  cparls_ctx *c;
+  double *acc;
+  cudaEvent_t a = nullptr, b = nullptr;
+  Phase(cparls_ctx *c_, double *acc_) : c(c_), acc(acc_) {
+    if (c->profiling) {
+      CK(cudaEventCreate(&a));
+      CK(cudaEventCreate(&b));
+      CK(cudaEventRecord(a, c->st));
+    }
+  }
+  void end() {
+    if (c->profiling && a) {
+      CK(cudaEventRecord(b, c->st));
+      CK(cudaEventSynchronize(b));
+      float ms = 0.f;
+      CK(cudaEventElapsedTime(&ms, a, b));
+      *acc += ms;
+      cudaEventDestroy(a);
+      cudaEventDestroy(b);
+      a = b = nullptr;
+    }
+  }
+  ~Phase() {
+    if (a) cudaEventDestroy(a);
+    if (b) cudaEventDestroy(b);
+  }
+};
+
+#define LAUNCHED(c, n) ((c)->stats.kernel_launches += (n))
+
+size_t lev_smem(int r, int ld) { return sizeof(double) * ((size_t)r * r + (size_t)kLevThreads * (ld + 1)); }
+size_t prep_smem(int r) { return sizeof(double) * 4 * (size_t)r * r; }
+
+void set_kernel_attrs(int r, int ld) {
+  int lev = (int)lev_smem(r, ld);
+  CK(cudaFuncSetAttribute(k_lev_rows, cudaFuncAttributeMaxDynamicSharedMemorySize, lev));
+  CK(cudaFuncSetAttribute(k_solve_rows, cudaFuncAttributeMaxDynamicSharedMemorySize, lev));
+  int prep = (int)prep_smem(r);
+  CK(cudaFuncSetAttribute(k_lev_prep, cudaFuncAttributeMaxDynamicSharedMemorySize, prep));
+  CK(cudaFuncSetAttribute(k_norm_prep, cudaFuncAttributeMaxDynamicSharedMemorySize, prep));
+  CK(cudaFuncSetAttribute(k_solve_prep, cudaFuncAttributeMaxDynamicSharedMemorySize, prep));
+}
+
+// ---------------------------------------------------------------- leverage
+// rows -> p~, integer CDF (AMB-9/11).  lam != null also
+// normalizes A_k in place by lam.
+void lev_rows_and_cdf(cparls_ctx *c, int k, const double *lam) {
+  const int64_t n = c->dims[k];
+  const int64_t nt = ceil_div(n, kLevThreads);
+  CK(cudaMemsetAsync(&c->md[k]->alpha, 0, sizeof(double), c->st));
+  CK(cudaMemsetAsync(&c->md[k]->drawable, 0, sizeof(long long), c->st));
+  k_lev_rows<<<(unsigned)nt, kLevThreads, lev_smem(c->r, c->ld), c->st>>>(
+      c->A[k], n, c->r, c->ld, lam, c->md[k], c->pt[k], c->C[k], c->tile_u64, &c->md[k]->alpha,
+      reinterpret_cast<unsigned long long *>(&c->md[k]->drawable));
+  CK_LAUNCH();
+  k_scan_u64_single<<<1, kScanThreads, 0, c->st>>>(c->tile_u64, nt);
+  CK_LAUNCH();
+  k_cdf_final<<<(unsigned)nt, kLevThreads, 0, c->st>>>(c->C[k], n, c->tile_u64);
+  CK_LAUNCH();
+  LAUNCHED(c, 3);
+  c->stats.bytes_leverage += (double)n * (c->r * 8.0 * (lam ? 2 : 1) + 16.0);
+}
+
+void gram_of_rows(cparls_ctx *c, const double *A, int64_t n, double *G_out) {
+  int64_t grid = std::min<int64_t>(ceil_div(n, kGramTile), c->gpart_blocks);
+  grid = std::max<int64_t>(grid, 1);
+  int64_t rpb = ceil_div(ceil_div(n, grid), kGramTile) * kGramTile;
+  grid = std::max<int64_t>(1, ceil_div(n, rpb));
+  k_gram_rows<<<(unsigned)grid, kGramThreads, 0, c->st>>>(A, n, c->r, c->ld, rpb, c->gpart);
+  CK_LAUNCH();
+  k_gram_reduce<<<1, 256, 0, c->st>>>(c->gpart, grid, c->r, G_out);
+  CK_LAUNCH();
+  LAUNCHED(c, 2);
+}
+
+void leverage_full(cparls_ctx *c, int k) {
+  Phase ph(c, &c->stats.ms_leverage);
+  gram_of_rows(c, c->A[k], c->dims[k], c->Gtmp);
+  k_lev_prep<<<1, 128, prep_smem(c->r), c->st>>>(c->r, c->Gtmp, c->md[k]);
+  CK_LAUNCH();
+  LAUNCHED(c, 1);
+  c->stats.bytes_leverage += (double)c->dims[k] * c->r * 8.0;
+  lev_rows_and_cdf(c, k, nullptr);
+  ph.end();
+}
+
+void reset_lambda(cparls_ctx *c) {
+  std::vector<double> ones(c->r, 1.0);
+  CK(cudaMemcpyAsync(c->lam_model, ones.data(), sizeof(double) * c->r, cudaMemcpyHostToDevice, c->st));
+  sync(c);
+}
+
+OtherModes other_modes(cparls_ctx *c, int k, bool need_alpha) {
+  OtherModes om{};
+  om.d = c->D - 1;
+  uint64_t mult = 1;
+  for (int m = 0, j = 0; m < c->D; ++m) {
+    if (m == k) continue;
+    om.mode[j] = m;
+    om.n[j] = c->dims[m];
+    om.pt[j] = c->pt[m];
+    om.C[j] = c->C[m];
+    om.A[j] = c->A[m];
+    om.mult[j] = mult;
+    mult *= (uint64_t)c->dims[m];
+    ++j;
+  }
+  if (need_alpha) {
+    for (int j = 0; j < om.d; ++j)
+      CK(cudaMemcpyAsync(&om.alpha[j], &c->md[om.mode[j]]->alpha, sizeof(double), cudaMemcpyDeviceToHost, c->st));
+    sync(c);
+  }
+  return om;
+}
+
+// ---------------------------------------------------------------- index build (K0)
+template <typename IT, typename VT>
+void build_index_mode(cparls_ctx *c, int k, const IT *coords, const VT *vals) {
+  const int64_t nnz = c->nnz;
+  ModeIndex &ix = c->idx[k];
+  const unsigned g = (unsigned)std::max<int64_t>(1, ceil_div(nnz, 256));
+  // pass 1: stable sort of nonzero ids by mode-k coordinate
+  uint32_t *ok0 = dalloc_t<uint32_t>(c, nnz), *ok1 = dalloc_t<uint32_t>(c, nnz);
+  uint32_t *id0 = dalloc_t<uint32_t>(c, nnz), *id1 = dalloc_t<uint32_t>(c, nnz);
+  if (nnz > 0) {
+    k_make_outkey<IT><<<g, 256, 0, c->st>>>(coords, nnz, c->D, k, ok0, id0);
+    CK_LAUNCH();
+  }
+  int obits = 1;
+  while ((int64_t(1) << obits) < c->dims[k]) ++obits;
+  cub::DoubleBuffer<uint32_t> kb(ok0, ok1);
+  cub::DoubleBuffer<uint32_t> vb(id0, id1);
+  size_t tb = 0;
+  CK(cub::DeviceRadixSort::SortPairs(nullptr, tb, kb, vb, nnz, 0, obits, c->st));
+  void *tmp = dalloc(c, tb);
+  CK(cub::DeviceRadixSort::SortPairs(tmp, tb, kb, vb, nnz, 0, obits, c->st));
+  sync(c);
+  dfree(c, tmp);
+  uint32_t *ids = vb.Current();
+  dfree(c, kb.Current());
+  dfree(c, kb.Alternate());
+  // pass 2: stable sort by key
+  KeySpec ks{};
+  ks.D = c->D;
+  ks.k = k;
+  for (int m = 0; m < c->D; ++m) ks.dims[m] = c->dims[m];
+  uint64_t *key0 = dalloc_t<uint64_t>(c, nnz), *key1 = dalloc_t<uint64_t>(c, nnz);
+  if (nnz > 0) {
+    k_make_keys<IT><<<g, 256, 0, c->st>>>(coords, nnz, ks, ids, key0);
+    CK_LAUNCH();
+  }
+  long double Nk = 1;
+  for (int m = 0; m < c->D; ++m)
+    if (m != k) Nk *= (long double)c->dims[m];
+  int kbits = 1;
+  while ((long double)((unsigned long long)1 << kbits) < Nk && kbits < 63) ++kbits;
+  cub::DoubleBuffer<uint64_t> kb2(key0, key1);
+  cub::DoubleBuffer<uint32_t> vb2(ids, ids == id0 ? id1 : id0);
+  tb = 0;
+  CK(cub::DeviceRadixSort::SortPairs(nullptr, tb, kb2, vb2, nnz, 0, kbits, c->st));
+  tmp = dalloc(c, tb);
+  CK(cub::DeviceRadixSort::SortPairs(tmp, tb, kb2, vb2, nnz, 0, kbits, c->st));
+  sync(c);
+  dfree(c, tmp);
+  ix.key = kb2.Current();
+  dfree(c, kb2.Alternate());
+  uint32_t *fids = vb2.Current();
+  dfree(c, vb2.Alternate());
+  ix.out = dalloc_t<int32_t>(c, nnz);
+  ix.val = dalloc(c, sizeof(VT) * (size_t)std::max<int64_t>(nnz, 1));
+  if (nnz > 0) {
+    k_gather_nz<IT, VT><<<g, 256, 0, c->st>>>(coords, vals, nnz, c->D, k, fids, ix.out, (VT *)ix.val);
+    CK_LAUNCH();
+  }
+  sync(c);
+  dfree(c, fids);
+  // top-level directory on the high key bits
+  int dbits = 1;
+  while (dbits < 26 && (int64_t(1) << (dbits + 1)) <= std::max<int64_t>(nnz / 8, 2)) ++dbits;
+  ix.shift = std::max(0, kbits - dbits);
+  unsigned long long Nk1 = (unsigned long long)(Nk - 1);
+  ix.nbkt = (int64_t)(Nk1 >> ix.shift) + 1;
+  ix.dir = dalloc_t<int64_t>(c, ix.nbkt + 1);
+  if (nnz > 0) {
+    k_dir_fill<<<g, 256, 0, c->st>>>(ix.key, nnz, ix.shift, ix.dir, ix.nbkt);
+    CK_LAUNCH();
+  } else {
+    CK(cudaMemsetAsync(ix.dir, 0, sizeof(int64_t) * (ix.nbkt + 1), c->st));
+  }
+  sync(c);
+}
+
+template <typename IT, typename VT>
+void build_all(cparls_ctx *c, const IT *coords, const VT *vals) {
+  KeySpec ks{};
+  ks.D = c->D;
+  for (int m = 0; m < c->D; ++m) ks.dims[m] = c->dims[m];
+  CK(cudaMemsetAsync(&c->dv->bad, 0, sizeof(unsigned long long), c->st));
+  if (c->nnz > 0) {
+    k_check_coords<IT><<<(unsigned)ceil_div(c->nnz, 256), 256, 0, c->st>>>(coords, c->nnz, ks, &c->dv->bad);
+    CK_LAUNCH();
+  }
+  if (read_dev(c, &c->dv->bad) != 0) throw ApiError(CPARLS_ERANGE, "coordinate out of range [0, n_k)");
+  // ||X||^2 (compensated)
+  const int nb = 296;
+  k_sumsq<VT><<<nb, 256, 0, c->st>>>(vals, c->nnz, c->ddpart);
+  CK_LAUNCH();
+  k_sum_dd_final<<<1, 32, 0, c->st>>>(c->ddpart, nb, &c->dv->normX2);
+  CK_LAUNCH();
+  c->normX2 = read_dev(c, &c->dv->normX2);
+  for (int k = 0; k < c->D; ++k) build_index_mode<IT, VT>(c, k, coords, vals);
+}
+
+void alloc_sample_buffers(cparls_ctx *c, int64_t s) {
+  if (s <= c->scap) return;
+  int64_t cap = std::max<int64_t>(s, 1024);
+  for (void *p : {(void *)c->skey, (void *)c->sw2, (void *)c->sp, (void *)c->scnt, (void *)c->sisdet, (void *)c->Z,
+                  (void *)c->lo, (void *)c->len, (void *)c->off, (void *)c->rkey, (void *)c->rp, (void *)c->hkey,
+                  (void *)c->hcnt, (void *)c->hp})
+    dfree(c, p);
+  c->skey = dalloc_t<uint64_t>(c, cap);
+  c->sw2 = dalloc_t<double>(c, cap);
+  c->sp = dalloc_t<double>(c, cap);
+  c->scnt = dalloc_t<int32_t>(c, cap);
+  c->sisdet = dalloc_t<uint8_t>(c, cap);
+  c->Z = dalloc_t<double>(c, cap * c->ld);
+  c->lo = dalloc_t<int64_t>(c, cap);
+  c->len = dalloc_t<int64_t>(c, cap);
+  c->off = dalloc_t<int64_t>(c, cap);
+  c->rkey = dalloc_t<uint64_t>(c, cap);
+  c->rp = dalloc_t<double>(c, cap);
+  uint64_t hs = 1;
+  while (hs < (uint64_t)(2 * cap)) hs <<= 1;
+  c->hsize = hs;
+  c->hkey = dalloc_t<unsigned long long>(c, (int64_t)hs);
+  c->hcnt = dalloc_t<uint32_t>(c, (int64_t)hs);
+  c->hp = dalloc_t<double>(c, (int64_t)hs);
+  CK(cudaMemsetAsync(c->hkey, 0xFF, sizeof(unsigned long long) * hs, c->st));
+  CK(cudaMemsetAsync(c->hcnt, 0, sizeof(uint32_t) * hs, c->st));
+  int64_t part_need = ceil_div(cap, kScanTile) + 16;
+  (void)part_need;
+  c->scap = cap;
+}
+
+void ensure_list_cap(cparls_ctx *c, int64_t need) {
+  if (need <= c->lcap) return;
+  int64_t cap = std::max<int64_t>(need, c->lcap * 2);
+  for (int i = 0; i < 2; ++i) {
+    dfree(c, c->lkey[i]);
+    dfree(c, c->lpp[i]);
+  }
+  dfree(c, c->lcnt);
+  dfree(c, c->loff);
+  for (int i = 0; i < 2; ++i) {
+    c->lkey[i] = dalloc_t<uint64_t>(c, cap);
+    c->lpp[i] = dalloc_t<double>(c, cap);
+  }
+  c->lcnt = dalloc_t<int64_t>(c, cap);
+  c->loff = dalloc_t<int64_t>(c, cap);
+  c->lcap = cap;
+}
+
+// ---------------------------------------------------------------- sampling
+// DIDX: returns s_det; list in lkey[res]/lpp[res] (res returned via *which)
+int64_t run_didx(cparls_ctx *c, const OtherModes &om, double tau, int *which) {
+  const int d = om.d;
+  int64_t ncand[kMaxModes] = {0};
+  // candidates per mode (ordered compaction), then stable sort by p~ descending
+  for (int j = 0; j < d; ++j) {
+    const int64_t n = om.n[j];
+    const int64_t nb = ceil_div(n, kScanTile);
+    k_cand_count<<<(unsigned)nb, kScanThreads, 0, c->st>>>(om, j, tau, c->i64part);
+    CK_LAUNCH();
+    k_scan_part<<<1, kScanThreads, 0, c->st>>>(c->i64part, nb, &c->dv->total);
+    CK_LAUNCH();
+    k_cand_scatter<<<(unsigned)nb, kScanThreads, 0, c->st>>>(om, j, tau, c->i64part, c->ckey[j], c->cidx[j]);
+    CK_LAUNCH();
+    LAUNCHED(c, 3);
+    const int64_t nc = read_dev(c, &c->dv->total);
+    if (nc > 1) {
+      int res = radix_sort_pairs(c->ckey[j], c->cidx[j], c->ckey_tmp, c->cidx_tmp, nc, 64, c->rhist, c->st,
+                                 &c->stats.kernel_launches);
+      if (res == 1) {
+        CK(cudaMemcpyAsync(c->ckey[j], c->ckey_tmp, sizeof(uint64_t) * nc, cudaMemcpyDeviceToDevice, c->st));
+        CK(cudaMemcpyAsync(c->cidx[j], c->cidx_tmp, sizeof(uint32_t) * nc, cudaMemcpyDeviceToDevice, c->st));
+      }
+    }
+    c->stats.bytes_sample += (double)n * 8.0;
+    ncand[j] = nc;
+  }
+  // level expansion (DetSet is a subset of the product of the
+  // candidate sets); the exact canonical predicate decides membership.
+  const int64_t n0 = ncand[0];
+  ensure_list_cap(c, std::max<int64_t>(n0, 1));
+  int cur = 0;
+  if (n0 > 0) {
+    k_didx_level0<<<(unsigned)ceil_div(n0, 256), 256, 0, c->st>>>(c->ckey[0], c->cidx[0], n0, c->lkey[0], c->lpp[0]);
+    CK_LAUNCH();
+    LAUNCHED(c, 1);
+  }
+  int64_t nlist = n0;
+  const int64_t cap = c->opts.didx_cap > 0 ? c->opts.didx_cap : (int64_t(1) << 22);
+  if (nlist > cap) throw ApiError(CPARLS_ESAMPLE, "DIDX list exceeds didx_cap");
+  for (int l = 1; l < d && nlist > 0; ++l) {
+    const int64_t ncl = ncand[l];
+    if (ncl == 0) {
+      nlist = 0;
+      break;
+    }
+    k_didx_count<<<(unsigned)ceil_div(nlist, 256), 256, 0, c->st>>>(c->lpp[cur], nlist, c->ckey[l], ncl, om, l, tau,
+                                                                    c->lcnt);
+    CK_LAUNCH();
+    exclusive_scan_i64(c->lcnt, c->loff, nlist, c->i64part, &c->dv->total, c->st);
+    LAUNCHED(c, 4);
+    const int64_t nn = read_dev(c, &c->dv->total);
+    if (nn > cap) throw ApiError(CPARLS_ESAMPLE, "DIDX list exceeds didx_cap (" + std::to_string(nn) + ")");
+    if (nn > c->lcap) {
+      // grow, keeping the current level
+      uint64_t *k0 = dalloc_t<uint64_t>(c, nlist);
+      double *p0 = dalloc_t<double>(c, nlist);
+      int64_t *cnt0 = dalloc_t<int64_t>(c, nlist), *off0 = dalloc_t<int64_t>(c, nlist);
+      CK(cudaMemcpyAsync(k0, c->lkey[cur], 8 * nlist, cudaMemcpyDeviceToDevice, c->st));
+      CK(cudaMemcpyAsync(p0, c->lpp[cur], 8 * nlist, cudaMemcpyDeviceToDevice, c->st));
+      CK(cudaMemcpyAsync(cnt0, c->lcnt, 8 * nlist, cudaMemcpyDeviceToDevice, c->st));
+      CK(cudaMemcpyAsync(off0, c->loff, 8 * nlist, cudaMemcpyDeviceToDevice, c->st));
+      sync(c);
+      ensure_list_cap(c, nn);
+      CK(cudaMemcpyAsync(c->lkey[cur], k0, 8 * nlist, cudaMemcpyDeviceToDevice, c->st));
+      CK(cudaMemcpyAsync(c->lpp[cur], p0, 8 * nlist, cudaMemcpyDeviceToDevice, c->st));
+      CK(cudaMemcpyAsync(c->lcnt, cnt0, 8 * nlist, cudaMemcpyDeviceToDevice, c->st));
+      CK(cudaMemcpyAsync(c->loff, off0, 8 * nlist, cudaMemcpyDeviceToDevice, c->st));
+      sync(c);
+      dfree(c, k0);
+      dfree(c, p0);
+      dfree(c, cnt0);
+      dfree(c, off0);
+    }
+    if (nn > 0) {
+      k_didx_emit<<<(unsigned)ceil_div(nlist * 32, 256), 256, 0, c->st>>>(c->lkey[cur], c->lpp[cur], nlist, c->lcnt,
+                                                                          c->loff, c->ckey[l], c->cidx[l], om.mult[l],
+                                                                          c->lkey[cur ^ 1], c->lpp[cur ^ 1]);
+      CK_LAUNCH();
+      LAUNCHED(c, 1);
+    }
+    cur ^= 1;
+    nlist = nn;
+  }
+  *which = cur;
+  return nlist;
+}
+
+void sample_impl(cparls_ctx *c, int k, int64_t s, uint64_t seed, uint64_t step, cparls_sample_info *info) {
+  Phase ph(c, &c->stats.ms_sample);
+  c->have_sample = false;
+  c->have_lookup = false;
+  if (s < 1) throw ApiError(CPARLS_EINVAL, "s must be >= 1");
+  alloc_sample_buffers(c, s);
+  double tau = c->tau;
+  if (tau < 0) tau = 1.0 / (double)s;   // tau = 1/s
+  OtherModes om = other_modes(c, k, true);
+  const int d = om.d;
+  // drawable counts (rows with q > 0)
+  long long drawable[kMaxModes];
+  for (int j = 0; j < d; ++j)
+    CK(cudaMemcpyAsync(&drawable[j], &c->md[om.mode[j]]->drawable, sizeof(long long), cudaMemcpyDeviceToHost,
+                       c->st));
+  sync(c);
+  // ---- DIDX
+  int which = 0;
+  int64_t sdet = run_didx(c, om, tau, &which);
+  uint64_t *dkey = c->lkey[which];
+  double *dp = c->lpp[which];
+  if (sdet > s) {
+    // keep the s largest p (ties: smaller key first), AMB-6
+    ensure_list_cap(c, sdet);
+    dkey = c->lkey[which];
+    dp = c->lpp[which];
+    uint64_t *k1 = dalloc_t<uint64_t>(c, sdet), *k2 = dalloc_t<uint64_t>(c, sdet);
+    uint32_t *v1 = dalloc_t<uint32_t>(c, sdet), *v2 = dalloc_t<uint32_t>(c, sdet);
+    uint32_t *h = dalloc_t<uint32_t>(c, 256 * (ceil_div(sdet, kScanTile) + 1));
+    unsigned g = (unsigned)ceil_div(sdet, 256);
+    CK(cudaMemcpyAsync(k1, dkey, 8 * sdet, cudaMemcpyDeviceToDevice, c->st));
+    k_iota_u32<<<g, 256, 0, c->st>>>(v1, sdet);
+    int res = radix_sort_pairs(k1, v1, k2, v2, sdet, 64, h, c->st, &c->stats.kernel_launches);
+    uint32_t *perm = res ? v2 : v1;
+    uint64_t *pk = res ? k1 : k2;   // free key buffer
+    k_gather_kp<<<g, 256, 0, c->st>>>(dkey, dp, perm, sdet, c->lkey[which ^ 1], c->lpp[which ^ 1]);
+    k_pbits_desc<<<g, 256, 0, c->st>>>(c->lpp[which ^ 1], sdet, pk);
+    uint32_t *vv = res ? v1 : v2;
+    k_iota_u32<<<g, 256, 0, c->st>>>(vv, sdet);
+    uint64_t *ko = (pk == k1) ? k2 : k1;
+    uint32_t *vo = (vv == v1) ? v2 : v1;
+    int res2 = radix_sort_pairs(pk, vv, ko, vo, sdet, 64, h, c->st, &c->stats.kernel_launches);
+    uint32_t *perm2 = res2 ? vo : vv;
+    k_gather_kp<<<g, 256, 0, c->st>>>(c->lkey[which ^ 1], c->lpp[which ^ 1], perm2, sdet, dkey, dp);
+    CK_LAUNCH();
+    sync(c);
+    dfree(c, k1); dfree(c, k2); dfree(c, v1); dfree(c, v2); dfree(c, h);
+    sdet = s;
+  }
+  // p_det = sum_{DetSet} p_i (compensated)
+  const int nbs = 64;
+  k_sum_dd<<<nbs, 256, 0, c->st>>>(dp, sdet, c->ddpart);
+  k_sum_dd_final<<<1, 32, 0, c->st>>>(c->ddpart, nbs, &c->dv->pdet);
+  CK_LAUNCH();
+  LAUNCHED(c, 2);
+  double p_det = read_dev(c, &c->dv->pdet);
+  if (sdet > 0) {
+    k_det_emit<<<(unsigned)ceil_div(sdet, 256), 256, 0, c->st>>>(dkey, dp, sdet, c->skey, c->sw2, c->sp, c->scnt,
+                                                                 c->sisdet);
+    CK_LAUNCH();
+    LAUNCHED(c, 1);
+  }
+  // ---- SIDX (Alg. 2)
+  int64_t s_rnd = s - sdet;
+  int64_t det_drawable = sdet;   // tau >= 2^-63 => every det index has q > 0
+  if (tau < 1.0842021724855044e-19 && sdet > 0) {
+    std::vector<uint64_t> hk(sdet);
+    CK(cudaMemcpyAsync(hk.data(), dkey, 8 * sdet, cudaMemcpyDeviceToHost, c->st));
+    std::vector<std::vector<double>> hp(d);
+    for (int j = 0; j < d; ++j) {
+      hp[j].resize(om.n[j]);
+      CK(cudaMemcpyAsync(hp[j].data(), om.pt[j], 8 * om.n[j], cudaMemcpyDeviceToHost, c->st));
+    }
+    sync(c);
+    det_drawable = 0;
+    for (int64_t i = 0; i < sdet; ++i) {
+      uint64_t t = hk[i];
+      bool ok = true;
+      for (int j = 0; j < d; ++j) {
+        uint64_t ii = t % (uint64_t)om.n[j];
+        t /= (uint64_t)om.n[j];
+        ok &= hp[j][ii] > 1.0842021724855044e-19;
+      }
+      det_drawable += ok;
+    }
+  }
+  double drawable_all = 1.0;
+  for (int j = 0; j < d; ++j) drawable_all *= (double)drawable[j];
+  int skipped = 0;
+  int64_t attempts = 0;
+  int64_t have = 0;
+  if (s_rnd > 0) {
+    if (1.0 - p_det <= 1e-12 || drawable_all <= (double)det_drawable) {
+      skipped = 1;   // AMB-7
+    } else {
+      const int64_t cap_att = c->opts.attempt_cap > 0 ? c->opts.attempt_cap : 1024 * s_rnd + 65536;
+      uint64_t a0 = 0;
+      const uint32_t slo = (uint32_t)seed, shi = (uint32_t)(seed >> 32);
+      while (have < s_rnd) {
+        if ((int64_t)a0 >= cap_att) throw ApiError(CPARLS_ESAMPLE, "SIDX attempt cap reached");
+        double accp = std::max(1.0 - p_det, 1e-3);
+        int64_t want = (int64_t)std::ceil((double)(s_rnd - have) / accp * 1.08) + 4096;
+        int64_t win = std::min<int64_t>(std::max<int64_t>(want, 4096), c->acap);
+        win = std::min<int64_t>(win, cap_att - (int64_t)a0);
+        int64_t nb = ceil_div(win, kSidxThreads);
+        k_sidx_gen<<<(unsigned)nb, kSidxThreads, 0, c->st>>>(om, a0, win, tau, slo, shi, (uint32_t)step, c->akey,
+                                                             c->ap, c->i64part);
+        CK_LAUNCH();
+        k_scan_part<<<1, kScanThreads, 0, c->st>>>(c->i64part, nb, &c->dv->total);
+        CK_LAUNCH();
+        k_sidx_scatter<<<(unsigned)nb, kSidxThreads, 0, c->st>>>(c->akey, c->ap, win, c->i64part, have, s_rnd, a0,
+                                                                 c->rkey, c->rp, &c->dv->last_attempt);
+        CK_LAUNCH();
+        LAUNCHED(c, 3);
+        int64_t got = read_dev(c, &c->dv->total);
+        have += std::min<int64_t>(got, s_rnd - have);
+        a0 += (uint64_t)win;
+        c->stats.bytes_sample += (double)win * d * 8.0;
+      }
+      attempts = (int64_t)read_dev(c, &c->dv->last_attempt) + 1;
+    }
+  }
+  // ---- CIDX (combine repeats)
+  int64_t nuniq = 0;
+  if (have > 0) {
+    CK(cudaMemsetAsync(&c->dv->counter, 0, sizeof(unsigned long long), c->st));
+    k_cidx_insert<<<(unsigned)ceil_div(have, 256), 256, 0, c->st>>>(c->rkey, c->rp, have, c->hkey, c->hcnt, c->hp,
+                                                                    c->hsize - 1);
+    CK_LAUNCH();
+    k_cidx_emit<<<(unsigned)ceil_div((int64_t)c->hsize, 256), 256, 0, c->st>>>(
+        c->hkey, c->hcnt, c->hp, c->hsize, &c->dv->pdet, s_rnd, sdet, &c->dv->counter, c->skey, c->sw2, c->sp,
+        c->scnt, c->sisdet);
+    CK_LAUNCH();
+    LAUNCHED(c, 2);
+    nuniq = (int64_t)read_dev(c, &c->dv->counter);
+  }
+  c->smode = k;
+  c->sdet = sdet;
+  c->s_rnd = s_rnd;
+  c->sbar = sdet + nuniq;
+  c->p_det = p_det;
+  c->attempts = attempts;
+  c->skipped = skipped;
+  c->have_sample = true;
+  c->stats.last_s_bar = c->sbar;
+  c->stats.last_attempts = attempts;
+  if (info) {
+    info->s_det = sdet;
+    info->s_rnd = s_rnd;
+    info->s_bar = c->sbar;
+    info->attempts = attempts;
+    info->p_det = p_det;
+    info->skipped_random = skipped;
+  }
+  ph.end();
+}
+
+// ---------------------------------------------------------------- solve
+void lookup_impl(cparls_ctx *c, int k) {
+  ModeIndex &ix = c->idx[k];
+  const int64_t sbar = c->sbar;
+  if (sbar > 0) {
+    k_lookup<<<(unsigned)ceil_div(sbar, 256), 256, 0, c->st>>>(c->skey, sbar, ix.key, ix.dir, ix.shift, ix.nbkt,
+                                                               c->lo, c->len);
+    CK_LAUNCH();
+    LAUNCHED(c, 1);
+  }
+  exclusive_scan_i64(c->len, c->off, sbar, c->i64part, &c->dv->mk, c->st);
+  LAUNCHED(c, 3);
+  c->have_lookup = true;
+  c->stats.bytes_lookup += (double)sbar * 16.0;
+}
+
+void solve_impl(cparls_ctx *c, int k, cparls_solve_info *info) {
+  if (!c->have_sample || c->smode != k) throw ApiError(CPARLS_ESTATE, "solve_mode without a current sample of this mode");
+  const int r = c->r, ld = c->ld;
+  const int64_t nk = c->dims[k];
+  const int64_t sbar = c->sbar;
+  OtherModes om = other_modes(c, k, false);
+  // K6: KrpSamp + sampled Gram
+  {
+    Phase ph(c, &c->stats.ms_gram);
+    if (sbar > 0) {
+      int64_t grid = std::min<int64_t>(ceil_div(sbar, kKrpChunk), c->gpart_blocks);
+      int64_t per = ceil_div(ceil_div(sbar, grid), kKrpChunk) * kKrpChunk;
+      grid = ceil_div(sbar, per);
+      k_krp_gram<<<(unsigned)grid, kKrpThreads, 0, c->st>>>(c->skey, c->sw2, sbar, om, r, ld, c->Z, per, c->gpart);
+      CK_LAUNCH();
+      k_gram_reduce<<<1, 256, 0, c->st>>>(c->gpart, grid, r, c->sd->G);
+      CK_LAUNCH();
+      LAUNCHED(c, 2);
+    } else {
+      CK(cudaMemsetAsync(c->sd->G, 0, sizeof(double) * r * r, c->st));
+    }
+    c->stats.bytes_gram += (double)sbar * (om.d * r * 8.0 + 16.0);
+    ph.end();
+  }
+  // K7: lookup of the sampled fibers
+  {
+    Phase ph(c, &c->stats.ms_lookup);
+    lookup_impl(c, k);
+    ph.end();
+  }
+  // K8: sampled RHS
+  {
+    Phase ph(c, &c->stats.ms_rhs);
+    const int64_t per_warp = 256;
+    const int grid = 148 * 8;
+    if (sbar > 0) {
+      if (c->vf32)
+        k_rhs<float><<<grid, kRhsThreads, 0, c->st>>>(c->off, c->lo, sbar, &c->dv->mk, c->idx[k].out,
+                                                      (const float *)c->idx[k].val, c->sw2, c->Z, r, ld, c->M,
+                                                      c->touched, per_warp);
+      else
+        k_rhs<double><<<grid, kRhsThreads, 0, c->st>>>(c->off, c->lo, sbar, &c->dv->mk, c->idx[k].out,
+                                                       (const double *)c->idx[k].val, c->sw2, c->Z, r, ld, c->M,
+                                                       c->touched, per_warp);
+      CK_LAUNCH();
+      LAUNCHED(c, 1);
+    }
+    CK(cudaMemsetAsync(&c->dv->touched, 0, sizeof(unsigned long long), c->st));
+    k_count_touched<<<296, 256, 0, c->st>>>(c->touched, nk, &c->dv->touched);
+    CK_LAUNCH();
+    LAUNCHED(c, 1);
+    ph.end();
+  }
+  // K9: solve + normalize + leverage refresh
+  {
+    Phase ph(c, &c->stats.ms_solve);
+    k_solve_prep<<<1, 128, prep_smem(r), c->st>>>(r, c->sd);
+    CK_LAUNCH();
+    int64_t nt = ceil_div(nk, kSolveThreads);
+    // partial buffer must hold nt blocks of pairs
+    double *part = c->gpart;
+    if (nt > c->gpart_blocks) part = dalloc_t<double>(c, nt * npairs(r));
+    k_solve_rows<<<(unsigned)nt, kSolveThreads, lev_smem(r, ld), c->st>>>(c->M, nk, r, ld, c->sd, c->A[k], part);
+    CK_LAUNCH();
+    k_gram_reduce<<<1, 256, 0, c->st>>>(part, nt, r, c->sd->BtB);
+    CK_LAUNCH();
+    k_norm_prep<<<1, 128, prep_smem(r), c->st>>>(r, c->sd, c->md[k]);
+    CK_LAUNCH();
+    LAUNCHED(c, 4);
+    lev_rows_and_cdf(c, k, c->sd->lambda);
+    CK(cudaMemcpyAsync(c->lam_model, c->sd->lambda, sizeof(double) * r, cudaMemcpyDeviceToDevice, c->st));
+    if (part != c->gpart) {
+      sync(c);
+      dfree(c, part);
+    }
+    c->stats.bytes_solve += (double)nk * r * 8.0 * 3;
+    ph.end();
+  }
+  // info (one sync)
+  struct {
+    int64_t mk;
+    unsigned long long touched;
+  } hv;
+  CK(cudaMemcpyAsync(&hv.mk, &c->dv->mk, sizeof(long long), cudaMemcpyDeviceToHost, c->st));
+  CK(cudaMemcpyAsync(&hv.touched, &c->dv->touched, sizeof(unsigned long long), cudaMemcpyDeviceToHost, c->st));
+  int ru = 0, fb = 0;
+  CK(cudaMemcpyAsync(&ru, &c->sd->rank_used, sizeof(int), cudaMemcpyDeviceToHost, c->st));
+  CK(cudaMemcpyAsync(&fb, &c->sd->chol_fallback, sizeof(int), cudaMemcpyDeviceToHost, c->st));
+  sync(c);
+  c->mk = hv.mk;
+  c->stats.bytes_rhs += (double)hv.mk * (4.0 + (c->vf32 ? 4.0 : 8.0)) + (double)hv.touched * r * 8.0 * 2;
+  c->stats.last_matched_nnz = hv.mk;
+  c->stats.mode_steps++;
+  if (info) {
+    info->matched_nnz = hv.mk;
+    info->touched_rows = (int64_t)hv.touched;
+    info->rank_used = ru;
+    info->chol_fallback = fb;
+  }
+  c->have_sample = false;   // a sample is consumed by its solve (factors changed)
+  c->smode_last_solved = k;
+}
+
+double fit_impl(cparls_ctx *c) {
+  Phase ph(c, &c->stats.ms_fit);
+  const int k = c->fit_mode;
+  OtherModes om = other_modes(c, k, false);
+  const int nb = 148 * 4;
+  if (c->vf32)
+    k_fit_inner<float><<<nb, kFitThreads, 0, c->st>>>(c->idx[k].key, c->idx[k].out, (const float *)c->idx[k].val,
+                                                      c->nnz, om, c->A[k], c->lam_model, c->r, c->ld, c->ddpart);
+  else
+    k_fit_inner<double><<<nb, kFitThreads, 0, c->st>>>(c->idx[k].key, c->idx[k].out, (const double *)c->idx[k].val,
+                                                       c->nnz, om, c->A[k], c->lam_model, c->r, c->ld, c->ddpart);
+  CK_LAUNCH();
+  FitModes fm{};
+  fm.D = c->D;
+  for (int m = 0; m < c->D; ++m) fm.md[m] = c->md[m];
+  k_fit_final<<<1, 32, 0, c->st>>>(c->ddpart, nb, fm, c->lam_model, c->r, c->normX2, c->dv->fit);
+  CK_LAUNCH();
+  LAUNCHED(c, 2);
+  double f = read_dev(c, &c->dv->fit[0]);
+  c->stats.fits++;
+  c->stats.bytes_fit += (double)c->nnz * (8.0 + 4.0 + (c->vf32 ? 4.0 : 8.0));
+  ph.end();
+  return f;
+}
+
+cparls_status fail(cparls_ctx *c, int st, const std::string &msg) {
+  if (c) {
+    c->err = msg;
+    if (st == CPARLS_ECUDA || st == CPARLS_ENCCL) c->poisoned = true;
+  }
+  return (cparls_status)st;
+}
+
+template <typename F>
+cparls_status guarded(cparls_ctx *c, F &&f) {
+  if (c && c->poisoned) return fail(c, CPARLS_ECUDA, "context poisoned by an earlier CUDA error: " + c->err);
+  try {
+    f();
+    return CPARLS_OK;
+  } catch (const ApiError &e) {
+    return fail(c, e.status, e.what());
+  } catch (const CudaError &e) {
+    if (e.code == cudaErrorMemoryAllocation) return fail(c, CPARLS_EOOM, e.what());
+    return fail(c, CPARLS_ECUDA, e.what());
+  } catch (const std::bad_alloc &) {
+    return fail(c, CPARLS_EOOM, "host allocation failed");
+  } catch (const std::exception &e) {
+    return fail(c, CPARLS_ECUDA, e.what());
+  }
+}
+
+void check_mode(cparls_ctx *c, int32_t mode) {
+  if (mode < 0 || mode >= c->D) throw ApiError(CPARLS_EINVAL, "mode out of range");
+}
+
+}  // namespace
+
+// =====================================================================
+// C ABI
+// =====================================================================
+extern "C" {
+
+static thread_local std::string g_create_err;
+
+cparls_status cparls_create(cparls_ctx **out, int32_t nmodes, const int64_t *dims, int64_t nnz_local,
+                            const void *coords, const void *vals, const cparls_opts *opts, uint64_t init_seed) {
+  if (!out || !dims || !opts) return CPARLS_EINVAL;
+  *out = nullptr;
+  cparls_ctx *c = new (std::nothrow) cparls_ctx();
+  if (!c) return CPARLS_EOOM;
+  cparls_status st = guarded(c, [&] {
+    if (nmodes < 2 || nmodes > kMaxModes) throw ApiError(CPARLS_EINVAL, "nmodes must be in [2, 8]");
+    if (opts->rank < 1 || opts->rank > kMaxRank) throw ApiError(CPARLS_EINVAL, "rank must be in [1, 64]");
+    if (nnz_local < 0) throw ApiError(CPARLS_EINVAL, "nnz < 0");
+    if (nnz_local >= (int64_t(1) << 32)) throw ApiError(CPARLS_ERANGE, "nnz_local must be < 2^32 per GPU");
+    if (nnz_local > 0 && (!coords || !vals)) throw ApiError(CPARLS_EINVAL, "null coords/vals");
+    if (opts->world_size > 1) throw ApiError(CPARLS_EINVAL, "world_size > 1 not supported by this build");
+    c->D = nmodes;
+    c->r = opts->rank;
+    c->ld = (c->r + 3) & ~3;
+    c->nnz = nnz_local;
+    c->vf32 = opts->value_dtype == 1;
+    c->opts = *opts;
+    c->tau = opts->tau;
+    c->st = static_cast<cudaStream_t>(opts->stream);
+    for (int m = 0; m < nmodes; ++m) {
+      if (dims[m] < 1) throw ApiError(CPARLS_EINVAL, "dims must be >= 1");
+      if (dims[m] >= (int64_t(1) << 31)) throw ApiError(CPARLS_ERANGE, "n_k must be < 2^31");
+      c->dims[m] = dims[m];
+      c->nmax = std::max(c->nmax, dims[m]);
+    }
+    for (int k = 0; k < nmodes; ++k) {
+      long double Nk = 1;
+      for (int m = 0; m < nmodes; ++m)
+        if (m != k) Nk *= (long double)dims[m];
+      if (Nk >= 9223372036854775808.0L) throw ApiError(CPARLS_ERANGE, "prod_{m!=k} n_m >= 2^63");
+    }
+    set_kernel_attrs(c->r, c->ld);
+    c->dv = dalloc_t<DevScalars>(c, 1);
+    CK(cudaMemsetAsync(c->dv, 0, sizeof(DevScalars), c->st));
+    c->sd = dalloc_t<SolveDev>(c, 1);
+    CK(cudaMemsetAsync(c->sd, 0, sizeof(SolveDev), c->st));
+    c->lam_model = dalloc_t<double>(c, kMaxRank);
+    c->ddpart = dalloc_t<dd>(c, 4096);
+    c->gpart_blocks = 148 * 4;
+    c->gpart = dalloc_t<double>(c, c->gpart_blocks * npairs(c->r));
+    c->Gtmp = dalloc_t<double>(c, kMaxRank * kMaxRank);
+    c->tile_u64 = dalloc_t<uint64_t>(c, ceil_div(c->nmax, kLevThreads) + 1);
+    c->i64part = dalloc_t<int64_t>(c, ceil_div(c->nmax, kScanTile) + 65536 + 64);
+    // COO to device if needed
+    const size_t isz = opts->index_dtype == 1 ? 8 : 4, vsz = c->vf32 ? 4 : 8;
+    const void *dco = coords, *dva = vals;
+    void *own_c = nullptr, *own_v = nullptr;
+    if (nnz_local > 0 && !is_device_ptr(coords)) {
+      own_c = dalloc(c, isz * nmodes * nnz_local);
+      CK(cudaMemcpyAsync(own_c, coords, isz * nmodes * nnz_local, cudaMemcpyHostToDevice, c->st));
+      dco = own_c;
+    }
+    if (nnz_local > 0 && !is_device_ptr(vals)) {
+      own_v = dalloc(c, vsz * nnz_local);
+      CK(cudaMemcpyAsync(own_v, vals, vsz * nnz_local, cudaMemcpyHostToDevice, c->st));
+      dva = own_v;
+    }
+    if (isz == 4 && vsz == 4) build_all<int32_t, float>(c, (const int32_t *)dco, (const float *)dva);
+    else if (isz == 4) build_all<int32_t, double>(c, (const int32_t *)dco, (const double *)dva);
+    else if (vsz == 4) build_all<int64_t, float>(c, (const int64_t *)dco, (const float *)dva);
+    else build_all<int64_t, double>(c, (const int64_t *)dco, (const double *)dva);
+    sync(c);
+    dfree(c, own_c);
+    dfree(c, own_v);
+    // factors, p~, CDF
+    for (int k = 0; k < nmodes; ++k) {
+      c->A[k] = dalloc_t<double>(c, c->dims[k] * c->ld);
+      c->pt[k] = dalloc_t<double>(c, c->dims[k]);
+      c->C[k] = dalloc_t<uint64_t>(c, c->dims[k]);
+      c->md[k] = dalloc_t<ModeDev>(c, 1);
+      CK(cudaMemsetAsync(c->md[k], 0, sizeof(ModeDev), c->st));
+      int64_t tot = c->dims[k] * c->ld;
+      k_init_uniform<<<(unsigned)ceil_div(tot, 256), 256, 0, c->st>>>(c->A[k], c->dims[k], c->r, c->ld, k,
+                                                                      (uint32_t)init_seed);
+      CK_LAUNCH();
+    }
+    c->M = dalloc_t<double>(c, c->nmax * c->ld);
+    CK(cudaMemsetAsync(c->M, 0, sizeof(double) * c->nmax * c->ld, c->st));
+    c->touched = dalloc_t<uint8_t>(c, c->nmax);
+    CK(cudaMemsetAsync(c->touched, 0, c->nmax, c->st));
+    // DIDX candidate buffers (n_m each, worst case)
+    int64_t cc = c->nmax;
+    for (int m = 0; m < nmodes; ++m) {
+      c->ckey[m] = dalloc_t<uint64_t>(c, c->dims[m]);
+      c->cidx[m] = dalloc_t<uint32_t>(c, c->dims[m]);
+    }
+    c->ckey_tmp = dalloc_t<uint64_t>(c, cc);
+    c->cidx_tmp = dalloc_t<uint32_t>(c, cc);
+    c->rhist = dalloc_t<uint32_t>(c, 256 * (ceil_div(cc, kScanTile) + 1));
+    c->ccap = cc;
+    ensure_list_cap(c, 1 << 16);
+    c->acap = int64_t(1) << 22;
+    c->akey = dalloc_t<uint64_t>(c, c->acap);
+    c->ap = dalloc_t<double>(c, c->acap);
+    alloc_sample_buffers(c, 1 << 17);
+    // fit streams the mode whose sorted copy has the most repeated keys: use
+    // the mode with the largest n_k (longest fibers on average)
+    c->fit_mode = 0;
+    for (int m = 1; m < nmodes; ++m)
+      if (c->dims[m] > c->dims[c->fit_mode]) c->fit_mode = m;
+    reset_lambda(c);
+    for (int k = 0; k < nmodes; ++k) leverage_full(c, k);
+    sync(c);
+  });
+  if (st != CPARLS_OK) {
+    g_create_err = c->err;
+    for (void *p : c->allocs) cudaFree(p);
+    delete c;
+    return st;
+  }
+  *out = c;
+  return CPARLS_OK;
+}
+
+cparls_status cparls_destroy(cparls_ctx *c) {
+  if (!c) return CPARLS_OK;
+  if (!c->poisoned) cudaStreamSynchronize(c->st);
+  for (void *p : c->allocs) cudaFree(p);
+  delete c;
+  return CPARLS_OK;
+}
+
+cparls_status cparls_set_factor(cparls_ctx *c, int32_t mode, const double *A) {
+  if (!c || !A) return CPARLS_EINVAL;
+  return guarded(c, [&] {
+    check_mode(c, mode);
+    const int64_t n = c->dims[mode];
+    CK(cudaMemcpy2DAsync(c->A[mode], sizeof(double) * c->ld, A, sizeof(double) * c->r, sizeof(double) * c->r, n,
+                         is_device_ptr(A) ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, c->st));
+    c->have_sample = false;
+    reset_lambda(c);
+    leverage_full(c, mode);
+    sync(c);
+  });
+}
+
+cparls_status cparls_get_factor(cparls_ctx *c, int32_t mode, double *A, double *lambda) {
+  if (!c) return CPARLS_EINVAL;
+  return guarded(c, [&] {
+    check_mode(c, mode);
+    if (A)
+      CK(cudaMemcpy2DAsync(A, sizeof(double) * c->r, c->A[mode], sizeof(double) * c->ld, sizeof(double) * c->r,
+                           c->dims[mode], cudaMemcpyDeviceToHost, c->st));
+    if (lambda) CK(cudaMemcpyAsync(lambda, c->lam_model, sizeof(double) * c->r, cudaMemcpyDeviceToHost, c->st));
+    sync(c);
+  });
+}
+
+cparls_status cparls_leverage(cparls_ctx *c, int32_t mode, double *scores, int32_t *rank_out) {
+  if (!c) return CPARLS_EINVAL;
+  return guarded(c, [&] {
+    check_mode(c, mode);
+    leverage_full(c, mode);
+    int rank = 0;
+    CK(cudaMemcpyAsync(&rank, &c->md[mode]->rank, sizeof(int), cudaMemcpyDeviceToHost, c->st));
+    if (scores)
+      CK(cudaMemcpyAsync(scores, c->pt[mode], sizeof(double) * c->dims[mode], cudaMemcpyDeviceToHost, c->st));
+    sync(c);
+    if (scores)
+      for (int64_t i = 0; i < c->dims[mode]; ++i) scores[i] *= (double)rank;   // l = p~ * rank
+    if (rank_out) *rank_out = rank;
+  });
+}
+
+cparls_status cparls_get_ptilde(cparls_ctx *c, int32_t mode, double *pt) {
+  if (!c || !pt) return CPARLS_EINVAL;
+  return guarded(c, [&] {
+    check_mode(c, mode);
+    CK(cudaMemcpyAsync(pt, c->pt[mode], sizeof(double) * c->dims[mode], cudaMemcpyDeviceToHost, c->st));
+    sync(c);
+  });
+}
+
+cparls_status cparls_set_ptilde(cparls_ctx *c, int32_t mode, const double *pt) {
+  if (!c || !pt) return CPARLS_EINVAL;
+  return guarded(c, [&] {
+    check_mode(c, mode);
+    const int64_t n = c->dims[mode];
+    CK(cudaMemcpyAsync(c->pt[mode], pt, sizeof(double) * n,
+                       is_device_ptr(pt) ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, c->st));
+    const int64_t nt = ceil_div(n, kLevThreads);
+    CK(cudaMemsetAsync(&c->md[mode]->alpha, 0, sizeof(double), c->st));
+    CK(cudaMemsetAsync(&c->md[mode]->drawable, 0, sizeof(long long), c->st));
+    k_q_from_pt<<<(unsigned)nt, kLevThreads, 0, c->st>>>(c->pt[mode], n, c->C[mode], c->tile_u64,
+                                                         &c->md[mode]->alpha,
+                                                         reinterpret_cast<unsigned long long *>(&c->md[mode]->drawable));
+    CK_LAUNCH();
+    k_scan_u64_single<<<1, kScanThreads, 0, c->st>>>(c->tile_u64, nt);
+    CK_LAUNCH();
+    k_cdf_final<<<(unsigned)nt, kLevThreads, 0, c->st>>>(c->C[mode], n, c->tile_u64);
+    CK_LAUNCH();
+    c->have_sample = false;
+    sync(c);
+  });
+}
+
+cparls_status cparls_set_tau(cparls_ctx *c, double tau) {
+  if (!c) return CPARLS_EINVAL;
+  c->tau = tau;
+  return CPARLS_OK;
+}
+
+cparls_status cparls_sample(cparls_ctx *c, int32_t mode, int64_t s, uint64_t seed, uint64_t step,
+                            cparls_sample_info *info) {
+  if (!c) return CPARLS_EINVAL;
+  return guarded(c, [&] {
+    check_mode(c, mode);
+    sample_impl(c, mode, s, seed, step, info);
+  });
+}
+
+namespace {
+std::vector<int64_t> canonical_order(const std::vector<uint64_t> &k, const std::vector<uint8_t> &det) {
+  std::vector<int64_t> o(k.size());
+  std::iota(o.begin(), o.end(), 0);
+  std::sort(o.begin(), o.end(), [&](int64_t a, int64_t b) {
+    if (det[a] != det[b]) return det[a] > det[b];
+    return k[a] < k[b];
+  });
+  return o;
+}
+}  // namespace
+
+cparls_status cparls_get_sample(cparls_ctx *c, int64_t cap, uint64_t *keys, int32_t *counts, double *w2, double *p,
+                                uint8_t *is_det, int64_t *n_out) {
+  if (!c) return CPARLS_EINVAL;
+  return guarded(c, [&] {
+    const int64_t n = c->sbar;
+    if (n_out) *n_out = n;
+    std::vector<uint64_t> hk(n);
+    std::vector<int32_t> hc(n);
+    std::vector<double> hw(n), hp(n);
+    std::vector<uint8_t> hd(n);
+    if (n > 0) {
+      CK(cudaMemcpyAsync(hk.data(), c->skey, 8 * n, cudaMemcpyDeviceToHost, c->st));
+      CK(cudaMemcpyAsync(hc.data(), c->scnt, 4 * n, cudaMemcpyDeviceToHost, c->st));
+      CK(cudaMemcpyAsync(hw.data(), c->sw2, 8 * n, cudaMemcpyDeviceToHost, c->st));
+      CK(cudaMemcpyAsync(hp.data(), c->sp, 8 * n, cudaMemcpyDeviceToHost, c->st));
+      CK(cudaMemcpyAsync(hd.data(), c->sisdet, n, cudaMemcpyDeviceToHost, c->st));
+      sync(c);
+    }
+    auto o = canonical_order(hk, hd);
+    int64_t m = std::min(cap, n);
+    for (int64_t i = 0; i < m; ++i) {
+      int64_t j = o[i];
+      if (keys) keys[i] = hk[j];
+      if (counts) counts[i] = hc[j];
+      if (w2) w2[i] = hw[j];
+      if (p) p[i] = hp[j];
+      if (is_det) is_det[i] = hd[j];
+    }
+  });
+}
+
+cparls_status cparls_get_fibers(cparls_ctx *c, int64_t cap, int64_t *len, int64_t *out, double *val,
+                                int64_t *m_out) {
+  if (!c) return CPARLS_EINVAL;
+  return guarded(c, [&] {
+    if (c->smode < 0 || c->sbar < 0) throw ApiError(CPARLS_ESTATE, "no sample");
+    const int k = c->smode;
+    if (!c->have_lookup) lookup_impl(c, k);
+    const int64_t n = c->sbar;
+    int64_t mk = read_dev(c, &c->dv->mk);
+    if (m_out) *m_out = mk;
+    std::vector<uint64_t> hk(n);
+    std::vector<uint8_t> hd(n);
+    std::vector<int64_t> hl(n), ho(n);
+    std::vector<int64_t> go(mk);
+    std::vector<double> gv(mk);
+    if (n > 0) {
+      CK(cudaMemcpyAsync(hk.data(), c->skey, 8 * n, cudaMemcpyDeviceToHost, c->st));
+      CK(cudaMemcpyAsync(hd.data(), c->sisdet, n, cudaMemcpyDeviceToHost, c->st));
+      CK(cudaMemcpyAsync(hl.data(), c->len, 8 * n, cudaMemcpyDeviceToHost, c->st));
+      CK(cudaMemcpyAsync(ho.data(), c->off, 8 * n, cudaMemcpyDeviceToHost, c->st));
+    }
+    if (mk > 0) {
+      int64_t *dO = dalloc_t<int64_t>(c, mk);
+      double *dV = dalloc_t<double>(c, mk);
+      if (c->vf32)
+        k_gather_fibers<float><<<(unsigned)n, 128, 0, c->st>>>(c->off, c->lo, c->len, n, c->idx[k].out,
+                                                                (const float *)c->idx[k].val, dO, dV);
+      else
+        k_gather_fibers<double><<<(unsigned)n, 128, 0, c->st>>>(c->off, c->lo, c->len, n, c->idx[k].out,
+                                                                 (const double *)c->idx[k].val, dO, dV);
+      CK_LAUNCH();
+      CK(cudaMemcpyAsync(go.data(), dO, 8 * mk, cudaMemcpyDeviceToHost, c->st));
+      CK(cudaMemcpyAsync(gv.data(), dV, 8 * mk, cudaMemcpyDeviceToHost, c->st));
+      sync(c);
+      dfree(c, dO);
+      dfree(c, dV);
+    }
+    sync(c);
+    auto o = canonical_order(hk, hd);
+    int64_t w = 0;
+    for (int64_t i = 0; i < n; ++i) {
+      int64_t j = o[i];
+      if (len) len[i] = hl[j];
+      for (int64_t t = 0; t < hl[j]; ++t, ++w) {
+        if (w < cap) {
+          if (out) out[w] = go[ho[j] + t];
+          if (val) val[w] = gv[ho[j] + t];
+        }
+      }
+    }
+  });
+}
+
+cparls_status cparls_solve_mode(cparls_ctx *c, int32_t mode, cparls_solve_info *info) {
+  if (!c) return CPARLS_EINVAL;
+  return guarded(c, [&] {
+    check_mode(c, mode);
+    solve_impl(c, mode, info);
+  });
+}
+
+cparls_status cparls_get_last_solve(cparls_ctx *c, double *G, double *B) {
+  if (!c) return CPARLS_EINVAL;
+  return guarded(c, [&] {
+    const int r = c->r;
+    if (G) CK(cudaMemcpyAsync(G, c->sd->G, sizeof(double) * r * r, cudaMemcpyDeviceToHost, c->st));
+    if (B) {
+      int k = c->smode_last_solved;
+      if (k < 0) throw ApiError(CPARLS_ESTATE, "no solve yet");
+      std::vector<double> lam(r);
+      CK(cudaMemcpy2DAsync(B, sizeof(double) * r, c->A[k], sizeof(double) * c->ld, sizeof(double) * r, c->dims[k],
+                           cudaMemcpyDeviceToHost, c->st));
+      CK(cudaMemcpyAsync(lam.data(), c->sd->lambda, sizeof(double) * r, cudaMemcpyDeviceToHost, c->st));
+      sync(c);
+      for (int64_t i = 0; i < c->dims[k]; ++i)
+        for (int q = 0; q < r; ++q) B[i * r + q] *= lam[q];
+    }
+    sync(c);
+  });
+}
+
+cparls_status cparls_fit(cparls_ctx *c, double *fit) {
+  if (!c) return CPARLS_EINVAL;
+  return guarded(c, [&] {
+    if (c->normX2 <= 0.0) throw ApiError(CPARLS_ENUMERIC, "||X|| = 0: fit undefined");
+    double f = fit_impl(c);
+    if (fit) *fit = f;
+  });
+}
+
+cparls_status cparls_run(cparls_ctx *c, int32_t iters, int64_t s, uint64_t seed, int32_t iter0, int32_t fit_every,
+                         double *fit_trace) {
+  if (!c) return CPARLS_EINVAL;
+  return guarded(c, [&] {
+    if (iters < 0) throw ApiError(CPARLS_EINVAL, "iters < 0");
+    for (int t = 0; t < iters; ++t) {
+      for (int k = 0; k < c->D; ++k) {
+        uint64_t step = (uint64_t)(iter0 + t) * c->D + k;   // AMB-10
+        sample_impl(c, k, s, seed, step, nullptr);
+        solve_impl(c, k, nullptr);
+      }
+      double f = NAN;
+      if (fit_every > 0 && (t + 1) % fit_every == 0) {
+        if (c->normX2 <= 0.0) throw ApiError(CPARLS_ENUMERIC, "||X|| = 0: fit undefined");
+        f = fit_impl(c);
+      }
+      if (fit_trace) fit_trace[t] = f;
+    }
+  });
+}
+
+cparls_status cparls_get_stats(cparls_ctx *c, cparls_stats *s) {
+  if (!c || !s) return CPARLS_EINVAL;
+  *s = c->stats;
+  return CPARLS_OK;
+}
+
+cparls_status cparls_reset_stats(cparls_ctx *c) {
+  if (!c) return CPARLS_EINVAL;
+  c->stats = cparls_stats{};
+  return CPARLS_OK;
+}
+
+cparls_status cparls_set_profiling(cparls_ctx *c, int32_t on) {
+  if (!c) return CPARLS_EINVAL;
+  c->profiling = on != 0;
+  return CPARLS_OK;
+}
+
+const char *cparls_last_error(const cparls_ctx *c) {
+  if (!c) return g_create_err.c_str();
+  return c->err.c_str();
+}
+
+const char *cparls_version(void) { return "cparls 0.1 (sm_100a, CP-ARLS-LEV hot path)"; }
+
+}  // extern "C"

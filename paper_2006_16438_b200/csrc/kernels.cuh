@@ -1,0 +1,1099 @@
+// kernels.cuh -- CP-ARLS-LEV hot-path kernels for sm_100a (B200).
+// "P:L" cites /root/reference/PAPER.md line L; AMB-n cites DESIGN.md readings.
+#pragma once
+#include "common.cuh"
+#include "prims.cuh"
+
+namespace cparls {
+
+// Per-mode device state written by the leverage preparation.
+struct ModeDev {
+  double alpha;            // max p~
+  long long drawable;      // #{i : p~_i > 2^-63}  (rows whose integer weight q_i > 0)
+  int rank;                // kept rank (AMB-11)
+  int tri;                 // 1: W upper triangular (Cholesky); 0: full (eigen)
+  double W[kMaxRank * kMaxRank];   // l_i = || a_i W ||^2
+  double GA[kMaxRank * kMaxRank];  // Gram of the (normalized) factor
+};
+
+// Per-solve device scalars.
+struct SolveDev {
+  double G[kMaxRank * kMaxRank];     // sampled Gram Z~^T Z~
+  double Ginv[kMaxRank * kMaxRank];  // (pseudo-)inverse used for B = M G^+
+  double BtB[kMaxRank * kMaxRank];
+  double lambda[kMaxRank];
+  double lambda_inv[kMaxRank];       // unused (division is used)
+  int rank_used;
+  int chol_fallback;
+  long long touched;
+};
+
+__host__ __device__ constexpr int npairs(int r) { return r * (r + 1) / 2; }
+
+// ======================================================================
+// Small dense r x r linear algebra, single block (r <= 64)
+// ======================================================================
+
+// Cyclic Jacobi eigensolver on shared-memory matrix a (r x r, row stride r),
+// V (r x r).  Executed by thread 0 only (fallback path; r <= 64).
+__device__ void jacobi_serial(int r, double *a, double *V) {
+  for (int i = 0; i < r; ++i)
+    for (int j = 0; j < r; ++j) V[i * r + j] = (i == j) ? 1.0 : 0.0;
+  for (int sweep = 0; sweep < 100; ++sweep) {
+    double off = 0.0, diag = 0.0;
+    for (int i = 0; i < r; ++i) {
+      diag += a[i * r + i] * a[i * r + i];
+      for (int j = i + 1; j < r; ++j) off += a[i * r + j] * a[i * r + j];
+    }
+    if (off <= 1e-34 * diag || off == 0.0) break;
+    for (int p = 0; p < r; ++p)
+      for (int q = p + 1; q < r; ++q) {
+        double apq = a[p * r + q];
+        if (apq == 0.0) continue;
+        double theta = (a[q * r + q] - a[p * r + p]) / (2.0 * apq);
+        double t = (theta >= 0 ? 1.0 : -1.0) / (fabs(theta) + sqrt(theta * theta + 1.0));
+        double c = 1.0 / sqrt(t * t + 1.0), s = t * c;
+        for (int k = 0; k < r; ++k) {
+          double akp = a[k * r + p], akq = a[k * r + q];
+          a[k * r + p] = c * akp - s * akq;
+          a[k * r + q] = s * akp + c * akq;
+        }
+        for (int k = 0; k < r; ++k) {
+          double apk = a[p * r + k], aqk = a[q * r + k];
+          a[p * r + k] = c * apk - s * aqk;
+          a[q * r + k] = s * apk + c * aqk;
+        }
+        for (int k = 0; k < r; ++k) {
+          double vkp = V[k * r + p], vkq = V[k * r + q];
+          V[k * r + p] = c * vkp - s * vkq;
+          V[k * r + q] = s * vkp + c * vkq;
+        }
+      }
+  }
+}
+
+// Cholesky G = L L^T in shared memory with the pivot test of AMB-12
+// (pivot > r*eps*max_diag).  Returns 1 on success.  L lower (row stride r).
+// Whole block participates.
+__device__ int block_cholesky(int r, const double *G, double *L, int *ok_flag) {
+  __shared__ double maxdiag;
+  if (threadIdx.x == 0) {
+    double m = 0.0;
+    for (int j = 0; j < r; ++j) m = fmax(m, G[j * r + j]);
+    maxdiag = m;
+    *ok_flag = m > 0.0;
+  }
+  for (int i = threadIdx.x; i < r * r; i += blockDim.x) L[i] = 0.0;
+  __syncthreads();
+  for (int j = 0; j < r; ++j) {
+    if (threadIdx.x == 0 && *ok_flag) {
+      double dj = G[j * r + j];
+      for (int q = 0; q < j; ++q) dj -= L[j * r + q] * L[j * r + q];
+      if (!(dj > (double)r * 2.220446049250313e-16 * maxdiag)) *ok_flag = 0;
+      else L[j * r + j] = sqrt(dj);
+    }
+    __syncthreads();
+    if (!*ok_flag) return 0;
+    for (int i = j + 1 + threadIdx.x; i < r; i += blockDim.x) {
+      double v = G[i * r + j];
+      for (int q = 0; q < j; ++q) v -= L[i * r + q] * L[j * r + q];
+      L[i * r + j] = v / L[j * r + j];
+    }
+    __syncthreads();
+  }
+  return 1;
+}
+
+// Lower-triangular inverse: Linv (row stride r), column c by thread c.
+__device__ void block_tri_inverse(int r, const double *L, double *Linv) {
+  for (int c = threadIdx.x; c < r; c += blockDim.x) {
+    for (int i = 0; i < r; ++i) {
+      if (i < c) { Linv[i * r + c] = 0.0; continue; }
+      double v = (i == c) ? 1.0 : 0.0;
+      for (int q = c; q < i; ++q) v -= L[i * r + q] * Linv[q * r + c];
+      Linv[i * r + c] = v / L[i * r + i];
+    }
+  }
+  __syncthreads();
+}
+
+// Leverage preparation from Gram G (r x r, global): W with l_i = ||a_i W||^2.
+// Cholesky: W = L^{-T} (upper triangular).  Fallback: W = V_kept diag(mu^{-1/2}).
+__device__ void lev_prep_body(int r, const double *Gg, ModeDev *md) {
+  extern __shared__ double sm[];
+  double *G = sm, *L = sm + r * r, *Li = sm + 2 * r * r;
+  __shared__ int ok;
+  for (int i = threadIdx.x; i < r * r; i += blockDim.x) { G[i] = Gg[i]; md->GA[i] = Gg[i]; }
+  __syncthreads();
+  int good = block_cholesky(r, G, L, &ok);
+  if (good) {
+    block_tri_inverse(r, L, Li);
+    // W = Li^T : W[p][c] = Li[c][p]
+    for (int i = threadIdx.x; i < r * r; i += blockDim.x) {
+      int p = i / r, c = i % r;
+      md->W[p * r + c] = Li[c * r + p];
+    }
+    if (threadIdx.x == 0) { md->tri = 1; md->rank = r; }
+    return;
+  }
+  // eigen fallback
+  if (threadIdx.x == 0) {
+    double *a = L, *V = Li;
+    for (int i = 0; i < r * r; ++i) a[i] = G[i];
+    jacobi_serial(r, a, V);
+    double mumax = 0.0;
+    for (int j = 0; j < r; ++j) mumax = fmax(mumax, a[j * r + j]);
+    int rank = 0;
+    for (int j = 0; j < r; ++j) {
+      double mu = a[j * r + j];
+      bool keep = mumax > 0.0 && mu > (double)r * 2.220446049250313e-16 * mumax;
+      rank += keep;
+      double s = keep ? 1.0 / sqrt(mu) : 0.0;
+      for (int p = 0; p < r; ++p) md->W[p * r + j] = V[p * r + j] * s;
+    }
+    md->tri = 0;
+    md->rank = rank;
+  }
+}
+
+__global__ void k_lev_prep(int r, const double *G, ModeDev *md) { lev_prep_body(r, G, md); }
+
+// ======================================================================
+// Gram of rows (optionally pairs-only partials per block)
+// ======================================================================
+// Block partial of sum_i a_i^T a_i over rows [blk*rows_per_block, ...).
+// Rows staged in smem tiles of 32 rows; thread t owns pairs t, t+256, ...
+constexpr int kGramThreads = 256;
+constexpr int kGramTile = 32;
+
+__global__ void __launch_bounds__(kGramThreads) k_gram_rows(const double *__restrict__ A, int64_t n, int r, int ld,
+                                                           int64_t rows_per_block, double *__restrict__ part) {
+  __shared__ double tile[kGramTile][kMaxRank + 1];
+  __shared__ int pp[npairs(kMaxRank)], qq[npairs(kMaxRank)];
+  const int P = npairs(r);
+  if (threadIdx.x == 0) {
+    int t = 0;
+    for (int p = 0; p < r; ++p)
+      for (int q = p; q < r; ++q, ++t) { pp[t] = p; qq[t] = q; }
+  }
+  double acc[9];
+#pragma unroll
+  for (int i = 0; i < 9; ++i) acc[i] = 0.0;
+  int64_t r0 = (int64_t)blockIdx.x * rows_per_block;
+  int64_t r1 = min(n, r0 + rows_per_block);
+  __syncthreads();
+  for (int64_t base = r0; base < r1; base += kGramTile) {
+    int rows = (int)min((int64_t)kGramTile, r1 - base);
+    for (int i = threadIdx.x; i < rows * r; i += blockDim.x) {
+      int row = i / r, c = i % r;
+      tile[row][c] = A[(base + row) * ld + c];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < 9; ++i) {
+      int t = threadIdx.x + i * kGramThreads;
+      if (t < P) {
+        int p = pp[t], q = qq[t];
+        double s = 0.0;
+        for (int row = 0; row < rows; ++row) s += tile[row][p] * tile[row][q];
+        acc[i] += s;
+      }
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < 9; ++i) {
+    int t = threadIdx.x + i * kGramThreads;
+    if (t < P) part[(int64_t)blockIdx.x * P + t] = acc[i];
+  }
+}
+
+// Sum block partials (fixed order, compensated) into a full symmetric r x r.
+__global__ void k_gram_reduce(const double *__restrict__ part, int64_t nblocks, int r, double *__restrict__ G) {
+  const int P = npairs(r);
+  for (int t = threadIdx.x; t < P; t += blockDim.x) {
+    int p = 0, rem = t;
+    while (rem >= r - p) { rem -= r - p; ++p; }
+    int q = p + rem;
+    dd s = {0.0, 0.0};
+    for (int64_t b = 0; b < nblocks; ++b) s = dd_add_d(s, part[b * P + t]);
+    double v = s.hi + s.lo;
+    G[p * r + q] = v;
+    G[q * r + p] = v;
+  }
+}
+
+// ======================================================================
+// K1/K2: leverage rows -> p~ -> integer weights q (CDF pass 1)
+// ======================================================================
+constexpr int kLevThreads = 256;
+
+// One row per thread; rows staged through smem (stride ld+1, conflict-free).
+// If lam != nullptr, a_i := b_i / lam (column normalization, P:925-926,
+// AMB-13) is written back to A.  Writes p~ (=l/rank), C[i] = q_i (temporary),
+// per-block sum of q, alpha (atomic max), drawable count.
+__global__ void __launch_bounds__(kLevThreads) k_lev_rows(double *__restrict__ A, int64_t n, int r, int ld,
+                                                         const double *__restrict__ lam, const ModeDev *__restrict__ md,
+                                                         double *__restrict__ pt, uint64_t *__restrict__ C,
+                                                         uint64_t *__restrict__ tile_sum, double *alpha_out,
+                                                         unsigned long long *drawable_out) {
+  extern __shared__ double smem[];
+  double *W = smem;                       // r*r
+  double *tile = smem + r * r;            // kLevThreads x (ld+1)
+  const int S = ld + 1;
+  const int tri = md->tri;
+  const int rank = md->rank;
+  for (int i = threadIdx.x; i < r * r; i += blockDim.x) W[i] = md->W[i];
+  int64_t base = (int64_t)blockIdx.x * kLevThreads;
+  int rows = (int)min((int64_t)kLevThreads, n - base);
+  const double *src = A + base * ld;
+  for (int i = threadIdx.x; i < rows * ld; i += blockDim.x) {
+    int row = i / ld, c = i - row * ld;
+    double v = src[i];
+    if (lam != nullptr && c < r) {
+      double l = lam[c];
+      v = l > 0.0 ? v / l : 0.0;
+    }
+    tile[row * S + c] = v;
+  }
+  __syncthreads();
+  if (lam != nullptr) {
+    double *dst = A + base * ld;
+    for (int i = threadIdx.x; i < rows * ld; i += blockDim.x) {
+      int row = i / ld, c = i - row * ld;
+      dst[i] = tile[row * S + c];
+    }
+  }
+  uint64_t q = 0;
+  double p = 0.0;
+  if (threadIdx.x < rows) {
+    const double *a = tile + threadIdx.x * S;
+    double l = 0.0;
+    if (rank > 0) {
+      for (int c = 0; c < r; ++c) {
+        double t = 0.0;
+        int pe = tri ? c + 1 : r;
+        for (int k = 0; k < pe; ++k) t += a[k] * W[k * r + c];
+        l += t * t;
+      }
+      p = l / (double)rank;
+    }
+    q = __double2ull_rn(p * kTwo62);
+    int64_t i = base + threadIdx.x;
+    pt[i] = p;
+    C[i] = q;
+  }
+  // block reductions: sum q, max p, drawable
+  unsigned long long qs = warp_sum<unsigned long long>(q);
+  double pm = p;
+#pragma unroll
+  for (int m = 16; m >= 1; m >>= 1) pm = fmax(pm, __shfl_xor_sync(0xffffffffu, pm, m));
+  unsigned dr = __popc(__ballot_sync(0xffffffffu, threadIdx.x < rows && p > 1.0842021724855044e-19));
+  __shared__ unsigned long long wq[kLevThreads / 32];
+  __shared__ double wp[kLevThreads / 32];
+  __shared__ unsigned wd[kLevThreads / 32];
+  int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  if (lane == 0) { wq[w] = qs; wp[w] = pm; wd[w] = dr; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long s = 0; double m = 0.0; unsigned long long d = 0;
+    for (int i = 0; i < kLevThreads / 32; ++i) { s += wq[i]; m = fmax(m, wp[i]); d += wd[i]; }
+    tile_sum[blockIdx.x] = s;
+    atomic_max_nonneg(alpha_out, m);
+    atomicAdd(drawable_out, d);
+  }
+}
+
+// CDF pass 3: C[i] = offset(tile) + inclusive scan of q within tile.
+__global__ void __launch_bounds__(kLevThreads) k_cdf_final(uint64_t *__restrict__ C, int64_t n,
+                                                           const uint64_t *__restrict__ tile_off) {
+  int64_t i = (int64_t)blockIdx.x * kLevThreads + threadIdx.x;
+  uint64_t q = i < n ? C[i] : 0ull;
+  uint64_t tot;
+  uint64_t ex = block_excl_scan<unsigned long long>(q, (unsigned long long *)&tot);
+  if (i < n) C[i] = tile_off[blockIdx.x] + ex + q;
+}
+
+// exclusive scan of u64 tile sums (single block)
+__global__ void k_scan_u64_single(uint64_t *part, int64_t nb) {
+  unsigned long long carry = 0;
+  for (int64_t base = 0; base < nb; base += kScanThreads) {
+    int64_t idx = base + threadIdx.x;
+    unsigned long long v = idx < nb ? part[idx] : 0ull;
+    unsigned long long tot;
+    unsigned long long ex = block_excl_scan<unsigned long long>(v, &tot);
+    if (idx < nb) part[idx] = carry + ex;
+    carry += tot;
+    __syncthreads();
+  }
+}
+
+// Recompute q from given p~ (set_ptilde path), same rounding as k_lev_rows.
+__global__ void k_q_from_pt(const double *__restrict__ pt, int64_t n, uint64_t *__restrict__ C,
+                            uint64_t *__restrict__ tile_sum, double *alpha_out, unsigned long long *drawable_out) {
+  int64_t i = (int64_t)blockIdx.x * kLevThreads + threadIdx.x;
+  double p = i < n ? pt[i] : 0.0;
+  uint64_t q = __double2ull_rn(p * kTwo62);
+  if (i < n) C[i] = q;
+  unsigned long long qs = warp_sum<unsigned long long>(q);
+  double pm = p;
+#pragma unroll
+  for (int m = 16; m >= 1; m >>= 1) pm = fmax(pm, __shfl_xor_sync(0xffffffffu, pm, m));
+  unsigned dr = __popc(__ballot_sync(0xffffffffu, i < n && p > 1.0842021724855044e-19));
+  __shared__ unsigned long long wq[kLevThreads / 32];
+  __shared__ double wp[kLevThreads / 32];
+  __shared__ unsigned wd[kLevThreads / 32];
+  int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  if (lane == 0) { wq[w] = qs; wp[w] = pm; wd[w] = dr; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long s = 0; double m = 0.0; unsigned long long d = 0;
+    for (int k = 0; k < kLevThreads / 32; ++k) { s += wq[k]; m = fmax(m, wp[k]); d += wd[k]; }
+    tile_sum[blockIdx.x] = s;
+    atomic_max_nonneg(alpha_out, m);
+    atomicAdd(drawable_out, d);
+  }
+}
+
+// U[0,1) factor init (AMB-21): entry (i,c) of mode m from Philox4x32-10 with
+// counter (i, c, m, 0x1417), key (seed, 0x55AA); u = (x1<<21 | x0>>11) 2^-53.
+__global__ void k_init_uniform(double *A, int64_t n, int r, int ld, int m, uint32_t seed) {
+  int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n * ld) return;
+  int64_t i = t / ld;
+  int c = (int)(t - i * ld);
+  double v = 0.0;
+  if (c < r) {
+    u32x4 x = philox4x32_10({(uint32_t)i, (uint32_t)c, (uint32_t)m, 0x1417u}, seed, 0x55AAu);
+    uint64_t w = ((uint64_t)x.y << 21) | (x.x >> 11);
+    v = (double)w * 1.1102230246251565e-16;
+  }
+  A[t] = v;
+}
+
+// ======================================================================
+// K3 DIDX
+// ======================================================================
+struct OtherModes {
+  int d;
+  int mode[kMaxModes];
+  int64_t n[kMaxModes];
+  const double *pt[kMaxModes];
+  const uint64_t *C[kMaxModes];
+  const double *A[kMaxModes];
+  uint64_t mult[kMaxModes];   // prod_{l<j} n_l
+  double alpha[kMaxModes];
+};
+
+// Canonical product with position j = x, every other position at alpha (the
+// largest p any index with i_j fixed can reach; fp multiply is monotone).
+__device__ __forceinline__ double prod_with(const OtherModes &om, int j, double x) {
+  double p = (j == 0) ? x : om.alpha[0];
+  for (int l = 1; l < om.d; ++l) p = p * ((l == j) ? x : om.alpha[l]);
+  return p;
+}
+
+// pass 1: per-tile counts of candidates of mode j
+__global__ void k_cand_count(OtherModes om, int j, double tau, int64_t *__restrict__ part) {
+  int64_t base = (int64_t)blockIdx.x * kScanTile;
+  int64_t s = 0;
+  const double *pt = om.pt[j];
+  for (int i = 0; i < kScanItems; ++i) {
+    int64_t idx = base + (int64_t)i * kScanThreads + threadIdx.x;
+    if (idx < om.n[j] && prod_with(om, j, pt[idx]) > tau) ++s;
+  }
+  int64_t tot;
+  block_excl_scan<int64_t>(s, &tot);
+  if (threadIdx.x == 0) part[blockIdx.x] = tot;
+}
+
+// pass 3: ordered scatter of candidates: key = ~bits(p~) (descending order
+// after an ascending stable sort), value = row index.
+__global__ void k_cand_scatter(OtherModes om, int j, double tau, const int64_t *__restrict__ part,
+                               uint64_t *__restrict__ ckey, uint32_t *__restrict__ cidx) {
+  int64_t base = (int64_t)blockIdx.x * kScanTile + (int64_t)threadIdx.x * kScanItems;
+  const double *pt = om.pt[j];
+  bool f[kScanItems];
+  int64_t s = 0;
+  for (int i = 0; i < kScanItems; ++i) {
+    int64_t idx = base + i;
+    f[i] = idx < om.n[j] && prod_with(om, j, pt[idx]) > tau;
+    s += f[i];
+  }
+  int64_t tot;
+  int64_t pos = block_excl_scan<int64_t>(s, &tot) + part[blockIdx.x];
+  for (int i = 0; i < kScanItems; ++i) {
+    if (f[i]) {
+      int64_t idx = base + i;
+      ckey[pos] = ~(uint64_t)__double_as_longlong(pt[idx]);
+      cidx[pos] = (uint32_t)idx;
+      ++pos;
+    }
+  }
+}
+
+__device__ __forceinline__ double cand_val(uint64_t k) { return __longlong_as_double((long long)~k); }
+
+// Level expansion count: entry e (partial product pp_e) x sorted candidates of
+// level l: count of the prefix with fl(pp*v)*alpha_{l+1}*... > tau.
+__global__ void k_didx_count(const double *__restrict__ pp, int64_t nlist, const uint64_t *__restrict__ ckey,
+                             int64_t ncand, OtherModes om, int l, double tau, int64_t *__restrict__ cnt) {
+  int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= nlist) return;
+  double base = pp[e];
+  int64_t lo = 0, len = ncand;  // first t where predicate fails
+  while (len > 0) {
+    int64_t half = len >> 1;
+    double b = base * cand_val(ckey[lo + half]);
+    for (int k = l + 1; k < om.d; ++k) b = b * om.alpha[k];
+    if (b > tau) { lo += half + 1; len -= half + 1; }
+    else len = half;
+  }
+  cnt[e] = lo;
+}
+
+// Level expansion emit: one warp per entry, lanes over its candidate prefix.
+__global__ void k_didx_emit(const uint64_t *__restrict__ pkey, const double *__restrict__ pp, int64_t nlist,
+                            const int64_t *__restrict__ cnt, const int64_t *__restrict__ off,
+                            const uint64_t *__restrict__ ckey, const uint32_t *__restrict__ cidx, uint64_t mult,
+                            uint64_t *__restrict__ nkey, double *__restrict__ npp) {
+  int64_t e = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  int lane = threadIdx.x & 31;
+  if (e >= nlist) return;
+  int64_t c = cnt[e], o = off[e];
+  uint64_t k0 = pkey[e];
+  double p0 = pp[e];
+  for (int64_t t = lane; t < c; t += 32) {
+    nkey[o + t] = k0 + (uint64_t)cidx[t] * mult;
+    npp[o + t] = p0 * cand_val(ckey[t]);
+  }
+}
+
+// Level-0 list from the sorted candidates of mode m_1.
+__global__ void k_didx_level0(const uint64_t *__restrict__ ckey, const uint32_t *__restrict__ cidx, int64_t n,
+                              uint64_t *__restrict__ key, double *__restrict__ pp) {
+  int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n) return;
+  key[t] = cidx[t];
+  pp[t] = cand_val(ckey[t]);
+}
+
+// compensated sum of n doubles -> block partial dd
+__global__ void k_sum_dd(const double *__restrict__ x, int64_t n, dd *__restrict__ part) {
+  dd s = {0.0, 0.0};
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    s = dd_add_d(s, x[i]);
+  s = warp_sum_dd(s);
+  __shared__ dd ws[32];
+  int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  if (lane == 0) ws[w] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    dd t = {0.0, 0.0};
+    for (int i = 0; i < (int)(blockDim.x >> 5); ++i) t = dd_add(t, ws[i]);
+    part[blockIdx.x] = t;
+  }
+}
+__global__ void k_sum_dd_final(const dd *__restrict__ part, int nb, double *out) {
+  if (threadIdx.x == 0) {
+    dd t = {0.0, 0.0};
+    for (int i = 0; i < nb; ++i) t = dd_add(t, part[i]);
+    *out = t.hi + t.lo;
+  }
+}
+
+// Deterministic block of the sample set: w^2 = 1.
+__global__ void k_det_emit(const uint64_t *__restrict__ key, const double *__restrict__ p, int64_t n,
+                           uint64_t *__restrict__ skey, double *__restrict__ sw2, double *__restrict__ sp,
+                           int32_t *__restrict__ scnt, uint8_t *__restrict__ sdet) {
+  int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n) return;
+  skey[t] = key[t]; sw2[t] = 1.0; sp[t] = p[t]; scnt[t] = 1; sdet[t] = 1;
+}
+
+// gather by index (u32) for the truncation path
+__global__ void k_gather_kp(const uint64_t *__restrict__ key, const double *__restrict__ p,
+                            const uint32_t *__restrict__ idx, int64_t n, uint64_t *__restrict__ okey,
+                            double *__restrict__ op) {
+  int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n) return;
+  okey[t] = key[idx[t]];
+  op[t] = p[idx[t]];
+}
+__global__ void k_iota_u32(uint32_t *v, int64_t n) {
+  int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t < n) v[t] = (uint32_t)t;
+}
+__global__ void k_pbits_desc(const double *__restrict__ p, int64_t n, uint64_t *__restrict__ k) {
+  int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t < n) k[t] = ~(uint64_t)__double_as_longlong(p[t]);
+}
+
+// ======================================================================
+// K4 SIDX (Alg. 2): attempts [a0, a0+cnt)
+// ======================================================================
+constexpr int kSidxThreads = 256;
+
+__global__ void __launch_bounds__(kSidxThreads) k_sidx_gen(OtherModes om, uint64_t a0, int64_t cnt, double tau,
+                                                           uint32_t seed_lo, uint32_t seed_hi, uint32_t step,
+                                                           uint64_t *__restrict__ akey, double *__restrict__ ap,
+                                                           int64_t *__restrict__ part) {
+  int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  int acc = 0;
+  if (t < cnt) {
+    uint64_t a = a0 + (uint64_t)t;
+    uint32_t words[2 * kMaxModes];
+    for (int lane = 0; lane < (om.d + 1) / 2; ++lane) {
+      u32x4 x = philox4x32_10({(uint32_t)a, (uint32_t)(a >> 32), step, (uint32_t)lane}, seed_lo, seed_hi);
+      words[4 * lane + 0] = x.x; words[4 * lane + 1] = x.y;
+      words[4 * lane + 2] = x.z; words[4 * lane + 3] = x.w;
+    }
+    uint64_t key = 0;
+    double p = 1.0;
+    for (int j = 0; j < om.d; ++j) {
+      uint32_t lo = words[4 * (j / 2) + 2 * (j % 2)], hi = words[4 * (j / 2) + 2 * (j % 2) + 1];
+      uint64_t R = ((uint64_t)hi << 32) | lo;
+      const uint64_t *C = om.C[j];
+      uint64_t W = __ldg(C + om.n[j] - 1);
+      uint64_t tt = __umul64hi(R, W);                       // AMB-9
+      int64_t i = upper_bound_u64(C, om.n[j], tt);          // i_k ~ Multi(p~_k)
+      double v = __ldg(om.pt[j] + i);
+      p = (j == 0) ? v : p * v;                              // canonical product (AMB-5)
+      key += (uint64_t)i * om.mult[j];
+    }
+    acc = (p <= tau);
+    akey[t] = acc ? key : kEmptyKey;
+    ap[t] = p;
+  }
+  int64_t tot;
+  block_excl_scan<int64_t>((int64_t)acc, &tot);
+  if (threadIdx.x == 0) part[blockIdx.x] = tot;
+}
+
+// Ordered compaction of accepted attempts; keeps positions < need (AMB-8).
+__global__ void __launch_bounds__(kSidxThreads) k_sidx_scatter(const uint64_t *__restrict__ akey,
+                                                               const double *__restrict__ ap, int64_t cnt,
+                                                               const int64_t *__restrict__ part, int64_t have,
+                                                               int64_t need, uint64_t a0, uint64_t *__restrict__ rkey,
+                                                               double *__restrict__ rp,
+                                                               unsigned long long *__restrict__ last_attempt) {
+  int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  int acc = (t < cnt) && akey[t] != kEmptyKey;
+  int64_t tot;
+  int64_t pos = have + part[blockIdx.x] + block_excl_scan<int64_t>((int64_t)acc, &tot);
+  if (acc && pos < need) {
+    rkey[pos] = akey[t];
+    rp[pos] = ap[t];
+    if (pos == need - 1) *last_attempt = a0 + (uint64_t)t;
+  }
+}
+
+// ======================================================================
+// K5 CIDX: combine repeats with a hash table
+// ======================================================================
+__device__ __forceinline__ uint64_t mix64(uint64_t k) {
+  k ^= k >> 33; k *= 0xff51afd7ed558ccdull; k ^= k >> 33; k *= 0xc4ceb9fe1a85ec53ull; k ^= k >> 33;
+  return k;
+}
+
+__global__ void k_cidx_insert(const uint64_t *__restrict__ rkey, const double *__restrict__ rp, int64_t n,
+                              unsigned long long *__restrict__ hkey, uint32_t *__restrict__ hcnt,
+                              double *__restrict__ hp, uint64_t hmask) {
+  int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n) return;
+  uint64_t k = rkey[t];
+  uint64_t h = mix64(k) & hmask;
+  while (true) {
+    unsigned long long prev = atomicCAS(&hkey[h], kEmptyKey, (unsigned long long)k);
+    if (prev == kEmptyKey || prev == k) {
+      atomicAdd(&hcnt[h], 1u);
+      if (prev == kEmptyKey) hp[h] = rp[t];
+      return;
+    }
+    h = (h + 1) & hmask;
+  }
+}
+
+// Emit unique random rows after the deterministic block:
+// w^2 = c (1 - p_det) / (s_rnd p)  (P:537 with s -> s_rnd, AMB-3)
+__global__ void k_cidx_emit(unsigned long long *__restrict__ hkey, uint32_t *__restrict__ hcnt,
+                            const double *__restrict__ hp, uint64_t hsize, const double *__restrict__ pdet_ptr,
+                            int64_t s_rnd, int64_t base, unsigned long long *__restrict__ counter,
+                            uint64_t *__restrict__ skey, double *__restrict__ sw2, double *__restrict__ sp,
+                            int32_t *__restrict__ scnt, uint8_t *__restrict__ sdet) {
+  uint64_t h = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (h >= hsize) return;
+  unsigned long long k = hkey[h];
+  if (k == kEmptyKey) return;
+  uint32_t c = hcnt[h];
+  double p = hp[h];
+  double pdet = *pdet_ptr;
+  unsigned long long o = base + atomicAdd(counter, 1ull);
+  skey[o] = k;
+  scnt[o] = (int32_t)c;
+  sp[o] = p;
+  sw2[o] = ((double)c * (1.0 - pdet)) / ((double)s_rnd * p);
+  sdet[o] = 0;
+  hkey[h] = kEmptyKey;   // reset for the next sample
+  hcnt[h] = 0;
+}
+
+// ======================================================================
+// K6 KrpSamp + sampled Gram
+// ======================================================================
+constexpr int kKrpThreads = 256;
+constexpr int kKrpChunk = 32;
+
+// z_j = A_{m_1}(i_1,:) * ... * A_{m_d}(i_d,:) (eq:Zrow, left to right).
+// Writes Z[j*ld + c]; accumulates block partials of sum_j w2_j z_j z_j^T.
+__global__ void __launch_bounds__(kKrpThreads) k_krp_gram(const uint64_t *__restrict__ skey,
+                                                         const double *__restrict__ sw2, int64_t sbar, OtherModes om,
+                                                         int r, int ld, double *__restrict__ Z,
+                                                         int64_t per_block, double *__restrict__ part) {
+  __shared__ double zs[kKrpChunk][kMaxRank + 1];
+  __shared__ double ws[kKrpChunk];
+  __shared__ int pp[npairs(kMaxRank)], qq[npairs(kMaxRank)];
+  const int P = npairs(r);
+  if (threadIdx.x == 0) {
+    int t = 0;
+    for (int p = 0; p < r; ++p)
+      for (int q = p; q < r; ++q, ++t) { pp[t] = p; qq[t] = q; }
+  }
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  double acc[9];
+#pragma unroll
+  for (int i = 0; i < 9; ++i) acc[i] = 0.0;
+  int64_t j0 = (int64_t)blockIdx.x * per_block, j1 = min(sbar, j0 + per_block);
+  __syncthreads();
+  for (int64_t base = j0; base < j1; base += kKrpChunk) {
+    int cnt = (int)min((int64_t)kKrpChunk, j1 - base);
+    for (int jj = w; jj < cnt; jj += kKrpThreads / 32) {
+      int64_t j = base + jj;
+      uint64_t key = skey[j];
+      double z = 1.0;
+      for (int m = 0; m < om.d; ++m) {
+        uint64_t i = key % (uint64_t)om.n[m];
+        key /= (uint64_t)om.n[m];
+        if (lane < r) {
+          double a = __ldg(om.A[m] + i * ld + lane);
+          z = (m == 0) ? a : z * a;
+        }
+      }
+      if (lane < r) {
+        zs[jj][lane] = z;
+        Z[j * ld + lane] = z;
+      }
+      if (lane == 0) ws[jj] = sw2[j];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < 9; ++i) {
+      int t = threadIdx.x + i * kKrpThreads;
+      if (t < P) {
+        int p = pp[t], q = qq[t];
+        double s = 0.0;
+        for (int jj = 0; jj < cnt; ++jj) s += (ws[jj] * zs[jj][p]) * zs[jj][q];
+        acc[i] += s;
+      }
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < 9; ++i) {
+    int t = threadIdx.x + i * kKrpThreads;
+    if (t < P) part[(int64_t)blockIdx.x * P + t] = acc[i];
+  }
+}
+
+// ======================================================================
+// K7 TnsrSamp lookup: equal_range of each sampled key in the
+// mode-k sorted keys, narrowed by the top-level directory.
+// ======================================================================
+__global__ void k_lookup(const uint64_t *__restrict__ skey, int64_t sbar, const uint64_t *__restrict__ keys,
+                         const int64_t *__restrict__ dir, int shift, int64_t nbkt, int64_t *__restrict__ lo_out,
+                         int64_t *__restrict__ len_out) {
+  int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= sbar) return;
+  uint64_t k = skey[j];
+  uint64_t b = k >> shift;
+  int64_t lo = 0, hi = 0;
+  if ((int64_t)b < nbkt) {
+    lo = __ldg(dir + b);
+    hi = __ldg(dir + b + 1);
+  }
+  // lower_bound
+  int64_t L = lo, len = hi - lo;
+  while (len > 0) {
+    int64_t half = len >> 1;
+    if (__ldg(keys + L + half) < k) { L += half + 1; len -= half + 1; }
+    else len = half;
+  }
+  int64_t U = L;
+  len = hi - L;
+  while (len > 0) {
+    int64_t half = len >> 1;
+    if (__ldg(keys + U + half) <= k) { U += half + 1; len -= half + 1; }
+    else len = half;
+  }
+  lo_out[j] = L;
+  len_out[j] = U - L;
+}
+
+// ======================================================================
+// K8 sampled RHS: M(out_e,:) += w2_j x_e z_j over matched nonzeros
+// ======================================================================
+constexpr int kRhsThreads = 256;
+
+template <typename VT>
+__global__ void __launch_bounds__(kRhsThreads) k_rhs(const int64_t *__restrict__ off, const int64_t *__restrict__ lo,
+                                                    int64_t sbar, const int64_t *__restrict__ mk_ptr,
+                                                    const int32_t *__restrict__ outidx, const VT *__restrict__ vals,
+                                                    const double *__restrict__ sw2, const double *__restrict__ Z,
+                                                    int r, int ld, double *__restrict__ M,
+                                                    uint8_t *__restrict__ touched, int64_t per_warp) {
+  const int64_t mk = *mk_ptr;
+  const int lane = threadIdx.x & 31;
+  const int64_t wid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t t0 = wid * per_warp; t0 < mk; t0 += nw * per_warp) {
+    const int64_t t1 = min(mk, t0 + per_warp);
+    // sample containing entry t0: last j with off[j] <= t0 (skips empty fibers)
+    int64_t a = 0, len = sbar;
+    while (len > 0) {
+      int64_t half = len >> 1;
+      if (__ldg(off + a + half) <= t0) { a += half + 1; len -= half + 1; }
+      else len = half;
+    }
+    int64_t jcur = a - 1;       // sample of the first entry of the current 32-group
+    int64_t jz = -1;            // sample whose (w2, z) are loaded
+    double coefw = 0.0, z = 0.0;
+    for (int64_t t = t0; t < t1; t += 32) {
+      const int64_t tt = t + lane;
+      int64_t jj = jcur;
+      while (jj + 1 < sbar && __ldg(off + jj + 1) <= tt) ++jj;
+      int32_t o_l = 0;
+      double x_l = 0.0;
+      if (tt < t1) {
+        int64_t e = __ldg(lo + jj) + (tt - __ldg(off + jj));
+        o_l = __ldg(outidx + e);
+        x_l = (double)__ldg(vals + e);
+      }
+      const int cnt = (int)min((int64_t)32, t1 - t);
+      for (int u = 0; u < cnt; ++u) {
+        const int32_t o = __shfl_sync(0xffffffffu, o_l, u);
+        const double x = __shfl_sync(0xffffffffu, x_l, u);
+        const int64_t ju = __shfl_sync(0xffffffffu, jj, u);
+        if (ju != jz) {
+          jz = ju;
+          coefw = __ldg(sw2 + ju);
+          z = lane < r ? __ldg(Z + ju * ld + lane) : 0.0;
+        }
+        if (lane < r) atomicAdd(M + (int64_t)o * ld + lane, (coefw * x) * z);
+        if (lane == 0) touched[o] = 1;
+      }
+      jcur = __shfl_sync(0xffffffffu, jj, 31);
+    }
+  }
+}
+
+// ======================================================================
+// K9 solve + normalize
+// ======================================================================
+// Single block: Cholesky of the sampled Gram with pivot test; fallback to the
+// eigen pseudo-inverse (AMB-12).  Ginv = G^{-1} (or G^+).
+__global__ void k_solve_prep(int r, SolveDev *sd) {
+  extern __shared__ double sm[];
+  double *G = sm, *L = sm + r * r, *Li = sm + 2 * r * r;
+  __shared__ int ok;
+  for (int i = threadIdx.x; i < r * r; i += blockDim.x) G[i] = sd->G[i];
+  __syncthreads();
+  int good = block_cholesky(r, G, L, &ok);
+  if (good) {
+    block_tri_inverse(r, L, Li);
+    // Ginv = Li^T Li
+    for (int i = threadIdx.x; i < r * r; i += blockDim.x) {
+      int p = i / r, q = i % r;
+      double s = 0.0;
+      for (int k = max(p, q); k < r; ++k) s += Li[k * r + p] * Li[k * r + q];
+      sd->Ginv[i] = s;
+    }
+    if (threadIdx.x == 0) { sd->rank_used = r; sd->chol_fallback = 0; }
+    return;
+  }
+  if (threadIdx.x == 0) {
+    double *a = L, *V = Li;
+    for (int i = 0; i < r * r; ++i) a[i] = G[i];
+    jacobi_serial(r, a, V);
+    double mumax = 0.0;
+    for (int j = 0; j < r; ++j) mumax = fmax(mumax, a[j * r + j]);
+    int rank = 0;
+    double inv[kMaxRank];
+    for (int j = 0; j < r; ++j) {
+      double mu = a[j * r + j];
+      bool keep = mumax > 0.0 && mu > (double)r * 2.220446049250313e-16 * mumax;
+      rank += keep;
+      inv[j] = keep ? 1.0 / mu : 0.0;
+    }
+    for (int p = 0; p < r; ++p)
+      for (int q = 0; q < r; ++q) {
+        double s = 0.0;
+        for (int j = 0; j < r; ++j) s += V[p * r + j] * inv[j] * V[q * r + j];
+        sd->Ginv[p * r + q] = s;
+      }
+    sd->rank_used = rank;
+    sd->chol_fallback = 1;
+  }
+}
+
+// B_i = M_i Ginv for every row (rows with M = 0 give B = 0); M is zeroed
+// after reading (ready for the next RHS).  Block partials of B^T B.
+constexpr int kSolveThreads = 256;
+__global__ void __launch_bounds__(kSolveThreads) k_solve_rows(double *__restrict__ M, int64_t n, int r, int ld,
+                                                             const SolveDev *__restrict__ sd, double *__restrict__ B,
+                                                             double *__restrict__ part) {
+  extern __shared__ double smem[];
+  double *Gi = smem;                  // r*r
+  double *tile = smem + r * r;        // kSolveThreads x (ld+1)
+  __shared__ int pp[npairs(kMaxRank)], qq[npairs(kMaxRank)];
+  const int S = ld + 1;
+  const int P = npairs(r);
+  for (int i = threadIdx.x; i < r * r; i += blockDim.x) Gi[i] = sd->Ginv[i];
+  if (threadIdx.x == 0) {
+    int t = 0;
+    for (int p = 0; p < r; ++p)
+      for (int q = p; q < r; ++q, ++t) { pp[t] = p; qq[t] = q; }
+  }
+  int64_t base = (int64_t)blockIdx.x * kSolveThreads;
+  int rows = (int)min((int64_t)kSolveThreads, n - base);
+  double *msrc = M + base * ld;
+  for (int i = threadIdx.x; i < rows * ld; i += blockDim.x) {
+    int row = i / ld, c = i - row * ld;
+    tile[row * S + c] = msrc[i];
+    msrc[i] = 0.0;
+  }
+  __syncthreads();
+  double out[kMaxRank];
+  if (threadIdx.x < rows) {
+    double *m = tile + threadIdx.x * S;
+    bool nz = false;
+    for (int p = 0; p < r; ++p) nz |= (m[p] != 0.0);
+    for (int c = 0; c < r; ++c) out[c] = 0.0;
+    if (nz) {
+      for (int p = 0; p < r; ++p) {
+        double mp = m[p];
+        for (int c = 0; c < r; ++c) out[c] += mp * Gi[p * r + c];
+      }
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x < rows) {
+    double *m = tile + threadIdx.x * S;
+    for (int c = 0; c < r; ++c) m[c] = out[c];
+  }
+  __syncthreads();
+  double *bdst = B + base * ld;
+  for (int i = threadIdx.x; i < rows * ld; i += blockDim.x) {
+    int row = i / ld, c = i - row * ld;
+    bdst[i] = c < r ? tile[row * S + c] : 0.0;
+  }
+  // B^T B partial over this tile
+  for (int t = threadIdx.x; t < P; t += blockDim.x) {
+    int p = pp[t], q = qq[t];
+    double s = 0.0;
+    for (int row = 0; row < rows; ++row) s += tile[row * S + p] * tile[row * S + q];
+    part[(int64_t)blockIdx.x * P + t] = s;
+  }
+}
+
+// lambda_c = ||B(:,c)||, G_A = B^T B / (lambda lambda^T), then the
+// leverage preparation of the normalized factor.
+__global__ void k_norm_prep(int r, SolveDev *sd, ModeDev *md) {
+  extern __shared__ double sm[];
+  double *GA = sm + 3 * r * r;   // beyond lev_prep's scratch
+  for (int c = threadIdx.x; c < r; c += blockDim.x) sd->lambda[c] = sqrt(fmax(sd->BtB[c * r + c], 0.0));
+  __syncthreads();
+  for (int i = threadIdx.x; i < r * r; i += blockDim.x) {
+    int p = i / r, q = i % r;
+    double lp = sd->lambda[p], lq = sd->lambda[q];
+    GA[i] = (lp > 0.0 && lq > 0.0) ? (sd->BtB[i] / lp) / lq : 0.0;
+  }
+  __syncthreads();
+  lev_prep_body(r, GA, md);
+}
+
+// ======================================================================
+// K10 exact fit: <X, M> streamed over mode-k* sorted copy
+// ======================================================================
+constexpr int kFitThreads = 256;
+
+template <typename VT>
+__global__ void __launch_bounds__(kFitThreads) k_fit_inner(const uint64_t *__restrict__ keys,
+                                                          const int32_t *__restrict__ outidx,
+                                                          const VT *__restrict__ vals, int64_t nnz, OtherModes om,
+                                                          const double *__restrict__ Ak, const double *__restrict__ lam,
+                                                          int r, int ld, dd *__restrict__ part) {
+  __shared__ double lam_s[kMaxRank];
+  for (int c = threadIdx.x; c < r; c += blockDim.x) lam_s[c] = lam[c];
+  __syncthreads();
+  dd acc = {0.0, 0.0};
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < nnz; e += (int64_t)gridDim.x * blockDim.x) {
+    uint64_t key = keys[e];
+    const double *rows[kMaxModes];
+    for (int m = 0; m < om.d; ++m) {
+      uint64_t i = key % (uint64_t)om.n[m];
+      key /= (uint64_t)om.n[m];
+      rows[m] = om.A[m] + i * ld;
+    }
+    const double *ak = Ak + (int64_t)outidx[e] * ld;
+    double mv = 0.0;
+    for (int c = 0; c < r; ++c) {
+      double t = lam_s[c] * __ldg(ak + c);
+      for (int m = 0; m < om.d; ++m) t *= __ldg(rows[m] + c);
+      mv += t;
+    }
+    acc = dd_add_d(acc, (double)vals[e] * mv);
+  }
+  acc = warp_sum_dd(acc);
+  __shared__ dd ws[kFitThreads / 32];
+  int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  if (lane == 0) ws[w] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    dd t = {0.0, 0.0};
+    for (int i = 0; i < kFitThreads / 32; ++i) t = dd_add(t, ws[i]);
+    part[blockIdx.x] = t;
+  }
+}
+
+struct FitModes {
+  int D;
+  const ModeDev *md[kMaxModes];
+};
+
+__global__ void k_fit_final(const dd *__restrict__ part, int nb, FitModes fm, const double *__restrict__ lam, int r,
+                            double normX2, double *out) {
+  if (threadIdx.x != 0) return;
+  dd inner = {0.0, 0.0};
+  for (int i = 0; i < nb; ++i) inner = dd_add(inner, part[i]);
+  dd nm = {0.0, 0.0};
+  for (int p = 0; p < r; ++p)
+    for (int q = 0; q < r; ++q) {
+      double h = lam[p] * lam[q];
+      for (int m = 0; m < fm.D; ++m) h *= fm.md[m]->GA[p * r + q];
+      nm = dd_add_d(nm, h);
+    }
+  double in = inner.hi + inner.lo;
+  double resid2 = normX2 - 2.0 * in + (nm.hi + nm.lo);
+  if (resid2 < 0.0) resid2 = 0.0;
+  out[0] = 1.0 - sqrt(resid2) / sqrt(normX2);
+  out[1] = in;
+  out[2] = nm.hi + nm.lo;
+}
+
+// ======================================================================
+// K0 index build helpers (one-time, in cparls_create)
+// ======================================================================
+template <typename IT>
+__global__ void k_make_outkey(const IT *__restrict__ coords, int64_t nnz, int D, int k, uint32_t *__restrict__ okey,
+                              uint32_t *__restrict__ ids) {
+  int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= nnz) return;
+  okey[e] = (uint32_t)coords[e * D + k];
+  ids[e] = (uint32_t)e;
+}
+
+struct KeySpec {
+  int D, k;
+  int64_t dims[kMaxModes];
+};
+
+template <typename IT>
+__global__ void k_make_keys(const IT *__restrict__ coords, int64_t nnz, KeySpec ks, const uint32_t *__restrict__ ids,
+                            uint64_t *__restrict__ keys) {
+  int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= nnz) return;
+  int64_t e = ids[t];
+  uint64_t key = 0, mult = 1;
+  for (int m = 0; m < ks.D; ++m) {
+    if (m == ks.k) continue;
+    key += (uint64_t)coords[e * ks.D + m] * mult;
+    mult *= (uint64_t)ks.dims[m];
+  }
+  keys[t] = key;
+}
+
+template <typename IT, typename VT>
+__global__ void k_gather_nz(const IT *__restrict__ coords, const VT *__restrict__ vals, int64_t nnz, int D, int k,
+                            const uint32_t *__restrict__ ids, int32_t *__restrict__ out, VT *__restrict__ v) {
+  int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= nnz) return;
+  int64_t e = ids[t];
+  out[t] = (int32_t)coords[e * D + k];
+  v[t] = vals[e];
+}
+
+template <typename IT>
+__global__ void k_check_coords(const IT *__restrict__ coords, int64_t nnz, KeySpec ks, unsigned long long *bad) {
+  int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= nnz) return;
+  for (int m = 0; m < ks.D; ++m) {
+    long long c = (long long)coords[e * ks.D + m];
+    if (c < 0 || c >= ks.dims[m]) { atomicAdd(bad, 1ull); return; }
+  }
+}
+
+__global__ void k_dir_fill(const uint64_t *__restrict__ keys, int64_t nnz, int shift, int64_t *__restrict__ dir,
+                           int64_t nbkt) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nnz) return;
+  int64_t b = (int64_t)(keys[i] >> shift);
+  int64_t bp = (i == 0) ? -1 : (int64_t)(keys[i - 1] >> shift);
+  for (int64_t bb = bp + 1; bb <= b && bb < nbkt; ++bb) dir[bb] = i;
+  if (i == nnz - 1)
+    for (int64_t bb = b + 1; bb <= nbkt; ++bb) dir[bb] = nnz;
+}
+
+template <typename VT>
+__global__ void k_sumsq(const VT *__restrict__ v, int64_t n, dd *__restrict__ part) {
+  dd s = {0.0, 0.0};
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    double x = (double)v[i];
+    s = dd_add_d(s, x * x);
+  }
+  s = warp_sum_dd(s);
+  __shared__ dd ws[32];
+  int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  if (lane == 0) ws[w] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    dd t = {0.0, 0.0};
+    for (int i = 0; i < (int)(blockDim.x >> 5); ++i) t = dd_add(t, ws[i]);
+    part[blockIdx.x] = t;
+  }
+}
+
+// count of touched rows (bytes) and reset of the flags
+__global__ void k_count_touched(uint8_t *__restrict__ f, int64_t n, unsigned long long *cnt) {
+  unsigned long long c = 0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    c += f[i];
+    f[i] = 0;
+  }
+  c = warp_sum<unsigned long long>(c);
+  if ((threadIdx.x & 31) == 0 && c) atomicAdd(cnt, c);
+}
+
+// gather matched (out, val) of all samples in current sample order
+template <typename VT>
+__global__ void k_gather_fibers(const int64_t *__restrict__ off, const int64_t *__restrict__ lo,
+                                const int64_t *__restrict__ len, int64_t sbar, const int32_t *__restrict__ outidx,
+                                const VT *__restrict__ vals, int64_t *__restrict__ o, double *__restrict__ v) {
+  int64_t j = blockIdx.x;
+  if (j >= sbar) return;
+  for (int64_t t = threadIdx.x; t < len[j]; t += blockDim.x) {
+    o[off[j] + t] = outidx[lo[j] + t];
+    v[off[j] + t] = (double)vals[lo[j] + t];
+  }
+}
+
+}  // namespace cparls

@@ -1,0 +1,228 @@
+// prims.cuh -- scan, ordered compaction and stable LSD radix sort used on the
+// per-iteration path (sizes up to a few million).  Hand-written for sm_100a:
+// 256-thread blocks, 8 items per thread, warp-shuffle scans, __match_any_sync
+// stable ranking.
+#pragma once
+#include "common.cuh"
+
+namespace cparls {
+
+constexpr int kScanThreads = 256;
+constexpr int kScanItems = 8;
+constexpr int kScanTile = kScanThreads * kScanItems;  // 2048
+
+// inclusive warp scan
+template <typename T>
+__device__ __forceinline__ T warp_incl_scan(T v) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    T n = __shfl_up_sync(0xffffffffu, v, o);
+    if (lane >= o) v += n;
+  }
+  return v;
+}
+
+// Block-wide exclusive scan of one value per thread (blockDim == kScanThreads).
+// Returns exclusive prefix; *total receives the block sum (all threads).
+template <typename T>
+__device__ __forceinline__ T block_excl_scan(T v, T *total) {
+  constexpr int kW = kScanThreads / 32;
+  __shared__ T wsum[kW + 1];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  T inc = warp_incl_scan(v);
+  if (lane == 31) wsum[w] = inc;
+  __syncthreads();
+  if (w == 0) {
+    T x = (lane < kW) ? wsum[lane] : T(0);
+    T xi = warp_incl_scan(x);
+    if (lane < kW) wsum[lane] = xi - x;
+    if (lane == kW - 1) wsum[kW] = xi;
+  }
+  __syncthreads();
+  T excl = wsum[w] + inc - v;
+  *total = wsum[kW];
+  __syncthreads();
+  return excl;
+}
+
+// ---- generic 3-phase exclusive scan of int64 counts ---------------------------
+__global__ void k_scan_partials(const int64_t *__restrict__ in, int64_t n, int64_t *__restrict__ part) {
+  int64_t base = (int64_t)blockIdx.x * kScanTile;
+  int64_t s = 0;
+#pragma unroll
+  for (int i = 0; i < kScanItems; ++i) {
+    int64_t idx = base + (int64_t)i * kScanThreads + threadIdx.x;
+    if (idx < n) s += in[idx];
+  }
+  int64_t tot;
+  block_excl_scan<int64_t>(s, &tot);
+  if (threadIdx.x == 0) part[blockIdx.x] = tot;
+}
+
+// single block: exclusive scan of part[0..nb) in place; total -> *total
+__global__ void k_scan_part(int64_t *part, int64_t nb, int64_t *total) {
+  int64_t carry = 0;
+  for (int64_t base = 0; base < nb; base += kScanThreads) {
+    int64_t idx = base + threadIdx.x;
+    int64_t v = idx < nb ? part[idx] : 0;
+    int64_t tot;
+    int64_t ex = block_excl_scan<int64_t>(v, &tot);
+    if (idx < nb) part[idx] = carry + ex;
+    carry += tot;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0 && total) *total = carry;
+}
+
+__global__ void k_scan_final(const int64_t *__restrict__ in, int64_t n, const int64_t *__restrict__ part,
+                             int64_t *__restrict__ out) {
+  int64_t base = (int64_t)blockIdx.x * kScanTile + (int64_t)threadIdx.x * kScanItems;
+  int64_t v[kScanItems];
+  int64_t s = 0;
+#pragma unroll
+  for (int i = 0; i < kScanItems; ++i) {
+    int64_t idx = base + i;
+    v[i] = idx < n ? in[idx] : 0;
+    s += v[i];
+  }
+  int64_t tot;
+  int64_t ex = block_excl_scan<int64_t>(s, &tot) + part[blockIdx.x];
+#pragma unroll
+  for (int i = 0; i < kScanItems; ++i) {
+    int64_t idx = base + i;
+    if (idx < n) out[idx] = ex;
+    ex += v[i];
+  }
+}
+
+// exclusive scan of n int64 values; part must hold ceil(n/2048) entries;
+// total (device pointer) may be null.  in and out may alias.
+inline int exclusive_scan_i64(const int64_t *in, int64_t *out, int64_t n, int64_t *part, int64_t *total,
+                              cudaStream_t st) {
+  if (n <= 0) {
+    if (total) CK(cudaMemsetAsync(total, 0, sizeof(int64_t), st));
+    return 1;
+  }
+  int64_t nb = ceil_div(n, kScanTile);
+  k_scan_partials<<<(unsigned)nb, kScanThreads, 0, st>>>(in, n, part);
+  CK_LAUNCH();
+  k_scan_part<<<1, kScanThreads, 0, st>>>(part, nb, total);
+  CK_LAUNCH();
+  k_scan_final<<<(unsigned)nb, kScanThreads, 0, st>>>(in, n, part, out);
+  CK_LAUNCH();
+  return 3;
+}
+
+// ---- stable LSD radix sort of (u64 key, u32 value) pairs ------------------------
+constexpr int kRadixBits = 8;
+constexpr int kRadixBins = 1 << kRadixBits;
+
+__global__ void k_radix_hist(const uint64_t *__restrict__ keys, int64_t n, int shift,
+                             uint32_t *__restrict__ hist /* [bins][nblocks] */) {
+  __shared__ uint32_t h[kRadixBins];
+  for (int i = threadIdx.x; i < kRadixBins; i += blockDim.x) h[i] = 0;
+  __syncthreads();
+  int64_t base = (int64_t)blockIdx.x * kScanTile;
+#pragma unroll
+  for (int i = 0; i < kScanItems; ++i) {
+    int64_t idx = base + (int64_t)i * kScanThreads + threadIdx.x;
+    if (idx < n) atomicAdd(&h[(keys[idx] >> shift) & (kRadixBins - 1)], 1u);
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < kRadixBins; i += blockDim.x) hist[(int64_t)i * gridDim.x + blockIdx.x] = h[i];
+}
+
+// single block: exclusive scan over hist (bins-major) in place
+__global__ void k_radix_scan(uint32_t *hist, int64_t len) {
+  uint32_t carry = 0;
+  for (int64_t base = 0; base < len; base += kScanThreads) {
+    int64_t idx = base + threadIdx.x;
+    uint32_t v = idx < len ? hist[idx] : 0u;
+    uint32_t tot;
+    uint32_t ex = block_excl_scan<uint32_t>(v, &tot);
+    if (idx < len) hist[idx] = carry + ex;
+    carry += tot;
+    __syncthreads();
+  }
+}
+
+// Stable scatter: warp w owns items [w*256, (w+1)*256) of the block tile,
+// processed as 8 coalesced chunks of 32; ranks via __match_any_sync.
+__global__ void k_radix_scatter(const uint64_t *__restrict__ kin, const uint32_t *__restrict__ vin, int64_t n,
+                                int shift, const uint32_t *__restrict__ hist, uint64_t *__restrict__ kout,
+                                uint32_t *__restrict__ vout) {
+  constexpr int kWarps = kScanThreads / 32;
+  __shared__ uint32_t wh[kWarps][kRadixBins];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (int i = threadIdx.x; i < kWarps * kRadixBins; i += blockDim.x) (&wh[0][0])[i] = 0;
+  __syncthreads();
+  int64_t base = (int64_t)blockIdx.x * kScanTile + (int64_t)w * (32 * kScanItems);
+  uint32_t rank[kScanItems];
+  uint32_t dig[kScanItems];
+#pragma unroll
+  for (int c = 0; c < kScanItems; ++c) {
+    int64_t idx = base + c * 32 + lane;
+    bool valid = idx < n;
+    uint32_t d = valid ? (uint32_t)((kin[idx] >> shift) & (kRadixBins - 1)) : 0u;
+    unsigned vmask = __ballot_sync(0xffffffffu, valid);
+    dig[c] = d;
+    if (valid) {
+      unsigned peers = __match_any_sync(vmask, d);
+      uint32_t before = wh[w][d];
+      rank[c] = before + __popc(peers & lanemask_lt());
+      __syncwarp(vmask);
+      int leader = __ffs(peers) - 1;
+      if (lane == leader) wh[w][d] = before + __popc(peers);
+    }
+    __syncwarp();
+  }
+  __syncthreads();
+  // exclusive prefix across warps per digit
+  for (int d = threadIdx.x; d < kRadixBins; d += blockDim.x) {
+    uint32_t run = 0;
+#pragma unroll
+    for (int ww = 0; ww < kWarps; ++ww) {
+      uint32_t t = wh[ww][d];
+      wh[ww][d] = run;
+      run += t;
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int c = 0; c < kScanItems; ++c) {
+    int64_t idx = base + c * 32 + lane;
+    if (idx < n) {
+      uint32_t d = dig[c];
+      uint64_t pos = (uint64_t)hist[(int64_t)d * gridDim.x + blockIdx.x] + wh[w][d] + rank[c];
+      kout[pos] = kin[idx];
+      vout[pos] = vin[idx];
+    }
+  }
+}
+
+// Sorts (keys, vals) by key bits [0, end_bit) stably.  Ping-pongs between the
+// given buffers; returns the index (0 = keys/vals, 1 = ktmp/vtmp) holding the
+// result.  hist needs 256*ceil(n/2048) entries.  n must be < 2^32.
+inline int radix_sort_pairs(uint64_t *keys, uint32_t *vals, uint64_t *ktmp, uint32_t *vtmp, int64_t n,
+                            int end_bit, uint32_t *hist, cudaStream_t st, int64_t *launches) {
+  if (n <= 1) return 0;
+  int64_t nb = ceil_div(n, kScanTile);
+  uint64_t *kb[2] = {keys, ktmp};
+  uint32_t *vb[2] = {vals, vtmp};
+  int cur = 0;
+  for (int shift = 0; shift < end_bit; shift += kRadixBits) {
+    k_radix_hist<<<(unsigned)nb, kScanThreads, 0, st>>>(kb[cur], n, shift, hist);
+    CK_LAUNCH();
+    k_radix_scan<<<1, kScanThreads, 0, st>>>(hist, nb * kRadixBins);
+    CK_LAUNCH();
+    k_radix_scatter<<<(unsigned)nb, kScanThreads, 0, st>>>(kb[cur], vb[cur], n, shift, hist, kb[cur ^ 1],
+                                                           vb[cur ^ 1]);
+    CK_LAUNCH();
+    cur ^= 1;
+    if (launches) *launches += 3;
+  }
+  return cur;
+}
+
+}  // namespace cparls

@@ -1,0 +1,269 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle on the
+same seeded inputs.  Bars (BASELINE.json north_star): sampled indices, dedup
+counts, s_det and fiber matches bit-exact given the same p~ bits, seed and
+step; leverage <= 1e-12 relative; per-mode solution <= 1e-9 relative
+Frobenius on the same sample set; fit <= 1e-8 absolute."""
+import math
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+
+pytestmark = pytest.mark.gpu
+
+
+def need_gpu():
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+
+
+def make_ctx(T, rank, tau=-1.0, init_seed=2, device="cuda"):
+    from paper_2006_16438_b200 import Cparls
+    coords = T.coords.to(device) if device else T.coords.numpy()
+    vals = T.vals.to(device) if device else T.vals.numpy()
+    return Cparls(T.dims, coords, vals, rank, tau=tau, init_seed=init_seed)
+
+
+def make_oracle(T, rank):
+    return oracle.Oracle(T.dims, T.coords.to(torch.int64).numpy(), T.vals.to(torch.float64).numpy(), rank)
+
+
+def sync_oracle_from_gpu(g, o):
+    for m in range(g.D):
+        A, lam = g.get_factor(m)
+        o.set_factor(m, A)
+        o.set_ptilde(m, g.get_ptilde(m))
+
+
+def assert_leverage_close(g, o, m):
+    """GPU p~ (computed inside the solve from the normalized factor) vs the
+    oracle's leverage of the exported factor: |dl| <= 1e-12 max(l, r/n) * kappa/1e3."""
+    A, _ = g.get_factor(m)
+    ell_ref, rank_ref = oracle.leverage(A)
+    pt = g.get_ptilde(m)
+    ell_gpu = pt * rank_ref
+    n, r = A.shape
+    G = A.T @ A
+    ev = np.linalg.eigvalsh(G)
+    kappa = ev[-1] / max(ev[0], 1e-300) if rank_ref == r else 1e3
+    tol = 1e-12 * max(1.0, kappa / 1e3)
+    scale = np.maximum(np.abs(ell_ref), r / n)
+    err = np.abs(ell_gpu - ell_ref) / scale
+    assert err.max() <= tol, (m, err.max(), kappa)
+
+
+def compare_sample(g, o):
+    a, b = g.get_sample(), o.get_sample()
+    assert len(a["keys"]) == len(b["keys"])
+    assert (a["keys"] == b["keys"]).all()
+    assert (a["counts"] == b["counts"]).all()
+    assert (a["is_det"] == b["is_det"]).all()
+    assert (a["p"] == b["p"]).all()               # same canonical product bits
+    np.testing.assert_allclose(a["w2"], b["w2"], rtol=1e-14, atol=0)
+    la, oa, va = g.get_fibers()
+    lb, ob, vb = o.get_fibers()
+    assert (la == lb).all() and (oa == ob).all() and (va == vb).all()
+    return a
+
+
+def lockstep(T, rank, iters, s, seed, tau=-1.0, check_fit=True):
+    need_gpu()
+    g = make_ctx(T, rank, tau=tau)
+    o = make_oracle(T, rank)
+    D = len(T.dims)
+    stats = []
+    for t in range(iters):
+        for k in range(D):
+            sync_oracle_from_gpu(g, o)
+            step = t * D + k
+            gi = g.sample(k, s, seed, step)
+            oi = o.sample(k, s, tau, seed, step)
+            assert (gi.s_det, gi.s_rnd, gi.s_bar, gi.attempts, gi.skipped_random) == \
+                   (oi.s_det, oi.s_rnd, oi.s_bar, oi.attempts, oi.skipped_random)
+            assert abs(gi.p_det - oi.p_det) <= 1e-14 * max(1.0, oi.p_det)
+            compare_sample(g, o)
+            gs = g.solve_mode(k)
+            os_ = o.solve_mode(k)
+            assert gs.matched_nnz == os_.matched_nnz
+            assert gs.touched_rows == os_.touched_rows
+            assert gs.chol_fallback == os_.chol_fallback
+            Gg, Bg = g.last_solve(k)
+            Go, Mo, Bo = o.last_solve(k)
+            np.testing.assert_allclose(Gg, Go, rtol=1e-11, atol=1e-13 * max(1.0, np.abs(Go).max()))
+            nb = np.linalg.norm(Bo)
+            if nb > 0:
+                assert np.linalg.norm(Bg - Bo) <= 1e-9 * nb, (t, k, np.linalg.norm(Bg - Bo) / nb)
+            else:
+                assert np.linalg.norm(Bg) == 0
+            Ag, lg = g.get_factor(k)
+            Ao, lo = o.get_factor(k)
+            np.testing.assert_allclose(lg, lo, rtol=1e-9, atol=1e-300)
+            assert_leverage_close(g, o, k)
+            stats.append((gi.s_det, gi.s_bar, gs.matched_nnz))
+        if check_fit:
+            fg, fo = g.fit(), o.fit()
+            assert abs(fg - fo) <= 1e-8, (t, fg, fo)
+    return g, o, stats
+
+
+def test_c1_lockstep_20_iterations():
+    T = synth.make("C1")
+    cfg = T.cfg
+    lockstep(T, cfg.rank, cfg.iters, cfg.s, cfg.sample_seed)
+
+
+def test_c1_random_only_tau1():
+    T = synth.make("C1")
+    lockstep(T, 3, 3, 256, 7, tau=1.0)
+
+
+def test_init_matches_synth_uniform_init():
+    need_gpu()
+    T = synth.make("C1")
+    g = make_ctx(T, 3, init_seed=2)
+    ref = synth.uniform_init(T.dims, 3, 2)
+    for m in range(3):
+        A, lam = g.get_factor(m)
+        assert (A == ref[m].numpy()).all()
+        assert (lam == 1).all()
+
+
+def test_leverage_parity_random_factors():
+    need_gpu()
+    T = synth.make("C1")
+    g = make_ctx(T, 3)
+    rng = np.random.default_rng(0)
+    for m in range(3):
+        A = rng.standard_normal((T.dims[m], 3)) * [1.0, 10.0, 0.1]
+        g.set_factor(m, A)
+        ell, rank = g.leverage(m)
+        ref, rref = oracle.leverage(A)
+        assert rank == rref == 3
+        assert np.abs(ell - ref).max() <= 1e-12 * max(1.0, 1.0)
+
+
+def test_leverage_rank_deficient_fallback():
+    need_gpu()
+    T = synth.make("C1")
+    from paper_2006_16438_b200 import Cparls
+    g = Cparls(T.dims, T.coords.cuda(), T.vals.cuda(), 5)
+    rng = np.random.default_rng(1)
+    A = rng.standard_normal((T.dims[0], 3)) @ rng.standard_normal((3, 5))
+    g.set_factor(0, A)
+    ell, rank = g.leverage(0)
+    ref, rref = oracle.leverage(A)
+    assert rank == rref == 3
+    np.testing.assert_allclose(ell, ref, atol=1e-9)
+
+
+def test_c2_lockstep_2_iterations():
+    T = synth.make("C2", device="cuda")
+    T = synth.Tensor(T.cfg, T.dims, T.coords.cpu(), T.vals.cpu())
+    lockstep(T, 25, 2, 1 << 17, 3)
+
+
+def test_generator_cpu_cuda_identical():
+    need_gpu()
+    cfg = synth.scaled("C2", 200_000)
+    a = synth.make(cfg, device="cpu")
+    b = synth.make(cfg, device="cuda")
+    assert torch.equal(a.coords, b.coords.cpu())
+    assert torch.equal(a.vals, b.vals.cpu())
+
+
+def test_full_inclusion_equals_exact_als_gpu():
+    """PIN-9 through the GPU: tau = 0, s = N_k -> every row deterministic with
+    w = 1, so B is the exact ALS update (oracle's own CP-ALS routine)."""
+    need_gpu()
+    dims = (5, 6, 4)
+    rng = np.random.default_rng(3)
+    lin = rng.choice(120, 70, replace=False)
+    coords = np.stack(np.unravel_index(lin, dims, order="F"), 1).astype(np.int32)
+    vals = rng.standard_normal(70)
+    T = synth.Tensor(synth.CONFIGS["C1"], dims, torch.from_numpy(coords), torch.from_numpy(vals))
+    g = make_ctx(T, 3, tau=0.0)
+    for k in range(3):
+        o = make_oracle(T, 3)
+        sync_oracle_from_gpu(g, o)
+        for m in range(3):
+            o.set_factor(m, g.get_factor(m)[0])
+        Nk = int(np.prod([n for m, n in enumerate(dims) if m != k]))
+        info = g.sample(k, Nk, 1, k)
+        assert info.s_det == Nk and info.s_bar == Nk
+        g.solve_mode(k)
+        _, Bg = g.last_solve(k)
+        o.als_update(k)
+        _, _, Bo = o.last_solve(k)
+        assert np.linalg.norm(Bg - Bo) <= 1e-9 * np.linalg.norm(Bo)
+
+
+def test_two_way_and_rank_edges():
+    need_gpu()
+    rng = np.random.default_rng(4)
+    for dims, r in (((37, 53), 1), ((37, 53), 4), ((9, 11, 13), 64)):
+        N = int(np.prod(dims))
+        nnz = min(N, 400)
+        lin = rng.choice(N, nnz, replace=False)
+        coords = np.stack(np.unravel_index(lin, dims, order="F"), 1).astype(np.int32)
+        vals = rng.standard_normal(nnz)
+        T = synth.Tensor(synth.CONFIGS["C1"], dims, torch.from_numpy(coords), torch.from_numpy(vals))
+        lockstep(T, r, 2, 64, 11)
+
+
+def test_empty_tensor_and_errors():
+    need_gpu()
+    from paper_2006_16438_b200 import Cparls, CparlsError
+    from paper_2006_16438_b200 import cparls as cp
+    g = Cparls((4, 5, 6), np.zeros((0, 3), dtype=np.int32), np.zeros(0), 2)
+    g.sample(0, 16, 1, 0)
+    info = g.solve_mode(0)
+    assert info.matched_nnz == 0
+    with pytest.raises(CparlsError) as e:
+        g.fit()
+    assert e.value.status == cp.ENUMERIC
+    with pytest.raises(CparlsError) as e:
+        g.solve_mode(1)
+    assert e.value.status == cp.ESTATE
+    with pytest.raises(CparlsError) as e:
+        g.sample(7, 16, 1, 0)
+    assert e.value.status == cp.EINVAL
+    with pytest.raises(CparlsError) as e:
+        Cparls((4, 5, 6), np.array([[0, 5, 0]], dtype=np.int32), np.ones(1), 2)
+    assert e.value.status == cp.ERANGE
+    with pytest.raises(CparlsError) as e:
+        Cparls((4, 5, 6), np.zeros((1, 3), dtype=np.int32), np.ones(1), 65)
+    assert e.value.status == cp.EINVAL
+
+
+def test_host_and_device_inputs_agree():
+    need_gpu()
+    T = synth.make("C1")
+    a = make_ctx(T, 3, device="cuda")
+    b = make_ctx(T, 3, device=None)
+    ta = a.run(3, 256, 3, fit_every=1)
+    tb = b.run(3, 256, 3, fit_every=1)
+    np.testing.assert_allclose(ta, tb, rtol=0, atol=1e-12)
+
+
+def test_planted_recovery_gpu():
+    """Fully populated planted rank-3 C1 variant: CP-ARLS-LEV reaches fit >= 0.999."""
+    need_gpu()
+    T = synth.make("C1", dense_planted=True)
+    g = make_ctx(T, 3)
+    trace = g.run(60, 256, 3, fit_every=1)
+    assert np.nanmax(trace) >= 0.999
+
+
+def test_free_running_matches_oracle():
+    need_gpu()
+    T = synth.make("C1", dense_planted=True)
+    g = make_ctx(T, 3)
+    o = make_oracle(T, 3)
+    for m in range(3):
+        o.set_factor(m, g.get_factor(m)[0])
+    tg = g.run(5, 256, 3, fit_every=1)
+    to = o.run(5, 256, -1, 3, 1)
+    np.testing.assert_allclose(tg, to, atol=1e-8)
