@@ -685,49 +685,17 @@ int64_t or_get_fibers(or_ctx *c, int64_t cap, int64_t *len, int64_t *out, double
 }
 
 /* ------------------------------------------------------------------ */
-/* O14: solve rows x G = m (G symmetric) for all rows of M: Cholesky with */
-/* pivot test, fallback to the eigen pseudo-inverse (AMB-12).           */
+/* O14: B = M G^+ for all rows: the minimum-norm least-squares   */
+/* solution, G^+ from the eigendecomposition with the cutoff            */
+/* mu_j > r*eps*mu_max (AMB-11/12).  The plain definition: no Cholesky   */
+/* shortcut (a pivot test is not rank revealing).  *fallback = rank < r. */
 /* ------------------------------------------------------------------ */
 static int solve_rows(int r, const double *G, int64_t n, const double *M, double *B,
                       int *fallback) {
-  double L[OR_MAXR * OR_MAXR];
-  double maxdiag = 0.0;
-  for (int j = 0; j < r; ++j) if (G[j * r + j] > maxdiag) maxdiag = G[j * r + j];
-  int ok = maxdiag > 0.0;
-  for (int j = 0; j < r && ok; ++j) {
-    double dj = G[j * r + j];
-    for (int q = 0; q < j; ++q) dj -= L[j * r + q] * L[j * r + q];
-    if (!(dj > (double)r * DBL_EPSILON * maxdiag)) { ok = 0; break; }
-    L[j * r + j] = sqrt(dj);
-    for (int i = j + 1; i < r; ++i) {
-      double v = G[i * r + j];
-      for (int q = 0; q < j; ++q) v -= L[i * r + q] * L[j * r + q];
-      L[i * r + j] = v / L[j * r + j];
-    }
-  }
-  if (ok) {
-    *fallback = 0;
-    for (int64_t i = 0; i < n; ++i) {
-      const double *m = M + i * r;
-      double *b = B + i * r;
-      double y[OR_MAXR];
-      for (int j = 0; j < r; ++j) {            /* L y = m */
-        double v = m[j];
-        for (int q = 0; q < j; ++q) v -= L[j * r + q] * y[q];
-        y[j] = v / L[j * r + j];
-      }
-      for (int j = r - 1; j >= 0; --j) {       /* L^T b = y */
-        double v = y[j];
-        for (int q = j + 1; q < r; ++q) v -= L[q * r + j] * b[q];
-        b[j] = v / L[j * r + j];
-      }
-    }
-    return r;
-  }
-  *fallback = 1;
   double w[OR_MAXR], V[OR_MAXR * OR_MAXR];
   int keep[OR_MAXR];
   int rank = pinv_eig(r, G, w, V, keep);
+  *fallback = rank < r;
   for (int64_t i = 0; i < n; ++i) {
     const double *m = M + i * r;
     double *b = B + i * r;

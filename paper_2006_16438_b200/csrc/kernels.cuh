@@ -34,46 +34,84 @@ __host__ __device__ constexpr int npairs(int r) { return r * (r + 1) / 2; }
 // Small dense r x r linear algebra, single block (r <= 64)
 // ======================================================================
 
-// Cyclic Jacobi eigensolver on shared-memory matrix a (r x r, row stride r),
-// V (r x r).  Executed by thread 0 only (fallback path; r <= 64).
-__device__ void jacobi_serial(int r, double *a, double *V) {
-  for (int i = 0; i < r; ++i)
-    for (int j = 0; j < r; ++j) V[i * r + j] = (i == j) ? 1.0 : 0.0;
-  for (int sweep = 0; sweep < 100; ++sweep) {
-    double off = 0.0, diag = 0.0;
-    for (int i = 0; i < r; ++i) {
-      diag += a[i * r + i] * a[i * r + i];
-      for (int j = i + 1; j < r; ++j) off += a[i * r + j] * a[i * r + j];
+// Parallel cyclic Jacobi eigensolver (round-robin ordering: R/2 disjoint
+// rotations per round, A <- J^T A J, V <- V J), whole block.  a, V: shared
+// r x r (row stride r).  Eigenvalues end on diag(a), vectors in V's columns.
+// Convergence test as the oracle's: off^2 <= 1e-34 diag^2.
+constexpr double kCholSafe = 1e-6;   // Cholesky fast path only if every pivot > kCholSafe * max_diag
+
+__device__ void block_jacobi(int r, double *a, double *V) {
+  __shared__ double cs[kMaxRank / 2 + 1], sn[kMaxRank / 2 + 1];
+  __shared__ int pp[kMaxRank / 2 + 1], qq[kMaxRank / 2 + 1];
+  __shared__ int done;
+  const int R = (r + 1) & ~1;
+  const int H = R / 2;
+  for (int i = threadIdx.x; i < r * r; i += blockDim.x) V[i] = (i / r == i % r) ? 1.0 : 0.0;
+  __syncthreads();
+  for (int sweep = 0; sweep < 60; ++sweep) {
+    if (threadIdx.x == 0) {
+      double off = 0.0, diag = 0.0;
+      for (int i = 0; i < r; ++i) {
+        diag += a[i * r + i] * a[i * r + i];
+        for (int j = i + 1; j < r; ++j) off += a[i * r + j] * a[i * r + j];
+      }
+      done = (off <= 1e-34 * diag || off == 0.0);
     }
-    if (off <= 1e-34 * diag || off == 0.0) break;
-    for (int p = 0; p < r; ++p)
-      for (int q = p + 1; q < r; ++q) {
-        double apq = a[p * r + q];
-        if (apq == 0.0) continue;
-        double theta = (a[q * r + q] - a[p * r + p]) / (2.0 * apq);
-        double t = (theta >= 0 ? 1.0 : -1.0) / (fabs(theta) + sqrt(theta * theta + 1.0));
-        double c = 1.0 / sqrt(t * t + 1.0), s = t * c;
-        for (int k = 0; k < r; ++k) {
-          double akp = a[k * r + p], akq = a[k * r + q];
-          a[k * r + p] = c * akp - s * akq;
-          a[k * r + q] = s * akp + c * akq;
+    __syncthreads();
+    if (done) break;
+    for (int t = 0; t < R - 1; ++t) {
+      for (int i = threadIdx.x; i < H; i += blockDim.x) {
+        int x = (i == 0) ? 0 : ((i - 1 + t) % (R - 1)) + 1;
+        int yi = R - 1 - i;
+        int y = ((yi - 1 + t) % (R - 1)) + 1;
+        int p = min(x, y), q = max(x, y);
+        double c = 1.0, sv = 0.0;
+        if (q < r) {
+          double apq = a[p * r + q];
+          if (apq != 0.0) {
+            double theta = (a[q * r + q] - a[p * r + p]) / (2.0 * apq);
+            double tt = (theta >= 0 ? 1.0 : -1.0) / (fabs(theta) + sqrt(theta * theta + 1.0));
+            c = 1.0 / sqrt(tt * tt + 1.0);
+            sv = tt * c;
+          }
         }
-        for (int k = 0; k < r; ++k) {
+        pp[i] = p; qq[i] = q; cs[i] = c; sn[i] = sv;
+      }
+      __syncthreads();
+      for (int idx = threadIdx.x; idx < H * r; idx += blockDim.x) {   // rows: J^T A
+        int i = idx / r, k = idx % r;
+        int p = pp[i], q = qq[i];
+        if (q < r && sn[i] != 0.0) {
+          double c = cs[i], sv = sn[i];
           double apk = a[p * r + k], aqk = a[q * r + k];
-          a[p * r + k] = c * apk - s * aqk;
-          a[q * r + k] = s * apk + c * aqk;
-        }
-        for (int k = 0; k < r; ++k) {
-          double vkp = V[k * r + p], vkq = V[k * r + q];
-          V[k * r + p] = c * vkp - s * vkq;
-          V[k * r + q] = s * vkp + c * vkq;
+          a[p * r + k] = c * apk - sv * aqk;
+          a[q * r + k] = sv * apk + c * aqk;
         }
       }
+      __syncthreads();
+      for (int idx = threadIdx.x; idx < H * r; idx += blockDim.x) {   // columns: A J, V J
+        int i = idx / r, k = idx % r;
+        int p = pp[i], q = qq[i];
+        if (q < r && sn[i] != 0.0) {
+          double c = cs[i], sv = sn[i];
+          double akp = a[k * r + p], akq = a[k * r + q];
+          a[k * r + p] = c * akp - sv * akq;
+          a[k * r + q] = sv * akp + c * akq;
+          double vkp = V[k * r + p], vkq = V[k * r + q];
+          V[k * r + p] = c * vkp - sv * vkq;
+          V[k * r + q] = sv * vkp + c * vkq;
+        }
+      }
+      __syncthreads();
+    }
   }
 }
 
-// Cholesky G = L L^T in shared memory with the pivot test of AMB-12
-// (pivot > r*eps*max_diag).  Returns 1 on success.  L lower (row stride r).
+// Cholesky G = L L^T in shared memory.  Fast path of G^+ only: accepted when
+// every pivot > kCholSafe * max_diag (G well conditioned, where Cholesky and the
+// eigen pseudo-inverse agree to kappa*eps); otherwise the caller takes the
+// eigen path whose cutoff mu_j > r*eps*mu_max defines the rank (AMB-11/12).
+// Returns 1 on success.  L lower (row stride r).
 // Whole block participates.
 __device__ int block_cholesky(int r, const double *G, double *L, int *ok_flag) {
   __shared__ double maxdiag;
@@ -89,7 +127,7 @@ __device__ int block_cholesky(int r, const double *G, double *L, int *ok_flag) {
     if (threadIdx.x == 0 && *ok_flag) {
       double dj = G[j * r + j];
       for (int q = 0; q < j; ++q) dj -= L[j * r + q] * L[j * r + q];
-      if (!(dj > (double)r * 2.220446049250313e-16 * maxdiag)) *ok_flag = 0;
+      if (!(dj > kCholSafe * maxdiag)) *ok_flag = 0;
       else L[j * r + j] = sqrt(dj);
     }
     __syncthreads();
@@ -136,24 +174,29 @@ __device__ void lev_prep_body(int r, const double *Gg, ModeDev *md) {
     if (threadIdx.x == 0) { md->tri = 1; md->rank = r; }
     return;
   }
-  // eigen fallback
+  // eigen fallback (AMB-11): W = V_kept diag(mu^{-1/2})
+  double *a = L, *V = Li;
+  for (int i = threadIdx.x; i < r * r; i += blockDim.x) a[i] = G[i];
+  __syncthreads();
+  block_jacobi(r, a, V);
+  __shared__ double mumax;
+  __shared__ int rank_s;
   if (threadIdx.x == 0) {
-    double *a = L, *V = Li;
-    for (int i = 0; i < r * r; ++i) a[i] = G[i];
-    jacobi_serial(r, a, V);
-    double mumax = 0.0;
-    for (int j = 0; j < r; ++j) mumax = fmax(mumax, a[j * r + j]);
-    int rank = 0;
-    for (int j = 0; j < r; ++j) {
-      double mu = a[j * r + j];
-      bool keep = mumax > 0.0 && mu > (double)r * 2.220446049250313e-16 * mumax;
-      rank += keep;
-      double s = keep ? 1.0 / sqrt(mu) : 0.0;
-      for (int p = 0; p < r; ++p) md->W[p * r + j] = V[p * r + j] * s;
-    }
-    md->tri = 0;
-    md->rank = rank;
+    double m = 0.0;
+    for (int j = 0; j < r; ++j) m = fmax(m, a[j * r + j]);
+    mumax = m;
+    int rk = 0;
+    for (int j = 0; j < r; ++j) rk += (m > 0.0 && a[j * r + j] > (double)r * 2.220446049250313e-16 * m);
+    rank_s = rk;
   }
+  __syncthreads();
+  for (int i = threadIdx.x; i < r * r; i += blockDim.x) {
+    int p = i / r, j = i % r;
+    double mu = a[j * r + j];
+    bool keep = mumax > 0.0 && mu > (double)r * 2.220446049250313e-16 * mumax;
+    md->W[p * r + j] = keep ? V[p * r + j] / sqrt(mu) : 0.0;
+  }
+  if (threadIdx.x == 0) { md->tri = 0; md->rank = rank_s; }
 }
 
 __global__ void k_lev_prep(int r, const double *G, ModeDev *md) { lev_prep_body(r, G, md); }
@@ -670,18 +713,27 @@ __global__ void __launch_bounds__(kKrpThreads) k_krp_gram(const uint64_t *__rest
     for (int jj = w; jj < cnt; jj += kKrpThreads / 32) {
       int64_t j = base + jj;
       uint64_t key = skey[j];
-      double z = 1.0;
+      double z0 = 1.0, z1 = 1.0;
       for (int m = 0; m < om.d; ++m) {
         uint64_t i = key % (uint64_t)om.n[m];
         key /= (uint64_t)om.n[m];
+        const double *row = om.A[m] + i * ld;
         if (lane < r) {
-          double a = __ldg(om.A[m] + i * ld + lane);
-          z = (m == 0) ? a : z * a;
+          double a = __ldg(row + lane);
+          z0 = (m == 0) ? a : z0 * a;
+        }
+        if (lane + 32 < r) {
+          double a = __ldg(row + lane + 32);
+          z1 = (m == 0) ? a : z1 * a;
         }
       }
       if (lane < r) {
-        zs[jj][lane] = z;
-        Z[j * ld + lane] = z;
+        zs[jj][lane] = z0;
+        Z[j * ld + lane] = z0;
+      }
+      if (lane + 32 < r) {
+        zs[jj][lane + 32] = z1;
+        Z[j * ld + lane + 32] = z1;
       }
       if (lane == 0) ws[jj] = sw2[j];
     }
@@ -766,7 +818,7 @@ __global__ void __launch_bounds__(kRhsThreads) k_rhs(const int64_t *__restrict__
     }
     int64_t jcur = a - 1;       // sample of the first entry of the current 32-group
     int64_t jz = -1;            // sample whose (w2, z) are loaded
-    double coefw = 0.0, z = 0.0;
+    double coefw = 0.0, z = 0.0, z1 = 0.0;
     for (int64_t t = t0; t < t1; t += 32) {
       const int64_t tt = t + lane;
       int64_t jj = jcur;
@@ -787,8 +839,10 @@ __global__ void __launch_bounds__(kRhsThreads) k_rhs(const int64_t *__restrict__
           jz = ju;
           coefw = __ldg(sw2 + ju);
           z = lane < r ? __ldg(Z + ju * ld + lane) : 0.0;
+          z1 = lane + 32 < r ? __ldg(Z + ju * ld + lane + 32) : 0.0;
         }
         if (lane < r) atomicAdd(M + (int64_t)o * ld + lane, (coefw * x) * z);
+        if (lane + 32 < r) atomicAdd(M + (int64_t)o * ld + lane + 32, (coefw * x) * z1);
         if (lane == 0) touched[o] = 1;
       }
       jcur = __shfl_sync(0xffffffffu, jj, 31);
@@ -820,28 +874,32 @@ __global__ void k_solve_prep(int r, SolveDev *sd) {
     if (threadIdx.x == 0) { sd->rank_used = r; sd->chol_fallback = 0; }
     return;
   }
+  double *a = L, *V = Li;
+  for (int i = threadIdx.x; i < r * r; i += blockDim.x) a[i] = G[i];
+  __syncthreads();
+  block_jacobi(r, a, V);
+  __shared__ double inv[kMaxRank];
+  __shared__ double mumax;
   if (threadIdx.x == 0) {
-    double *a = L, *V = Li;
-    for (int i = 0; i < r * r; ++i) a[i] = G[i];
-    jacobi_serial(r, a, V);
-    double mumax = 0.0;
-    for (int j = 0; j < r; ++j) mumax = fmax(mumax, a[j * r + j]);
-    int rank = 0;
-    double inv[kMaxRank];
+    double m = 0.0;
+    for (int j = 0; j < r; ++j) m = fmax(m, a[j * r + j]);
+    mumax = m;
+    int rk = 0;
     for (int j = 0; j < r; ++j) {
       double mu = a[j * r + j];
-      bool keep = mumax > 0.0 && mu > (double)r * 2.220446049250313e-16 * mumax;
-      rank += keep;
+      bool keep = m > 0.0 && mu > (double)r * 2.220446049250313e-16 * m;
+      rk += keep;
       inv[j] = keep ? 1.0 / mu : 0.0;
     }
-    for (int p = 0; p < r; ++p)
-      for (int q = 0; q < r; ++q) {
-        double s = 0.0;
-        for (int j = 0; j < r; ++j) s += V[p * r + j] * inv[j] * V[q * r + j];
-        sd->Ginv[p * r + q] = s;
-      }
-    sd->rank_used = rank;
+    sd->rank_used = rk;
     sd->chol_fallback = 1;
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < r * r; i += blockDim.x) {
+    int p = i / r, q = i % r;
+    double sum = 0.0;
+    for (int j = 0; j < r; ++j) sum += V[p * r + j] * inv[j] * V[q * r + j];
+    sd->Ginv[i] = sum;
   }
 }
 
