@@ -1,0 +1,329 @@
+#!/usr/bin/env python
+"""CP-ARLS-LEV outer iterations/s on B200 (BASELINE.json metric).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config C4] [--impl ours|reference]
+
+A "step" is one CP-ARLS-LEV outer iteration (all D mode updates: sample ->
+KrpSamp/Gram -> fiber lookup -> RHS -> solve/normalize/leverage, Alg. 3
+P:917-928) with the exact fit amortized once per epoch of eta = 5 iterations
+(P:930): the timed K iterations include a fit after every 5th global
+iteration.  Inputs are synthetic Zipf tensors shaped like the paper's
+workloads (synth/).  Prints ONE JSON line on rank 0.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+ETA = 5                       # epoch length
+METRIC = "CP-ARLS-LEV ALS iterations/sec (r=25, s=2^17) and % of HBM roofline"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="C4")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--tau", type=float, default=-1.0, help="-1 = 1/s (hybrid, P:999); 1 = random")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--profile-phases", action="store_true", help="per-phase breakdown (stderr)")
+    ap.add_argument("--sample-frac", type=float, default=0.001,
+                    help="oracle sample: this fraction of the config's nonzeros (a prefix)")
+    return ap.parse_args()
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rk = int(os.environ.get("RANK", "0"))
+    lrk = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rk, lrk
+
+
+# ---------------------------------------------------------------- clocks
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md)."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.idx = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.idx}", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1])); mx.append(float(f[2]))
+            except ValueError:
+                continue
+            for n, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        sm.sort()
+        return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+# ---------------------------------------------------------------- oracle leg
+def oracle_sample(cfg_name, frac, steps, tau):
+    """Time the plain-C oracle (as it stands) for `steps` outer iterations on
+    the first frac*nnz nonzeros of the config (a prefix of the same seeded
+    draw sequence), same dims / r / s / tau.  Single-threaded."""
+    import dataclasses
+    import numpy as np
+    import torch
+    import oracle
+    import synth
+    cfg = synth.CONFIGS[cfg_name]
+    nnz = max(1000, int(cfg.nnz * frac))
+    sub = dataclasses.replace(cfg, nnz=nnz)
+    T = synth.make(sub, device="cpu", index_dtype=torch.int64)
+    o = oracle.Oracle(cfg.dims, T.coords.numpy(), T.vals.to(torch.float64).numpy(), cfg.rank)
+    init = synth.uniform_init(cfg.dims, cfg.rank, cfg.init_seed)
+    for k in range(len(cfg.dims)):
+        o.set_factor(k, init[k].numpy())
+    times = []
+    D = len(cfg.dims)
+    for t in range(steps):
+        t0 = time.perf_counter()
+        for k in range(D):
+            o.sample(k, cfg.s, tau, cfg.sample_seed, t * D + k)
+            o.solve_mode(k)
+        if (t + 1) % ETA == 0:
+            o.fit()
+        times.append(time.perf_counter() - t0)
+    # amortize one fit per ETA iterations even if steps < ETA
+    tf0 = time.perf_counter(); o.fit(); tfit = time.perf_counter() - tf0
+    nfits = steps // ETA
+    total = sum(times) + (steps / ETA - nfits) * tfit
+    return {"value": steps / total, "unit": "iterations/s", "cores": 1, "kind": "oracle",
+            "sample": f"{steps} outer iteration(s) of the plain-C oracle (1 thread) on the first {nnz} "
+                      f"nonzeros ({frac:.4%}) of {cfg_name}'s seeded draw sequence, full dims "
+                      f"{cfg.dims}, r={cfg.rank}, s={cfg.s}, tau={'1/s' if tau < 0 else tau}, "
+                      f"exact fit amortized 1/{ETA}"}
+
+
+def run_reference(args):
+    ws, rk, _ = dist_env()
+    if rk != 0:
+        return
+    import synth
+    cfg = synth.CONFIGS[args.config]
+    steps = max(1, args.steps)
+    # warmup iterations of a CPU program are not needed for timing; keep the
+    # run bounded: W is honored only up to 1
+    if args.warmup > 0:
+        oracle_sample(args.config, args.sample_frac, 1, args.tau)
+    cb = oracle_sample(args.config, args.sample_frac, steps, args.tau)
+    line = {"impl": "reference", "metric": METRIC, "value": cb["value"], "unit": "iterations/s",
+            "n_gpus": args.gpus, "steps": steps, "warmup": args.warmup,
+            "ms_per_step": 1000.0 / cb["value"], "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": args.config, "dims": list(cfg.dims), "rank": cfg.rank, "s": cfg.s,
+                       "tau": "1/s" if args.tau < 0 else args.tau, "oracle_sample": cb["sample"]},
+            "cpu_baseline": cb,
+            "e2e": {"value": cb["value"], "unit": "iterations/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------- our arm
+def run_ours(args):
+    import numpy as np
+    import torch
+    import synth
+    from paper_2006_16438_b200 import Cparls
+
+    ws, rk, lrk = dist_env()
+    if args.gpus > 1 or ws > 1:
+        raise SystemExit("multi-GPU sharding is not built yet in this round (see DESIGN.md)")
+    torch.cuda.set_device(lrk)
+    dev = torch.device("cuda", lrk)
+    cfg = synth.CONFIGS[args.config]
+    D = len(cfg.dims)
+    t0 = time.perf_counter()
+    T = synth.make(cfg, device=dev, index_dtype=torch.int32)
+    torch.cuda.synchronize()
+    t_gen = time.perf_counter() - t0
+    coords, vals = T.coords, T.vals
+    nnz = coords.shape[0]
+    host = None
+    if not args.no_e2e:
+        host = (torch.empty(coords.shape, dtype=coords.dtype, pin_memory=True),
+                torch.empty(vals.shape, dtype=vals.dtype, pin_memory=True))
+        host[0].copy_(coords)
+        host[1].copy_(vals)
+    torch.cuda.empty_cache()
+    stream = torch.cuda.current_stream(dev)
+    t0 = time.perf_counter()
+    g = Cparls(cfg.dims, coords, vals, cfg.rank, tau=args.tau, init_seed=cfg.init_seed,
+               stream=stream.cuda_stream)
+    torch.cuda.synchronize()
+    t_build = time.perf_counter() - t0
+    del coords, vals, T
+    torch.cuda.empty_cache()
+
+    seed = cfg.sample_seed
+    # warmup
+    for t in range(args.warmup):
+        g.run(1, cfg.s, seed, iter0=t, fit_every=0)
+    if args.profile_phases:
+        g.set_profiling(True)
+    g.reset_stats()
+    K = args.steps
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    fit_events = []
+    torch.cuda.synchronize()
+    with Clocks(lrk) as clk:
+        ev0.record(stream)
+        for t in range(K):
+            it = args.warmup + t
+            g.run(1, cfg.s, seed, iter0=it, fit_every=0)
+            if (it + 1) % ETA == 0:
+                fa = torch.cuda.Event(enable_timing=True); fb = torch.cuda.Event(enable_timing=True)
+                fa.record(stream)
+                fval = g.fit()
+                fb.record(stream)
+                fit_events.append((fa, fb))
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    ms = ev0.elapsed_time(ev1)
+    st = g.stats()
+    fit_ms = [a.elapsed_time(b) for a, b in fit_events]
+    value = K / (ms / 1000.0)
+    # fit kernel alone, timed live: bytes = streamed nonzeros (key u64 + out i32 + value)
+    vbytes = 4 if cfg.value_dtype == "f32" else 8
+    fit_alg_bytes = nnz * (8 + 4 + vbytes)
+    if not fit_ms:
+        fa = torch.cuda.Event(enable_timing=True); fb = torch.cuda.Event(enable_timing=True)
+        fa.record(stream); g.fit(); fb.record(stream); torch.cuda.synchronize()
+        fit_ms = [fa.elapsed_time(fb)]
+    fit_avg = sum(fit_ms) / len(fit_ms)
+    peak, peak_src = measured_peaks()
+    achieved = fit_alg_bytes / (fit_avg / 1000.0) / 1e9
+    final_fit = g.fit()
+    if args.profile_phases:
+        sys.stderr.write(json.dumps({k: v for k, v in st.items()}, indent=1) + "\n")
+    g.close()
+    del g
+    torch.cuda.empty_cache()
+
+    # e2e: public API from pinned host buffers (create + K iterations + fits + factors back)
+    e2e = None
+    if host is not None:
+        torch.cuda.synchronize()
+        hc, hv = host
+        e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        g2 = Cparls(cfg.dims, hc.numpy(), hv.numpy(), cfg.rank, tau=args.tau, init_seed=cfg.init_seed,
+                    stream=stream.cuda_stream)
+        d2h = 0
+        for t in range(K):
+            g2.run(1, cfg.s, seed, iter0=t, fit_every=0)
+            if (t + 1) % ETA == 0:
+                g2.fit(); d2h += 8
+        for m in range(D):
+            A, lam = g2.get_factor(m)
+            d2h += A.nbytes + lam.nbytes
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ems = e0.elapsed_time(e1)
+        g2.close()
+        h2d = hc.numel() * hc.element_size() + hv.numel() * hv.element_size()
+        e2e = {"value": K / (ems / 1000.0), "unit": "iterations/s", "h2d_bytes_per_step": h2d // K,
+               "d2h_bytes_per_step": d2h // K,
+               "includes": "cparls_create from pinned host COO (H2D + per-mode index build) + K iterations + "
+                           "fits every 5 + factors back to host"}
+
+    cpu = None
+    if not args.no_cpu_baseline and rk == 0:
+        cpu = oracle_sample(args.config, args.sample_frac, 1, args.tau)
+
+    line = {
+        "metric": METRIC, "value": value, "unit": "iterations/s", "n_gpus": 1, "steps": K,
+        "warmup": args.warmup, "ms_per_step": ms / K, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": args.config, "dims": list(cfg.dims), "nnz": int(nnz), "rank": cfg.rank,
+                   "s": cfg.s, "tau": "1/s" if args.tau < 0 else args.tau, "fit_every": ETA,
+                   "values": cfg.value_dtype, "l2": "inputs larger than L2 (per-mode sorted copies "
+                   f"{nnz * (16 if cfg.value_dtype == 'f32' else 20) * D / 1e9:.1f} GB >> 126 MB)",
+                   "parallelism": "single GPU"},
+        "roofline": {"bound": "hbm", "kernel": "k_fit_inner (exact fit, streams all nonzeros)",
+                     "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                     "traffic": None, "alg_bytes_per_launch": fit_alg_bytes, "avg_launch_ms": fit_avg,
+                     "peak_source": peak_src},
+        "clocks": clk.summary(),
+        "gpu_launches": int(st["kernel_launches"]),
+        "e2e": e2e,
+        "cpu_baseline": cpu,
+        "fit": final_fit,
+        "setup": {"generate_s": t_gen, "create_s": t_build},
+        "phases_ms": {k[3:]: st[k] for k in st if k.startswith("ms_")} if args.profile_phases else None,
+        "counters": {"last_matched_nnz": st["last_matched_nnz"], "last_s_bar": st["last_s_bar"],
+                     "last_attempts": st["last_attempts"]},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

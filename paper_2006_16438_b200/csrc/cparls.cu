@@ -6,6 +6,8 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <cub/device/device_radix_sort.cuh>
 #include <new>
@@ -115,6 +117,14 @@ struct cparls_ctx {
   bool profiling = false;
   int fit_mode = 0;
   int smode_last_solved = -1;
+  // RHS output-row windows (see rhs.cuh)
+  int64_t segcap = 0;
+  int64_t *seg_lo = nullptr, *seg_len = nullptr, *seg_off = nullptr, *i64part_seg = nullptr;
+  int32_t *seg_j = nullptr;
+  // RHS hot rows per mode (warp-private accumulation, see rhs.cuh)
+  int16_t *hot_slot[kMaxModes] = {nullptr};
+  int32_t *hot_row[kMaxModes] = {nullptr};
+  int64_t nfib[kMaxModes] = {0};
 };
 
 namespace {
@@ -193,18 +203,66 @@ struct Phase {
 
 #define LAUNCHED(c, n) ((c)->stats.kernel_launches += (n))
 
-size_t lev_smem(int r, int ld) { return sizeof(double) * ((size_t)r * r + (size_t)kLevThreads * (ld + 1)); }
+inline int rmax_bucket(int r) { return r <= 4 ? 4 : r <= 8 ? 8 : r <= 16 ? 16 : r <= 32 ? 32 : 64; }
+
+#define RSWITCH(r, ...)                                      \
+  do {                                                       \
+    switch (rmax_bucket(r)) {                                \
+      case 4: { constexpr int RM = 4; __VA_ARGS__; } break;   \
+      case 8: { constexpr int RM = 8; __VA_ARGS__; } break;   \
+      case 16: { constexpr int RM = 16; __VA_ARGS__; } break; \
+      case 32: { constexpr int RM = 32; __VA_ARGS__; } break; \
+      default: { constexpr int RM = 64; __VA_ARGS__; } break; \
+    }                                                        \
+  } while (0)
+
+// dynamic shared memory (doubles) of the row kernels; +RMAX slack covers the
+// unconditional register loads of padded columns
+size_t tile_d(int ld) { return (size_t)kRowThreads * (ld + 1); }
+size_t gram_smem(int r, int ld) { return sizeof(double) * (tile_d(ld) + 64); }
+size_t lev_smem(int r, int ld) { return sizeof(double) * ((size_t)r * r + 64 + tile_d(ld) + 64); }
+size_t solve_smem(int r, int ld) { return sizeof(double) * ((size_t)r * r + tile_d(ld) + 64); }
+size_t krp_smem(int r, int ld) { return sizeof(double) * (tile_d(ld) + kRowThreads + 64); }
 size_t prep_smem(int r) { return sizeof(double) * 4 * (size_t)r * r; }
 
+// allow the largest dynamic shared memory the kernel can take (opt-in limit
+// minus its static shared memory)
+template <typename F>
+void max_dyn_smem(F func) {
+  static int optin = -1;
+  if (optin < 0) {
+    int dev = 0;
+    CK(cudaGetDevice(&dev));
+    CK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+  }
+  cudaFuncAttributes fa;
+  CK(cudaFuncGetAttributes(&fa, func));
+  CK(cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, optin - (int)fa.sharedSizeBytes));
+}
+
+template <int RM>
+void set_attrs_rm() {
+  max_dyn_smem(k_gram_rows_t<RM>);
+  max_dyn_smem(k_lev_rows_t<RM>);
+  max_dyn_smem(k_solve_rows_t<RM>);
+  max_dyn_smem(k_krp_gram_t<RM>);
+  max_dyn_smem(k_fit_thread<float, RM>);
+  max_dyn_smem(k_fit_thread<double, RM>);
+}
+
 void set_kernel_attrs(int r, int ld) {
-  int lev = (int)lev_smem(r, ld);
-  CK(cudaFuncSetAttribute(k_lev_rows, cudaFuncAttributeMaxDynamicSharedMemorySize, lev));
-  CK(cudaFuncSetAttribute(k_solve_rows, cudaFuncAttributeMaxDynamicSharedMemorySize, lev));
+  set_attrs_rm<4>(); set_attrs_rm<8>(); set_attrs_rm<16>(); set_attrs_rm<32>(); set_attrs_rm<64>();
   int prep = (int)prep_smem(r);
   CK(cudaFuncSetAttribute(k_lev_prep, cudaFuncAttributeMaxDynamicSharedMemorySize, prep));
   CK(cudaFuncSetAttribute(k_norm_prep, cudaFuncAttributeMaxDynamicSharedMemorySize, prep));
   CK(cudaFuncSetAttribute(k_solve_prep, cudaFuncAttributeMaxDynamicSharedMemorySize, prep));
+  max_dyn_smem(k_rhs<float, false>);
+  max_dyn_smem(k_rhs<float, true>);
+  max_dyn_smem(k_rhs<double, false>);
+  max_dyn_smem(k_rhs<double, true>);
 }
+
+int64_t row_grid(cparls_ctx *c, int64_t ntiles) { return std::max<int64_t>(1, std::min<int64_t>(ntiles, c->gpart_blocks)); }
 
 // ---------------------------------------------------------------- leverage
 // rows -> p~, integer CDF (AMB-9/11).  lam != null also
@@ -214,9 +272,12 @@ void lev_rows_and_cdf(cparls_ctx *c, int k, const double *lam) {
   const int64_t nt = ceil_div(n, kLevThreads);
   CK(cudaMemsetAsync(&c->md[k]->alpha, 0, sizeof(double), c->st));
   CK(cudaMemsetAsync(&c->md[k]->drawable, 0, sizeof(long long), c->st));
-  k_lev_rows<<<(unsigned)nt, kLevThreads, lev_smem(c->r, c->ld), c->st>>>(
-      c->A[k], n, c->r, c->ld, lam, c->md[k], c->pt[k], c->C[k], c->tile_u64, &c->md[k]->alpha,
-      reinterpret_cast<unsigned long long *>(&c->md[k]->drawable));
+  {
+    const unsigned g = (unsigned)row_grid(c, nt);
+    RSWITCH(c->r, k_lev_rows_t<RM><<<g, kRowThreads, lev_smem(c->r, c->ld), c->st>>>(
+                      c->A[k], n, c->r, c->ld, lam, c->md[k], c->pt[k], c->C[k], c->tile_u64, &c->md[k]->alpha,
+                      reinterpret_cast<unsigned long long *>(&c->md[k]->drawable)));
+  }
   CK_LAUNCH();
   k_scan_u64_single<<<1, kScanThreads, 0, c->st>>>(c->tile_u64, nt);
   CK_LAUNCH();
@@ -227,13 +288,11 @@ void lev_rows_and_cdf(cparls_ctx *c, int k, const double *lam) {
 }
 
 void gram_of_rows(cparls_ctx *c, const double *A, int64_t n, double *G_out) {
-  int64_t grid = std::min<int64_t>(ceil_div(n, kGramTile), c->gpart_blocks);
-  grid = std::max<int64_t>(grid, 1);
-  int64_t rpb = ceil_div(ceil_div(n, grid), kGramTile) * kGramTile;
-  grid = std::max<int64_t>(1, ceil_div(n, rpb));
-  k_gram_rows<<<(unsigned)grid, kGramThreads, 0, c->st>>>(A, n, c->r, c->ld, rpb, c->gpart);
+  const int64_t grid = row_grid(c, ceil_div(n, kRowThreads));
+  RSWITCH(c->r, k_gram_rows_t<RM><<<(unsigned)grid, kRowThreads, gram_smem(c->r, c->ld), c->st>>>(A, n, c->r, c->ld,
+                                                                                                  c->gpart));
   CK_LAUNCH();
-  k_gram_reduce<<<1, 256, 0, c->st>>>(c->gpart, grid, c->r, G_out);
+  k_pairs_reduce<<<pairs_reduce_grid(c->r), 256, 0, c->st>>>(c->gpart, grid, c->r, G_out);
   CK_LAUNCH();
   LAUNCHED(c, 2);
 }
@@ -339,6 +398,34 @@ void build_index_mode(cparls_ctx *c, int k, const IT *coords, const VT *vals) {
   }
   sync(c);
   dfree(c, fids);
+  // hot rows of this mode for the RHS: the kRhsHot rows with most nonzeros
+  {
+    const int64_t n = c->dims[k];
+    const unsigned gn = (unsigned)std::max<int64_t>(1, ceil_div(n, 256));
+    unsigned *deg = dalloc_t<unsigned>(c, n);
+    CK(cudaMemsetAsync(deg, 0, sizeof(unsigned) * n, c->st));
+    if (nnz > 0) {
+      k_row_degree<<<1184, 256, 0, c->st>>>(ix.out, nnz, deg);
+      CK_LAUNCH();
+    }
+    uint32_t *dk0 = dalloc_t<uint32_t>(c, n), *dk1 = dalloc_t<uint32_t>(c, n);
+    uint32_t *dv0 = dalloc_t<uint32_t>(c, n), *dv1 = dalloc_t<uint32_t>(c, n);
+    k_deg_keys<<<gn, 256, 0, c->st>>>(deg, n, dk0, dv0);
+    CK_LAUNCH();
+    cub::DoubleBuffer<uint32_t> hk(dk0, dk1), hv(dv0, dv1);
+    size_t tb2 = 0;
+    CK(cub::DeviceRadixSort::SortPairs(nullptr, tb2, hk, hv, n, 0, 32, c->st));
+    void *tmp2 = dalloc(c, tb2);
+    CK(cub::DeviceRadixSort::SortPairs(tmp2, tb2, hk, hv, n, 0, 32, c->st));
+    c->hot_slot[k] = dalloc_t<int16_t>(c, n);
+    c->hot_row[k] = dalloc_t<int32_t>(c, kRhsHot);
+    CK(cudaMemsetAsync(c->hot_slot[k], 0xFF, sizeof(int16_t) * n, c->st));
+    k_hot_slots<<<1, kRhsHot, 0, c->st>>>(hv.Current(), (int)std::min<int64_t>(n, kRhsHot), c->hot_slot[k],
+                                          c->hot_row[k]);
+    CK_LAUNCH();
+    sync(c);
+    dfree(c, tmp2); dfree(c, deg); dfree(c, dk0); dfree(c, dk1); dfree(c, dv0); dfree(c, dv1);
+  }
   // top-level directory on the high key bits
   int dbits = 1;
   while (dbits < 26 && (int64_t(1) << (dbits + 1)) <= std::max<int64_t>(nnz / 8, 2)) ++dbits;
@@ -697,12 +784,11 @@ void solve_impl(cparls_ctx *c, int k, cparls_solve_info *info) {
   {
     Phase ph(c, &c->stats.ms_gram);
     if (sbar > 0) {
-      int64_t grid = std::min<int64_t>(ceil_div(sbar, kKrpChunk), c->gpart_blocks);
-      int64_t per = ceil_div(ceil_div(sbar, grid), kKrpChunk) * kKrpChunk;
-      grid = ceil_div(sbar, per);
-      k_krp_gram<<<(unsigned)grid, kKrpThreads, 0, c->st>>>(c->skey, c->sw2, sbar, om, r, ld, c->Z, per, c->gpart);
+      const int64_t grid = row_grid(c, ceil_div(sbar, kRowThreads));
+      RSWITCH(r, k_krp_gram_t<RM><<<(unsigned)grid, kRowThreads, krp_smem(r, ld), c->st>>>(c->skey, c->sw2, sbar, om,
+                                                                                             r, ld, c->Z, c->gpart));
       CK_LAUNCH();
-      k_gram_reduce<<<1, 256, 0, c->st>>>(c->gpart, grid, r, c->sd->G);
+      k_pairs_reduce<<<pairs_reduce_grid(r), 256, 0, c->st>>>(c->gpart, grid, r, c->sd->G);
       CK_LAUNCH();
       LAUNCHED(c, 2);
     } else {
@@ -717,27 +803,48 @@ void solve_impl(cparls_ctx *c, int k, cparls_solve_info *info) {
     lookup_impl(c, k);
     ph.end();
   }
-  // K8: sampled RHS
+  // K8: sampled RHS (fp64 red per entry in L2-sized output-row windows; hot
+  // rows privatized per warp)
   {
     Phase ph(c, &c->stats.ms_rhs);
-    const int64_t per_warp = 256;
-    const int grid = 148 * 8;
     if (sbar > 0) {
-      if (c->vf32)
-        k_rhs<float><<<grid, kRhsThreads, 0, c->st>>>(c->off, c->lo, sbar, &c->dv->mk, c->idx[k].out,
-                                                      (const float *)c->idx[k].val, c->sw2, c->Z, r, ld, c->M,
-                                                      c->touched, per_warp);
-      else
-        k_rhs<double><<<grid, kRhsThreads, 0, c->st>>>(c->off, c->lo, sbar, &c->dv->mk, c->idx[k].out,
-                                                       (const double *)c->idx[k].val, c->sw2, c->Z, r, ld, c->M,
-                                                       c->touched, per_warp);
+      const int64_t RW = std::max<int64_t>(1, (int64_t(48) << 20) / ((int64_t)ld * 8));
+      const int nwin = (int)ceil_div(nk, RW);
+      const int64_t nseg = (int64_t)nwin * sbar;
+      if (nseg > c->segcap) {
+        dfree(c, c->seg_lo); dfree(c, c->seg_len); dfree(c, c->seg_off); dfree(c, c->seg_j);
+        dfree(c, c->i64part_seg);
+        c->segcap = nseg;
+        c->seg_lo = dalloc_t<int64_t>(c, nseg);
+        c->seg_len = dalloc_t<int64_t>(c, nseg);
+        c->seg_off = dalloc_t<int64_t>(c, nseg);
+        c->seg_j = dalloc_t<int32_t>(c, nseg);
+        c->i64part_seg = dalloc_t<int64_t>(c, ceil_div(nseg, kScanTile) + 16);
+      }
+      if (nwin == 1) {
+        CK(cudaMemcpyAsync(c->seg_lo, c->lo, 8 * sbar, cudaMemcpyDeviceToDevice, c->st));
+        CK(cudaMemcpyAsync(c->seg_off, c->off, 8 * sbar, cudaMemcpyDeviceToDevice, c->st));
+      } else {
+        k_win_bounds<<<(unsigned)ceil_div(nseg, 256), 256, 0, c->st>>>(c->lo, c->len, sbar, c->idx[k].out, nwin, RW,
+                                                                       c->seg_lo, c->seg_len, c->seg_j);
+        CK_LAUNCH();
+        exclusive_scan_i64(c->seg_len, c->seg_off, nseg, c->i64part_seg, nullptr, c->st);
+        LAUNCHED(c, 4);
+      }
+      CK(cudaMemsetAsync(&c->dv->counter, 0, sizeof(unsigned long long), c->st));
+      const int grid = 148 * 2;
+      const int64_t per_warp = 512;
+#define RHS(VT, HI)                                                                                               \
+  k_rhs<VT, HI><<<grid, kRhsThreads, rhs_smem(r), c->st>>>(c->seg_off, c->seg_lo, nwin > 1 ? c->seg_j : nullptr, nseg, &c->dv->mk,          \
+                                                           &c->dv->counter, c->idx[k].out, (const VT *)c->idx[k].val, \
+                                                           c->sw2, c->Z, c->hot_slot[k], c->hot_row[k],            \
+                                                           rhs_nhot(r), r, ld, c->M, per_warp)
+      if (c->vf32) { if (r > 32) RHS(float, true); else RHS(float, false); }
+      else { if (r > 32) RHS(double, true); else RHS(double, false); }
+#undef RHS
       CK_LAUNCH();
       LAUNCHED(c, 1);
     }
-    CK(cudaMemsetAsync(&c->dv->touched, 0, sizeof(unsigned long long), c->st));
-    k_count_touched<<<296, 256, 0, c->st>>>(c->touched, nk, &c->dv->touched);
-    CK_LAUNCH();
-    LAUNCHED(c, 1);
     ph.end();
   }
   // K9: solve + normalize + leverage refresh
@@ -745,23 +852,18 @@ void solve_impl(cparls_ctx *c, int k, cparls_solve_info *info) {
     Phase ph(c, &c->stats.ms_solve);
     k_solve_prep<<<1, 128, prep_smem(r), c->st>>>(r, c->sd);
     CK_LAUNCH();
-    int64_t nt = ceil_div(nk, kSolveThreads);
-    // partial buffer must hold nt blocks of pairs
-    double *part = c->gpart;
-    if (nt > c->gpart_blocks) part = dalloc_t<double>(c, nt * npairs(r));
-    k_solve_rows<<<(unsigned)nt, kSolveThreads, lev_smem(r, ld), c->st>>>(c->M, nk, r, ld, c->sd, c->A[k], part);
+    const int64_t grid = row_grid(c, ceil_div(nk, kRowThreads));
+    CK(cudaMemsetAsync(&c->dv->touched, 0, sizeof(unsigned long long), c->st));
+    RSWITCH(r, k_solve_rows_t<RM><<<(unsigned)grid, kRowThreads, solve_smem(r, ld), c->st>>>(
+                   c->M, nk, r, ld, c->sd, c->A[k], c->gpart, &c->dv->touched));
     CK_LAUNCH();
-    k_gram_reduce<<<1, 256, 0, c->st>>>(part, nt, r, c->sd->BtB);
+    k_pairs_reduce<<<pairs_reduce_grid(r), 256, 0, c->st>>>(c->gpart, grid, r, c->sd->BtB);
     CK_LAUNCH();
     k_norm_prep<<<1, 128, prep_smem(r), c->st>>>(r, c->sd, c->md[k]);
     CK_LAUNCH();
     LAUNCHED(c, 4);
     lev_rows_and_cdf(c, k, c->sd->lambda);
     CK(cudaMemcpyAsync(c->lam_model, c->sd->lambda, sizeof(double) * r, cudaMemcpyDeviceToDevice, c->st));
-    if (part != c->gpart) {
-      sync(c);
-      dfree(c, part);
-    }
     c->stats.bytes_solve += (double)nk * r * 8.0 * 3;
     ph.end();
   }
@@ -793,19 +895,33 @@ void solve_impl(cparls_ctx *c, int k, cparls_solve_info *info) {
 double fit_impl(cparls_ctx *c) {
   Phase ph(c, &c->stats.ms_fit);
   const int k = c->fit_mode;
-  OtherModes om = other_modes(c, k, false);
+  FitDecode fd{};
+  fd.d = c->D - 1;
+  long double N = 1;
+  for (int m = 0, j = 0; m < c->D; ++m) {
+    if (m == k) continue;
+    fd.n[j] = c->dims[m];
+    fd.inv[j] = 1.0 / (double)c->dims[m];
+    fd.A[j] = c->A[m];
+    N *= (long double)c->dims[m];
+    ++j;
+  }
+  fd.fast = N < 9007199254740992.0L;   // keys < 2^53
   const int nb = 148 * 4;
+  const size_t smem = sizeof(double) * kFitThreads * (size_t)(c->r | 1);
   if (c->vf32)
-    k_fit_inner<float><<<nb, kFitThreads, 0, c->st>>>(c->idx[k].key, c->idx[k].out, (const float *)c->idx[k].val,
-                                                      c->nnz, om, c->A[k], c->lam_model, c->r, c->ld, c->ddpart);
+    RSWITCH(c->r, k_fit_thread<float, RM><<<nb, kFitThreads, smem, c->st>>>(
+                      c->idx[k].key, c->idx[k].out, (const float *)c->idx[k].val, c->nnz, fd, c->A[k], c->lam_model,
+                      c->r, c->ld, c->ddpart));
   else
-    k_fit_inner<double><<<nb, kFitThreads, 0, c->st>>>(c->idx[k].key, c->idx[k].out, (const double *)c->idx[k].val,
-                                                       c->nnz, om, c->A[k], c->lam_model, c->r, c->ld, c->ddpart);
+    RSWITCH(c->r, k_fit_thread<double, RM><<<nb, kFitThreads, smem, c->st>>>(
+                      c->idx[k].key, c->idx[k].out, (const double *)c->idx[k].val, c->nnz, fd, c->A[k], c->lam_model,
+                      c->r, c->ld, c->ddpart));
   CK_LAUNCH();
   FitModes fm{};
   fm.D = c->D;
-  for (int m = 0; m < c->D; ++m) fm.md[m] = c->md[m];
-  k_fit_final<<<1, 32, 0, c->st>>>(c->ddpart, nb, fm, c->lam_model, c->r, c->normX2, c->dv->fit);
+  for (int m = 0; m < c->D; ++m) fm.GA[m] = c->md[m]->GA;
+  k_fit_final<<<1, 256, 0, c->st>>>(c->ddpart, nb, fm, c->lam_model, c->r, c->normX2, c->dv->fit);
   CK_LAUNCH();
   LAUNCHED(c, 2);
   double f = read_dev(c, &c->dv->fit[0]);
@@ -894,8 +1010,8 @@ cparls_status cparls_create(cparls_ctx **out, int32_t nmodes, const int64_t *dim
     CK(cudaMemsetAsync(c->sd, 0, sizeof(SolveDev), c->st));
     c->lam_model = dalloc_t<double>(c, kMaxRank);
     c->ddpart = dalloc_t<dd>(c, 4096);
-    c->gpart_blocks = 148 * 4;
-    c->gpart = dalloc_t<double>(c, c->gpart_blocks * npairs(c->r));
+    c->gpart_blocks = 148 * 2;
+    c->gpart = dalloc_t<double>(c, c->gpart_blocks * (int64_t)c->r * c->r);
     c->Gtmp = dalloc_t<double>(c, kMaxRank * kMaxRank);
     c->tile_u64 = dalloc_t<uint64_t>(c, ceil_div(c->nmax, kLevThreads) + 1);
     c->i64part = dalloc_t<int64_t>(c, ceil_div(c->nmax, kScanTile) + 65536 + 64);
@@ -934,8 +1050,6 @@ cparls_status cparls_create(cparls_ctx **out, int32_t nmodes, const int64_t *dim
     }
     c->M = dalloc_t<double>(c, c->nmax * c->ld);
     CK(cudaMemsetAsync(c->M, 0, sizeof(double) * c->nmax * c->ld, c->st));
-    c->touched = dalloc_t<uint8_t>(c, c->nmax);
-    CK(cudaMemsetAsync(c->touched, 0, c->nmax, c->st));
     // DIDX candidate buffers (n_m each, worst case)
     int64_t cc = c->nmax;
     for (int m = 0; m < nmodes; ++m) {
@@ -951,11 +1065,33 @@ cparls_status cparls_create(cparls_ctx **out, int32_t nmodes, const int64_t *dim
     c->akey = dalloc_t<uint64_t>(c, c->acap);
     c->ap = dalloc_t<double>(c, c->acap);
     alloc_sample_buffers(c, 1 << 17);
-    // fit streams the mode whose sorted copy has the most repeated keys: use
-    // the mode with the largest n_k (longest fibers on average)
-    c->fit_mode = 0;
-    for (int m = 1; m < nmodes; ++m)
-      if (c->dims[m] > c->dims[c->fit_mode]) c->fit_mode = m;
+    // fit streams the mode copy with the fewest fibers (longest runs of equal
+    // keys: most reuse of the fiber vector h), ties -> smaller n_k
+    for (int m = 0; m < nmodes; ++m) {
+      CK(cudaMemsetAsync(&c->dv->counter, 0, sizeof(unsigned long long), c->st));
+      if (c->nnz > 0) {
+        k_count_fibers<<<592, 256, 0, c->st>>>(c->idx[m].key, c->nnz, &c->dv->counter);
+        CK_LAUNCH();
+      }
+      c->nfib[m] = (int64_t)read_dev(c, &c->dv->counter);
+    }
+    // per nonzero one A_{k*} row; per fiber one A_{m_1} row (m_1 = fastest key
+    // mode); expected miss traffic grows with the factor sizes
+    {
+      double best = 0;
+      for (int m = 0; m < nmodes; ++m) {
+        const int m1 = (m == 0) ? 1 : 0;
+        const double cost = (double)c->nnz * (double)c->dims[m] + (double)c->nfib[m] * (double)c->dims[m1];
+        if (m == 0 || cost < best) { best = cost; c->fit_mode = m; }
+      }
+    }
+    if (getenv("CPARLS_DEBUG")) {
+      for (int m = 0; m < nmodes; ++m)
+        fprintf(stderr, "[cparls] mode %d: n=%lld fibers=%lld (avg len %.2f) dir_buckets=%lld\n", m,
+                (long long)c->dims[m], (long long)c->nfib[m], c->nfib[m] ? (double)c->nnz / c->nfib[m] : 0.0,
+                (long long)c->idx[m].nbkt);
+      fprintf(stderr, "[cparls] fit mode %d\n", c->fit_mode);
+    }
     reset_lambda(c);
     for (int k = 0; k < nmodes; ++k) leverage_full(c, k);
     sync(c);

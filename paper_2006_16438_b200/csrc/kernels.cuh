@@ -202,150 +202,9 @@ __device__ void lev_prep_body(int r, const double *Gg, ModeDev *md) {
 __global__ void k_lev_prep(int r, const double *G, ModeDev *md) { lev_prep_body(r, G, md); }
 
 // ======================================================================
-// Gram of rows (optionally pairs-only partials per block)
-// ======================================================================
-// Block partial of sum_i a_i^T a_i over rows [blk*rows_per_block, ...).
-// Rows staged in smem tiles of 32 rows; thread t owns pairs t, t+256, ...
-constexpr int kGramThreads = 256;
-constexpr int kGramTile = 32;
-
-__global__ void __launch_bounds__(kGramThreads) k_gram_rows(const double *__restrict__ A, int64_t n, int r, int ld,
-                                                           int64_t rows_per_block, double *__restrict__ part) {
-  __shared__ double tile[kGramTile][kMaxRank + 1];
-  __shared__ int pp[npairs(kMaxRank)], qq[npairs(kMaxRank)];
-  const int P = npairs(r);
-  if (threadIdx.x == 0) {
-    int t = 0;
-    for (int p = 0; p < r; ++p)
-      for (int q = p; q < r; ++q, ++t) { pp[t] = p; qq[t] = q; }
-  }
-  double acc[9];
-#pragma unroll
-  for (int i = 0; i < 9; ++i) acc[i] = 0.0;
-  int64_t r0 = (int64_t)blockIdx.x * rows_per_block;
-  int64_t r1 = min(n, r0 + rows_per_block);
-  __syncthreads();
-  for (int64_t base = r0; base < r1; base += kGramTile) {
-    int rows = (int)min((int64_t)kGramTile, r1 - base);
-    for (int i = threadIdx.x; i < rows * r; i += blockDim.x) {
-      int row = i / r, c = i % r;
-      tile[row][c] = A[(base + row) * ld + c];
-    }
-    __syncthreads();
-#pragma unroll
-    for (int i = 0; i < 9; ++i) {
-      int t = threadIdx.x + i * kGramThreads;
-      if (t < P) {
-        int p = pp[t], q = qq[t];
-        double s = 0.0;
-        for (int row = 0; row < rows; ++row) s += tile[row][p] * tile[row][q];
-        acc[i] += s;
-      }
-    }
-    __syncthreads();
-  }
-#pragma unroll
-  for (int i = 0; i < 9; ++i) {
-    int t = threadIdx.x + i * kGramThreads;
-    if (t < P) part[(int64_t)blockIdx.x * P + t] = acc[i];
-  }
-}
-
-// Sum block partials (fixed order, compensated) into a full symmetric r x r.
-__global__ void k_gram_reduce(const double *__restrict__ part, int64_t nblocks, int r, double *__restrict__ G) {
-  const int P = npairs(r);
-  for (int t = threadIdx.x; t < P; t += blockDim.x) {
-    int p = 0, rem = t;
-    while (rem >= r - p) { rem -= r - p; ++p; }
-    int q = p + rem;
-    dd s = {0.0, 0.0};
-    for (int64_t b = 0; b < nblocks; ++b) s = dd_add_d(s, part[b * P + t]);
-    double v = s.hi + s.lo;
-    G[p * r + q] = v;
-    G[q * r + p] = v;
-  }
-}
-
-// ======================================================================
 // K1/K2: leverage rows -> p~ -> integer weights q (CDF pass 1)
 // ======================================================================
 constexpr int kLevThreads = 256;
-
-// One row per thread; rows staged through smem (stride ld+1, conflict-free).
-// If lam != nullptr, a_i := b_i / lam (column normalization, P:925-926,
-// AMB-13) is written back to A.  Writes p~ (=l/rank), C[i] = q_i (temporary),
-// per-block sum of q, alpha (atomic max), drawable count.
-__global__ void __launch_bounds__(kLevThreads) k_lev_rows(double *__restrict__ A, int64_t n, int r, int ld,
-                                                         const double *__restrict__ lam, const ModeDev *__restrict__ md,
-                                                         double *__restrict__ pt, uint64_t *__restrict__ C,
-                                                         uint64_t *__restrict__ tile_sum, double *alpha_out,
-                                                         unsigned long long *drawable_out) {
-  extern __shared__ double smem[];
-  double *W = smem;                       // r*r
-  double *tile = smem + r * r;            // kLevThreads x (ld+1)
-  const int S = ld + 1;
-  const int tri = md->tri;
-  const int rank = md->rank;
-  for (int i = threadIdx.x; i < r * r; i += blockDim.x) W[i] = md->W[i];
-  int64_t base = (int64_t)blockIdx.x * kLevThreads;
-  int rows = (int)min((int64_t)kLevThreads, n - base);
-  const double *src = A + base * ld;
-  for (int i = threadIdx.x; i < rows * ld; i += blockDim.x) {
-    int row = i / ld, c = i - row * ld;
-    double v = src[i];
-    if (lam != nullptr && c < r) {
-      double l = lam[c];
-      v = l > 0.0 ? v / l : 0.0;
-    }
-    tile[row * S + c] = v;
-  }
-  __syncthreads();
-  if (lam != nullptr) {
-    double *dst = A + base * ld;
-    for (int i = threadIdx.x; i < rows * ld; i += blockDim.x) {
-      int row = i / ld, c = i - row * ld;
-      dst[i] = tile[row * S + c];
-    }
-  }
-  uint64_t q = 0;
-  double p = 0.0;
-  if (threadIdx.x < rows) {
-    const double *a = tile + threadIdx.x * S;
-    double l = 0.0;
-    if (rank > 0) {
-      for (int c = 0; c < r; ++c) {
-        double t = 0.0;
-        int pe = tri ? c + 1 : r;
-        for (int k = 0; k < pe; ++k) t += a[k] * W[k * r + c];
-        l += t * t;
-      }
-      p = l / (double)rank;
-    }
-    q = __double2ull_rn(p * kTwo62);
-    int64_t i = base + threadIdx.x;
-    pt[i] = p;
-    C[i] = q;
-  }
-  // block reductions: sum q, max p, drawable
-  unsigned long long qs = warp_sum<unsigned long long>(q);
-  double pm = p;
-#pragma unroll
-  for (int m = 16; m >= 1; m >>= 1) pm = fmax(pm, __shfl_xor_sync(0xffffffffu, pm, m));
-  unsigned dr = __popc(__ballot_sync(0xffffffffu, threadIdx.x < rows && p > 1.0842021724855044e-19));
-  __shared__ unsigned long long wq[kLevThreads / 32];
-  __shared__ double wp[kLevThreads / 32];
-  __shared__ unsigned wd[kLevThreads / 32];
-  int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  if (lane == 0) { wq[w] = qs; wp[w] = pm; wd[w] = dr; }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    unsigned long long s = 0; double m = 0.0; unsigned long long d = 0;
-    for (int i = 0; i < kLevThreads / 32; ++i) { s += wq[i]; m = fmax(m, wp[i]); d += wd[i]; }
-    tile_sum[blockIdx.x] = s;
-    atomic_max_nonneg(alpha_out, m);
-    atomicAdd(drawable_out, d);
-  }
-}
 
 // CDF pass 3: C[i] = offset(tile) + inclusive scan of q within tile.
 __global__ void __launch_bounds__(kLevThreads) k_cdf_final(uint64_t *__restrict__ C, int64_t n,
@@ -682,82 +541,6 @@ __global__ void k_cidx_emit(unsigned long long *__restrict__ hkey, uint32_t *__r
 }
 
 // ======================================================================
-// K6 KrpSamp + sampled Gram
-// ======================================================================
-constexpr int kKrpThreads = 256;
-constexpr int kKrpChunk = 32;
-
-// z_j = A_{m_1}(i_1,:) * ... * A_{m_d}(i_d,:) (eq:Zrow, left to right).
-// Writes Z[j*ld + c]; accumulates block partials of sum_j w2_j z_j z_j^T.
-__global__ void __launch_bounds__(kKrpThreads) k_krp_gram(const uint64_t *__restrict__ skey,
-                                                         const double *__restrict__ sw2, int64_t sbar, OtherModes om,
-                                                         int r, int ld, double *__restrict__ Z,
-                                                         int64_t per_block, double *__restrict__ part) {
-  __shared__ double zs[kKrpChunk][kMaxRank + 1];
-  __shared__ double ws[kKrpChunk];
-  __shared__ int pp[npairs(kMaxRank)], qq[npairs(kMaxRank)];
-  const int P = npairs(r);
-  if (threadIdx.x == 0) {
-    int t = 0;
-    for (int p = 0; p < r; ++p)
-      for (int q = p; q < r; ++q, ++t) { pp[t] = p; qq[t] = q; }
-  }
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  double acc[9];
-#pragma unroll
-  for (int i = 0; i < 9; ++i) acc[i] = 0.0;
-  int64_t j0 = (int64_t)blockIdx.x * per_block, j1 = min(sbar, j0 + per_block);
-  __syncthreads();
-  for (int64_t base = j0; base < j1; base += kKrpChunk) {
-    int cnt = (int)min((int64_t)kKrpChunk, j1 - base);
-    for (int jj = w; jj < cnt; jj += kKrpThreads / 32) {
-      int64_t j = base + jj;
-      uint64_t key = skey[j];
-      double z0 = 1.0, z1 = 1.0;
-      for (int m = 0; m < om.d; ++m) {
-        uint64_t i = key % (uint64_t)om.n[m];
-        key /= (uint64_t)om.n[m];
-        const double *row = om.A[m] + i * ld;
-        if (lane < r) {
-          double a = __ldg(row + lane);
-          z0 = (m == 0) ? a : z0 * a;
-        }
-        if (lane + 32 < r) {
-          double a = __ldg(row + lane + 32);
-          z1 = (m == 0) ? a : z1 * a;
-        }
-      }
-      if (lane < r) {
-        zs[jj][lane] = z0;
-        Z[j * ld + lane] = z0;
-      }
-      if (lane + 32 < r) {
-        zs[jj][lane + 32] = z1;
-        Z[j * ld + lane + 32] = z1;
-      }
-      if (lane == 0) ws[jj] = sw2[j];
-    }
-    __syncthreads();
-#pragma unroll
-    for (int i = 0; i < 9; ++i) {
-      int t = threadIdx.x + i * kKrpThreads;
-      if (t < P) {
-        int p = pp[t], q = qq[t];
-        double s = 0.0;
-        for (int jj = 0; jj < cnt; ++jj) s += (ws[jj] * zs[jj][p]) * zs[jj][q];
-        acc[i] += s;
-      }
-    }
-    __syncthreads();
-  }
-#pragma unroll
-  for (int i = 0; i < 9; ++i) {
-    int t = threadIdx.x + i * kKrpThreads;
-    if (t < P) part[(int64_t)blockIdx.x * P + t] = acc[i];
-  }
-}
-
-// ======================================================================
 // K7 TnsrSamp lookup: equal_range of each sampled key in the
 // mode-k sorted keys, narrowed by the top-level directory.
 // ======================================================================
@@ -789,65 +572,6 @@ __global__ void k_lookup(const uint64_t *__restrict__ skey, int64_t sbar, const 
   }
   lo_out[j] = L;
   len_out[j] = U - L;
-}
-
-// ======================================================================
-// K8 sampled RHS: M(out_e,:) += w2_j x_e z_j over matched nonzeros
-// ======================================================================
-constexpr int kRhsThreads = 256;
-
-template <typename VT>
-__global__ void __launch_bounds__(kRhsThreads) k_rhs(const int64_t *__restrict__ off, const int64_t *__restrict__ lo,
-                                                    int64_t sbar, const int64_t *__restrict__ mk_ptr,
-                                                    const int32_t *__restrict__ outidx, const VT *__restrict__ vals,
-                                                    const double *__restrict__ sw2, const double *__restrict__ Z,
-                                                    int r, int ld, double *__restrict__ M,
-                                                    uint8_t *__restrict__ touched, int64_t per_warp) {
-  const int64_t mk = *mk_ptr;
-  const int lane = threadIdx.x & 31;
-  const int64_t wid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t t0 = wid * per_warp; t0 < mk; t0 += nw * per_warp) {
-    const int64_t t1 = min(mk, t0 + per_warp);
-    // sample containing entry t0: last j with off[j] <= t0 (skips empty fibers)
-    int64_t a = 0, len = sbar;
-    while (len > 0) {
-      int64_t half = len >> 1;
-      if (__ldg(off + a + half) <= t0) { a += half + 1; len -= half + 1; }
-      else len = half;
-    }
-    int64_t jcur = a - 1;       // sample of the first entry of the current 32-group
-    int64_t jz = -1;            // sample whose (w2, z) are loaded
-    double coefw = 0.0, z = 0.0, z1 = 0.0;
-    for (int64_t t = t0; t < t1; t += 32) {
-      const int64_t tt = t + lane;
-      int64_t jj = jcur;
-      while (jj + 1 < sbar && __ldg(off + jj + 1) <= tt) ++jj;
-      int32_t o_l = 0;
-      double x_l = 0.0;
-      if (tt < t1) {
-        int64_t e = __ldg(lo + jj) + (tt - __ldg(off + jj));
-        o_l = __ldg(outidx + e);
-        x_l = (double)__ldg(vals + e);
-      }
-      const int cnt = (int)min((int64_t)32, t1 - t);
-      for (int u = 0; u < cnt; ++u) {
-        const int32_t o = __shfl_sync(0xffffffffu, o_l, u);
-        const double x = __shfl_sync(0xffffffffu, x_l, u);
-        const int64_t ju = __shfl_sync(0xffffffffu, jj, u);
-        if (ju != jz) {
-          jz = ju;
-          coefw = __ldg(sw2 + ju);
-          z = lane < r ? __ldg(Z + ju * ld + lane) : 0.0;
-          z1 = lane + 32 < r ? __ldg(Z + ju * ld + lane + 32) : 0.0;
-        }
-        if (lane < r) atomicAdd(M + (int64_t)o * ld + lane, (coefw * x) * z);
-        if (lane + 32 < r) atomicAdd(M + (int64_t)o * ld + lane + 32, (coefw * x) * z1);
-        if (lane == 0) touched[o] = 1;
-      }
-      jcur = __shfl_sync(0xffffffffu, jj, 31);
-    }
-  }
 }
 
 // ======================================================================
@@ -903,66 +627,6 @@ __global__ void k_solve_prep(int r, SolveDev *sd) {
   }
 }
 
-// B_i = M_i Ginv for every row (rows with M = 0 give B = 0); M is zeroed
-// after reading (ready for the next RHS).  Block partials of B^T B.
-constexpr int kSolveThreads = 256;
-__global__ void __launch_bounds__(kSolveThreads) k_solve_rows(double *__restrict__ M, int64_t n, int r, int ld,
-                                                             const SolveDev *__restrict__ sd, double *__restrict__ B,
-                                                             double *__restrict__ part) {
-  extern __shared__ double smem[];
-  double *Gi = smem;                  // r*r
-  double *tile = smem + r * r;        // kSolveThreads x (ld+1)
-  __shared__ int pp[npairs(kMaxRank)], qq[npairs(kMaxRank)];
-  const int S = ld + 1;
-  const int P = npairs(r);
-  for (int i = threadIdx.x; i < r * r; i += blockDim.x) Gi[i] = sd->Ginv[i];
-  if (threadIdx.x == 0) {
-    int t = 0;
-    for (int p = 0; p < r; ++p)
-      for (int q = p; q < r; ++q, ++t) { pp[t] = p; qq[t] = q; }
-  }
-  int64_t base = (int64_t)blockIdx.x * kSolveThreads;
-  int rows = (int)min((int64_t)kSolveThreads, n - base);
-  double *msrc = M + base * ld;
-  for (int i = threadIdx.x; i < rows * ld; i += blockDim.x) {
-    int row = i / ld, c = i - row * ld;
-    tile[row * S + c] = msrc[i];
-    msrc[i] = 0.0;
-  }
-  __syncthreads();
-  double out[kMaxRank];
-  if (threadIdx.x < rows) {
-    double *m = tile + threadIdx.x * S;
-    bool nz = false;
-    for (int p = 0; p < r; ++p) nz |= (m[p] != 0.0);
-    for (int c = 0; c < r; ++c) out[c] = 0.0;
-    if (nz) {
-      for (int p = 0; p < r; ++p) {
-        double mp = m[p];
-        for (int c = 0; c < r; ++c) out[c] += mp * Gi[p * r + c];
-      }
-    }
-  }
-  __syncthreads();
-  if (threadIdx.x < rows) {
-    double *m = tile + threadIdx.x * S;
-    for (int c = 0; c < r; ++c) m[c] = out[c];
-  }
-  __syncthreads();
-  double *bdst = B + base * ld;
-  for (int i = threadIdx.x; i < rows * ld; i += blockDim.x) {
-    int row = i / ld, c = i - row * ld;
-    bdst[i] = c < r ? tile[row * S + c] : 0.0;
-  }
-  // B^T B partial over this tile
-  for (int t = threadIdx.x; t < P; t += blockDim.x) {
-    int p = pp[t], q = qq[t];
-    double s = 0.0;
-    for (int row = 0; row < rows; ++row) s += tile[row * S + p] * tile[row * S + q];
-    part[(int64_t)blockIdx.x * P + t] = s;
-  }
-}
-
 // lambda_c = ||B(:,c)||, G_A = B^T B / (lambda lambda^T), then the
 // leverage preparation of the normalized factor.
 __global__ void k_norm_prep(int r, SolveDev *sd, ModeDev *md) {
@@ -977,75 +641,6 @@ __global__ void k_norm_prep(int r, SolveDev *sd, ModeDev *md) {
   }
   __syncthreads();
   lev_prep_body(r, GA, md);
-}
-
-// ======================================================================
-// K10 exact fit: <X, M> streamed over mode-k* sorted copy
-// ======================================================================
-constexpr int kFitThreads = 256;
-
-template <typename VT>
-__global__ void __launch_bounds__(kFitThreads) k_fit_inner(const uint64_t *__restrict__ keys,
-                                                          const int32_t *__restrict__ outidx,
-                                                          const VT *__restrict__ vals, int64_t nnz, OtherModes om,
-                                                          const double *__restrict__ Ak, const double *__restrict__ lam,
-                                                          int r, int ld, dd *__restrict__ part) {
-  __shared__ double lam_s[kMaxRank];
-  for (int c = threadIdx.x; c < r; c += blockDim.x) lam_s[c] = lam[c];
-  __syncthreads();
-  dd acc = {0.0, 0.0};
-  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < nnz; e += (int64_t)gridDim.x * blockDim.x) {
-    uint64_t key = keys[e];
-    const double *rows[kMaxModes];
-    for (int m = 0; m < om.d; ++m) {
-      uint64_t i = key % (uint64_t)om.n[m];
-      key /= (uint64_t)om.n[m];
-      rows[m] = om.A[m] + i * ld;
-    }
-    const double *ak = Ak + (int64_t)outidx[e] * ld;
-    double mv = 0.0;
-    for (int c = 0; c < r; ++c) {
-      double t = lam_s[c] * __ldg(ak + c);
-      for (int m = 0; m < om.d; ++m) t *= __ldg(rows[m] + c);
-      mv += t;
-    }
-    acc = dd_add_d(acc, (double)vals[e] * mv);
-  }
-  acc = warp_sum_dd(acc);
-  __shared__ dd ws[kFitThreads / 32];
-  int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  if (lane == 0) ws[w] = acc;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    dd t = {0.0, 0.0};
-    for (int i = 0; i < kFitThreads / 32; ++i) t = dd_add(t, ws[i]);
-    part[blockIdx.x] = t;
-  }
-}
-
-struct FitModes {
-  int D;
-  const ModeDev *md[kMaxModes];
-};
-
-__global__ void k_fit_final(const dd *__restrict__ part, int nb, FitModes fm, const double *__restrict__ lam, int r,
-                            double normX2, double *out) {
-  if (threadIdx.x != 0) return;
-  dd inner = {0.0, 0.0};
-  for (int i = 0; i < nb; ++i) inner = dd_add(inner, part[i]);
-  dd nm = {0.0, 0.0};
-  for (int p = 0; p < r; ++p)
-    for (int q = 0; q < r; ++q) {
-      double h = lam[p] * lam[q];
-      for (int m = 0; m < fm.D; ++m) h *= fm.md[m]->GA[p * r + q];
-      nm = dd_add_d(nm, h);
-    }
-  double in = inner.hi + inner.lo;
-  double resid2 = normX2 - 2.0 * in + (nm.hi + nm.lo);
-  if (resid2 < 0.0) resid2 = 0.0;
-  out[0] = 1.0 - sqrt(resid2) / sqrt(normX2);
-  out[1] = in;
-  out[2] = nm.hi + nm.lo;
 }
 
 // ======================================================================
@@ -1130,17 +725,6 @@ __global__ void k_sumsq(const VT *__restrict__ v, int64_t n, dd *__restrict__ pa
   }
 }
 
-// count of touched rows (bytes) and reset of the flags
-__global__ void k_count_touched(uint8_t *__restrict__ f, int64_t n, unsigned long long *cnt) {
-  unsigned long long c = 0;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    c += f[i];
-    f[i] = 0;
-  }
-  c = warp_sum<unsigned long long>(c);
-  if ((threadIdx.x & 31) == 0 && c) atomicAdd(cnt, c);
-}
-
 // gather matched (out, val) of all samples in current sample order
 template <typename VT>
 __global__ void k_gather_fibers(const int64_t *__restrict__ off, const int64_t *__restrict__ lo,
@@ -1155,3 +739,7 @@ __global__ void k_gather_fibers(const int64_t *__restrict__ off, const int64_t *
 }
 
 }  // namespace cparls
+
+#include "rows.cuh"
+#include "rhs.cuh"
+#include "fit.cuh"

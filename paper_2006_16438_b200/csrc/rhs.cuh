@@ -1,0 +1,167 @@
+// rhs.cuh -- K8 sampled right-hand side M = Xs^T diag(w^2) Z_S (P:949-958,
+// AMB-14): M(out_e,:) += w_j^2 x_e z_j for every matched nonzero e of every
+// sampled fiber j.
+//
+// Warps walk the concatenated matched entries (fiber after fiber, so z_j and
+// w_j^2 stay in registers across a fiber); lanes = columns, so one entry is one
+// r-wide fp64 reduction into M's row.  Global fp64 `red` runs at the SM's
+// atomic issue rate (~0.8 lane-ops/cycle/SM; sm_100a has no f64 vector red),
+// which bounds this kernel.  Zipf heads concentrate the entries on a few
+// output rows, so the top kRhsHot rows of mode k (by nonzero count, chosen at
+// index build) are accumulated in warp-private shared-memory rows instead and
+// flushed with one red per (warp, row, column) at the end.
+//
+// M (n_k x ld fp64) is far larger than L2 for the big modes, so random reds
+// would each be a DRAM read-modify-write.  The entries are therefore visited
+// in output-row windows of ~48 MB of M: each fiber is sorted by output row, so
+// its entries inside window w are the sub-range found by k_win_bounds; the
+// (window, fiber) segments are concatenated window-major and warps take
+// chunks from a global counter, so the rows being reduced stay in L2.
+#pragma once
+#include <algorithm>
+
+#include "common.cuh"
+
+namespace cparls {
+
+constexpr int kRhsThreads = 256;
+constexpr int kRhsWarps = kRhsThreads / 32;
+constexpr int kRhsHot = 64;   // privatized hot rows per warp
+
+template <typename VT, bool HI>
+__global__ void __launch_bounds__(kRhsThreads) k_rhs(const int64_t *__restrict__ off, const int64_t *__restrict__ lo,
+                                                    const int32_t *__restrict__ seg_j, int64_t nseg,
+                                                    const int64_t *__restrict__ mk_ptr,
+                                                    unsigned long long *__restrict__ work,
+                                                    const int32_t *__restrict__ outidx, const VT *__restrict__ vals,
+                                                    const double *__restrict__ sw2, const double *__restrict__ Z,
+                                                    const int16_t *__restrict__ hot_slot,
+                                                    const int32_t *__restrict__ hot_row, int nhot, int r, int ld,
+                                                    double *__restrict__ M, int64_t per_warp) {
+  extern __shared__ double priv[];   // kRhsWarps x nhot x r
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  double *mine = priv + (size_t)w * nhot * r;
+  for (int i = threadIdx.x; i < kRhsWarps * nhot * r; i += blockDim.x) priv[i] = 0.0;
+  __syncthreads();
+  const int64_t mk = *mk_ptr;
+  while (true) {
+    int64_t t0 = 0;
+    if (lane == 0) t0 = (int64_t)atomicAdd(work, (unsigned long long)per_warp);
+    t0 = __shfl_sync(0xffffffffu, t0, 0);
+    if (t0 >= mk) break;
+    const int64_t t1 = min(mk, t0 + per_warp);
+    // segment containing entry t0: last g with off[g] <= t0 (skips empty ones)
+    int64_t a = 0, len = nseg;
+    while (len > 0) {
+      int64_t half = len >> 1;
+      if (__ldg(off + a + half) <= t0) { a += half + 1; len -= half + 1; }
+      else len = half;
+    }
+    int64_t jcur = a - 1;   // segment of the first entry of the current 32-group
+    int64_t jz = -1;        // sample whose (w^2, z) are loaded
+    double coefw = 0.0, z0 = 0.0, z1 = 0.0;
+    for (int64_t t = t0; t < t1; t += 32) {
+      const int64_t tt = t + lane;
+      int64_t jj = jcur;
+      while (jj + 1 < nseg && __ldg(off + jj + 1) <= tt) ++jj;
+      int32_t o_l = 0;
+      int s_l = -1;
+      double x_l = 0.0;
+      int64_t j_l = 0;
+      if (tt < t1) {
+        j_l = seg_j ? (int64_t)__ldg(seg_j + jj) : jj;
+        const int64_t e = __ldg(lo + jj) + (tt - __ldg(off + jj));
+        o_l = __ldg(outidx + e);
+        x_l = (double)__ldg(vals + e);
+        s_l = __ldg(hot_slot + o_l);
+        if (s_l >= nhot) s_l = -1;
+      }
+      const int cnt = (int)min((int64_t)32, t1 - t);
+      for (int u = 0; u < cnt; ++u) {
+        const int32_t o = __shfl_sync(0xffffffffu, o_l, u);
+        const double x = __shfl_sync(0xffffffffu, x_l, u);
+        const int s = __shfl_sync(0xffffffffu, s_l, u);
+        const int64_t ju = __shfl_sync(0xffffffffu, j_l, u);   // sample of the entry
+        if (ju != jz) {
+          jz = ju;
+          coefw = __ldg(sw2 + ju);
+          z0 = lane < r ? __ldg(Z + ju * ld + lane) : 0.0;
+          if (HI) z1 = lane + 32 < r ? __ldg(Z + ju * ld + lane + 32) : 0.0;
+        }
+        const double cx = coefw * x;
+        if (s >= 0) {   // hot row: warp-private shared accumulator, no atomics
+          if (lane < r) mine[s * r + lane] += cx * z0;
+          if (HI && lane + 32 < r) mine[s * r + lane + 32] += cx * z1;
+        } else {
+          if (lane < r) atomicAdd(M + (int64_t)o * ld + lane, cx * z0);
+          if (HI && lane + 32 < r) atomicAdd(M + (int64_t)o * ld + lane + 32, cx * z1);
+        }
+      }
+      jcur = __shfl_sync(0xffffffffu, jj, 31);
+    }
+  }
+  __syncwarp();
+  for (int s = 0; s < nhot; ++s) {
+    const int row = hot_row[s];
+    if (row < 0) break;
+    for (int c = lane; c < r; c += 32) {
+      const double v = mine[s * r + c];
+      if (v != 0.0) atomicAdd(M + (int64_t)row * ld + c, v);
+    }
+  }
+}
+
+// privatized rows per warp that fit ~200 KB of shared memory
+inline int rhs_nhot(int r) { return std::min(kRhsHot, (int)(200 * 1024 / (sizeof(double) * kRhsWarps * r))); }
+// For every (window w, sample j): the sub-range of fiber j whose output rows
+// fall in [w*RW, (w+1)*RW) (fibers are sorted by output row).
+__global__ void k_win_bounds(const int64_t *__restrict__ lo, const int64_t *__restrict__ len, int64_t sbar,
+                             const int32_t *__restrict__ outidx, int nwin, int64_t RW,
+                             int64_t *__restrict__ seg_lo, int64_t *__restrict__ seg_len,
+                             int32_t *__restrict__ seg_j) {
+  const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= (int64_t)nwin * sbar) return;
+  const int w = (int)(g / sbar);
+  const int64_t j = g - (int64_t)w * sbar;
+  const int64_t f0 = lo[j], f1 = f0 + len[j];
+  auto lb = [&](int64_t o) {   // first e in [f0, f1) with outidx[e] >= o
+    int64_t a = f0, n = f1 - f0;
+    while (n > 0) {
+      int64_t h = n >> 1;
+      if (__ldg(outidx + a + h) < o) { a += h + 1; n -= h + 1; }
+      else n = h;
+    }
+    return a;
+  };
+  const int64_t b0 = (w == 0) ? f0 : lb((int64_t)w * RW);
+  const int64_t b1 = (w == nwin - 1) ? f1 : lb((int64_t)(w + 1) * RW);
+  seg_lo[g] = b0;
+  seg_len[g] = b1 - b0;
+  seg_j[g] = (int32_t)j;
+}
+
+inline size_t rhs_smem(int r) { return sizeof(double) * (size_t)kRhsWarps * rhs_nhot(r) * r; }
+
+// ---- hot rows (index build): nonzero count per mode-k row ---------------------
+__global__ void k_row_degree(const int32_t *__restrict__ outidx, int64_t nnz, unsigned *__restrict__ deg) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nnz; i += (int64_t)gridDim.x * blockDim.x)
+    atomicAdd(deg + outidx[i], 1u);
+}
+
+__global__ void k_deg_keys(const unsigned *__restrict__ deg, int64_t n, uint32_t *__restrict__ key,
+                           uint32_t *__restrict__ row) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) { key[i] = ~deg[i]; row[i] = (uint32_t)i; }   // ascending ~deg = descending degree
+}
+
+__global__ void k_hot_slots(const uint32_t *__restrict__ sorted_rows, int nhot, int16_t *__restrict__ hot_slot,
+                            int32_t *__restrict__ hot_row) {
+  const int s = threadIdx.x;
+  if (s < kRhsHot) {
+    const int row = s < nhot ? (int)sorted_rows[s] : -1;
+    hot_row[s] = row;
+    if (row >= 0) hot_slot[row] = (int16_t)s;
+  }
+}
+
+}  // namespace cparls

@@ -210,22 +210,46 @@ def _draw_coords(first: int, count: int, cdfs, perms, seed: int, device):
     return out
 
 
-def _select_first_unique(keys: torch.Tensor, target: int):
-    """The `target` distinct keys with the earliest first occurrence, in that
-    order.  Returns None if fewer than target distinct keys exist."""
-    sk, pos = torch.sort(keys, stable=True)
-    first = torch.ones_like(sk, dtype=torch.bool)
-    first[1:] = sk[1:] != sk[:-1]
-    del sk
-    upos = pos[first]
-    del pos, first
-    if upos.numel() < target:
+_NB = 8           # dedup buckets (key & 7): keeps every sort below torch's INT_MAX limit
+_CH = 1 << 30     # scan chunk for first-occurrence selection
+
+
+def _first_unique_positions(parts, total, target, device):
+    """Positions (ascending) of the first `target` distinct keys by first
+    occurrence, from draw-ordered key chunks.  Returns None if fewer exist."""
+    first = torch.zeros(total, dtype=torch.bool, device=device)
+    for b in range(_NB):
+        ks, ps = [], []
+        base = 0
+        for k in parts:
+            m = (k & (_NB - 1)) == b
+            ks.append(k[m])
+            ps.append(torch.nonzero(m).squeeze(1) + base)
+            base += k.numel()
+        kb = torch.cat(ks)
+        pb = torch.cat(ps)
+        del ks, ps
+        if kb.numel() == 0:
+            continue
+        sk, order = torch.sort(kb, stable=True)
+        f = torch.ones_like(sk, dtype=torch.bool)
+        f[1:] = sk[1:] != sk[:-1]
+        first[pb[order[f]]] = True
+        del kb, pb, sk, order, f
+    out, have = [], 0
+    for c0 in range(0, total, _CH):
+        idx = torch.nonzero(first[c0:c0 + _CH]).squeeze(1) + c0
+        take = min(idx.numel(), target - have)
+        out.append(idx[:take])
+        have += take
+        if have >= target:
+            break
+    if have < target:
         return None
-    upos, _ = torch.sort(upos)
-    return keys[upos[:target]]
+    return torch.cat(out)
 
 
-def generate_coords(cfg: Config, device="cpu", chunk: int = 1 << 27) -> torch.Tensor:
+def generate_coords(cfg: Config, device="cpu", chunk: int = 1 << 27, out_dtype=torch.int64) -> torch.Tensor:
     """nnz x D int64 coordinates (0-based), distinct, in first-draw order."""
     dims = cfg.dims
     D = len(dims)
@@ -250,15 +274,25 @@ def generate_coords(cfg: Config, device="cpu", chunk: int = 1 << 27) -> torch.Te
             parts.append(_pack(cs, dims, lo_bits))
             del cs
             drawn += cnt
-        keys = torch.cat(parts) if len(parts) > 1 else parts[0]
-        parts = [keys]
-        sel = _select_first_unique(keys, target)
-        if sel is not None:
+        pos = _first_unique_positions(parts, drawn, target, device)
+        if pos is not None:
             break
         total = int(total * 1.25) + 1024
-    del parts, keys
-    cs = _unpack(sel, dims, lo_bits)
-    return torch.stack(cs, dim=1)
+    # gather the selected keys chunk by chunk (positions ascending)
+    sel = torch.empty(target, dtype=torch.int64, device=device)
+    base = 0
+    for k in parts:
+        n = k.numel()
+        lo_i = torch.searchsorted(pos, torch.tensor([base, base + n], device=device))
+        a_, b_ = int(lo_i[0]), int(lo_i[1])
+        sel[a_:b_] = k[pos[a_:b_] - base]
+        base += n
+    del parts, pos
+    out = torch.empty((target, D), dtype=out_dtype, device=device)
+    for c0 in range(0, target, chunk):
+        cs = _unpack(sel[c0:c0 + chunk], dims, lo_bits)
+        out[c0:c0 + chunk] = torch.stack(cs, dim=1).to(out_dtype)
+    return out
 
 
 def _uniform53(c0, c1, c2, c3, seed):
@@ -288,7 +322,7 @@ def uniform_init(dims, rank, seed, device="cpu"):
     return out
 
 
-def generate_values(cfg: Config, coords: torch.Tensor) -> torch.Tensor:
+def generate_values(cfg: Config, coords: torch.Tensor, chunk: int = 1 << 27) -> torch.Tensor:
     device = coords.device
     dims = cfg.dims
     if cfg.value == "planted":
@@ -307,19 +341,23 @@ def generate_values(cfg: Config, coords: torch.Tensor) -> torch.Tensor:
         z = torch.sqrt(-2.0 * torch.log(u1)) * torch.cos(2.0 * math.pi * u2)
         return v + 1e-4 * z
     lo_bits = packed_key_layout(dims)
-    keys = _pack([coords[:, m] for m in range(len(dims))], dims, lo_bits)
-    x = philox4x32_10(keys & M32, (keys >> 32) & M32, 0x7A1E, 0, cfg.value_seed, 0x7A1E0000)
-    u = _word62(x[0], x[1])
     thr = torch.from_numpy(geometric_table(cfg.geom_p)).to(device)
-    g = thr.numel() - torch.searchsorted(thr, u, right=True)      # #thr > u
-    c = 1 + g
-    if cfg.value == "geom":
-        vals = c.to(torch.float64)
-    else:  # 'loggeom': fp32(log(1+c)) from a host table (no device libm)
+    tab = None
+    if cfg.value == "loggeom":   # fp32(log(1+c)) from a host table (no device libm)
         tab = torch.tensor([math.log1p(float(k)) for k in range(thr.numel() + 2)],
                            dtype=torch.float64).to(device)
-        vals = tab[c]
-    return vals.to(torch.float32 if cfg.value_dtype == "f32" else torch.float64)
+    out_dtype = torch.float32 if cfg.value_dtype == "f32" else torch.float64
+    out = torch.empty(coords.shape[0], dtype=out_dtype, device=device)
+    for c0 in range(0, coords.shape[0], chunk):
+        cc = coords[c0:c0 + chunk].to(torch.int64)
+        keys = _pack([cc[:, m] for m in range(len(dims))], dims, lo_bits)
+        x = philox4x32_10(keys & M32, (keys >> 32) & M32, 0x7A1E, 0, cfg.value_seed, 0x7A1E0000)
+        u = _word62(x[0], x[1])
+        g = thr.numel() - torch.searchsorted(thr, u, right=True)      # #thr > u
+        c = 1 + g
+        vals = c.to(torch.float64) if tab is None else tab[c]
+        out[c0:c0 + chunk] = vals.to(out_dtype)
+    return out
 
 
 @dataclasses.dataclass
@@ -338,9 +376,15 @@ def make(name_or_cfg, device="cpu", index_dtype=torch.int32, dense_planted=False
         coords = torch.stack([g.reshape(-1) for g in grids], dim=1).to(torch.int64)
         cfg = dataclasses.replace(cfg, nnz=coords.shape[0])
     else:
-        coords = generate_coords(cfg, device=device)
+        coords = generate_coords(cfg, device=device, out_dtype=index_dtype)
     vals = generate_values(cfg, coords)
-    return Tensor(cfg, tuple(cfg.dims), coords.to(index_dtype), vals)
+    if coords.dtype != index_dtype:
+        out = torch.empty(coords.shape, dtype=index_dtype, device=coords.device)
+        for c0 in range(0, coords.shape[0], 1 << 27):
+            out[c0:c0 + (1 << 27)] = coords[c0:c0 + (1 << 27)].to(index_dtype)
+        del coords
+        coords = out
+    return Tensor(cfg, tuple(cfg.dims), coords, vals)
 
 
 def scaled(cfg_name: str, nnz: int, dims=None, **kw) -> Config:
