@@ -106,6 +106,17 @@ class Clocks:
                 "samples": len(sm)}
 
 
+def traffic_for(kernel, config):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of `kernel` from
+    the committed ncu --set full capture (profiles/traffic.json), else None."""
+    try:
+        d = json.load(open(os.path.join(ROOT, "profiles", "traffic.json")))
+        e = d[config][kernel]
+        return float(e["dram_bytes_per_launch"])
+    except Exception:
+        return None
+
+
 def measured_peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     try:
@@ -245,7 +256,10 @@ def run_ours(args):
     value = K / (ms / 1000.0)
     # fit kernel alone, timed live: bytes = streamed nonzeros (key u64 + out i32 + value)
     vbytes = 4 if cfg.value_dtype == "f32" else 8
-    fit_alg_bytes = nnz * (8 + 4 + vbytes)
+    # algorithmic bytes of one exact-fit launch: every
+    # nonzero of the fit mode's copy (key u64 + out i32 + value) plus every
+    # factor row once
+    fit_alg_bytes = nnz * (8 + 4 + vbytes) + sum(cfg.dims) * cfg.rank * 8
     if not fit_ms:
         fa = torch.cuda.Event(enable_timing=True); fb = torch.cuda.Event(enable_timing=True)
         fa.record(stream); g.fit(); fb.record(stream); torch.cuda.synchronize()
@@ -300,10 +314,10 @@ def run_ours(args):
                    "values": cfg.value_dtype, "l2": "inputs larger than L2 (per-mode sorted copies "
                    f"{nnz * (16 if cfg.value_dtype == 'f32' else 20) * D / 1e9:.1f} GB >> 126 MB)",
                    "parallelism": "single GPU"},
-        "roofline": {"bound": "hbm", "kernel": "k_fit_inner (exact fit, streams all nonzeros)",
+        "roofline": {"bound": "hbm", "kernel": "k_fit_thread (exact fit, P:867-875; dominant per iteration)",
                      "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                     "traffic": None, "alg_bytes_per_launch": fit_alg_bytes, "avg_launch_ms": fit_avg,
-                     "peak_source": peak_src},
+                     "traffic": traffic_for("k_fit_thread", args.config), "alg_bytes_per_launch": fit_alg_bytes,
+                     "avg_launch_ms": fit_avg, "launches_timed": len(fit_ms), "peak_source": peak_src},
         "clocks": clk.summary(),
         "gpu_launches": int(st["kernel_launches"]),
         "e2e": e2e,
