@@ -106,6 +106,15 @@ class Clocks:
                 "samples": len(sm)}
 
 
+def fit_kernel_name(cfg):
+    """The fit kernel libcparls picks (k_fit_stage when the fit-mode factor is
+    larger than ~half of L2, else k_fit_thread); the fit mode is one of the
+    modes, and for C4/C5 every factor exceeds 64 MB."""
+    ld = (cfg.rank + 3) // 4 * 4
+    big = min(cfg.dims) * ld * 8 > 64 * (1 << 20)
+    return ("k_fit_stage" if big else "k_fit_thread") + " (exact fit, P:867-875; dominant kernel per iteration)"
+
+
 def traffic_for(kernel, config):
     """dram__bytes_read.sum + dram__bytes_write.sum per launch of `kernel` from
     the committed ncu --set full capture (profiles/traffic.json), else None."""
@@ -314,9 +323,9 @@ def run_ours(args):
                    "values": cfg.value_dtype, "l2": "inputs larger than L2 (per-mode sorted copies "
                    f"{nnz * (16 if cfg.value_dtype == 'f32' else 20) * D / 1e9:.1f} GB >> 126 MB)",
                    "parallelism": "single GPU"},
-        "roofline": {"bound": "hbm", "kernel": "k_fit_thread (exact fit, P:867-875; dominant per iteration)",
+        "roofline": {"bound": "hbm", "kernel": fit_kernel_name(cfg),
                      "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                     "traffic": traffic_for("k_fit_thread", args.config), "alg_bytes_per_launch": fit_alg_bytes,
+                     "traffic": traffic_for(fit_kernel_name(cfg).split(" ")[0], args.config), "alg_bytes_per_launch": fit_alg_bytes,
                      "avg_launch_ms": fit_avg, "launches_timed": len(fit_ms), "peak_source": peak_src},
         "clocks": clk.summary(),
         "gpu_launches": int(st["kernel_launches"]),
@@ -326,7 +335,7 @@ def run_ours(args):
         "setup": {"generate_s": t_gen, "create_s": t_build},
         "phases_ms": {k[3:]: st[k] for k in st if k.startswith("ms_")} if args.profile_phases else None,
         "counters": {"last_matched_nnz": st["last_matched_nnz"], "last_s_bar": st["last_s_bar"],
-                     "last_attempts": st["last_attempts"]},
+                     "last_attempts": st["last_attempts"], "touched_rows": st["touched_rows"][:D]},
     }
     print(json.dumps(line), flush=True)
 

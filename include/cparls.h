@@ -86,6 +86,7 @@ typedef struct {
   double bytes_leverage, bytes_sample, bytes_gram, bytes_lookup, bytes_rhs, bytes_solve, bytes_fit;
   int64_t mode_steps, fits, kernel_launches;
   int64_t last_matched_nnz, last_s_bar, last_attempts;
+  int64_t touched_rows[8];   /* rows of A_k nonzero after its last solve, per mode */
 } cparls_stats;
 
 /* Build the context: validates sizes (ERANGE if some prod_{m!=k} n_m >= 2^63 or

@@ -47,10 +47,13 @@ class Stats(C.Structure):
         "ms_leverage", "ms_sample", "ms_gram", "ms_lookup", "ms_rhs", "ms_solve", "ms_fit",
         "bytes_leverage", "bytes_sample", "bytes_gram", "bytes_lookup", "bytes_rhs", "bytes_solve",
         "bytes_fit")] + [(n, C.c_int64) for n in (
-        "mode_steps", "fits", "kernel_launches", "last_matched_nnz", "last_s_bar", "last_attempts")]
+        "mode_steps", "fits", "kernel_launches", "last_matched_nnz", "last_s_bar", "last_attempts")] + [
+        ("touched_rows", C.c_int64 * 8)]
 
     def as_dict(self):
-        return {n: getattr(self, n) for n, _ in self._fields_}
+        d = {n: getattr(self, n) for n, _ in self._fields_}
+        d["touched_rows"] = list(self.touched_rows)
+        return d
 
 
 _lib = None

@@ -248,6 +248,8 @@ void set_attrs_rm() {
   max_dyn_smem(k_krp_gram_t<RM>);
   max_dyn_smem(k_fit_thread<float, RM>);
   max_dyn_smem(k_fit_thread<double, RM>);
+  max_dyn_smem(k_fit_stage<float, RM>);
+  max_dyn_smem(k_fit_stage<double, RM>);
 }
 
 void set_kernel_attrs(int r, int ld) {
@@ -881,6 +883,7 @@ void solve_impl(cparls_ctx *c, int k, cparls_solve_info *info) {
   c->mk = hv.mk;
   c->stats.bytes_rhs += (double)hv.mk * (4.0 + (c->vf32 ? 4.0 : 8.0)) + (double)hv.touched * r * 8.0 * 2;
   c->stats.last_matched_nnz = hv.mk;
+  c->stats.touched_rows[k] = (int64_t)hv.touched;
   c->stats.mode_steps++;
   if (info) {
     info->matched_nnz = hv.mk;
@@ -908,15 +911,30 @@ double fit_impl(cparls_ctx *c) {
   }
   fd.fast = N < 9007199254740992.0L;   // keys < 2^53
   const int nb = 148 * 4;
-  const size_t smem = sizeof(double) * kFitThreads * (size_t)(c->r | 1);
-  if (c->vf32)
-    RSWITCH(c->r, k_fit_thread<float, RM><<<nb, kFitThreads, smem, c->st>>>(
-                      c->idx[k].key, c->idx[k].out, (const float *)c->idx[k].val, c->nnz, fd, c->A[k], c->lam_model,
-                      c->r, c->ld, c->ddpart));
-  else
-    RSWITCH(c->r, k_fit_thread<double, RM><<<nb, kFitThreads, smem, c->st>>>(
-                      c->idx[k].key, c->idx[k].out, (const double *)c->idx[k].val, c->nnz, fd, c->A[k], c->lam_model,
-                      c->r, c->ld, c->ddpart));
+  // factor of the fit mode larger than ~half of L2: stage its rows with
+  // coalesced cp.async (k_fit_stage); otherwise plain per-thread gathers hit L2
+  const bool stage = (double)c->dims[k] * c->ld * 8.0 > 64.0 * (1 << 20) && fit_stage_smem(c->r, c->ld) <= 200 * 1024;
+  if (stage) {
+    const size_t smem = fit_stage_smem(c->r, c->ld);
+    if (c->vf32)
+      RSWITCH(c->r, k_fit_stage<float, RM><<<nb, kFitThreads, smem, c->st>>>(
+                        c->idx[k].key, c->idx[k].out, (const float *)c->idx[k].val, c->nnz, fd, c->A[k],
+                        c->lam_model, c->r, c->ld, c->ddpart));
+    else
+      RSWITCH(c->r, k_fit_stage<double, RM><<<nb, kFitThreads, smem, c->st>>>(
+                        c->idx[k].key, c->idx[k].out, (const double *)c->idx[k].val, c->nnz, fd, c->A[k],
+                        c->lam_model, c->r, c->ld, c->ddpart));
+  } else {
+    const size_t smem = sizeof(double) * kFitThreads * (size_t)(c->r | 1);
+    if (c->vf32)
+      RSWITCH(c->r, k_fit_thread<float, RM><<<nb, kFitThreads, smem, c->st>>>(
+                        c->idx[k].key, c->idx[k].out, (const float *)c->idx[k].val, c->nnz, fd, c->A[k],
+                        c->lam_model, c->r, c->ld, c->ddpart));
+    else
+      RSWITCH(c->r, k_fit_thread<double, RM><<<nb, kFitThreads, smem, c->st>>>(
+                        c->idx[k].key, c->idx[k].out, (const double *)c->idx[k].val, c->nnz, fd, c->A[k],
+                        c->lam_model, c->r, c->ld, c->ddpart));
+  }
   CK_LAUNCH();
   FitModes fm{};
   fm.D = c->D;

@@ -114,6 +114,107 @@ __global__ void __launch_bounds__(kFitThreads, 2) k_fit_thread(const uint64_t *_
   }
 }
 
+__device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit_wait() {
+  asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
+}
+
+// As k_fit_thread, but each warp stages the 32 A_{k*}(out,:) rows of its tile
+// into shared memory with coalesced 16-byte cp.async chunks (about 2.3 rows per
+// instruction instead of one row per lane), overlapping the fiber leaders' h
+// computation; lanes then read their own row from shared memory.
+template <typename VT, int RMAX>
+__global__ void __launch_bounds__(kFitThreads) k_fit_stage(const uint64_t *__restrict__ keys,
+                                                          const int32_t *__restrict__ outidx,
+                                                          const VT *__restrict__ vals, int64_t nnz, FitDecode fd,
+                                                          const double *__restrict__ Ak,
+                                                          const double *__restrict__ lam, int r, int ld,
+                                                          dd *__restrict__ part) {
+  extern __shared__ __align__(16) double fsm[];
+  const int S = ld + 2;              // even (16-byte aligned rows), 2-way conflicts at most
+  const int RS = r | 1;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  double *tile = fsm + (size_t)w * 32 * S;                                   // 32 rows x S
+  double *hw = fsm + (size_t)(kFitThreads / 32) * 32 * S + (size_t)w * 32 * RS;   // 32 slots x RS
+  __shared__ double lam_s[kMaxRank + 1];
+  for (int c = threadIdx.x; c <= kMaxRank; c += blockDim.x) lam_s[c] = c < r ? lam[c] : 0.0;
+  __syncthreads();
+  const int H = ld / 2;              // 16-byte chunks per row
+  const uint64_t pstream = l2_evict_first();
+  dd acc = {0.0, 0.0};
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t e0 = (int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31); e0 < nnz; e0 += stride) {
+    const int64_t e = e0 + lane;
+    const bool valid = e < nnz;
+    const int n = (int)min((int64_t)32, nnz - e0);
+    const uint64_t key = valid ? ld_stream(keys + e, pstream) : ~0ull;
+    const int32_t o = valid ? ld_stream(outidx + e, pstream) : 0;
+    const double x = valid ? (double)ld_stream(vals + e, pstream) : 0.0;
+    // stage A rows: chunk f = lane + 32q  ->  row rho = f / H, part = f % H
+    {
+      int rho = lane / H, part = lane - (lane / H) * H;
+      for (int f = lane; f < 32 * H; f += 32) {
+        const int orow = __shfl_sync(0xffffffffu, o, rho & 31);
+        if (rho < n) cp_async16(tile + rho * S + 2 * part, Ak + (int64_t)orow * ld + 2 * part);
+        part += 32;
+        while (part >= H) { part -= H; ++rho; }
+      }
+      asm volatile("cp.async.commit_group;\n" ::: "memory");
+    }
+    uint64_t prev = __shfl_up_sync(0xffffffffu, key, 1);
+    if (lane == 0) prev = ~key;
+    const bool lead = valid && key != prev;
+    const unsigned lm = __ballot_sync(0xffffffffu, lead);
+    if (lead) {
+      double *h = hw + lane * RS;
+      for (int c = 0; c < r; ++c) h[c] = lam_s[c];
+      uint64_t t = key;
+      for (int m = 0; m < fd.d; ++m) {
+        uint64_t rem;
+        t = divmod_fast(t, fd.n[m], fd.inv[m], rem, fd.fast);
+        const double2 *row = reinterpret_cast<const double2 *>(fd.A[m] + rem * ld);
+        double2 v[RMAX / 2];
+#pragma unroll
+        for (int c2 = 0; c2 < RMAX / 2; ++c2) v[c2] = (2 * c2 < r) ? __ldg(row + c2) : make_double2(0.0, 0.0);
+#pragma unroll
+        for (int c2 = 0; c2 < RMAX / 2; ++c2) {
+          if (2 * c2 < r) h[2 * c2] *= v[c2].x;
+          if (2 * c2 + 1 < r) h[2 * c2 + 1] *= v[c2].y;
+        }
+      }
+    }
+    asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+    __syncwarp();
+    if (valid) {
+      const int src = 31 - __clz(lm & (0xffffffffu >> (31 - lane)));   // last leader at or before lane
+      const double *h = hw + src * RS;
+      const double *a = tile + lane * S;
+      double mv = 0.0;
+#pragma unroll
+      for (int c = 0; c < RMAX; ++c)
+        if (c < r) mv += h[c] * a[c];
+      acc = dd_add_d(acc, x * mv);
+    }
+    __syncwarp();
+  }
+  acc = warp_sum_dd(acc);
+  __shared__ dd ws[kFitThreads / 32];
+  if (lane == 0) ws[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    dd tt = {0.0, 0.0};
+    for (int i = 0; i < kFitThreads / 32; ++i) tt = dd_add(tt, ws[i]);
+    part[blockIdx.x] = tt;
+  }
+}
+
+inline size_t fit_stage_smem(int r, int ld) {
+  return sizeof(double) * ((size_t)kFitThreads * (ld + 2) + (size_t)kFitThreads * (r | 1)) + 16;
+}
+
 // <X,M> from block partials; ||M||^2 = lambda^T (*_m G_m) lambda with the
 // factors' Grams G_m (P:146-148 structure); fit = 1 - sqrt(max(0, ||X||^2 -
 // 2<X,M> + ||M||^2)) / ||X|| (AMB-16).

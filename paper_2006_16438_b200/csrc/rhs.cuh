@@ -44,6 +44,7 @@ __global__ void __launch_bounds__(kRhsThreads) k_rhs(const int64_t *__restrict__
   for (int i = threadIdx.x; i < kRhsWarps * nhot * r; i += blockDim.x) priv[i] = 0.0;
   __syncthreads();
   const int64_t mk = *mk_ptr;
+  const uint64_t pstream = l2_evict_first();
   while (true) {
     int64_t t0 = 0;
     if (lane == 0) t0 = (int64_t)atomicAdd(work, (unsigned long long)per_warp);
@@ -71,8 +72,8 @@ __global__ void __launch_bounds__(kRhsThreads) k_rhs(const int64_t *__restrict__
       if (tt < t1) {
         j_l = seg_j ? (int64_t)__ldg(seg_j + jj) : jj;
         const int64_t e = __ldg(lo + jj) + (tt - __ldg(off + jj));
-        o_l = __ldg(outidx + e);
-        x_l = (double)__ldg(vals + e);
+        o_l = ld_stream(outidx + e, pstream);
+        x_l = (double)ld_stream(vals + e, pstream);
         s_l = __ldg(hot_slot + o_l);
         if (s_l >= nhot) s_l = -1;
       }

@@ -12,16 +12,28 @@ namespace cparls {
 
 constexpr int kRowThreads = 256;   // rows per tile = threads per block
 
-// stage rows [base, base+rows) of a (ld-strided) matrix into tile (stride S)
+// stage rows [base, base+rows) of a (ld-strided) matrix into tile (stride S);
+// 4 independent 16-byte loads in flight per thread
 __device__ __forceinline__ void stage_rows(const double *__restrict__ src, int rows, int ld, double *tile, int S) {
   const double2 *s2 = reinterpret_cast<const double2 *>(src);
   const int n2 = rows * ld / 2;
-  for (int i = threadIdx.x; i < n2; i += blockDim.x) {
-    double2 v = s2[i];
-    int e = 2 * i;
-    int row = e / ld, c = e - row * ld;
-    tile[row * S + c] = v.x;
-    tile[row * S + c + 1] = v.y;
+  const int B = blockDim.x;
+  for (int i0 = threadIdx.x; i0 < n2; i0 += 4 * B) {
+    double2 v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int i = i0 + u * B;
+      v[u] = i < n2 ? __ldg(s2 + i) : make_double2(0.0, 0.0);
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int i = i0 + u * B;
+      if (i < n2) {
+        const int e = 2 * i, row = e / ld, c = e - row * ld;
+        tile[row * S + c] = v[u].x;
+        tile[row * S + c + 1] = v[u].y;
+      }
+    }
   }
 }
 
@@ -29,8 +41,7 @@ __device__ __forceinline__ void store_rows(double *__restrict__ dst, int rows, i
   double2 *d2 = reinterpret_cast<double2 *>(dst);
   const int n2 = rows * ld / 2;
   for (int i = threadIdx.x; i < n2; i += blockDim.x) {
-    int e = 2 * i;
-    int row = e / ld, c = e - row * ld;
+    const int e = 2 * i, row = e / ld, c = e - row * ld;
     d2[i] = make_double2(tile[row * S + c], tile[row * S + c + 1]);
   }
 }
