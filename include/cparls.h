@@ -34,7 +34,8 @@
 extern "C" {
 #endif
 
-typedef struct cparls_ctx cparls_ctx; /* opaque */
+typedef struct cparls_ctx cparls_ctx;   /* opaque */
+typedef struct cparls_comm cparls_comm; /* opaque communicator (NCCL or in-process group) */
 
 typedef enum {
   CPARLS_OK = 0,
@@ -56,9 +57,9 @@ typedef struct {
                               accumulation is always fp64)                           */
   int32_t index_dtype;     /* coords of cparls_create: 0 int32, 1 int64              */
   void *stream;            /* cudaStream_t                                            */
-  int32_t world_size;      /* 1 = single GPU                                          */
-  int32_t world_rank;
-  void *nccl_comm;         /* ncclComm_t when world_size > 1, else NULL               */
+  int32_t world_size;      /* 1 = single GPU; > 1 = row-sharded SPMD     */
+  int32_t world_rank;      /* this shard, 0 <= world_rank < world_size                */
+  cparls_comm *comm;       /* required when world_size > 1 (cparls_comm_create_*)      */
   int64_t didx_cap;        /* max DIDX list length per level (0 -> default 1<<22)     */
   int64_t attempt_cap;     /* max SIDX attempts (0 -> 1024*s_rnd + 65536, AMB-7)      */
 } cparls_opts;
@@ -150,6 +151,30 @@ cparls_status cparls_fit(cparls_ctx *ctx, double *fit);
  * be resumed exactly (counter-based RNG). */
 cparls_status cparls_run(cparls_ctx *ctx, int32_t iters, int64_t s, uint64_t seed, int32_t iter0,
                          int32_t fit_every, double *fit_trace);
+
+/* ---- multi-GPU (SURVEY 8(e), P:1797-1801 sketches the distributed variant) ----
+ * Row sharding: for every mode k the rows of B (and the nonzeros whose mode-k
+ * index is one of them) are split into world_size contiguous blocks balanced
+ * by nonzero count (cparls_plan_rows).  Sampling is replicated (same p~ bits,
+ * seed, step on every rank: no communication); per mode step the ranks
+ * allreduce the r x r Gram of their B rows and allgather the B rows; the fit
+ * allreduces one scalar.  cparls_create routes each rank's COO chunk to the
+ * row owners with one all-to-all per mode. */
+/* NCCL: rank 0 creates the id, the caller broadcasts the 128 bytes (e.g. with
+ * torch.distributed), every rank then creates its communicator. */
+cparls_status cparls_comm_nccl_unique_id(uint8_t id[128]);
+cparls_status cparls_comm_create_nccl(int32_t world_size, int32_t rank, const uint8_t id[128], cparls_comm **out);
+/* In-process group of world_size shards on the current GPU, driven by
+ * world_size host threads (one cparls_ctx each, opts.world_rank = its shard):
+ * the shard simulator for single-GPU testing of the sharded path.  One object
+ * is shared by all shards. */
+cparls_status cparls_comm_create_local(int32_t world_size, cparls_comm **out);
+cparls_status cparls_comm_destroy(cparls_comm *comm);
+/* Host-only: row blocks of a mode from its global per-row nonzero counts deg[n]
+ * (bound[p]..bound[p+1]-1 owned by rank p; bound has world_size+1 entries). */
+cparls_status cparls_plan_rows(int64_t n, const uint64_t *deg, int32_t world_size, int64_t *bound);
+/* Rows of mode `mode` owned by this rank. */
+cparls_status cparls_owned_rows(const cparls_ctx *ctx, int32_t mode, int64_t *lo, int64_t *hi);
 
 cparls_status cparls_get_stats(cparls_ctx *ctx, cparls_stats *stats);
 cparls_status cparls_reset_stats(cparls_ctx *ctx);

@@ -7,8 +7,23 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 SRC = os.path.join(HERE, "csrc", "cparls.cu")
 LIB = os.path.join(HERE, "libcparls.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+def _nccl_dir():
+    """NCCL shipped with torch (the library torch.distributed loads)."""
+    import importlib.util
+    spec = importlib.util.find_spec("nvidia")
+    for base in (spec.submodule_search_locations if spec else []):
+        d = os.path.join(base, "nccl")
+        if os.path.exists(os.path.join(d, "include", "nccl.h")):
+            return d
+    return None
+
+
+NCCL = _nccl_dir()
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC,-O2", "-shared", "--expt-relaxed-constexpr", "-Xptxas", "-v"]
+if NCCL:
+    FLAGS += ["-I" + os.path.join(NCCL, "include"), "-L" + os.path.join(NCCL, "lib"),
+              "-Xlinker", "-rpath," + os.path.join(NCCL, "lib")]
 
 
 def sources():
@@ -20,7 +35,7 @@ def sources():
 def build(force=False, verbose=False):
     if not force and os.path.exists(LIB) and os.path.getmtime(LIB) >= max(os.path.getmtime(s) for s in sources()):
         return LIB
-    cmd = [NVCC] + FLAGS + ["-o", LIB + ".tmp", SRC, "-lcudart"]
+    cmd = [NVCC] + FLAGS + ["-o", LIB + ".tmp", SRC, "-lcudart", "-l:libnccl.so.2"]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         sys.stderr.write(res.stdout + res.stderr)

@@ -28,7 +28,7 @@ class CparlsError(RuntimeError):
 class Opts(C.Structure):
     _fields_ = [("rank", C.c_int32), ("tau", C.c_double), ("value_dtype", C.c_int32),
                 ("index_dtype", C.c_int32), ("stream", C.c_void_p), ("world_size", C.c_int32),
-                ("world_rank", C.c_int32), ("nccl_comm", C.c_void_p), ("didx_cap", C.c_int64),
+                ("world_rank", C.c_int32), ("comm", C.c_void_p), ("didx_cap", C.c_int64),
                 ("attempt_cap", C.c_int64)]
 
 
@@ -86,6 +86,12 @@ def lib():
             "cparls_get_stats": [P, C.POINTER(Stats)],
             "cparls_reset_stats": [P],
             "cparls_set_profiling": [P, I32],
+            "cparls_comm_nccl_unique_id": [P],
+            "cparls_comm_create_nccl": [I32, I32, P, C.POINTER(P)],
+            "cparls_comm_create_local": [I32, C.POINTER(P)],
+            "cparls_comm_destroy": [P],
+            "cparls_plan_rows": [I64, P, I32, P],
+            "cparls_owned_rows": [P, I32, P, P],
         }
         for name, args in sig.items():
             f = getattr(L, name)
@@ -103,7 +109,9 @@ EXPORTED = ["cparls_create", "cparls_destroy", "cparls_set_factor", "cparls_get_
             "cparls_leverage", "cparls_get_ptilde", "cparls_set_ptilde", "cparls_sample",
             "cparls_set_tau", "cparls_get_sample", "cparls_get_fibers", "cparls_solve_mode",
             "cparls_get_last_solve", "cparls_fit", "cparls_run", "cparls_get_stats",
-            "cparls_reset_stats", "cparls_set_profiling", "cparls_last_error", "cparls_version"]
+            "cparls_reset_stats", "cparls_set_profiling", "cparls_last_error", "cparls_version",
+            "cparls_comm_nccl_unique_id", "cparls_comm_create_nccl", "cparls_comm_create_local",
+            "cparls_comm_destroy", "cparls_plan_rows", "cparls_owned_rows"]
 
 
 def _ptr(x):
@@ -120,7 +128,7 @@ class Cparls:
     """One CP-ARLS-LEV context (the C ABI's cparls_ctx)."""
 
     def __init__(self, dims, coords, vals, rank, tau=-1.0, init_seed=2, stream=None,
-                 didx_cap=0, attempt_cap=0):
+                 didx_cap=0, attempt_cap=0, comm=None, world_size=1, world_rank=0):
         import torch
         if not torch.cuda.is_available():
             raise RuntimeError("cparls needs a CUDA device (B200); no CPU fallback exists")
@@ -146,7 +154,8 @@ class Cparls:
             stream = torch.cuda.current_stream().cuda_stream
         self.stream = stream
         o = Opts(rank=self.r, tau=float(tau), value_dtype=vdt, index_dtype=idt,
-                 stream=C.c_void_p(stream), world_size=1, world_rank=0, nccl_comm=None,
+                 stream=C.c_void_p(stream), world_size=int(world_size), world_rank=int(world_rank),
+                 comm=(comm.handle if comm is not None else None),
                  didx_cap=int(didx_cap), attempt_cap=int(attempt_cap))
         d = np.array(self.dims, dtype=np.int64)
         h = C.c_void_p()
@@ -250,6 +259,11 @@ class Cparls:
                                      int(fit_every), trace.ctypes.data))
         return trace[:iters]
 
+    def owned_rows(self, k):
+        lo, hi = C.c_int64(), C.c_int64()
+        self._check(lib().cparls_owned_rows(self._h, k, C.byref(lo), C.byref(hi)))
+        return lo.value, hi.value
+
     def stats(self):
         s = Stats()
         self._check(lib().cparls_get_stats(self._h, C.byref(s)))
@@ -260,6 +274,57 @@ class Cparls:
 
     def set_profiling(self, on=True):
         self._check(lib().cparls_set_profiling(self._h, 1 if on else 0))
+
+
+class Comm:
+    """A cparls_comm: NCCL (one process per GPU) or an in-process local group
+    (shard simulator: world_size shards on the current GPU, one host thread
+    each)."""
+
+    def __init__(self, handle, kind):
+        self.handle = handle
+        self.kind = kind
+
+    @staticmethod
+    def nccl_unique_id() -> bytes:
+        buf = (C.c_uint8 * 128)()
+        st = lib().cparls_comm_nccl_unique_id(buf)
+        if st != OK:
+            raise CparlsError(st, "ncclGetUniqueId failed")
+        return bytes(buf)
+
+    @classmethod
+    def nccl(cls, world_size, rank, uid: bytes):
+        buf = (C.c_uint8 * 128).from_buffer_copy(uid)
+        h = C.c_void_p()
+        st = lib().cparls_comm_create_nccl(int(world_size), int(rank), buf, C.byref(h))
+        if st != OK:
+            raise CparlsError(st, "ncclCommInitRank failed")
+        return cls(h, "nccl")
+
+    @classmethod
+    def local(cls, world_size):
+        h = C.c_void_p()
+        st = lib().cparls_comm_create_local(int(world_size), C.byref(h))
+        if st != OK:
+            raise CparlsError(st, "local group creation failed")
+        return cls(h, "local")
+
+    def close(self):
+        if self.handle:
+            lib().cparls_comm_destroy(self.handle)
+            self.handle = None
+
+
+def plan_rows(deg, world_size):
+    """Row blocks (world_size + 1 bounds) balanced by the per-row counts deg
+    (host-only library call; cparls_plan_rows)."""
+    deg = np.ascontiguousarray(deg, dtype=np.uint64)
+    bound = np.zeros(int(world_size) + 1, dtype=np.int64)
+    st = lib().cparls_plan_rows(len(deg), deg.ctypes.data, int(world_size), bound.ctypes.data)
+    if st != OK:
+        raise CparlsError(st, "plan_rows")
+    return bound
 
 
 def version():

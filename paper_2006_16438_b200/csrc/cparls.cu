@@ -16,6 +16,7 @@
 #include <vector>
 
 #include "../../include/cparls.h"
+#include "comm.cuh"
 #include "kernels.cuh"
 
 using namespace cparls;
@@ -29,6 +30,7 @@ struct ModeIndex {
   int64_t *dir = nullptr;    // dir[b] = first position with key >> shift >= b
   int shift = 0;
   int64_t nbkt = 0;
+  int64_t nnz = 0;           // nonzeros of this rank's slice of mode k
 };
 
 struct DevScalars {
@@ -117,6 +119,11 @@ struct cparls_ctx {
   bool profiling = false;
   int fit_mode = 0;
   int smode_last_solved = -1;
+  // row sharding: this rank owns rows [row_lo, row_hi) of mode k
+  Comm *comm = nullptr;
+  int world = 1, wrank = 0;
+  int64_t row_lo[kMaxModes] = {0}, row_hi[kMaxModes] = {0};
+  std::vector<int64_t> bounds[kMaxModes];   // row blocks of every rank per mode
   // RHS output-row windows (see rhs.cuh)
   int64_t segcap = 0;
   int64_t *seg_lo = nullptr, *seg_len = nullptr, *seg_off = nullptr, *i64part_seg = nullptr;
@@ -127,7 +134,36 @@ struct cparls_ctx {
   int64_t nfib[kMaxModes] = {0};
 };
 
+struct cparls_comm {
+  int kind = 0;   // 0 NCCL, 1 local group
+  int world = 1, rank = 0;
+  ncclComm_t nccl = nullptr;
+  cparls::LocalGroup *group = nullptr;
+};
+
 namespace {
+
+int64_t row_start(const cparls_ctx *c, int k, int q) { return c->bounds[k][q]; }
+
+Comm *make_comm(cparls_comm *cc, int rank) {
+  if (cc->kind == 0) {
+    auto *n = new NcclComm();
+    n->c = cc->nccl;
+    n->owns = false;
+    n->world = cc->world;
+    n->rank = cc->rank;
+    if (n->rank != rank) {
+      delete n;
+      throw ApiError(CPARLS_EINVAL, "NCCL communicator rank != opts.world_rank");
+    }
+    return n;
+  }
+  auto *l = new LocalComm();
+  l->g = cc->group;
+  l->world = cc->world;
+  l->rank = rank;
+  return l;
+}
 
 void *dalloc(cparls_ctx *c, size_t bytes) {
   void *p = nullptr;
@@ -341,9 +377,9 @@ OtherModes other_modes(cparls_ctx *c, int k, bool need_alpha) {
 
 // ---------------------------------------------------------------- index build (K0)
 template <typename IT, typename VT>
-void build_index_mode(cparls_ctx *c, int k, const IT *coords, const VT *vals) {
-  const int64_t nnz = c->nnz;
+void build_index_mode(cparls_ctx *c, int k, const IT *coords, const VT *vals, int64_t nnz) {
   ModeIndex &ix = c->idx[k];
+  ix.nnz = nnz;
   const unsigned g = (unsigned)std::max<int64_t>(1, ceil_div(nnz, 256));
   // pass 1: stable sort of nonzero ids by mode-k coordinate
   uint32_t *ok0 = dalloc_t<uint32_t>(c, nnz), *ok1 = dalloc_t<uint32_t>(c, nnz);
@@ -444,6 +480,102 @@ void build_index_mode(cparls_ctx *c, int k, const IT *coords, const VT *vals) {
   sync(c);
 }
 
+// Row partition of mode k into world contiguous blocks balanced by nonzeros:
+// bound[p] = first row whose exclusive prefix of deg reaches p*total/world.
+void plan_rows(int64_t n, const unsigned long long *deg, int world, int64_t *bound) {
+  unsigned long long total = 0;
+  for (int64_t i = 0; i < n; ++i) total += deg[i];
+  bound[0] = 0;
+  unsigned long long run = 0;
+  int64_t i = 0;
+  for (int p = 1; p < world; ++p) {
+    const unsigned long long t = (unsigned long long)(((unsigned __int128)total * p) / world);
+    while (i < n && run < t) run += deg[i++];
+    bound[p] = i;
+  }
+  bound[world] = n;
+}
+
+// Sharded build of mode k: global row degrees (allreduce), row blocks
+// (plan_rows), all-to-all of the local COO chunk to the owners of the mode-k
+// rows, then the usual sorted copy of the received slice.
+template <typename IT, typename VT>
+void route_and_build(cparls_ctx *c, int k, const IT *coords, const VT *vals) {
+  const int P = c->world, D = c->D;
+  const int64_t n = c->dims[k], nnz = c->nnz;
+  unsigned long long *deg = dalloc_t<unsigned long long>(c, n);
+  CK(cudaMemsetAsync(deg, 0, sizeof(unsigned long long) * n, c->st));
+  if (nnz > 0) {
+    k_coord_degree<IT><<<1184, 256, 0, c->st>>>(coords, nnz, D, k, deg);
+    CK_LAUNCH();
+  }
+  c->comm->allreduce_u64(deg, n, c->st);
+  std::vector<unsigned long long> hdeg(n);
+  CK(cudaMemcpyAsync(hdeg.data(), deg, sizeof(unsigned long long) * n, cudaMemcpyDeviceToHost, c->st));
+  sync(c);
+  dfree(c, deg);
+  std::vector<int64_t> bound(P + 1);
+  plan_rows(n, hdeg.data(), P, bound.data());
+  c->row_lo[k] = bound[c->wrank];
+  c->row_hi[k] = bound[c->wrank + 1];
+  c->bounds[k] = bound;
+  // destination rank per local nonzero, stable order by destination
+  int64_t *dbound = dalloc_t<int64_t>(c, P + 1);
+  CK(cudaMemcpyAsync(dbound, bound.data(), sizeof(int64_t) * (P + 1), cudaMemcpyHostToDevice, c->st));
+  uint32_t *dk0 = dalloc_t<uint32_t>(c, nnz), *dk1 = dalloc_t<uint32_t>(c, nnz);
+  uint32_t *ix0 = dalloc_t<uint32_t>(c, nnz), *ix1 = dalloc_t<uint32_t>(c, nnz);
+  unsigned long long *dcnt = dalloc_t<unsigned long long>(c, P);
+  CK(cudaMemsetAsync(dcnt, 0, sizeof(unsigned long long) * P, c->st));
+  if (nnz > 0) {
+    k_dest_rank<IT><<<(unsigned)ceil_div(nnz, 256), 256, 0, c->st>>>(coords, nnz, D, k, dbound, P, dk0, ix0, dcnt);
+    CK_LAUNCH();
+  }
+  std::vector<unsigned long long> hcnt(P);
+  CK(cudaMemcpyAsync(hcnt.data(), dcnt, sizeof(unsigned long long) * P, cudaMemcpyDeviceToHost, c->st));
+  cub::DoubleBuffer<uint32_t> kb(dk0, dk1), vb(ix0, ix1);
+  int dbits = 1;
+  while ((1 << dbits) < P) ++dbits;
+  size_t tb = 0;
+  CK(cub::DeviceRadixSort::SortPairs(nullptr, tb, kb, vb, nnz, 0, dbits, c->st));
+  void *tmp = dalloc(c, tb);
+  CK(cub::DeviceRadixSort::SortPairs(tmp, tb, kb, vb, nnz, 0, dbits, c->st));
+  // pack coords (D x IT) and vals in destination order
+  IT *scoord = dalloc_t<IT>(c, nnz * D);
+  VT *sval = dalloc_t<VT>(c, nnz);
+  if (nnz > 0) {
+    k_pack_nz<IT, VT><<<(unsigned)ceil_div(nnz, 256), 256, 0, c->st>>>(coords, vals, nnz, D, vb.Current(), scoord,
+                                                                       sval);
+    CK_LAUNCH();
+  }
+  sync(c);
+  dfree(c, tmp); dfree(c, dk0); dfree(c, dk1); dfree(c, ix0); dfree(c, ix1); dfree(c, dcnt); dfree(c, dbound);
+  // exchange counts, then coordinates and values
+  std::vector<int64_t> mine(P);
+  for (int q = 0; q < P; ++q) mine[q] = (int64_t)hcnt[q];
+  std::vector<int64_t> all = c->comm->allgather_host(mine, c->st);   // all[p*P + q] = count p -> q
+  std::vector<int64_t> soff_c(P + 1, 0), roff_c(P + 1, 0), soff_v(P + 1, 0), roff_v(P + 1, 0);
+  for (int q = 0; q < P; ++q) {
+    soff_c[q + 1] = soff_c[q] + mine[q] * D * (int64_t)sizeof(IT);
+    soff_v[q + 1] = soff_v[q] + mine[q] * (int64_t)sizeof(VT);
+    const int64_t rc = all[(int64_t)q * P + c->wrank];
+    roff_c[q + 1] = roff_c[q] + rc * D * (int64_t)sizeof(IT);
+    roff_v[q + 1] = roff_v[q] + rc * (int64_t)sizeof(VT);
+  }
+  const int64_t nrecv = roff_v[P] / (int64_t)sizeof(VT);
+  if (nrecv >= (int64_t(1) << 32)) throw ApiError(CPARLS_ERANGE, "a rank's slice of a mode exceeds 2^32 nonzeros");
+  IT *rcoord = dalloc_t<IT>(c, nrecv * D);
+  VT *rval = dalloc_t<VT>(c, nrecv);
+  c->comm->alltoallv((const char *)scoord, soff_c, (char *)rcoord, roff_c, c->st);
+  c->comm->alltoallv((const char *)sval, soff_v, (char *)rval, roff_v, c->st);
+  sync(c);
+  dfree(c, scoord);
+  dfree(c, sval);
+  build_index_mode<IT, VT>(c, k, rcoord, rval, nrecv);
+  sync(c);
+  dfree(c, rcoord);
+  dfree(c, rval);
+}
+
 template <typename IT, typename VT>
 void build_all(cparls_ctx *c, const IT *coords, const VT *vals) {
   KeySpec ks{};
@@ -455,14 +587,23 @@ void build_all(cparls_ctx *c, const IT *coords, const VT *vals) {
     CK_LAUNCH();
   }
   if (read_dev(c, &c->dv->bad) != 0) throw ApiError(CPARLS_ERANGE, "coordinate out of range [0, n_k)");
-  // ||X||^2 (compensated)
+  // ||X||^2 (compensated; summed over ranks)
   const int nb = 296;
   k_sumsq<VT><<<nb, 256, 0, c->st>>>(vals, c->nnz, c->ddpart);
   CK_LAUNCH();
   k_sum_dd_final<<<1, 32, 0, c->st>>>(c->ddpart, nb, &c->dv->normX2);
   CK_LAUNCH();
+  if (c->world > 1) c->comm->allreduce_f64(&c->dv->normX2, 1, c->st);
   c->normX2 = read_dev(c, &c->dv->normX2);
-  for (int k = 0; k < c->D; ++k) build_index_mode<IT, VT>(c, k, coords, vals);
+  for (int k = 0; k < c->D; ++k) {
+    if (c->world == 1) {
+      c->row_lo[k] = 0;
+      c->row_hi[k] = c->dims[k];
+      build_index_mode<IT, VT>(c, k, coords, vals, c->nnz);
+    } else {
+      route_and_build<IT, VT>(c, k, coords, vals);
+    }
+  }
 }
 
 void alloc_sample_buffers(cparls_ctx *c, int64_t s) {
@@ -854,13 +995,23 @@ void solve_impl(cparls_ctx *c, int k, cparls_solve_info *info) {
     Phase ph(c, &c->stats.ms_solve);
     k_solve_prep<<<1, 128, prep_smem(r), c->st>>>(r, c->sd);
     CK_LAUNCH();
-    const int64_t grid = row_grid(c, ceil_div(nk, kRowThreads));
+    // this rank's rows of B (all rows on one GPU); M is zero elsewhere
+    const int64_t r0 = c->row_lo[k], nown = c->row_hi[k] - c->row_lo[k];
+    const int64_t grid = row_grid(c, ceil_div(std::max<int64_t>(nown, 1), kRowThreads));
     CK(cudaMemsetAsync(&c->dv->touched, 0, sizeof(unsigned long long), c->st));
     RSWITCH(r, k_solve_rows_t<RM><<<(unsigned)grid, kRowThreads, solve_smem(r, ld), c->st>>>(
-                   c->M, nk, r, ld, c->sd, c->A[k], c->gpart, &c->dv->touched));
+                   c->M + r0 * ld, nown, r, ld, c->sd, c->A[k] + r0 * ld, c->gpart, &c->dv->touched));
     CK_LAUNCH();
     k_pairs_reduce<<<pairs_reduce_grid(r), 256, 0, c->st>>>(c->gpart, grid, r, c->sd->BtB);
     CK_LAUNCH();
+    if (c->world > 1) {
+      // Gram of B over all ranks' rows (r x r), then every rank gets all B rows
+      c->comm->allreduce_f64(c->sd->BtB, (size_t)r * r, c->st);
+      std::vector<int64_t> off(c->world + 1);
+      for (int q = 0; q <= c->world; ++q) off[q] = q < c->world ? row_start(c, k, q) * ld : nk * ld;
+      c->comm->allgatherv_f64(c->A[k], off, c->st);
+      c->comm->allreduce_u64(&c->dv->touched, 1, c->st);
+    }
     k_norm_prep<<<1, 128, prep_smem(r), c->st>>>(r, c->sd, c->md[k]);
     CK_LAUNCH();
     LAUNCHED(c, 4);
@@ -874,6 +1025,7 @@ void solve_impl(cparls_ctx *c, int k, cparls_solve_info *info) {
     int64_t mk;
     unsigned long long touched;
   } hv;
+  if (c->world > 1) c->comm->allreduce_u64(reinterpret_cast<unsigned long long *>(&c->dv->mk), 1, c->st);
   CK(cudaMemcpyAsync(&hv.mk, &c->dv->mk, sizeof(long long), cudaMemcpyDeviceToHost, c->st));
   CK(cudaMemcpyAsync(&hv.touched, &c->dv->touched, sizeof(unsigned long long), cudaMemcpyDeviceToHost, c->st));
   int ru = 0, fb = 0;
@@ -918,21 +1070,21 @@ double fit_impl(cparls_ctx *c) {
     const size_t smem = fit_stage_smem(c->r, c->ld);
     if (c->vf32)
       RSWITCH(c->r, k_fit_stage<float, RM><<<nb, kFitThreads, smem, c->st>>>(
-                        c->idx[k].key, c->idx[k].out, (const float *)c->idx[k].val, c->nnz, fd, c->A[k],
+                        c->idx[k].key, c->idx[k].out, (const float *)c->idx[k].val, c->idx[k].nnz, fd, c->A[k],
                         c->lam_model, c->r, c->ld, c->ddpart));
     else
       RSWITCH(c->r, k_fit_stage<double, RM><<<nb, kFitThreads, smem, c->st>>>(
-                        c->idx[k].key, c->idx[k].out, (const double *)c->idx[k].val, c->nnz, fd, c->A[k],
+                        c->idx[k].key, c->idx[k].out, (const double *)c->idx[k].val, c->idx[k].nnz, fd, c->A[k],
                         c->lam_model, c->r, c->ld, c->ddpart));
   } else {
     const size_t smem = sizeof(double) * kFitThreads * (size_t)(c->r | 1);
     if (c->vf32)
       RSWITCH(c->r, k_fit_thread<float, RM><<<nb, kFitThreads, smem, c->st>>>(
-                        c->idx[k].key, c->idx[k].out, (const float *)c->idx[k].val, c->nnz, fd, c->A[k],
+                        c->idx[k].key, c->idx[k].out, (const float *)c->idx[k].val, c->idx[k].nnz, fd, c->A[k],
                         c->lam_model, c->r, c->ld, c->ddpart));
     else
       RSWITCH(c->r, k_fit_thread<double, RM><<<nb, kFitThreads, smem, c->st>>>(
-                        c->idx[k].key, c->idx[k].out, (const double *)c->idx[k].val, c->nnz, fd, c->A[k],
+                        c->idx[k].key, c->idx[k].out, (const double *)c->idx[k].val, c->idx[k].nnz, fd, c->A[k],
                         c->lam_model, c->r, c->ld, c->ddpart));
   }
   CK_LAUNCH();
@@ -942,9 +1094,21 @@ double fit_impl(cparls_ctx *c) {
   k_fit_final<<<1, 256, 0, c->st>>>(c->ddpart, nb, fm, c->lam_model, c->r, c->normX2, c->dv->fit);
   CK_LAUNCH();
   LAUNCHED(c, 2);
-  double f = read_dev(c, &c->dv->fit[0]);
+  double f;
+  if (c->world > 1) {
+    // <X,M> is a sum over the ranks' slices of the fit mode
+    c->comm->allreduce_f64(&c->dv->fit[1], 1, c->st);
+    double hv[3];
+    CK(cudaMemcpyAsync(hv, c->dv->fit, sizeof(hv), cudaMemcpyDeviceToHost, c->st));
+    sync(c);
+    double resid2 = c->normX2 - 2.0 * hv[1] + hv[2];
+    if (resid2 < 0.0) resid2 = 0.0;
+    f = 1.0 - std::sqrt(resid2) / std::sqrt(c->normX2);
+  } else {
+    f = read_dev(c, &c->dv->fit[0]);
+  }
   c->stats.fits++;
-  c->stats.bytes_fit += (double)c->nnz * (8.0 + 4.0 + (c->vf32 ? 4.0 : 8.0));
+  c->stats.bytes_fit += (double)c->idx[k].nnz * (8.0 + 4.0 + (c->vf32 ? 4.0 : 8.0));
   ph.end();
   return f;
 }
@@ -1000,7 +1164,15 @@ cparls_status cparls_create(cparls_ctx **out, int32_t nmodes, const int64_t *dim
     if (nnz_local < 0) throw ApiError(CPARLS_EINVAL, "nnz < 0");
     if (nnz_local >= (int64_t(1) << 32)) throw ApiError(CPARLS_ERANGE, "nnz_local must be < 2^32 per GPU");
     if (nnz_local > 0 && (!coords || !vals)) throw ApiError(CPARLS_EINVAL, "null coords/vals");
-    if (opts->world_size > 1) throw ApiError(CPARLS_EINVAL, "world_size > 1 not supported by this build");
+    if (opts->world_size < 1 || opts->world_rank < 0 || opts->world_rank >= opts->world_size)
+      throw ApiError(CPARLS_EINVAL, "bad world_size / world_rank");
+    if (opts->world_size > 1) {
+      if (!opts->comm) throw ApiError(CPARLS_EINVAL, "world_size > 1 needs opts.comm");
+      if (opts->comm->world != opts->world_size) throw ApiError(CPARLS_EINVAL, "comm size != world_size");
+      c->comm = make_comm(opts->comm, opts->world_rank);
+    }
+    c->world = opts->world_size;
+    c->wrank = opts->world_rank;
     c->D = nmodes;
     c->r = opts->rank;
     c->ld = (c->r + 3) & ~3;
@@ -1087,11 +1259,18 @@ cparls_status cparls_create(cparls_ctx **out, int32_t nmodes, const int64_t *dim
     // keys: most reuse of the fiber vector h), ties -> smaller n_k
     for (int m = 0; m < nmodes; ++m) {
       CK(cudaMemsetAsync(&c->dv->counter, 0, sizeof(unsigned long long), c->st));
-      if (c->nnz > 0) {
-        k_count_fibers<<<592, 256, 0, c->st>>>(c->idx[m].key, c->nnz, &c->dv->counter);
+      if (c->idx[m].nnz > 0) {
+        k_count_fibers<<<592, 256, 0, c->st>>>(c->idx[m].key, c->idx[m].nnz, &c->dv->counter);
         CK_LAUNCH();
       }
+      if (c->world > 1) c->comm->allreduce_u64(&c->dv->counter, 1, c->st);   // same fit mode on all ranks
       c->nfib[m] = (int64_t)read_dev(c, &c->dv->counter);
+    }
+    int64_t nnz_global = c->nnz;
+    if (c->world > 1) {
+      std::vector<int64_t> all = c->comm->allgather_host({c->nnz}, c->st);
+      nnz_global = 0;
+      for (int64_t v : all) nnz_global += v;
     }
     // per nonzero one A_{k*} row; per fiber one A_{m_1} row (m_1 = fastest key
     // mode); expected miss traffic grows with the factor sizes
@@ -1099,7 +1278,7 @@ cparls_status cparls_create(cparls_ctx **out, int32_t nmodes, const int64_t *dim
       double best = 0;
       for (int m = 0; m < nmodes; ++m) {
         const int m1 = (m == 0) ? 1 : 0;
-        const double cost = (double)c->nnz * (double)c->dims[m] + (double)c->nfib[m] * (double)c->dims[m1];
+        const double cost = (double)nnz_global * (double)c->dims[m] + (double)c->nfib[m] * (double)c->dims[m1];
         if (m == 0 || cost < best) { best = cost; c->fit_mode = m; }
       }
     }
@@ -1117,6 +1296,7 @@ cparls_status cparls_create(cparls_ctx **out, int32_t nmodes, const int64_t *dim
   if (st != CPARLS_OK) {
     g_create_err = c->err;
     for (void *p : c->allocs) cudaFree(p);
+    delete c->comm;
     delete c;
     return st;
   }
@@ -1128,6 +1308,7 @@ cparls_status cparls_destroy(cparls_ctx *c) {
   if (!c) return CPARLS_OK;
   if (!c->poisoned) cudaStreamSynchronize(c->st);
   for (void *p : c->allocs) cudaFree(p);
+  delete c->comm;
   delete c;
   return CPARLS_OK;
 }
@@ -1373,6 +1554,64 @@ cparls_status cparls_run(cparls_ctx *c, int32_t iters, int64_t s, uint64_t seed,
       if (fit_trace) fit_trace[t] = f;
     }
   });
+}
+
+cparls_status cparls_comm_nccl_unique_id(uint8_t id[128]) {
+  if (!id) return CPARLS_EINVAL;
+  static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
+  ncclUniqueId u;
+  if (ncclGetUniqueId(&u) != ncclSuccess) return CPARLS_ENCCL;
+  std::memcpy(id, &u, 128);
+  return CPARLS_OK;
+}
+
+cparls_status cparls_comm_create_nccl(int32_t world_size, int32_t rank, const uint8_t id[128], cparls_comm **out) {
+  if (!out || !id || world_size < 1 || rank < 0 || rank >= world_size) return CPARLS_EINVAL;
+  ncclUniqueId u;
+  std::memcpy(&u, id, 128);
+  auto *cc = new (std::nothrow) cparls_comm();
+  if (!cc) return CPARLS_EOOM;
+  cc->kind = 0;
+  cc->world = world_size;
+  cc->rank = rank;
+  if (ncclCommInitRank(&cc->nccl, world_size, u, rank) != ncclSuccess) {
+    delete cc;
+    return CPARLS_ENCCL;
+  }
+  *out = cc;
+  return CPARLS_OK;
+}
+
+cparls_status cparls_comm_create_local(int32_t world_size, cparls_comm **out) {
+  if (!out || world_size < 1) return CPARLS_EINVAL;
+  auto *cc = new (std::nothrow) cparls_comm();
+  if (!cc) return CPARLS_EOOM;
+  cc->kind = 1;
+  cc->world = world_size;
+  cc->group = new cparls::LocalGroup(world_size);
+  *out = cc;
+  return CPARLS_OK;
+}
+
+cparls_status cparls_comm_destroy(cparls_comm *cc) {
+  if (!cc) return CPARLS_OK;
+  if (cc->kind == 0 && cc->nccl) ncclCommDestroy(cc->nccl);
+  delete cc->group;
+  delete cc;
+  return CPARLS_OK;
+}
+
+cparls_status cparls_plan_rows(int64_t n, const uint64_t *deg, int32_t world_size, int64_t *bound) {
+  if (n < 0 || world_size < 1 || !bound || (n > 0 && !deg)) return CPARLS_EINVAL;
+  plan_rows(n, reinterpret_cast<const unsigned long long *>(deg), world_size, bound);
+  return CPARLS_OK;
+}
+
+cparls_status cparls_owned_rows(const cparls_ctx *c, int32_t mode, int64_t *lo, int64_t *hi) {
+  if (!c || mode < 0 || mode >= c->D) return CPARLS_EINVAL;
+  if (lo) *lo = c->row_lo[mode];
+  if (hi) *hi = c->row_hi[mode];
+  return CPARLS_OK;
 }
 
 cparls_status cparls_get_stats(cparls_ctx *c, cparls_stats *s) {

@@ -738,7 +738,51 @@ __global__ void k_gather_fibers(const int64_t *__restrict__ off, const int64_t *
   }
 }
 
+// ---- sharded build: row degrees, destination ranks, packing ----
+template <typename IT>
+__global__ void k_coord_degree(const IT *__restrict__ coords, int64_t nnz, int D, int k,
+                               unsigned long long *__restrict__ deg) {
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < nnz; e += (int64_t)gridDim.x * blockDim.x)
+    atomicAdd(deg + (int64_t)coords[e * D + k], 1ull);
+}
+
+template <typename IT>
+__global__ void k_dest_rank(const IT *__restrict__ coords, int64_t nnz, int D, int k,
+                            const int64_t *__restrict__ bound, int P, uint32_t *__restrict__ dest,
+                            uint32_t *__restrict__ idx, unsigned long long *__restrict__ cnt) {
+  __shared__ unsigned long long h[256];
+  for (int i = threadIdx.x; i < P; i += blockDim.x) h[i] = 0;
+  __syncthreads();
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e < nnz) {
+    const int64_t row = (int64_t)coords[e * D + k];
+    int lo = 0, len = P;   // last p with bound[p] <= row
+    while (len > 0) {
+      int half = len >> 1;
+      if (bound[lo + half + 1] <= row) { lo += half + 1; len -= half + 1; }
+      else len = half;
+    }
+    dest[e] = (uint32_t)lo;
+    idx[e] = (uint32_t)e;
+    atomicAdd(&h[lo], 1ull);
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < P; i += blockDim.x)
+    if (h[i]) atomicAdd(cnt + i, h[i]);
+}
+
+template <typename IT, typename VT>
+__global__ void k_pack_nz(const IT *__restrict__ coords, const VT *__restrict__ vals, int64_t nnz, int D,
+                          const uint32_t *__restrict__ perm, IT *__restrict__ sc, VT *__restrict__ sv) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= nnz) return;
+  const int64_t e = perm[t];
+  for (int m = 0; m < D; ++m) sc[t * D + m] = coords[e * D + m];
+  sv[t] = vals[e];
+}
+
 }  // namespace cparls
+
 
 #include "rows.cuh"
 #include "rhs.cuh"
