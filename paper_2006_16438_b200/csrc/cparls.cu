@@ -239,7 +239,7 @@ struct Phase {
 
 #define LAUNCHED(c, n) ((c)->stats.kernel_launches += (n))
 
-inline int rmax_bucket(int r) { return r <= 4 ? 4 : r <= 8 ? 8 : r <= 16 ? 16 : r <= 32 ? 32 : 64; }
+inline int rmax_bucket(int r) { return r <= 4 ? 4 : r <= 8 ? 8 : r <= 16 ? 16 : r <= 28 ? 28 : r <= 32 ? 32 : 64; }
 
 #define RSWITCH(r, ...)                                      \
   do {                                                       \
@@ -247,6 +247,7 @@ inline int rmax_bucket(int r) { return r <= 4 ? 4 : r <= 8 ? 8 : r <= 16 ? 16 : 
       case 4: { constexpr int RM = 4; __VA_ARGS__; } break;   \
       case 8: { constexpr int RM = 8; __VA_ARGS__; } break;   \
       case 16: { constexpr int RM = 16; __VA_ARGS__; } break; \
+      case 28: { constexpr int RM = 28; __VA_ARGS__; } break; \
       case 32: { constexpr int RM = 32; __VA_ARGS__; } break; \
       default: { constexpr int RM = 64; __VA_ARGS__; } break; \
     }                                                        \
@@ -289,7 +290,8 @@ void set_attrs_rm() {
 }
 
 void set_kernel_attrs(int r, int ld) {
-  set_attrs_rm<4>(); set_attrs_rm<8>(); set_attrs_rm<16>(); set_attrs_rm<32>(); set_attrs_rm<64>();
+  set_attrs_rm<4>(); set_attrs_rm<8>(); set_attrs_rm<16>(); set_attrs_rm<28>(); set_attrs_rm<32>();
+  set_attrs_rm<64>();
   int prep = (int)prep_smem(r);
   CK(cudaFuncSetAttribute(k_lev_prep, cudaFuncAttributeMaxDynamicSharedMemorySize, prep));
   CK(cudaFuncSetAttribute(k_norm_prep, cudaFuncAttributeMaxDynamicSharedMemorySize, prep));

@@ -59,43 +59,65 @@ __global__ void __launch_bounds__(kRhsThreads) k_rhs(const int64_t *__restrict__
       else len = half;
     }
     int64_t jcur = a - 1;   // segment of the first entry of the current 32-group
-    int64_t jz = -1;        // sample whose (w^2, z) are loaded
-    double coefw = 0.0, z0 = 0.0, z1 = 0.0;
+    int64_t jz = -1;        // sample whose z row is loaded
+    double z0 = 0.0, z1 = 0.0;
     for (int64_t t = t0; t < t1; t += 32) {
       const int64_t tt = t + lane;
+      const bool valid = tt < t1;
       int64_t jj = jcur;
       while (jj + 1 < nseg && __ldg(off + jj + 1) <= tt) ++jj;
-      int32_t o_l = 0;
-      int s_l = -1;
-      double x_l = 0.0;
-      int64_t j_l = 0;
-      if (tt < t1) {
+      int64_t j_l = -1;
+      long long os_l = 0;    // (hot slot << 32) | output row
+      double cx_l = 0.0;     // w_j^2 * x_e
+      if (valid) {
         j_l = seg_j ? (int64_t)__ldg(seg_j + jj) : jj;
         const int64_t e = __ldg(lo + jj) + (tt - __ldg(off + jj));
-        o_l = ld_stream(outidx + e, pstream);
-        x_l = (double)ld_stream(vals + e, pstream);
-        s_l = __ldg(hot_slot + o_l);
-        if (s_l >= nhot) s_l = -1;
+        const int32_t o = ld_stream(outidx + e, pstream);
+        int sl = __ldg(hot_slot + o);
+        if (sl >= nhot) sl = -1;
+        os_l = ((long long)sl << 32) | (unsigned)o;
+        cx_l = __ldg(sw2 + j_l) * (double)ld_stream(vals + e, pstream);
       }
       const int cnt = (int)min((int64_t)32, t1 - t);
-      for (int u = 0; u < cnt; ++u) {
-        const int32_t o = __shfl_sync(0xffffffffu, o_l, u);
-        const double x = __shfl_sync(0xffffffffu, x_l, u);
-        const int s = __shfl_sync(0xffffffffu, s_l, u);
-        const int64_t ju = __shfl_sync(0xffffffffu, j_l, u);   // sample of the entry
-        if (ju != jz) {
-          jz = ju;
-          coefw = __ldg(sw2 + ju);
-          z0 = lane < r ? __ldg(Z + ju * ld + lane) : 0.0;
-          if (HI) z1 = lane + 32 < r ? __ldg(Z + ju * ld + lane + 32) : 0.0;
+      const int64_t j0 = __shfl_sync(0xffffffffu, j_l, 0);
+      if (__all_sync(0xffffffffu, !valid || j_l == j0)) {
+        // whole group inside one fiber: one z row for all 32 entries
+        if (j0 != jz) {
+          jz = j0;
+          z0 = lane < r ? __ldg(Z + j0 * ld + lane) : 0.0;
+          if (HI) z1 = lane + 32 < r ? __ldg(Z + j0 * ld + lane + 32) : 0.0;
         }
-        const double cx = coefw * x;
-        if (s >= 0) {   // hot row: warp-private shared accumulator, no atomics
-          if (lane < r) mine[s * r + lane] += cx * z0;
-          if (HI && lane + 32 < r) mine[s * r + lane + 32] += cx * z1;
-        } else {
-          if (lane < r) atomicAdd(M + (int64_t)o * ld + lane, cx * z0);
-          if (HI && lane + 32 < r) atomicAdd(M + (int64_t)o * ld + lane + 32, cx * z1);
+#pragma unroll 4
+        for (int u = 0; u < cnt; ++u) {
+          const long long os = __shfl_sync(0xffffffffu, os_l, u);
+          const double cx = __shfl_sync(0xffffffffu, cx_l, u);
+          const int o = (int)(unsigned)os, sl = (int)(os >> 32);
+          if (sl >= 0) {   // hot row: warp-private shared accumulator, no atomics
+            if (lane < r) mine[sl * r + lane] += cx * z0;
+            if (HI && lane + 32 < r) mine[sl * r + lane + 32] += cx * z1;
+          } else {
+            if (lane < r) atomicAdd(M + (int64_t)o * ld + lane, cx * z0);
+            if (HI && lane + 32 < r) atomicAdd(M + (int64_t)o * ld + lane + 32, cx * z1);
+          }
+        }
+      } else {
+        for (int u = 0; u < cnt; ++u) {
+          const long long os = __shfl_sync(0xffffffffu, os_l, u);
+          const double cx = __shfl_sync(0xffffffffu, cx_l, u);
+          const int64_t ju = __shfl_sync(0xffffffffu, j_l, u);
+          if (ju != jz) {
+            jz = ju;
+            z0 = lane < r ? __ldg(Z + ju * ld + lane) : 0.0;
+            if (HI) z1 = lane + 32 < r ? __ldg(Z + ju * ld + lane + 32) : 0.0;
+          }
+          const int o = (int)(unsigned)os, sl = (int)(os >> 32);
+          if (sl >= 0) {
+            if (lane < r) mine[sl * r + lane] += cx * z0;
+            if (HI && lane + 32 < r) mine[sl * r + lane + 32] += cx * z1;
+          } else {
+            if (lane < r) atomicAdd(M + (int64_t)o * ld + lane, cx * z0);
+            if (HI && lane + 32 < r) atomicAdd(M + (int64_t)o * ld + lane + 32, cx * z1);
+          }
         }
       }
       jcur = __shfl_sync(0xffffffffu, jj, 31);
