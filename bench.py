@@ -107,12 +107,8 @@ class Clocks:
 
 
 def fit_kernel_name(cfg):
-    """The fit kernel libcparls picks (k_fit_stage when the fit-mode factor is
-    larger than ~half of L2, else k_fit_thread); the fit mode is one of the
-    modes, and for C4/C5 every factor exceeds 64 MB."""
-    ld = (cfg.rank + 3) // 4 * 4
-    big = min(cfg.dims) * ld * 8 > 64 * (1 << 20)
-    return ("k_fit_stage" if big else "k_fit_thread") + " (exact fit, P:867-875; dominant kernel per iteration)"
+    """The exact-fit kernel libcparls launches for D <= 4 (k_fit_cols)."""
+    return "k_fit_cols (exact fit, P:867-875; dominant kernel per iteration)"
 
 
 def traffic_for(kernel, config):

@@ -285,8 +285,6 @@ void set_attrs_rm() {
   max_dyn_smem(k_krp_gram_t<RM>);
   max_dyn_smem(k_fit_thread<float, RM>);
   max_dyn_smem(k_fit_thread<double, RM>);
-  max_dyn_smem(k_fit_stage<float, RM>);
-  max_dyn_smem(k_fit_stage<double, RM>);
 }
 
 void set_kernel_attrs(int r, int ld) {
@@ -953,7 +951,11 @@ void solve_impl(cparls_ctx *c, int k, cparls_solve_info *info) {
   {
     Phase ph(c, &c->stats.ms_rhs);
     if (sbar > 0) {
-      const int64_t RW = std::max<int64_t>(1, (int64_t(48) << 20) / ((int64_t)ld * 8));
+      static const int win_mb = getenv("CPARLS_RHS_WIN_MB") ? atoi(getenv("CPARLS_RHS_WIN_MB")) : 96;
+      static const int grid_mult = getenv("CPARLS_RHS_GRID") ? atoi(getenv("CPARLS_RHS_GRID")) : 8;
+      static const int nhot_env = getenv("CPARLS_RHS_NHOT") ? atoi(getenv("CPARLS_RHS_NHOT")) : 0;
+      const int nhot = nhot_env >= 0 ? std::min(nhot_env, rhs_nhot(r)) : rhs_nhot(r);
+      const int64_t RW = std::max<int64_t>(1, (int64_t(win_mb) << 20) / ((int64_t)ld * 8));
       const int nwin = (int)ceil_div(nk, RW);
       const int64_t nseg = (int64_t)nwin * sbar;
       if (nseg > c->segcap) {
@@ -977,13 +979,13 @@ void solve_impl(cparls_ctx *c, int k, cparls_solve_info *info) {
         LAUNCHED(c, 4);
       }
       CK(cudaMemsetAsync(&c->dv->counter, 0, sizeof(unsigned long long), c->st));
-      const int grid = 148 * 2;
+      const int grid = 148 * grid_mult;
       const int64_t per_warp = 512;
 #define RHS(VT, HI)                                                                                               \
-  k_rhs<VT, HI><<<grid, kRhsThreads, rhs_smem(r), c->st>>>(c->seg_off, c->seg_lo, nwin > 1 ? c->seg_j : nullptr, nseg, &c->dv->mk,          \
+  k_rhs<VT, HI><<<grid, kRhsThreads, sizeof(double) * (size_t)kRhsWarps * nhot * r, c->st>>>(c->seg_off, c->seg_lo, nwin > 1 ? c->seg_j : nullptr, nseg, &c->dv->mk,          \
                                                            &c->dv->counter, c->idx[k].out, (const VT *)c->idx[k].val, \
                                                            c->sw2, c->Z, c->hot_slot[k], c->hot_row[k],            \
-                                                           rhs_nhot(r), r, ld, c->M, per_warp)
+                                                           nhot, r, ld, c->M, per_warp)
       if (c->vf32) { if (r > 32) RHS(float, true); else RHS(float, false); }
       else { if (r > 32) RHS(double, true); else RHS(double, false); }
 #undef RHS
@@ -1064,20 +1066,31 @@ double fit_impl(cparls_ctx *c) {
     ++j;
   }
   fd.fast = N < 9007199254740992.0L;   // keys < 2^53
-  const int nb = 148 * 4;
-  // factor of the fit mode larger than ~half of L2: stage its rows with
-  // coalesced cp.async (k_fit_stage); otherwise plain per-thread gathers hit L2
-  const bool stage = (double)c->dims[k] * c->ld * 8.0 > 64.0 * (1 << 20) && fit_stage_smem(c->r, c->ld) <= 200 * 1024;
-  if (stage) {
-    const size_t smem = fit_stage_smem(c->r, c->ld);
-    if (c->vf32)
-      RSWITCH(c->r, k_fit_stage<float, RM><<<nb, kFitThreads, smem, c->st>>>(
-                        c->idx[k].key, c->idx[k].out, (const float *)c->idx[k].val, c->idx[k].nnz, fd, c->A[k],
-                        c->lam_model, c->r, c->ld, c->ddpart));
-    else
-      RSWITCH(c->r, k_fit_stage<double, RM><<<nb, kFitThreads, smem, c->st>>>(
-                        c->idx[k].key, c->idx[k].out, (const double *)c->idx[k].val, c->idx[k].nnz, fd, c->A[k],
-                        c->lam_model, c->r, c->ld, c->ddpart));
+  int nb = 148 * 4;
+  if (fd.d <= 3) {
+    // sub-warp per entry, 4 columns per lane (k_fit_sub)
+    nb = 148 * 2;
+    CK(cudaMemsetAsync(&c->dv->counter, 0, sizeof(unsigned long long), c->st));
+#define FITS(VT, SW, DM)                                                                                         \
+  k_fit_sub<VT, SW, DM, (SW >= CPARLS_FIT_U ? CPARLS_FIT_U : SW)><<<nb, kFitThreads, 0, c->st>>>(c->idx[k].key, c->idx[k].out, (const VT *)c->idx[k].val, \
+                                                          c->idx[k].nnz, fd, c->A[k], c->lam_model, c->r, c->ld,  \
+                                                          c->ddpart, &c->dv->counter)
+#define FITSD(VT, SW)                          \
+  do {                                         \
+    if (fd.d == 1) FITS(VT, SW, 1);            \
+    else if (fd.d == 2) FITS(VT, SW, 2);       \
+    else FITS(VT, SW, 3);                      \
+  } while (0)
+#define FITSV(VT)                                        \
+  do {                                                   \
+    if (c->ld <= 8) FITSD(VT, 2);                        \
+    else if (c->ld <= 32) FITSD(VT, 8);                  \
+    else FITSD(VT, 16);                                  \
+  } while (0)
+    if (c->vf32) FITSV(float); else FITSV(double);
+#undef FITSV
+#undef FITSD
+#undef FITS
   } else {
     const size_t smem = sizeof(double) * kFitThreads * (size_t)(c->r | 1);
     if (c->vf32)

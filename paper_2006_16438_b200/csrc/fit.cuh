@@ -1,11 +1,13 @@
 // fit.cuh -- K10 exact fit (eq:fit P:867-875): the inner product <X, M> of the
 // tensor with the Kruskal model, streamed over the fit mode k*'s sorted copy.
 //
-// Nonzeros of one fiber share the other-mode rows, so per fiber the leader
-// lane forms h = lambda * A_{m_1}(i_1,:) * ... * A_{m_d}(i_d,:) once (into a
-// per-lane shared slot) and every nonzero then needs only its own
-// A_{k*}(out,:) row: <X,M> = sum_e x_e <h_fiber(e), A_{k*}(out_e,:)>.  Keys
-// are decoded with an fp64 reciprocal plus an exact integer correction.
+// Nonzeros of one fiber share the other-mode rows, so per fiber
+// h = lambda * A_{m_1}(i_1,:) * ... * A_{m_d}(i_d,:) is formed once and every
+// nonzero then needs only its own A_{k*}(out,:) row:
+// <X,M> = sum_e x_e <h_fiber(e), A_{k*}(out_e,:)>.  k_fit_sub (D <= 4) maps one
+// entry to a sub-warp of ld/4 lanes; k_fit_thread (D > 4) maps one entry to a
+// thread.  Keys are decoded with an fp64 reciprocal plus an exact integer
+// correction.
 #pragma once
 #include "common.cuh"
 
@@ -114,91 +116,154 @@ __global__ void __launch_bounds__(kFitThreads, 2) k_fit_thread(const uint64_t *_
   }
 }
 
-__device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
-  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit_wait() {
-  asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
-}
+// Work is taken in kFitChunk-entry chunks from a global counter; h depends only
+// on the key, so a fiber split across chunks is simply restarted.
+constexpr int kFitChunk = 2048;
+#ifndef CPARLS_FIT_U
+#define CPARLS_FIT_U 4   // entries per sub-warp issued before any is consumed
+#endif
 
-// As k_fit_thread, but each warp stages the 32 A_{k*}(out,:) rows of its tile
-// into shared memory with coalesced 16-byte cp.async chunks (about 2.3 rows per
-// instruction instead of one row per lane), overlapping the fiber leaders' h
-// computation; lanes then read their own row from shared memory.
-template <typename VT, int RMAX>
-__global__ void __launch_bounds__(kFitThreads) k_fit_stage(const uint64_t *__restrict__ keys,
+// Sub-warp fit: SW lanes per entry, 4 columns per lane (two 16-byte loads; ld
+// is a multiple of 4, so a row is ld/4 lanes), NS = 32/SW entries per warp
+// step.  (k_fit_cols, one column per lane, spent ~45 warp instructions per
+// nonzero and was issue-bound.)  A warp takes a kFitChunk-entry chunk; sub-warp
+// s walks its own contiguous 1/NS of it, SW entries per batch loaded by its
+// own lanes, so a fiber is only restarted at a sub-range start.  Per fiber
+// h = g * A_{m_1}(i_1,:) * ... * A_{m_{d-1}}(i_{d-1},:) where g = lambda *
+// A_{m_d}(i_d,:) is cached per sub-warp: m_d is the slowest key mode, so the
+// copy is sorted by it and g changes only every ~nnz/n_{m_d} entries.
+// acc_c += x_e * A_{k*}(out_e,c) * h_c per lane: plain fp64 within a chunk,
+// folded into a double-double per chunk (AMB-16).
+template <typename VT, int SW, int DM, int U>
+__global__ void __launch_bounds__(kFitThreads, 2) k_fit_sub(const uint64_t *__restrict__ keys,
                                                           const int32_t *__restrict__ outidx,
                                                           const VT *__restrict__ vals, int64_t nnz, FitDecode fd,
                                                           const double *__restrict__ Ak,
                                                           const double *__restrict__ lam, int r, int ld,
-                                                          dd *__restrict__ part) {
-  extern __shared__ __align__(16) double fsm[];
-  const int S = ld + 2;              // even (16-byte aligned rows), 2-way conflicts at most
-  const int RS = r | 1;
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  double *tile = fsm + (size_t)w * 32 * S;                                   // 32 rows x S
-  double *hw = fsm + (size_t)(kFitThreads / 32) * 32 * S + (size_t)w * 32 * RS;   // 32 slots x RS
-  __shared__ double lam_s[kMaxRank + 1];
-  for (int c = threadIdx.x; c <= kMaxRank; c += blockDim.x) lam_s[c] = c < r ? lam[c] : 0.0;
-  __syncthreads();
-  const int H = ld / 2;              // 16-byte chunks per row
+                                                          dd *__restrict__ part,
+                                                          unsigned long long *__restrict__ work) {
+  static_assert(SW >= 2 && SW <= 32 && (SW & (SW - 1)) == 0, "SW power of two");
+  constexpr int NS = 32 / SW;
+  constexpr int SUB = kFitChunk / NS;    // entries per sub-warp per chunk (multiple of SW)
+  const int lane = threadIdx.x & 31;
+  const int sl = lane & (SW - 1);        // lane within the sub-warp
+  const int sbase = lane & ~(SW - 1);
+  const int c0 = 4 * sl;
+  const bool colok = c0 < ld;            // ld % 4 == 0: all 4 columns in bounds
+  const unsigned smask = (SW == 32) ? 0xffffffffu : (((1u << SW) - 1u) << sbase);
+  double lam4[4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) lam4[q] = (c0 + q < r) ? lam[c0 + q] : 0.0;
   const uint64_t pstream = l2_evict_first();
+  const double *Aslow = fd.A[DM - 1];
   dd acc = {0.0, 0.0};
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t e0 = (int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31); e0 < nnz; e0 += stride) {
-    const int64_t e = e0 + lane;
-    const bool valid = e < nnz;
-    const int n = (int)min((int64_t)32, nnz - e0);
-    const uint64_t key = valid ? ld_stream(keys + e, pstream) : ~0ull;
-    const int32_t o = valid ? ld_stream(outidx + e, pstream) : 0;
-    const double x = valid ? (double)ld_stream(vals + e, pstream) : 0.0;
-    // stage A rows: chunk f = lane + 32q  ->  row rho = f / H, part = f % H
-    {
-      int rho = lane / H, part = lane - (lane / H) * H;
-      for (int f = lane; f < 32 * H; f += 32) {
-        const int orow = __shfl_sync(0xffffffffu, o, rho & 31);
-        if (rho < n) cp_async16(tile + rho * S + 2 * part, Ak + (int64_t)orow * ld + 2 * part);
-        part += 32;
-        while (part >= H) { part -= H; ++rho; }
+  while (true) {
+    int64_t cb = 0;
+    if (lane == 0) cb = (int64_t)atomicAdd(work, (unsigned long long)kFitChunk);
+    cb = __shfl_sync(0xffffffffu, cb, 0);
+    if (cb >= nnz) break;
+    const int64_t s0 = cb + (int64_t)(lane / SW) * SUB;
+    const int64_t s1 = min(nnz, s0 + SUB);
+    double h[4] = {0.0, 0.0, 0.0, 0.0};
+    double g[4] = {0.0, 0.0, 0.0, 0.0};
+    double cacc[4] = {0.0, 0.0, 0.0, 0.0};
+    uint64_t last_key = ~0ull;
+    uint32_t cur_slow = 0xffffffffu;
+    // the next batch's stream entries are loaded while this batch's rows are
+    // in flight (register double buffer)
+    uint64_t nkey = (s0 + sl < s1) ? ld_stream(keys + s0 + sl, pstream) : ~0ull;
+    int32_t no = (s0 + sl < s1) ? ld_stream(outidx + s0 + sl, pstream) : 0;
+    VT nx = (s0 + sl < s1) ? ld_stream(vals + s0 + sl, pstream) : VT(0);
+    for (int64_t b0 = 0; b0 < SUB; b0 += SW) {
+      // warp-uniform trip count; a sub-warp past its end has no valid entries
+      const int64_t e = s0 + b0 + sl;
+      const bool valid = e < s1;
+      const uint64_t key = nkey;
+      const int32_t o = no;
+      const double x = (double)nx;
+      {
+        const int64_t en = e + SW;
+        const bool vn = en < s1 && b0 + SW < SUB;
+        nkey = vn ? ld_stream(keys + en, pstream) : ~0ull;
+        no = vn ? ld_stream(outidx + en, pstream) : 0;
+        nx = vn ? ld_stream(vals + en, pstream) : VT(0);
       }
-      asm volatile("cp.async.commit_group;\n" ::: "memory");
-    }
-    uint64_t prev = __shfl_up_sync(0xffffffffu, key, 1);
-    if (lane == 0) prev = ~key;
-    const bool lead = valid && key != prev;
-    const unsigned lm = __ballot_sync(0xffffffffu, lead);
-    if (lead) {
-      double *h = hw + lane * RS;
-      for (int c = 0; c < r; ++c) h[c] = lam_s[c];
-      uint64_t t = key;
-      for (int m = 0; m < fd.d; ++m) {
-        uint64_t rem;
-        t = divmod_fast(t, fd.n[m], fd.inv[m], rem, fd.fast);
-        const double2 *row = reinterpret_cast<const double2 *>(fd.A[m] + rem * ld);
-        double2 v[RMAX / 2];
+      uint64_t prev = __shfl_up_sync(0xffffffffu, key, 1, SW);
+      if (sl == 0) prev = last_key;
+      const bool lead = valid && key != prev;
+      const unsigned lm = __ballot_sync(0xffffffffu, lead);
+      const unsigned vm = __ballot_sync(0xffffffffu, valid);
+      if (vm == 0u) break;
+      uint32_t id[DM];
+      {
+        uint64_t t = key;
 #pragma unroll
-        for (int c2 = 0; c2 < RMAX / 2; ++c2) v[c2] = (2 * c2 < r) ? __ldg(row + c2) : make_double2(0.0, 0.0);
-#pragma unroll
-        for (int c2 = 0; c2 < RMAX / 2; ++c2) {
-          if (2 * c2 < r) h[2 * c2] *= v[c2].x;
-          if (2 * c2 + 1 < r) h[2 * c2 + 1] *= v[c2].y;
+        for (int m = 0; m < DM; ++m) {
+          uint64_t rem;
+          t = divmod_fast(t, fd.n[m], fd.inv[m], rem, fd.fast);
+          id[m] = (uint32_t)rem;
         }
       }
-    }
-    asm volatile("cp.async.wait_group 0;\n" ::: "memory");
-    __syncwarp();
-    if (valid) {
-      const int src = 31 - __clz(lm & (0xffffffffu >> (31 - lane)));   // last leader at or before lane
-      const double *h = hw + src * RS;
-      const double *a = tile + lane * S;
-      double mv = 0.0;
+      last_key = __shfl_sync(0xffffffffu, key, sbase + SW - 1);
 #pragma unroll
-      for (int c = 0; c < RMAX; ++c)
-        if (c < r) mv += h[c] * a[c];
-      acc = dd_add_d(acc, x * mv);
+      for (int t0 = 0; t0 < SW; t0 += U) {
+        double av[U][4];
+        double hv[U][DM > 1 ? DM - 1 : 1][4];
+        double gv[U][4];
+        bool lead_[U], slow_[U];
+        uint32_t sid[U];
+        double xv[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int src = sbase + t0 + u;
+          const bool ok = (vm >> src) & 1u;
+          lead_[u] = (lm >> src) & 1u;
+          const int ou = __shfl_sync(0xffffffffu, o, src);
+          xv[u] = __shfl_sync(0xffffffffu, x, src);
+          const double2 *row = reinterpret_cast<const double2 *>(Ak + (int64_t)ou * ld + c0);
+          double2 p0 = make_double2(0.0, 0.0), p1 = make_double2(0.0, 0.0);
+          if (ok && colok) { p0 = __ldg(row); p1 = __ldg(row + 1); }
+          av[u][0] = p0.x; av[u][1] = p0.y; av[u][2] = p1.x; av[u][3] = p1.y;
+#pragma unroll
+          for (int m = 0; m + 1 < DM; ++m) {
+            const uint32_t im = __shfl_sync(0xffffffffu, id[m], src);
+            const double2 *hr = reinterpret_cast<const double2 *>(fd.A[m] + (int64_t)im * ld + c0);
+            double2 q0 = make_double2(0.0, 0.0), q1 = make_double2(0.0, 0.0);
+            if (lead_[u] && colok) { q0 = __ldg(hr); q1 = __ldg(hr + 1); }
+            hv[u][m][0] = q0.x; hv[u][m][1] = q0.y; hv[u][m][2] = q1.x; hv[u][m][3] = q1.y;
+          }
+          sid[u] = __shfl_sync(0xffffffffu, id[DM - 1], src);
+          slow_[u] = lead_[u] && sid[u] != (u == 0 ? cur_slow : sid[u - 1]);
+          {
+            const double2 *gr = reinterpret_cast<const double2 *>(Aslow + (int64_t)sid[u] * ld + c0);
+            double2 q0 = make_double2(0.0, 0.0), q1 = make_double2(0.0, 0.0);
+            if (slow_[u] && colok) { q0 = __ldg(gr); q1 = __ldg(gr + 1); }
+            gv[u][0] = q0.x; gv[u][1] = q0.y; gv[u][2] = q1.x; gv[u][3] = q1.y;
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          if (slow_[u]) {
+#pragma unroll
+            for (int q = 0; q < 4; ++q) g[q] = lam4[q] * gv[u][q];
+          }
+          if (lead_[u]) {
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              double hh = g[q];
+#pragma unroll
+              for (int m = 0; m + 1 < DM; ++m) hh *= hv[u][m][q];
+              h[q] = hh;
+            }
+          }
+#pragma unroll
+          for (int q = 0; q < 4; ++q) cacc[q] = fma(xv[u] * av[u][q], h[q], cacc[q]);
+        }
+        // g now belongs to the fiber of the batch's last entry
+        if ((vm >> (sbase + t0 + U - 1)) & 1u) cur_slow = sid[U - 1];
+      }
     }
-    __syncwarp();
+    acc = dd_add_d(acc, (cacc[0] + cacc[1]) + (cacc[2] + cacc[3]));
   }
   acc = warp_sum_dd(acc);
   __shared__ dd ws[kFitThreads / 32];
@@ -209,10 +274,6 @@ __global__ void __launch_bounds__(kFitThreads) k_fit_stage(const uint64_t *__res
     for (int i = 0; i < kFitThreads / 32; ++i) tt = dd_add(tt, ws[i]);
     part[blockIdx.x] = tt;
   }
-}
-
-inline size_t fit_stage_smem(int r, int ld) {
-  return sizeof(double) * ((size_t)kFitThreads * (ld + 2) + (size_t)kFitThreads * (r | 1)) + 16;
 }
 
 // <X,M> from block partials; ||M||^2 = lambda^T (*_m G_m) lambda with the
