@@ -106,9 +106,35 @@ class Clocks:
                 "samples": len(sm)}
 
 
-def fit_kernel_name(cfg):
-    """The exact-fit kernel libcparls launches for D <= 4 (k_fit_cols)."""
-    return "k_fit_cols (exact fit, P:867-875; dominant kernel per iteration)"
+KERNEL_NAMES = {"rhs": "k_rhs", "fit": "k_fit_sub", "solve_rows": "k_solve_rows_t", "lev_rows": "k_lev_rows_t"}
+
+
+def measure_peaks(cfg, dev, window_rows, fit_rows):
+    """Ceilings of the hot kernels' own access patterns on this GPU, measured
+    here (libcparls_peaks.so, not part of the method): fp64 r-lane reductions
+    into random rows of an L2-sized window (k_rhs) and r-wide fp64 row gathers
+    from random rows of a factor-sized matrix (k_fit_sub)."""
+    import ctypes as C
+    import torch
+    lib = C.CDLL(os.path.join(ROOT, "paper_2006_16438_b200", "libcparls_peaks.so"))
+    lib.cparls_peak_red_f64.restype = C.c_double
+    lib.cparls_peak_red_f64.argtypes = [C.c_void_p, C.c_int64, C.c_int, C.c_int, C.c_int64, C.c_int, C.c_int]
+    lib.cparls_peak_gather.restype = C.c_double
+    lib.cparls_peak_gather.argtypes = [C.c_void_p, C.c_int64, C.c_int, C.c_int64, C.c_int, C.c_int, C.c_void_p]
+    r = cfg.rank
+    ld = (r + 3) // 4 * 4
+    torch.cuda.synchronize()
+    M = torch.zeros(window_rows * ld, dtype=torch.float64, device=dev)
+    red = lib.cparls_peak_red_f64(M.data_ptr(), window_rows, r, ld, 8192, 148 * 8, 5)
+    del M
+    A = torch.rand(fit_rows * ld, dtype=torch.float64, device=dev)
+    scr = torch.zeros(1, dtype=torch.float64, device=dev)
+    gat = lib.cparls_peak_gather(A.data_ptr(), fit_rows, ld, 32768, 148 * 8, 5, scr.data_ptr())
+    del A, scr
+    torch.cuda.synchronize()
+    torch.cuda.empty_cache()
+    return {"red_f64_lane_ops_per_s": red, "red_window_rows": window_rows,
+            "gather_bytes_per_s": gat, "gather_rows": fit_rows, "rank": r, "ld": ld}
 
 
 def traffic_for(kernel, config):
@@ -249,12 +275,11 @@ def run_ours(args):
         g.run(1, cfg.s, seed, iter0=t, fit_every=0)
     if args.profile_phases:
         g.set_profiling(True)
-    g.reset_stats()
     K = args.steps
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
-    fit_events = []
     torch.cuda.synchronize()
+    g.reset_stats()
     if ws > 1:
         dist.barrier()
     with Clocks(lrk) as clk:
@@ -263,11 +288,7 @@ def run_ours(args):
             it = args.warmup + t
             g.run(1, cfg.s, seed, iter0=it, fit_every=0)
             if (it + 1) % ETA == 0:
-                fa = torch.cuda.Event(enable_timing=True); fb = torch.cuda.Event(enable_timing=True)
-                fa.record(stream)
-                fval = g.fit()
-                fb.record(stream)
-                fit_events.append((fa, fb))
+                g.fit()
         ev1.record(stream)
         torch.cuda.synchronize()
         if ws > 1:
@@ -277,28 +298,69 @@ def run_ours(args):
         tt = torch.tensor([ms], dtype=torch.float64)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         ms = float(tt[0])
-    st = g.stats()
-    fit_ms = [a.elapsed_time(b) for a, b in fit_events]
+    st = g.stats()          # resolves the per-kernel event timers of the timed region
+    if st["fits"] == 0:     # K < ETA: time one fit so the fit kernel is still reported
+        g.fit()
+        st_fit = g.stats()
+        st["kernel_ms"]["fit"] = st_fit["kernel_ms"]["fit"]
+        st["kernel_launches_by_id"]["fit"] = st_fit["kernel_launches_by_id"]["fit"]
     value = K / (ms / 1000.0)
-    # fit kernel alone, timed live: bytes = streamed nonzeros (key u64 + out i32 + value)
     vbytes = 4 if cfg.value_dtype == "f32" else 8
-    # algorithmic bytes of one exact-fit launch: every
-    # nonzero of the fit mode's copy (key u64 + out i32 + value) plus every
-    # factor row once
-    fit_alg_bytes = nnz * (8 + 4 + vbytes) + sum(cfg.dims) * cfg.rank * 8
-    if not fit_ms:
-        fa = torch.cuda.Event(enable_timing=True); fb = torch.cuda.Event(enable_timing=True)
-        fa.record(stream); g.fit(); fb.record(stream); torch.cuda.synchronize()
-        fit_ms = [fa.elapsed_time(fb)]
-    fit_avg = sum(fit_ms) / len(fit_ms)
-    peak, peak_src = measured_peaks()
-    achieved = fit_alg_bytes / (fit_avg / 1000.0) / 1e9
     final_fit = g.fit()
     if args.profile_phases:
         sys.stderr.write(json.dumps({k: v for k, v in st.items()}, indent=1) + "\n")
     g.close()
     del g
     torch.cuda.empty_cache()
+    kms, kn = st["kernel_ms"], st["kernel_launches_by_id"]
+    # share of the timed region; a fit timed outside it (K < eta) is amortized 1/eta per step
+    share = {k: kms[k] / ms for k in kms}
+    if st["fits"] == 0 and kn["fit"]:
+        share["fit"] = kms["fit"] / kn["fit"] / ETA / (ms / K)
+    kernels = {KERNEL_NAMES[k]: {"launches": int(kn[k]), "avg_ms": (kms[k] / kn[k]) if kn[k] else None,
+                                 "share_of_step": share[k]} for k in kms}
+    dominant = max(share, key=lambda k: share[k])
+    # measured ceilings of the hot kernels' access patterns (same GPU, same run)
+    ld = (cfg.rank + 3) // 4 * 4
+    window_rows = min(max(cfg.dims), (96 << 20) // (ld * 8))
+    peaks = measure_peaks(cfg, dev, window_rows, int(sorted(cfg.dims)[len(cfg.dims) // 2]))
+    hbm_peak, peak_src = measured_peaks()
+    # k_rhs: algorithmic work = m_k * r fp64 reductions per launch (SURVEY 8(d):
+    # every matched nonzero adds w^2 x z_j to its output row); bytes = matched
+    # entries (out + value) + touched output rows read and written once
+    n_rhs = max(1, kn["rhs"])
+    rhs_red = st["sum_matched_nnz"] * cfg.rank / n_rhs
+    rhs_bytes = st["sum_matched_nnz"] * (4 + vbytes) / n_rhs + sum(cfg.dims) / D * cfg.rank * 8 * 2
+    rhs_avg_s = (kms["rhs"] / n_rhs) / 1000.0 if kn["rhs"] else None
+    # exact fit: algorithmic bytes: every nonzero of the fit
+    # mode's copy (key u64 + out i32 + value) plus every factor row once
+    fit_alg_bytes = nnz * (8 + 4 + vbytes) + sum(cfg.dims) * cfg.rank * 8
+    fit_avg_s = (kms["fit"] / max(1, kn["fit"])) / 1000.0 if kn["fit"] else None
+    rl = {}
+    if rhs_avg_s:
+        rl["rhs"] = {"bound": "l2_atomic", "kernel": "k_rhs (sampled RHS, P:949-958)",
+                     "achieved": rhs_red / rhs_avg_s / 1e9, "peak": peaks["red_f64_lane_ops_per_s"] / 1e9,
+                     "unit": "G fp64 reductions/s", "frac": (rhs_red / rhs_avg_s) / peaks["red_f64_lane_ops_per_s"],
+                     "traffic": traffic_for("k_rhs", args.config),
+                     "peak_source": "measured here: cparls_peak_red_f64, r-lane fp64 red into random rows of a "
+                                    f"{window_rows}-row window (the k_rhs pattern)",
+                     "alg_bytes_per_launch": rhs_bytes, "avg_launch_ms": rhs_avg_s * 1e3,
+                     "hbm_view": {"achieved": rhs_bytes / rhs_avg_s / 1e9, "peak": hbm_peak, "unit": "GB/s",
+                                  "frac": rhs_bytes / rhs_avg_s / 1e9 / hbm_peak}}
+    if fit_avg_s:
+        gather_bytes = nnz * ld * 8.0     # one A_{k*} row per nonzero (the per-entry gather)
+        rl["fit"] = {"bound": "hbm", "kernel": "k_fit_sub (exact fit, P:867-875)",
+                     "achieved": fit_alg_bytes / fit_avg_s / 1e9, "peak": hbm_peak, "unit": "GB/s",
+                     "frac": fit_alg_bytes / fit_avg_s / 1e9 / hbm_peak,
+                     "traffic": traffic_for("k_fit_sub", args.config), "alg_bytes_per_launch": fit_alg_bytes,
+                     "avg_launch_ms": fit_avg_s * 1e3, "peak_source": peak_src,
+                     "gather_view": {"achieved": gather_bytes / fit_avg_s / 1e9,
+                                     "peak": peaks["gather_bytes_per_s"] / 1e9, "unit": "GB/s",
+                                     "frac": gather_bytes / fit_avg_s / peaks["gather_bytes_per_s"],
+                                     "what": "per-nonzero A_k* row gathers vs measured random-row gather rate"}}
+    roofline = dict(rl.get(dominant, rl.get("rhs") or rl.get("fit") or {}))
+    roofline["dominant"] = KERNEL_NAMES[dominant]
+    roofline["others"] = {KERNEL_NAMES[k]: v for k, v in rl.items() if k != dominant}
 
     # e2e: public API from pinned host buffers (create + K iterations + fits + factors back)
     e2e = None
@@ -346,10 +408,9 @@ def run_ours(args):
                    f"{nnz * (16 if cfg.value_dtype == 'f32' else 20) * D / 1e9:.1f} GB >> 126 MB)",
                    "parallelism": f"row-sharded x{ws} (NCCL allreduce r x r + allgather of B rows per mode step)"
                    if ws > 1 else "single GPU"},
-        "roofline": {"bound": "hbm", "kernel": fit_kernel_name(cfg),
-                     "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                     "traffic": traffic_for(fit_kernel_name(cfg).split(" ")[0], args.config), "alg_bytes_per_launch": fit_alg_bytes,
-                     "avg_launch_ms": fit_avg, "launches_timed": len(fit_ms), "peak_source": peak_src},
+        "roofline": roofline,
+        "kernels": kernels,
+        "peaks_measured": peaks,
         "clocks": clk.summary(),
         "gpu_launches": int(st["kernel_launches"]),
         "e2e": e2e,

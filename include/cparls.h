@@ -88,6 +88,15 @@ typedef struct {
   int64_t mode_steps, fits, kernel_launches;
   int64_t last_matched_nnz, last_s_bar, last_attempts;
   int64_t touched_rows[8];   /* rows of A_k nonzero after its last solve, per mode */
+  /* Device time (ms) and launch count of the hot kernels alone, from CUDA
+   * events recorded around every launch on the context's stream (always on,
+   * no host synchronisation; resolved when the stats are read).
+   * Index: 0 = sampled RHS reduction (k_rhs), 1 = exact fit (k_fit_sub /
+   * k_fit_thread), 2 = solve rows (k_solve_rows_t), 3 = leverage rows
+   * (k_lev_rows_t). */
+  double kernel_ms[4];
+  int64_t kernel_launches_by_id[4];
+  int64_t sum_matched_nnz;   /* sum of m_k over the solves since the last reset   */
 } cparls_stats;
 
 /* Build the context: validates sizes (ERANGE if some prod_{m!=k} n_m >= 2^63 or

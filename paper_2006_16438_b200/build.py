@@ -32,17 +32,29 @@ def sources():
         os.path.join(HERE, "..", "include", "cparls.h")]
 
 
-def build(force=False, verbose=False):
-    if not force and os.path.exists(LIB) and os.path.getmtime(LIB) >= max(os.path.getmtime(s) for s in sources()):
-        return LIB
-    cmd = [NVCC] + FLAGS + ["-o", LIB + ".tmp", SRC, "-lcudart", "-l:libnccl.so.2"]
+PEAKS_SRC = os.path.join(HERE, "csrc", "peaks.cu")
+PEAKS_LIB = os.path.join(HERE, "libcparls_peaks.so")
+
+
+def _nvcc(out, src, libs, verbose):
+    cmd = [NVCC] + FLAGS + ["-o", out + ".tmp", src] + libs
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         sys.stderr.write(res.stdout + res.stderr)
-        raise RuntimeError("nvcc failed")
+        raise RuntimeError("nvcc failed: " + src)
     if verbose:
         sys.stderr.write(res.stderr)
-    os.replace(LIB + ".tmp", LIB)
+    os.replace(out + ".tmp", out)
+
+
+def build(force=False, verbose=False):
+    """libcparls.so (the product) and libcparls_peaks.so (bench-only microbenchmarks)."""
+    if force or not os.path.exists(PEAKS_LIB) or os.path.getmtime(PEAKS_LIB) < os.path.getmtime(PEAKS_SRC):
+        _nvcc(PEAKS_LIB, PEAKS_SRC, ["-lcudart"], verbose)
+    srcs = [s for s in sources() if s != PEAKS_SRC]
+    if not force and os.path.exists(LIB) and os.path.getmtime(LIB) >= max(os.path.getmtime(s) for s in srcs):
+        return LIB
+    _nvcc(LIB, SRC, ["-lcudart", "-l:libnccl.so.2"], verbose)
     return LIB
 
 

@@ -48,11 +48,16 @@ class Stats(C.Structure):
         "bytes_leverage", "bytes_sample", "bytes_gram", "bytes_lookup", "bytes_rhs", "bytes_solve",
         "bytes_fit")] + [(n, C.c_int64) for n in (
         "mode_steps", "fits", "kernel_launches", "last_matched_nnz", "last_s_bar", "last_attempts")] + [
-        ("touched_rows", C.c_int64 * 8)]
+        ("touched_rows", C.c_int64 * 8), ("kernel_ms", C.c_double * 4),
+        ("kernel_launches_by_id", C.c_int64 * 4), ("sum_matched_nnz", C.c_int64)]
+
+    KERNELS = ("rhs", "fit", "solve_rows", "lev_rows")
 
     def as_dict(self):
         d = {n: getattr(self, n) for n, _ in self._fields_}
         d["touched_rows"] = list(self.touched_rows)
+        d["kernel_ms"] = {k: self.kernel_ms[i] for i, k in enumerate(self.KERNELS)}
+        d["kernel_launches_by_id"] = {k: self.kernel_launches_by_id[i] for i, k in enumerate(self.KERNELS)}
         return d
 
 

@@ -117,6 +117,8 @@ struct cparls_ctx {
   std::vector<void *> allocs;
   cparls_stats stats{};
   bool profiling = false;
+  std::vector<cudaEvent_t> ev_pool;                             // free events
+  std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> ev_pending;
   int fit_mode = 0;
   int smode_last_solved = -1;
   // row sharding: this rank owns rows [row_lo, row_hi) of mode k
@@ -237,6 +239,50 @@ struct Phase {
   }
 };
 
+// Always-on per-kernel device timers: an event pair around every launch of a
+// hot kernel, resolved (synchronised and summed) only when stats are read.
+enum { KT_RHS = 0, KT_FIT = 1, KT_SOLVE = 2, KT_LEV = 3, KT_N = 4 };
+struct KTimer {
+  cparls_ctx *c;
+  int id;
+  cudaEvent_t a = nullptr, b = nullptr;
+  KTimer(cparls_ctx *c_, int id_);
+  void stop();
+};
+
+cudaEvent_t ev_get(cparls_ctx *c) {
+  if (!c->ev_pool.empty()) {
+    cudaEvent_t e = c->ev_pool.back();
+    c->ev_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  CK(cudaEventCreate(&e));
+  return e;
+}
+KTimer::KTimer(cparls_ctx *c_, int id_) : c(c_), id(id_) {
+  a = ev_get(c);
+  b = ev_get(c);
+  CK(cudaEventRecord(a, c->st));
+}
+void KTimer::stop() {
+  CK(cudaEventRecord(b, c->st));
+  c->ev_pending.push_back({id, {a, b}});
+  c->stats.kernel_launches_by_id[id]++;
+}
+// sum the elapsed times of all recorded launches into the stats
+void ktimers_resolve(cparls_ctx *c) {
+  for (auto &p : c->ev_pending) {
+    CK(cudaEventSynchronize(p.second.second));
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, p.second.first, p.second.second));
+    c->stats.kernel_ms[p.first] += ms;
+    c->ev_pool.push_back(p.second.first);
+    c->ev_pool.push_back(p.second.second);
+  }
+  c->ev_pending.clear();
+}
+
 #define LAUNCHED(c, n) ((c)->stats.kernel_launches += (n))
 
 inline int rmax_bucket(int r) { return r <= 4 ? 4 : r <= 8 ? 8 : r <= 16 ? 16 : r <= 28 ? 28 : r <= 32 ? 32 : 64; }
@@ -312,9 +358,11 @@ void lev_rows_and_cdf(cparls_ctx *c, int k, const double *lam) {
   CK(cudaMemsetAsync(&c->md[k]->drawable, 0, sizeof(long long), c->st));
   {
     const unsigned g = (unsigned)row_grid(c, nt);
+    KTimer kt(c, KT_LEV);
     RSWITCH(c->r, k_lev_rows_t<RM><<<g, kRowThreads, lev_smem(c->r, c->ld), c->st>>>(
                       c->A[k], n, c->r, c->ld, lam, c->md[k], c->pt[k], c->C[k], c->tile_u64, &c->md[k]->alpha,
                       reinterpret_cast<unsigned long long *>(&c->md[k]->drawable)));
+    kt.stop();
   }
   CK_LAUNCH();
   k_scan_u64_single<<<1, kScanThreads, 0, c->st>>>(c->tile_u64, nt);
@@ -986,8 +1034,10 @@ void solve_impl(cparls_ctx *c, int k, cparls_solve_info *info) {
                                                            &c->dv->counter, c->idx[k].out, (const VT *)c->idx[k].val, \
                                                            c->sw2, c->Z, c->hot_slot[k], c->hot_row[k],            \
                                                            nhot, r, ld, c->M, per_warp)
+      KTimer kt(c, KT_RHS);
       if (c->vf32) { if (r > 32) RHS(float, true); else RHS(float, false); }
       else { if (r > 32) RHS(double, true); else RHS(double, false); }
+      kt.stop();
 #undef RHS
       CK_LAUNCH();
       LAUNCHED(c, 1);
@@ -1003,8 +1053,10 @@ void solve_impl(cparls_ctx *c, int k, cparls_solve_info *info) {
     const int64_t r0 = c->row_lo[k], nown = c->row_hi[k] - c->row_lo[k];
     const int64_t grid = row_grid(c, ceil_div(std::max<int64_t>(nown, 1), kRowThreads));
     CK(cudaMemsetAsync(&c->dv->touched, 0, sizeof(unsigned long long), c->st));
+    KTimer kts(c, KT_SOLVE);
     RSWITCH(r, k_solve_rows_t<RM><<<(unsigned)grid, kRowThreads, solve_smem(r, ld), c->st>>>(
                    c->M + r0 * ld, nown, r, ld, c->sd, c->A[k] + r0 * ld, c->gpart, &c->dv->touched));
+    kts.stop();
     CK_LAUNCH();
     k_pairs_reduce<<<pairs_reduce_grid(r), 256, 0, c->st>>>(c->gpart, grid, r, c->sd->BtB);
     CK_LAUNCH();
@@ -1039,6 +1091,7 @@ void solve_impl(cparls_ctx *c, int k, cparls_solve_info *info) {
   c->mk = hv.mk;
   c->stats.bytes_rhs += (double)hv.mk * (4.0 + (c->vf32 ? 4.0 : 8.0)) + (double)hv.touched * r * 8.0 * 2;
   c->stats.last_matched_nnz = hv.mk;
+  c->stats.sum_matched_nnz += hv.mk;
   c->stats.touched_rows[k] = (int64_t)hv.touched;
   c->stats.mode_steps++;
   if (info) {
@@ -1067,6 +1120,7 @@ double fit_impl(cparls_ctx *c) {
   }
   fd.fast = N < 9007199254740992.0L;   // keys < 2^53
   int nb = 148 * 4;
+  KTimer kt(c, KT_FIT);
   if (fd.d <= 3) {
     // sub-warp per entry, 4 columns per lane (k_fit_sub)
     nb = 148 * 2;
@@ -1102,6 +1156,7 @@ double fit_impl(cparls_ctx *c) {
                         c->idx[k].key, c->idx[k].out, (const double *)c->idx[k].val, c->idx[k].nnz, fd, c->A[k],
                         c->lam_model, c->r, c->ld, c->ddpart));
   }
+  kt.stop();
   CK_LAUNCH();
   FitModes fm{};
   fm.D = c->D;
@@ -1322,6 +1377,8 @@ cparls_status cparls_create(cparls_ctx **out, int32_t nmodes, const int64_t *dim
 cparls_status cparls_destroy(cparls_ctx *c) {
   if (!c) return CPARLS_OK;
   if (!c->poisoned) cudaStreamSynchronize(c->st);
+  for (auto &p : c->ev_pending) { cudaEventDestroy(p.second.first); cudaEventDestroy(p.second.second); }
+  for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
   for (void *p : c->allocs) cudaFree(p);
   delete c->comm;
   delete c;
@@ -1631,14 +1688,18 @@ cparls_status cparls_owned_rows(const cparls_ctx *c, int32_t mode, int64_t *lo, 
 
 cparls_status cparls_get_stats(cparls_ctx *c, cparls_stats *s) {
   if (!c || !s) return CPARLS_EINVAL;
-  *s = c->stats;
-  return CPARLS_OK;
+  return guarded(c, [&] {
+    ktimers_resolve(c);
+    *s = c->stats;
+  });
 }
 
 cparls_status cparls_reset_stats(cparls_ctx *c) {
   if (!c) return CPARLS_EINVAL;
-  c->stats = cparls_stats{};
-  return CPARLS_OK;
+  return guarded(c, [&] {
+    ktimers_resolve(c);
+    c->stats = cparls_stats{};
+  });
 }
 
 cparls_status cparls_set_profiling(cparls_ctx *c, int32_t on) {
