@@ -106,7 +106,7 @@ class Clocks:
                 "samples": len(sm)}
 
 
-KERNEL_NAMES = {"rhs": "k_rhs", "fit": "k_fit_sub", "solve_rows": "k_solve_rows_t", "lev_rows": "k_lev_rows_t"}
+KERNEL_NAMES = {"rhs": "k_rhs", "fit": "k_fit_sub", "solve_rows": "k_solve_rows_t", "lev_rows": "k_lev_rows_w"}
 
 
 def measure_peaks(cfg, dev, window_rows, fit_rows):

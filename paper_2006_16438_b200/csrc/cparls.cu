@@ -303,10 +303,16 @@ inline int rmax_bucket(int r) { return r <= 4 ? 4 : r <= 8 ? 8 : r <= 16 ? 16 : 
 // unconditional register loads of padded columns
 size_t tile_d(int ld) { return (size_t)kRowThreads * (ld + 1); }
 size_t gram_smem(int r, int ld) { return sizeof(double) * (tile_d(ld) + 64); }
-size_t lev_smem(int r, int ld) { return sizeof(double) * ((size_t)r * r + 64 + tile_d(ld) + 64); }
 size_t solve_smem(int r, int ld) { return sizeof(double) * ((size_t)r * r + tile_d(ld) + 64); }
 size_t krp_smem(int r, int ld) { return sizeof(double) * (tile_d(ld) + kRowThreads + 64); }
 size_t prep_smem(int r) { return sizeof(double) * 4 * (size_t)r * r; }
+size_t warp_tiles_d(int ld) { return (size_t)(kRowThreads / 32) * kWarpRows * warp_tile_stride(ld); }
+// + 64 doubles of slack: the register loads of padded columns (c < RMAX) may
+// run past the last row of the last tile
+size_t lev_w_smem(int r, int ld) {
+  const size_t rm = rmax_bucket(r);
+  return sizeof(double) * (rm * rm + kMaxRank + warp_tiles_d(ld) + 64);
+}
 
 // allow the largest dynamic shared memory the kernel can take (opt-in limit
 // minus its static shared memory)
@@ -326,8 +332,8 @@ void max_dyn_smem(F func) {
 template <int RM>
 void set_attrs_rm() {
   max_dyn_smem(k_gram_rows_t<RM>);
-  max_dyn_smem(k_lev_rows_t<RM>);
   max_dyn_smem(k_solve_rows_t<RM>);
+  max_dyn_smem(k_lev_rows_w<RM>);
   max_dyn_smem(k_krp_gram_t<RM>);
   max_dyn_smem(k_fit_thread<float, RM>);
   max_dyn_smem(k_fit_thread<double, RM>);
@@ -357,10 +363,12 @@ void lev_rows_and_cdf(cparls_ctx *c, int k, const double *lam) {
   CK(cudaMemsetAsync(&c->md[k]->alpha, 0, sizeof(double), c->st));
   CK(cudaMemsetAsync(&c->md[k]->drawable, 0, sizeof(long long), c->st));
   {
-    const unsigned g = (unsigned)row_grid(c, nt);
+    const unsigned g = (unsigned)row_grid(c, ceil_div(n, kWarpRows * (kRowThreads / 32)));
+    CK(cudaMemsetAsync(c->tile_u64, 0, sizeof(uint64_t) * nt, c->st));
     KTimer kt(c, KT_LEV);
-    RSWITCH(c->r, k_lev_rows_t<RM><<<g, kRowThreads, lev_smem(c->r, c->ld), c->st>>>(
-                      c->A[k], n, c->r, c->ld, lam, c->md[k], c->pt[k], c->C[k], c->tile_u64, &c->md[k]->alpha,
+    RSWITCH(c->r, k_lev_rows_w<RM><<<g, kRowThreads, lev_w_smem(c->r, c->ld), c->st>>>(
+                      c->A[k], n, c->r, c->ld, lam, c->md[k], c->pt[k], c->C[k],
+                      reinterpret_cast<unsigned long long *>(c->tile_u64), &c->md[k]->alpha,
                       reinterpret_cast<unsigned long long *>(&c->md[k]->drawable)));
     kt.stop();
   }

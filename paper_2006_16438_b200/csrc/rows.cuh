@@ -68,91 +68,6 @@ __global__ void __launch_bounds__(kRowThreads) k_gram_rows_t(const double *__res
   sy.finish(r, smem, part + (int64_t)blockIdx.x * r * r);
 }
 
-// ---------------------------------------------------------------- leverage rows
-// l_i = ||a_i W||^2 (W = L^{-T} upper triangular, or V_kept mu^{-1/2}),
-// p~_i = l_i / rank (AMB-11), q_i = rint(p~_i 2^62) (AMB-9)
-// written to C (CDF pass 1), per-tile q sums, alpha = max p~, drawable count.
-// lam != nullptr: normalize A in place first, a_i = b_i / lambda.
-template <int RMAX>
-__global__ void __launch_bounds__(kRowThreads) k_lev_rows_t(double *__restrict__ A, int64_t n, int r, int ld,
-                                                           const double *__restrict__ lam,
-                                                           const ModeDev *__restrict__ md, double *__restrict__ pt,
-                                                           uint64_t *__restrict__ C, uint64_t *__restrict__ tile_sum,
-                                                           double *alpha_out, unsigned long long *drawable_out) {
-  extern __shared__ double smem[];
-  const int S = ld + 1;
-  double *W = smem;
-  double *lam_s = smem + r * r;
-  double *tile = lam_s + RMAX;
-  const int tri = md->tri, rank = md->rank;
-  for (int i = threadIdx.x; i < r * r; i += blockDim.x) W[i] = md->W[i];
-  for (int i = threadIdx.x; i < RMAX; i += blockDim.x) lam_s[i] = (lam != nullptr && i < r) ? lam[i] : 1.0;
-  double pmax = 0.0;
-  unsigned long long dcnt = 0;
-  __shared__ unsigned long long wq[kRowThreads / 32];
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int64_t ntiles = ceil_div(n, kRowThreads);
-  for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
-    const int64_t base = t * kRowThreads;
-    const int rows = (int)min((int64_t)kRowThreads, n - base);
-    __syncthreads();
-    stage_rows(A + base * ld, rows, ld, tile, S);
-    __syncthreads();
-    if (lam != nullptr) {
-      for (int i = threadIdx.x; i < rows * ld; i += blockDim.x) {
-        int row = i / ld, c = i - row * ld;
-        if (c < r) {
-          double l = lam_s[c];
-          tile[row * S + c] = l > 0.0 ? tile[row * S + c] / l : 0.0;
-        }
-      }
-      __syncthreads();
-      store_rows(A + base * ld, rows, ld, tile, S);
-    }
-    uint64_t q = 0;
-    if (threadIdx.x < rows) {
-      const double *x = tile + threadIdx.x * S;
-      double a[RMAX];
-#pragma unroll
-      for (int c = 0; c < RMAX; ++c) a[c] = (c < r) ? x[c] : 0.0;
-      double l = 0.0;
-      if (rank > 0) {
-        // outer loop over output columns stays rolled (keeps W loads inside it);
-        // the inner loop is unrolled so a[] lives in registers
-        for (int c = 0; c < r; ++c) {
-          const double *Wc = W + c;
-          double s = 0.0;
-#pragma unroll
-          for (int k = 0; k < RMAX; ++k)
-            if (k < r && (!tri || k <= c)) s += a[k] * Wc[k * r];
-          l += s * s;
-        }
-      }
-      double p = rank > 0 ? l / (double)rank : 0.0;
-      q = __double2ull_rn(p * kTwo62);
-      pt[base + threadIdx.x] = p;
-      C[base + threadIdx.x] = q;
-      pmax = fmax(pmax, p);
-      dcnt += (p > 1.0842021724855044e-19);
-    }
-    unsigned long long qs = warp_sum<unsigned long long>(q);
-    if (lane == 0) wq[w] = qs;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      unsigned long long s = 0;
-      for (int i = 0; i < kRowThreads / 32; ++i) s += wq[i];
-      tile_sum[t] = s;
-    }
-  }
-#pragma unroll
-  for (int m = 16; m >= 1; m >>= 1) pmax = fmax(pmax, __shfl_xor_sync(0xffffffffu, pmax, m));
-  dcnt = warp_sum<unsigned long long>(dcnt);
-  if (lane == 0) {
-    atomic_max_nonneg(alpha_out, pmax);
-    if (dcnt) atomicAdd(drawable_out, dcnt);
-  }
-}
-
 // ---------------------------------------------------------------- solve rows
 // B_i = M_i G^+ (rows with M_i = 0 give 0), M zeroed behind the read,
 // block partial of B^T B (column norms lambda, and the normalized
@@ -192,13 +107,22 @@ __global__ void __launch_bounds__(kRowThreads) k_solve_rows_t(double *__restrict
       }
       if (nz) {
         ++ntouch;
-        for (int c = 0; c < r; ++c) {
-          const double *Gc = Gi + c;
-          double s = 0.0;
+        // four output columns per pass: four independent FMA chains
+        for (int c = 0; c < r; c += 4) {
+          double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
 #pragma unroll
           for (int p = 0; p < RMAX; ++p)
-            if (p < r) s += m[p] * Gc[p * r];
-          x[c] = s;
+            if (p < r) {
+              const double *Gp = Gi + p * r + c;
+              s0 += m[p] * Gp[0];
+              if (c + 1 < r) s1 += m[p] * Gp[1];
+              if (c + 2 < r) s2 += m[p] * Gp[2];
+              if (c + 3 < r) s3 += m[p] * Gp[3];
+            }
+          x[c] = s0;
+          if (c + 1 < r) x[c + 1] = s1;
+          if (c + 2 < r) x[c + 2] = s2;
+          if (c + 3 < r) x[c + 3] = s3;
         }
       }
     }
@@ -210,6 +134,169 @@ __global__ void __launch_bounds__(kRowThreads) k_solve_rows_t(double *__restrict
   if ((threadIdx.x & 31) == 0 && nt) atomicAdd(touched, nt);
   __syncthreads();
   sy.finish(r, smem, part + (int64_t)blockIdx.x * r * r);
+}
+
+// ---------------------------------------------------------------- warp-tiled row passes
+// The leverage pass (normalize, l_i, p~, q) has no cross-row reduction besides
+// integer/max atomics, so every warp owns 32-row tiles end to end: coalesced
+// 16-byte loads of 32 contiguous rows into a private smem tile, thread-per-row
+// compute, coalesced stores, no block barriers inside the loop (the
+// block-synchronous stage -> compute -> store version reached ~13% of HBM
+// bandwidth: every phase waited for the slowest warp).
+constexpr int kWarpRows = 32;
+
+// Tiles use stride S = ld + 2 (even, so 16-byte aligned rows; conflict-free
+// 16-byte loads when lane t reads row t) and the r x r operands use row stride
+// ld (a multiple of 4), so every shared-memory access below is 16 bytes wide.
+__host__ __device__ constexpr int warp_tile_stride(int ld) { return ld + 2; }
+
+// contiguous rows [0, rows) of an ld-strided matrix <-> a warp's tile (stride S).
+// 16-byte chunk i = lane + 32u holds doubles e = 2i, 2i+1 of row e / ld; the
+// (row, column) of the next chunk of a lane advances by 64 doubles, so it is
+// updated incrementally instead of dividing by the runtime ld.
+struct ChunkWalk {
+  int row, c, drow, dc, ld;
+  __device__ __forceinline__ ChunkWalk(int lane, int ld_) : ld(ld_) {
+    row = (2 * lane) / ld; c = 2 * lane - row * ld;
+    drow = 64 / ld; dc = 64 - drow * ld;
+  }
+  __device__ __forceinline__ void next() {
+    row += drow; c += dc;
+    if (c >= ld) { c -= ld; ++row; }
+  }
+};
+
+__device__ __forceinline__ void warp_stage(const double *__restrict__ src, int rows, int ld, double *tile, int S,
+                                           double *zero_after) {
+  const int lane = threadIdx.x & 31;
+  const double2 *s2 = reinterpret_cast<const double2 *>(src);
+  const int n2 = rows * ld / 2;
+  constexpr int U = 7;
+  ChunkWalk cw(lane, ld);
+  for (int i0 = lane; i0 < n2; i0 += 32 * U) {
+    double2 v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int i = i0 + 32 * u;
+      v[u] = i < n2 ? __ldg(s2 + i) : make_double2(0.0, 0.0);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int i = i0 + 32 * u;
+      if (i < n2) {
+        *reinterpret_cast<double2 *>(tile + cw.row * S + cw.c) = v[u];
+        if (zero_after) reinterpret_cast<double2 *>(zero_after)[i] = make_double2(0.0, 0.0);
+      }
+      cw.next();
+    }
+  }
+}
+__device__ __forceinline__ void warp_store(double *__restrict__ dst, int rows, int ld, const double *tile, int S) {
+  const int lane = threadIdx.x & 31;
+  double2 *d2 = reinterpret_cast<double2 *>(dst);
+  const int n2 = rows * ld / 2;
+  ChunkWalk cw(lane, ld);
+  for (int i = lane; i < n2; i += 32) {
+    d2[i] = *reinterpret_cast<const double2 *>(tile + cw.row * S + cw.c);
+    cw.next();
+  }
+}
+
+// l_i = ||a_i W||^2, p~_i = l_i / rank, q_i = rint(p~_i 2^62) into C, q summed
+// into the 256-row tile sums of the CDF scan (integer adds: order-free, exact);
+// lam != nullptr normalizes A in place first.  Same arithmetic,
+// in the same order, as the earlier block-synchronous version.
+template <int RMAX>
+__global__ void __launch_bounds__(kRowThreads, 2) k_lev_rows_w(double *__restrict__ A, int64_t n, int r, int ld,
+                                                              const double *__restrict__ lam,
+                                                              const ModeDev *__restrict__ md, double *__restrict__ pt,
+                                                              uint64_t *__restrict__ C,
+                                                              unsigned long long *__restrict__ tile_sum,
+                                                              double *alpha_out,
+                                                              unsigned long long *drawable_out) {
+  extern __shared__ __align__(16) double smem[];
+  const int S = warp_tile_stride(ld);
+  double *W = smem;                  // RMAX x RMAX, zero padded (and zero below the diagonal if tri)
+  double *lam_s = smem + RMAX * RMAX;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  double *tile = lam_s + kMaxRank + (size_t)w * kWarpRows * S;
+  const int tri = md->tri, rank = md->rank;
+  for (int i = threadIdx.x; i < RMAX * RMAX; i += blockDim.x) {
+    const int k = i / RMAX, c = i - k * RMAX;
+    W[i] = (k < r && c < r && (!tri || k <= c)) ? md->W[k * r + c] : 0.0;
+  }
+  for (int i = threadIdx.x; i < RMAX; i += blockDim.x) lam_s[i] = (lam != nullptr && i < r) ? lam[i] : 1.0;
+  __syncthreads();
+  double pmax = 0.0;
+  unsigned long long dcnt = 0;
+  const int64_t ntiles = ceil_div(n, kWarpRows);
+  const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t t = (int64_t)blockIdx.x * (blockDim.x >> 5) + w; t < ntiles; t += nwarps) {
+    const int64_t base = t * kWarpRows;
+    const int rows = (int)min((int64_t)kWarpRows, n - base);
+    warp_stage(A + base * ld, rows, ld, tile, S, nullptr);
+    __syncwarp();
+    if (lam != nullptr) {
+      for (int i = lane; i < rows * ld; i += 32) {
+        const int row = i / ld, c = i - row * ld;
+        if (c < r) {
+          const double l = lam_s[c];
+          tile[row * S + c] = l > 0.0 ? tile[row * S + c] / l : 0.0;
+        }
+      }
+      __syncwarp();
+      warp_store(A + base * ld, rows, ld, tile, S);
+    }
+    uint64_t q = 0;
+    if (lane < rows) {
+      const double *x = tile + lane * S;
+      double a[RMAX];
+#pragma unroll
+      for (int c = 0; c < RMAX; c += 2) {
+        const double2 v = *reinterpret_cast<const double2 *>(x + c);
+        a[c] = (c < r) ? v.x : 0.0;
+        if (c + 1 < RMAX) a[c + 1] = (c + 1 < r) ? v.y : 0.0;
+      }
+      double l = 0.0;
+      if (rank > 0) {
+        // s_c = sum_{k < r} a_k W_kc over the zero-padded W (an upper
+        // triangular W's zeros below the diagonal leave the sums unchanged)
+        for (int c = 0; c < r; c += 4) {
+          double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+#pragma unroll
+          for (int k = 0; k < RMAX; ++k)
+            if (k < r && (!tri || k <= c + 3)) {
+              const double2 w01 = *reinterpret_cast<const double2 *>(W + k * RMAX + c);
+              const double2 w23 = *reinterpret_cast<const double2 *>(W + k * RMAX + c + 2);
+              s0 += a[k] * w01.x;
+              s1 += a[k] * w01.y;
+              s2 += a[k] * w23.x;
+              s3 += a[k] * w23.y;
+            }
+          l += s0 * s0;
+          if (c + 1 < r) l += s1 * s1;
+          if (c + 2 < r) l += s2 * s2;
+          if (c + 3 < r) l += s3 * s3;
+        }
+      }
+      const double p = rank > 0 ? l / (double)rank : 0.0;
+      q = __double2ull_rn(p * kTwo62);
+      pt[base + lane] = p;
+      C[base + lane] = q;
+      pmax = fmax(pmax, p);
+      dcnt += (p > 1.0842021724855044e-19);
+    }
+    const unsigned long long qs = warp_sum<unsigned long long>(q);
+    if (lane == 0 && qs) atomicAdd(tile_sum + (base >> 8), qs);   // 256-row CDF tiles (kLevThreads)
+    __syncwarp();
+  }
+#pragma unroll
+  for (int m = 16; m >= 1; m >>= 1) pmax = fmax(pmax, __shfl_xor_sync(0xffffffffu, pmax, m));
+  dcnt = warp_sum<unsigned long long>(dcnt);
+  if (lane == 0) {
+    atomic_max_nonneg(alpha_out, pmax);
+    if (dcnt) atomicAdd(drawable_out, dcnt);
+  }
 }
 
 // ---------------------------------------------------------------- KrpSamp + Gram
