@@ -31,7 +31,15 @@ struct ModeIndex {
   int shift = 0;
   int64_t nbkt = 0;
   int64_t nnz = 0;           // nonzeros of this rank's slice of mode k
+  // order of the other modes in this copy's keys, fastest first: ascending
+  // n_m, so the largest factor is the slowest (sequentially swept) key mode of
+  // the exact fit and the per-fiber random gathers hit the smallest factors.
+  // Sample keys stay canonical (AMB-1) and are re-encoded by the lookup.
+  int order[kMaxModes] = {};
 };
+
+// other modes of k, ascending n_m (ties: lower mode first)
+void copy_order(const cparls_ctx *c, int k, int *order);
 
 struct DevScalars {
   double pdet;
@@ -431,6 +439,30 @@ OtherModes other_modes(cparls_ctx *c, int k, bool need_alpha) {
   return om;
 }
 
+void copy_order(const cparls_ctx *c, int k, int *order) {
+  int d = 0;
+  for (int m = 0; m < c->D; ++m)
+    if (m != k) order[d++] = m;
+  std::stable_sort(order, order + d, [&](int a, int b) { return c->dims[a] < c->dims[b]; });
+}
+
+KeyRemap key_remap(const cparls_ctx *c, int k) {
+  KeyRemap rm{};
+  rm.d = c->D - 1;
+  rm.identity = 1;
+  const int *order = c->idx[k].order;
+  for (int j = 0, m = 0; m < c->D; ++m) {
+    if (m == k) continue;
+    rm.n[j] = c->dims[m];
+    uint64_t mult = 1;
+    for (int q = 0; q < rm.d && order[q] != m; ++q) mult *= (uint64_t)c->dims[order[q]];
+    rm.cmult[j] = mult;
+    rm.identity &= (order[j] == m);
+    ++j;
+  }
+  return rm;
+}
+
 // ---------------------------------------------------------------- index build (K0)
 template <typename IT, typename VT>
 void build_index_mode(cparls_ctx *c, int k, const IT *coords, const VT *vals, int64_t nnz) {
@@ -462,6 +494,8 @@ void build_index_mode(cparls_ctx *c, int k, const IT *coords, const VT *vals, in
   ks.D = c->D;
   ks.k = k;
   for (int m = 0; m < c->D; ++m) ks.dims[m] = c->dims[m];
+  copy_order(c, k, ix.order);
+  for (int j = 0; j < c->D - 1; ++j) ks.order[j] = ix.order[j];
   uint64_t *key0 = dalloc_t<uint64_t>(c, nnz), *key1 = dalloc_t<uint64_t>(c, nnz);
   if (nnz > 0) {
     k_make_keys<IT><<<g, 256, 0, c->st>>>(coords, nnz, ks, ids, key0);
@@ -963,6 +997,7 @@ void lookup_impl(cparls_ctx *c, int k) {
   const int64_t sbar = c->sbar;
   if (sbar > 0) {
     k_lookup<<<(unsigned)ceil_div(sbar, 256), 256, 0, c->st>>>(c->skey, sbar, ix.key, ix.dir, ix.shift, ix.nbkt,
+                                                               key_remap(c, k),
                                                                c->lo, c->len);
     CK_LAUNCH();
     LAUNCHED(c, 1);
@@ -1118,13 +1153,12 @@ double fit_impl(cparls_ctx *c) {
   FitDecode fd{};
   fd.d = c->D - 1;
   long double N = 1;
-  for (int m = 0, j = 0; m < c->D; ++m) {
-    if (m == k) continue;
+  for (int j = 0; j < fd.d; ++j) {   // the copy's key order (fastest first)
+    const int m = c->idx[k].order[j];
     fd.n[j] = c->dims[m];
     fd.inv[j] = 1.0 / (double)c->dims[m];
     fd.A[j] = c->A[m];
     N *= (long double)c->dims[m];
-    ++j;
   }
   fd.fast = N < 9007199254740992.0L;   // keys < 2^53
   int nb = 148 * 4;
@@ -1350,13 +1384,15 @@ cparls_status cparls_create(cparls_ctx **out, int32_t nmodes, const int64_t *dim
       nnz_global = 0;
       for (int64_t v : all) nnz_global += v;
     }
-    // per nonzero one A_{k*} row; per fiber one A_{m_1} row (m_1 = fastest key
-    // mode); expected miss traffic grows with the factor sizes
+    // per nonzero one A_{k*} row; per fiber one row of every other key mode but
+    // the slowest (whose row is cached while the copy sweeps it); expected miss
+    // traffic grows with the sizes of the randomly gathered factors
     {
       double best = 0;
       for (int m = 0; m < nmodes; ++m) {
-        const int m1 = (m == 0) ? 1 : 0;
-        const double cost = (double)nnz_global * (double)c->dims[m] + (double)c->nfib[m] * (double)c->dims[m1];
+        double fib = 0;
+        for (int j = 0; j + 1 < nmodes - 1; ++j) fib += (double)c->dims[c->idx[m].order[j]];
+        const double cost = (double)nnz_global * (double)c->dims[m] + (double)c->nfib[m] * fib;
         if (m == 0 || cost < best) { best = cost; c->fit_mode = m; }
       }
     }

@@ -544,12 +544,31 @@ __global__ void k_cidx_emit(unsigned long long *__restrict__ hkey, uint32_t *__r
 // K7 TnsrSamp lookup: equal_range of each sampled key in the
 // mode-k sorted keys, narrowed by the top-level directory.
 // ======================================================================
+// Sample keys are canonical (eq:bijection, AMB-1: other modes ascending, first
+// fastest); a mode copy may store its keys with another order of the other
+// modes (ModeIndex::order), so the key is re-encoded before the search.
+struct KeyRemap {
+  int d;
+  int identity;
+  int64_t n[kMaxModes];       // canonical order dims
+  uint64_t cmult[kMaxModes];  // multiplier of canonical digit j in the copy's key
+};
+
 __global__ void k_lookup(const uint64_t *__restrict__ skey, int64_t sbar, const uint64_t *__restrict__ keys,
-                         const int64_t *__restrict__ dir, int shift, int64_t nbkt, int64_t *__restrict__ lo_out,
-                         int64_t *__restrict__ len_out) {
+                         const int64_t *__restrict__ dir, int shift, int64_t nbkt, KeyRemap rm,
+                         int64_t *__restrict__ lo_out, int64_t *__restrict__ len_out) {
   int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= sbar) return;
   uint64_t k = skey[j];
+  if (!rm.identity) {
+    uint64_t t = k, kk = 0;
+    for (int m = 0; m < rm.d; ++m) {
+      const uint64_t q = t / (uint64_t)rm.n[m];
+      kk += (t - q * (uint64_t)rm.n[m]) * rm.cmult[m];
+      t = q;
+    }
+    k = kk;
+  }
   uint64_t b = k >> shift;
   int64_t lo = 0, hi = 0;
   if ((int64_t)b < nbkt) {
@@ -658,6 +677,7 @@ __global__ void k_make_outkey(const IT *__restrict__ coords, int64_t nnz, int D,
 struct KeySpec {
   int D, k;
   int64_t dims[kMaxModes];
+  int order[kMaxModes];   // the copy's other modes, fastest-varying first
 };
 
 template <typename IT>
@@ -667,8 +687,8 @@ __global__ void k_make_keys(const IT *__restrict__ coords, int64_t nnz, KeySpec 
   if (t >= nnz) return;
   int64_t e = ids[t];
   uint64_t key = 0, mult = 1;
-  for (int m = 0; m < ks.D; ++m) {
-    if (m == ks.k) continue;
+  for (int j = 0; j < ks.D - 1; ++j) {
+    const int m = ks.order[j];
     key += (uint64_t)coords[e * ks.D + m] * mult;
     mult *= (uint64_t)ks.dims[m];
   }
