@@ -29,7 +29,7 @@ class Opts(C.Structure):
     _fields_ = [("rank", C.c_int32), ("tau", C.c_double), ("value_dtype", C.c_int32),
                 ("index_dtype", C.c_int32), ("stream", C.c_void_p), ("world_size", C.c_int32),
                 ("world_rank", C.c_int32), ("comm", C.c_void_p), ("didx_cap", C.c_int64),
-                ("attempt_cap", C.c_int64)]
+                ("attempt_cap", C.c_int64), ("rhs_path", C.c_int32)]
 
 
 class SampleInfo(C.Structure):
@@ -133,7 +133,7 @@ class Cparls:
     """One CP-ARLS-LEV context (the C ABI's cparls_ctx)."""
 
     def __init__(self, dims, coords, vals, rank, tau=-1.0, init_seed=2, stream=None,
-                 didx_cap=0, attempt_cap=0, comm=None, world_size=1, world_rank=0):
+                 didx_cap=0, attempt_cap=0, comm=None, world_size=1, world_rank=0, rhs_path=0):
         import torch
         if not torch.cuda.is_available():
             raise RuntimeError("cparls needs a CUDA device (B200); no CPU fallback exists")
@@ -161,7 +161,7 @@ class Cparls:
         o = Opts(rank=self.r, tau=float(tau), value_dtype=vdt, index_dtype=idt,
                  stream=C.c_void_p(stream), world_size=int(world_size), world_rank=int(world_rank),
                  comm=(comm.handle if comm is not None else None),
-                 didx_cap=int(didx_cap), attempt_cap=int(attempt_cap))
+                 didx_cap=int(didx_cap), attempt_cap=int(attempt_cap), rhs_path=int(rhs_path))
         d = np.array(self.dims, dtype=np.int64)
         h = C.c_void_p()
         st = L.cparls_create(C.byref(h), self.D, d.ctypes.data, nnz, _ptr(coords), _ptr(vals),

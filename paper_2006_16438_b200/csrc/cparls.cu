@@ -137,6 +137,13 @@ struct cparls_ctx {
   // RHS output-row windows (see rhs.cuh)
   int64_t segcap = 0;
   int64_t *seg_lo = nullptr, *seg_len = nullptr, *seg_off = nullptr, *i64part_seg = nullptr;
+  // bucketed RHS (rhs_bucket.cuh)
+  int64_t *bkt_cnt = nullptr, *bkt_start = nullptr, *bkt_part = nullptr;
+  unsigned long long *bkt_cursor = nullptr;
+  int64_t bkt_cap = 0, rec_cap = 0;
+  uint32_t *rec = nullptr;
+  double *recc = nullptr;
+  bool m_dirty = false;   // M holds rows written by the bucketed RHS (not zero)
   int32_t *seg_j = nullptr;
   // RHS hot rows per mode (warp-private accumulation, see rhs.cuh)
   int16_t *hot_slot[kMaxModes] = {nullptr};
@@ -348,6 +355,7 @@ void set_attrs_rm() {
 }
 
 void set_kernel_attrs(int r, int ld) {
+  max_dyn_smem(k_bkt_accum<4>);
   set_attrs_rm<4>(); set_attrs_rm<8>(); set_attrs_rm<16>(); set_attrs_rm<28>(); set_attrs_rm<32>();
   set_attrs_rm<64>();
   int prep = (int)prep_smem(r);
@@ -1037,9 +1045,99 @@ void solve_impl(cparls_ctx *c, int k, cparls_solve_info *info) {
     lookup_impl(c, k);
     ph.end();
   }
+  // this rank's rows of B (all rows on one GPU); M is zero elsewhere
+  const int64_t r0 = c->row_lo[k], nown = c->row_hi[k] - c->row_lo[k];
+  // K8+K9a path: bucketed RHS with the solve fused (rhs_bucket.cuh) for big
+  // modes, atomic reductions into M + k_solve_rows_t otherwise (same math)
+  int64_t mk_host = -1;
+  bool use_bkt = false;
+  {
+    const int path = c->opts.rhs_path;
+    const bool ok = r <= 32 && sbar < kBktMaxSbar;
+    // auto = atomic: on C4 the bucketed path measured 14.8 ms per mode step
+    // (count 0.6 + place 2.2 + accumulate 7.2 + solve 1.3) against 7.0 + 0.8
+    // for k_rhs at its reduction ceiling + k_solve_rows_t
+    use_bkt = ok && path == 2;
+    if (path == 2 && !ok) throw ApiError(CPARLS_EINVAL, "rhs_path 2 needs r <= 32 and s_bar < 2^24");
+    if (use_bkt) {
+      mk_host = read_dev(c, &c->dv->mk);
+      if (mk_host >= (int64_t(1) << 32)) {
+        if (path == 2) throw ApiError(CPARLS_EINVAL, "rhs_path 2 needs m_k < 2^32");
+        use_bkt = false;
+      }
+    }
+  }
+  if (use_bkt) {
+    Phase ph(c, &c->stats.ms_rhs);
+    k_solve_prep<<<1, 128, prep_smem(r), c->st>>>(r, c->sd);
+    CK_LAUNCH();
+    const int64_t nbkt = std::max<int64_t>(1, ceil_div(nown, kBktRows));
+    if (nbkt + 1 > c->bkt_cap) {
+      dfree(c, c->bkt_cnt); dfree(c, c->bkt_start); dfree(c, c->bkt_cursor); dfree(c, c->bkt_part);
+      c->bkt_cap = nbkt + 1;
+      c->bkt_cnt = dalloc_t<int64_t>(c, c->bkt_cap);
+      c->bkt_start = dalloc_t<int64_t>(c, c->bkt_cap);
+      c->bkt_cursor = dalloc_t<unsigned long long>(c, c->bkt_cap);
+      c->bkt_part = dalloc_t<int64_t>(c, ceil_div(c->bkt_cap, kScanTile) + 16);
+    }
+    if (mk_host > c->rec_cap) {
+      dfree(c, c->rec); dfree(c, c->recc);
+      c->rec_cap = std::max<int64_t>(mk_host, 1) + (mk_host >> 3);
+      c->rec = dalloc_t<uint32_t>(c, c->rec_cap);
+      c->recc = dalloc_t<double>(c, c->rec_cap);
+    }
+    KTimer kt(c, KT_RHS);
+    CK(cudaMemsetAsync(c->bkt_cnt, 0, sizeof(int64_t) * (nbkt + 1), c->st));
+    const int grid = 148 * 8;
+    const int64_t per_warp = 512;
+    if (mk_host > 0) {
+      CK(cudaMemsetAsync(&c->dv->counter, 0, sizeof(unsigned long long), c->st));
+      k_bkt_count<<<grid, 256, 0, c->st>>>(c->off, c->lo, sbar, &c->dv->mk, &c->dv->counter, per_warp,
+                                           c->idx[k].out, r0, reinterpret_cast<unsigned long long *>(c->bkt_cnt));
+      CK_LAUNCH();
+    }
+    // starts of the nbkt buckets (+ the total at [nbkt]); placement cursors
+    exclusive_scan_i64(c->bkt_cnt, c->bkt_start, nbkt + 1, c->bkt_part, nullptr, c->st);
+    k_bkt_cursor<<<(unsigned)ceil_div(nbkt, 256), 256, 0, c->st>>>(c->bkt_start, nbkt, c->bkt_cursor);
+    CK_LAUNCH();
+    if (mk_host > 0) {
+      CK(cudaMemsetAsync(&c->dv->counter, 0, sizeof(unsigned long long), c->st));
+      if (c->vf32)
+        k_bkt_place<float><<<grid, 256, 0, c->st>>>(c->off, c->lo, sbar, &c->dv->mk, &c->dv->counter, per_warp,
+                                                    c->idx[k].out, (const float *)c->idx[k].val, c->sw2, r0,
+                                                    c->bkt_cursor, c->rec, c->recc);
+      else
+        k_bkt_place<double><<<grid, 256, 0, c->st>>>(c->off, c->lo, sbar, &c->dv->mk, &c->dv->counter, per_warp,
+                                                     c->idx[k].out, (const double *)c->idx[k].val, c->sw2, r0,
+                                                     c->bkt_cursor, c->rec, c->recc);
+      CK_LAUNCH();
+    }
+    {
+      const int64_t agrid = std::max<int64_t>(1, std::min<int64_t>(ceil_div(nbkt, kBktThreads / 32), 148 * 3));
+      k_bkt_accum<4><<<(unsigned)agrid, kBktThreads, bkt_accum_smem(ld), c->st>>>(c->bkt_start, nbkt, c->rec, c->recc,
+                                                                                  c->Z, nown, ld, c->M + r0 * ld);
+      CK_LAUNCH();
+    }
+    CK(cudaMemsetAsync(&c->dv->touched, 0, sizeof(unsigned long long), c->st));
+    const int64_t bgrid = row_grid(c, ceil_div(std::max<int64_t>(nown, 1), kRowThreads));
+    RSWITCH(r, k_solve_rows_t<RM><<<(unsigned)bgrid, kRowThreads, solve_smem(r, ld), c->st>>>(
+                   c->M + r0 * ld, nown, r, ld, c->sd, c->A[k] + r0 * ld, c->gpart, &c->dv->touched, 0));
+    CK_LAUNCH();
+    c->m_dirty = true;   // M holds this mode's rows (no zeroing pass)
+    kt.stop();
+    k_pairs_reduce<<<pairs_reduce_grid(r), 256, 0, c->st>>>(c->gpart, bgrid, r, c->sd->BtB);
+    CK_LAUNCH();
+    LAUNCHED(c, 8);
+    c->stats.bytes_rhs += (double)mk_host * (4.0 + (c->vf32 ? 4.0 : 8.0)) + (double)nown * r * 8.0;
+    ph.end();
+  } else
   // K8: sampled RHS (fp64 red per entry in L2-sized output-row windows; hot
   // rows privatized per warp)
   {
+    if (c->m_dirty) {   // a bucketed step left rows in M
+      CK(cudaMemsetAsync(c->M, 0, sizeof(double) * c->nmax * c->ld, c->st));
+      c->m_dirty = false;
+    }
     Phase ph(c, &c->stats.ms_rhs);
     if (sbar > 0) {
       static const int win_mb = getenv("CPARLS_RHS_WIN_MB") ? atoi(getenv("CPARLS_RHS_WIN_MB")) : 96;
@@ -1090,19 +1188,19 @@ void solve_impl(cparls_ctx *c, int k, cparls_solve_info *info) {
   // K9: solve + normalize + leverage refresh
   {
     Phase ph(c, &c->stats.ms_solve);
+    if (!use_bkt) {
     k_solve_prep<<<1, 128, prep_smem(r), c->st>>>(r, c->sd);
     CK_LAUNCH();
-    // this rank's rows of B (all rows on one GPU); M is zero elsewhere
-    const int64_t r0 = c->row_lo[k], nown = c->row_hi[k] - c->row_lo[k];
     const int64_t grid = row_grid(c, ceil_div(std::max<int64_t>(nown, 1), kRowThreads));
     CK(cudaMemsetAsync(&c->dv->touched, 0, sizeof(unsigned long long), c->st));
     KTimer kts(c, KT_SOLVE);
     RSWITCH(r, k_solve_rows_t<RM><<<(unsigned)grid, kRowThreads, solve_smem(r, ld), c->st>>>(
-                   c->M + r0 * ld, nown, r, ld, c->sd, c->A[k] + r0 * ld, c->gpart, &c->dv->touched));
+                   c->M + r0 * ld, nown, r, ld, c->sd, c->A[k] + r0 * ld, c->gpart, &c->dv->touched, 1));
     kts.stop();
     CK_LAUNCH();
     k_pairs_reduce<<<pairs_reduce_grid(r), 256, 0, c->st>>>(c->gpart, grid, r, c->sd->BtB);
     CK_LAUNCH();
+    }
     if (c->world > 1) {
       // Gram of B over all ranks' rows (r x r), then every rank gets all B rows
       c->comm->allreduce_f64(c->sd->BtB, (size_t)r * r, c->st);

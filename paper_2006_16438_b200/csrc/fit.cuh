@@ -150,7 +150,6 @@ __global__ void __launch_bounds__(kFitThreads, 2) k_fit_sub(const uint64_t *__re
   const int sbase = lane & ~(SW - 1);
   const int c0 = 4 * sl;
   const bool colok = c0 < ld;            // ld % 4 == 0: all 4 columns in bounds
-  const unsigned smask = (SW == 32) ? 0xffffffffu : (((1u << SW) - 1u) << sbase);
   double lam4[4];
 #pragma unroll
   for (int q = 0; q < 4; ++q) lam4[q] = (c0 + q < r) ? lam[c0 + q] : 0.0;

@@ -806,4 +806,5 @@ __global__ void k_pack_nz(const IT *__restrict__ coords, const VT *__restrict__ 
 
 #include "rows.cuh"
 #include "rhs.cuh"
+#include "rhs_bucket.cuh"
 #include "fit.cuh"

@@ -76,7 +76,8 @@ template <int RMAX>
 __global__ void __launch_bounds__(kRowThreads) k_solve_rows_t(double *__restrict__ M, int64_t n, int r, int ld,
                                                              const SolveDev *__restrict__ sd, double *__restrict__ B,
                                                              double *__restrict__ part,
-                                                             unsigned long long *__restrict__ touched) {
+                                                             unsigned long long *__restrict__ touched,
+                                                             int zero_m) {
   extern __shared__ double smem[];
   const int S = ld + 1;
   double *Gi = smem;
@@ -91,8 +92,8 @@ __global__ void __launch_bounds__(kRowThreads) k_solve_rows_t(double *__restrict
     const int rows = (int)min((int64_t)kRowThreads, n - base);
     __syncthreads();
     stage_rows(M + base * ld, rows, ld, tile, S);
-    {
-      double2 *d2 = reinterpret_cast<double2 *>(M + base * ld);   // keep M zero for the next RHS
+    if (zero_m) {   // keep M zero for the next atomic RHS (the bucketed RHS overwrites every row)
+      double2 *d2 = reinterpret_cast<double2 *>(M + base * ld);
       for (int i = threadIdx.x; i < rows * ld / 2; i += blockDim.x) d2[i] = make_double2(0.0, 0.0);
     }
     __syncthreads();

@@ -61,6 +61,26 @@ struct Syrk {
     }
   }
 
+  // Warp-private variant: this warp's lanes walk every row of a tile the warp
+  // owns (rows [0, rows), stride S); finish() still sums the 8 warps.
+  __device__ __forceinline__ void accumulate_warp(const double *tile, int rows, int S) {
+#pragma unroll
+    for (int k = 0; k < PER; ++k) {
+      if (bp[k] < 0) continue;
+      const int p0 = 4 * bp[k], q0 = 4 * bq[k];
+      for (int row = 0; row < rows; ++row) {
+        const double *x = tile + row * S;
+        double xp[4], xq[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) { xp[i] = x[p0 + i]; xq[i] = x[q0 + i]; }
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) acc[k][4 * i + j] += xp[i] * xq[j];
+      }
+    }
+  }
+
   // Reduce the 8 row groups (group g adds into group 0 through a small shared
   // buffer of PER*32*16 doubles) and write the block's upper-triangle partial
   // (full r*r layout; entries p > q are not written) to out.

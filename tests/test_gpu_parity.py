@@ -20,11 +20,11 @@ def need_gpu():
         pytest.skip("needs a CUDA device")
 
 
-def make_ctx(T, rank, tau=-1.0, init_seed=2, device="cuda"):
+def make_ctx(T, rank, tau=-1.0, init_seed=2, device="cuda", rhs_path=0):
     from paper_2006_16438_b200 import Cparls
     coords = T.coords.to(device) if device else T.coords.numpy()
     vals = T.vals.to(device) if device else T.vals.numpy()
-    return Cparls(T.dims, coords, vals, rank, tau=tau, init_seed=init_seed)
+    return Cparls(T.dims, coords, vals, rank, tau=tau, init_seed=init_seed, rhs_path=rhs_path)
 
 
 def make_oracle(T, rank):
@@ -83,9 +83,9 @@ def compare_sample(g, o):
     return a
 
 
-def lockstep(T, rank, iters, s, seed, tau=-1.0, check_fit=True):
+def lockstep(T, rank, iters, s, seed, tau=-1.0, check_fit=True, rhs_path=0):
     need_gpu()
-    g = make_ctx(T, rank, tau=tau)
+    g = make_ctx(T, rank, tau=tau, rhs_path=rhs_path)
     o = make_oracle(T, rank)
     D = len(T.dims)
     stats = []
@@ -128,6 +128,45 @@ def test_c1_lockstep_20_iterations():
     T = synth.make("C1")
     cfg = T.cfg
     lockstep(T, cfg.rank, cfg.iters, cfg.s, cfg.sample_seed)
+
+
+@pytest.mark.parametrize("rhs_path", [1, 2])
+def test_c1_lockstep_rhs_paths(rhs_path):
+    """Both RHS + solve implementations (atomic reductions into M, and the
+    bucketed RHS with the fused solve) against the oracle."""
+    T = synth.make("C1")
+    cfg = T.cfg
+    lockstep(T, cfg.rank, 6, cfg.s, cfg.sample_seed, rhs_path=rhs_path)
+
+
+def test_c2_lockstep_bucket_path():
+    T = synth.make("C2", device="cuda")
+    T = synth.Tensor(T.cfg, T.dims, T.coords.cpu(), T.vals.cpu())
+    lockstep(T, 25, 1, 1 << 17, 3, rhs_path=2)
+
+
+def test_rhs_paths_agree_f32_values():
+    """fp32-valued tensor (the C4/C5 storage): atomic and bucketed paths give
+    the same B to rounding (<= 1e-12 relative), over a few free-running steps."""
+    need_gpu()
+    cfg = synth.scaled("C2", 300_000)
+    T = synth.make(cfg, device="cuda")
+    from paper_2006_16438_b200 import Cparls
+    a = Cparls(T.dims, T.coords, T.vals.float(), 25, rhs_path=1)
+    b = Cparls(T.dims, T.coords, T.vals.float(), 25, rhs_path=2)
+    for t in range(2):
+        for k in range(len(T.dims)):
+            ia, ib = a.sample(k, 4096, 5, 4 * t + k), b.sample(k, 4096, 5, 4 * t + k)
+            assert ia.s_bar == ib.s_bar
+            sa, sb = a.solve_mode(k), b.solve_mode(k)
+            assert (sa.matched_nnz, sa.touched_rows) == (sb.matched_nnz, sb.touched_rows)
+            _, Ba = a.last_solve(k)
+            _, Bb = b.last_solve(k)
+            assert np.linalg.norm(Ba - Bb) <= 1e-12 * np.linalg.norm(Ba), (t, k)
+            # continue both from identical factors so the comparison stays per-step
+            A, _ = a.get_factor(k)
+            b.set_factor(k, A)
+            b.set_ptilde(k, a.get_ptilde(k))
 
 
 def test_c1_random_only_tau1():
