@@ -1,0 +1,177 @@
+"""Parity at the benchmark's full size (BASELINE.json configs[3] = C4: 4.8M x 1.8M
+x 1.8M, 1.74B nonzeros, r = 25, s = 2^17), in the launch configuration bench.py
+times (default options, after bench.py's 3 warm-up iterations).
+
+The CPU oracle cannot hold the whole C4 tensor, so every check here either
+gives the oracle exactly the data the checked step depends on, or checks a
+property that holds at any size:
+
+* sampling (DIDX/SIDX/CIDX) depends on the p~ vectors only: an oracle with C4's
+  dims and no nonzeros, given the GPU's p~ bits (the lockstep protocol of
+  test_gpu_parity.py), must draw the identical sample -- bit-exact keys,
+  counts, det flags and w^2 to 1e-14;
+* a mode step reads only the nonzeros of the sampled fibers: torch selects
+  them from the COO by brute force (isin over the canonical keys -- code that
+  shares nothing with the CUDA path), the oracle is built on that subset and
+  given the GPU's factors, and then its fibers, matched-nonzero count, touched
+  rows, sampled Gram and B must match the GPU exactly as in the small cases;
+* leverage of every row of the solved factor against oracle.leverage;
+* the exact fit against its definition evaluated by torch in fp64 over all
+  1.74B nonzeros (chunked), to 1e-8 absolute.
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+
+pytestmark = pytest.mark.gpu
+
+SEED = 3
+
+
+def need_gpu():
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+
+
+@pytest.fixture(scope="module")
+def c4():
+    need_gpu()
+    from paper_2006_16438_b200 import Cparls
+    cfg = synth.CONFIGS["C4"]
+    dev = torch.device("cuda", 0)
+    T = synth.make(cfg, device=dev, index_dtype=torch.int32)
+    torch.cuda.empty_cache()
+    g = Cparls(cfg.dims, T.coords, T.vals, cfg.rank, tau=-1.0, init_seed=cfg.init_seed)
+    g.run(3, cfg.s, SEED, iter0=0, fit_every=0)        # bench.py's warm-up
+    yield cfg, T, g
+    g.close()
+    del T
+    torch.cuda.empty_cache()
+
+
+def canonical_keys(coords, dims, k, lo, hi):
+    """eq:bijection (AMB-1): other modes ascending, first fastest, int64."""
+    key = torch.zeros(hi - lo, dtype=torch.int64, device=coords.device)
+    mult = 1
+    for m in range(len(dims)):
+        if m == k:
+            continue
+        key += coords[lo:hi, m].to(torch.int64) * mult
+        mult *= dims[m]
+    return key
+
+
+def fiber_subset(T, k, skeys):
+    """All nonzeros whose other-mode coordinates form a sampled key (brute force)."""
+    dims = T.dims
+    sk = torch.from_numpy(skeys.astype(np.int64)).to(T.coords.device)
+    sk, _ = torch.sort(sk)
+    parts_c, parts_v = [], []
+    n = T.coords.shape[0]
+    step = 1 << 27
+    for lo in range(0, n, step):
+        hi = min(n, lo + step)
+        key = canonical_keys(T.coords, dims, k, lo, hi)
+        pos = torch.searchsorted(sk, key).clamp_(max=sk.numel() - 1)
+        hit = sk[pos] == key
+        idx = torch.nonzero(hit).squeeze(1) + lo
+        parts_c.append(T.coords[idx].to(torch.int64).cpu())
+        parts_v.append(T.vals[idx].to(torch.float64).cpu())
+    return torch.cat(parts_c).numpy(), torch.cat(parts_v).numpy()
+
+
+def test_c4_sampling_bit_exact_all_modes(c4):
+    cfg, T, g = c4
+    o = oracle.Oracle(cfg.dims, np.zeros((0, 3), dtype=np.int64), np.zeros(0), cfg.rank)
+    for m in range(3):
+        o.set_ptilde(m, g.get_ptilde(m))
+    for k in range(3):
+        step = 3 * 3 + k
+        gi = g.sample(k, cfg.s, SEED, step)
+        oi = o.sample(k, cfg.s, -1.0, SEED, step)
+        assert (gi.s_det, gi.s_rnd, gi.s_bar, gi.attempts, gi.skipped_random) == \
+               (oi.s_det, oi.s_rnd, oi.s_bar, oi.attempts, oi.skipped_random)
+        a, b = g.get_sample(), o.get_sample()
+        assert (a["keys"] == b["keys"]).all()
+        assert (a["counts"] == b["counts"]).all()
+        assert (a["is_det"] == b["is_det"]).all()
+        assert (a["p"] == b["p"]).all()
+        np.testing.assert_allclose(a["w2"], b["w2"], rtol=1e-14, atol=0)
+    o.close()
+
+
+def test_c4_mode0_step_against_oracle_on_the_sampled_fibers(c4):
+    cfg, T, g = c4
+    k = 0
+    step = 3 * 3 + 3          # the next step of the sequence (after the sampling test's steps)
+    gi = g.sample(k, cfg.s, SEED, step)
+    smp = g.get_sample()
+    coords, vals = fiber_subset(T, k, smp["keys"])
+    o = oracle.Oracle(cfg.dims, coords, vals, cfg.rank)
+    for m in range(3):
+        A, _ = g.get_factor(m)
+        o.set_factor(m, A)
+        o.set_ptilde(m, g.get_ptilde(m))
+    oi = o.sample(k, cfg.s, -1.0, SEED, step)
+    assert (gi.s_det, gi.s_bar, gi.attempts) == (oi.s_det, oi.s_bar, oi.attempts)
+    b = o.get_sample()
+    assert (smp["keys"] == b["keys"]).all() and (smp["counts"] == b["counts"]).all()
+    la, oa, va = g.get_fibers()
+    lb, ob, vb = o.get_fibers()
+    assert (la == lb).all() and (oa == ob).all() and (va == vb).all()
+    gs = g.solve_mode(k)
+    os_ = o.solve_mode(k)
+    assert gs.matched_nnz == os_.matched_nnz == int(la.sum())
+    assert gs.touched_rows == os_.touched_rows
+    assert gs.rank_used == os_.rank_used
+    Gg, Bg = g.last_solve(k)
+    Go, _, Bo = o.last_solve(k)
+    np.testing.assert_allclose(Gg, Go, rtol=1e-11, atol=1e-13 * np.abs(Go).max())
+    ev = np.linalg.eigvalsh(Go)
+    keep = ev[ev > 25 * np.finfo(float).eps * ev[-1]]
+    tol = max(1e-9, 1e-15 * keep[-1] / keep[0])
+    assert np.linalg.norm(Bg - Bo) <= tol * np.linalg.norm(Bo)
+    Ag, lg = g.get_factor(k)
+    Ao, lo = o.get_factor(k)
+    np.testing.assert_allclose(lg, lo, rtol=1e-9, atol=1e-300)
+    # leverage of the solved factor, every row
+    ell_ref, rank_ref = oracle.leverage(Ag)
+    ell = g.get_ptilde(k) * rank_ref
+    n, r = Ag.shape
+    err = np.abs(ell - ell_ref) / np.maximum(np.abs(ell_ref), r / n)
+    assert err.max() <= 1e-12 * 10, err.max()   # kappa-scaled bar; kappa << 1e4 here
+    o.close()
+
+
+def test_c4_exact_fit_against_its_definition(c4):
+    """fit = 1 - ||X - M|| / ||X|| (eq:fit), <X, M> and ||X||^2 summed by torch
+    in fp64 over all nonzeros, ||M||^2 = lambda^T (*_m A_m^T A_m) lambda."""
+    cfg, T, g = c4
+    fg = g.fit()
+    dev = T.coords.device
+    A = []
+    for m in range(3):
+        Am, lam = g.get_factor(m)        # lam = the model's lambda (AMB-31)
+        A.append(torch.from_numpy(Am).to(dev))
+    lam_model = torch.from_numpy(lam).to(dev)
+    inner = torch.zeros((), dtype=torch.float64, device=dev)
+    nx2 = torch.zeros((), dtype=torch.float64, device=dev)
+    n = T.coords.shape[0]
+    step = 1 << 24
+    for lo in range(0, n, step):
+        hi = min(n, lo + step)
+        c = T.coords[lo:hi].to(torch.int64)
+        x = T.vals[lo:hi].to(torch.float64)
+        h = A[0][c[:, 0]] * A[1][c[:, 1]] * A[2][c[:, 2]]
+        inner += (x * (h @ lam_model)).sum()
+        nx2 += (x * x).sum()
+    V = torch.ones((cfg.rank, cfg.rank), dtype=torch.float64, device=dev)
+    for m in range(3):
+        V = V * (A[m].T @ A[m])
+    nm2 = lam_model @ V @ lam_model
+    resid2 = torch.clamp(nx2 - 2 * inner + nm2, min=0.0)
+    fref = float(1.0 - torch.sqrt(resid2) / torch.sqrt(nx2))
+    assert abs(fg - fref) <= 1e-8, (fg, fref)
