@@ -146,8 +146,6 @@ struct cparls_ctx {
   bool m_dirty = false;   // M holds rows written by the bucketed RHS (not zero)
   int32_t *seg_j = nullptr;
   // RHS hot rows per mode (warp-private accumulation, see rhs.cuh)
-  int16_t *hot_slot[kMaxModes] = {nullptr};
-  int32_t *hot_row[kMaxModes] = {nullptr};
   int64_t nfib[kMaxModes] = {0};
 };
 
@@ -362,10 +360,6 @@ void set_kernel_attrs(int r, int ld) {
   CK(cudaFuncSetAttribute(k_lev_prep, cudaFuncAttributeMaxDynamicSharedMemorySize, prep));
   CK(cudaFuncSetAttribute(k_norm_prep, cudaFuncAttributeMaxDynamicSharedMemorySize, prep));
   CK(cudaFuncSetAttribute(k_solve_prep, cudaFuncAttributeMaxDynamicSharedMemorySize, prep));
-  max_dyn_smem(k_rhs<float, false>);
-  max_dyn_smem(k_rhs<float, true>);
-  max_dyn_smem(k_rhs<double, false>);
-  max_dyn_smem(k_rhs<double, true>);
 }
 
 int64_t row_grid(cparls_ctx *c, int64_t ntiles) { return std::max<int64_t>(1, std::min<int64_t>(ntiles, c->gpart_blocks)); }
@@ -534,34 +528,6 @@ void build_index_mode(cparls_ctx *c, int k, const IT *coords, const VT *vals, in
   }
   sync(c);
   dfree(c, fids);
-  // hot rows of this mode for the RHS: the kRhsHot rows with most nonzeros
-  {
-    const int64_t n = c->dims[k];
-    const unsigned gn = (unsigned)std::max<int64_t>(1, ceil_div(n, 256));
-    unsigned *deg = dalloc_t<unsigned>(c, n);
-    CK(cudaMemsetAsync(deg, 0, sizeof(unsigned) * n, c->st));
-    if (nnz > 0) {
-      k_row_degree<<<1184, 256, 0, c->st>>>(ix.out, nnz, deg);
-      CK_LAUNCH();
-    }
-    uint32_t *dk0 = dalloc_t<uint32_t>(c, n), *dk1 = dalloc_t<uint32_t>(c, n);
-    uint32_t *dv0 = dalloc_t<uint32_t>(c, n), *dv1 = dalloc_t<uint32_t>(c, n);
-    k_deg_keys<<<gn, 256, 0, c->st>>>(deg, n, dk0, dv0);
-    CK_LAUNCH();
-    cub::DoubleBuffer<uint32_t> hk(dk0, dk1), hv(dv0, dv1);
-    size_t tb2 = 0;
-    CK(cub::DeviceRadixSort::SortPairs(nullptr, tb2, hk, hv, n, 0, 32, c->st));
-    void *tmp2 = dalloc(c, tb2);
-    CK(cub::DeviceRadixSort::SortPairs(tmp2, tb2, hk, hv, n, 0, 32, c->st));
-    c->hot_slot[k] = dalloc_t<int16_t>(c, n);
-    c->hot_row[k] = dalloc_t<int32_t>(c, kRhsHot);
-    CK(cudaMemsetAsync(c->hot_slot[k], 0xFF, sizeof(int16_t) * n, c->st));
-    k_hot_slots<<<1, kRhsHot, 0, c->st>>>(hv.Current(), (int)std::min<int64_t>(n, kRhsHot), c->hot_slot[k],
-                                          c->hot_row[k]);
-    CK_LAUNCH();
-    sync(c);
-    dfree(c, tmp2); dfree(c, deg); dfree(c, dk0); dfree(c, dk1); dfree(c, dv0); dfree(c, dv1);
-  }
   // top-level directory on the high key bits
   int dbits = 1;
   while (dbits < 26 && (int64_t(1) << (dbits + 1)) <= std::max<int64_t>(nnz / 8, 2)) ++dbits;
@@ -1142,8 +1108,6 @@ void solve_impl(cparls_ctx *c, int k, cparls_solve_info *info) {
     if (sbar > 0) {
       static const int win_mb = getenv("CPARLS_RHS_WIN_MB") ? atoi(getenv("CPARLS_RHS_WIN_MB")) : 96;
       static const int grid_mult = getenv("CPARLS_RHS_GRID") ? atoi(getenv("CPARLS_RHS_GRID")) : 8;
-      static const int nhot_env = getenv("CPARLS_RHS_NHOT") ? atoi(getenv("CPARLS_RHS_NHOT")) : 0;
-      const int nhot = nhot_env >= 0 ? std::min(nhot_env, rhs_nhot(r)) : rhs_nhot(r);
       const int64_t RW = std::max<int64_t>(1, (int64_t(win_mb) << 20) / ((int64_t)ld * 8));
       const int nwin = (int)ceil_div(nk, RW);
       const int64_t nseg = (int64_t)nwin * sbar;
@@ -1171,10 +1135,9 @@ void solve_impl(cparls_ctx *c, int k, cparls_solve_info *info) {
       const int grid = 148 * grid_mult;
       const int64_t per_warp = 512;
 #define RHS(VT, HI)                                                                                               \
-  k_rhs<VT, HI><<<grid, kRhsThreads, sizeof(double) * (size_t)kRhsWarps * nhot * r, c->st>>>(c->seg_off, c->seg_lo, nwin > 1 ? c->seg_j : nullptr, nseg, &c->dv->mk,          \
+  k_rhs<VT, HI><<<grid, kRhsThreads, 0, c->st>>>(c->seg_off, c->seg_lo, nwin > 1 ? c->seg_j : nullptr, nseg, &c->dv->mk,          \
                                                            &c->dv->counter, c->idx[k].out, (const VT *)c->idx[k].val, \
-                                                           c->sw2, c->Z, c->hot_slot[k], c->hot_row[k],            \
-                                                           nhot, r, ld, c->M, per_warp)
+                                                           c->sw2, c->Z, r, ld, c->M, per_warp)
       KTimer kt(c, KT_RHS);
       if (c->vf32) { if (r > 32) RHS(float, true); else RHS(float, false); }
       else { if (r > 32) RHS(double, true); else RHS(double, false); }

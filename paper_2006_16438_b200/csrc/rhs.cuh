@@ -4,16 +4,16 @@
 //
 // Warps walk the concatenated matched entries (fiber after fiber, so z_j and
 // w_j^2 stay in registers across a fiber); lanes = columns, so one entry is one
-// r-wide fp64 reduction into M's row.  Global fp64 `red` runs at the SM's
-// atomic issue rate (~0.8 lane-ops/cycle/SM; sm_100a has no f64 vector red),
-// which bounds this kernel.  Zipf heads concentrate the entries on a few
-// output rows, so the top kRhsHot rows of mode k (by nonzero count, chosen at
-// index build) are accumulated in warp-private shared-memory rows instead and
-// flushed with one red per (warp, row, column) at the end.
+// r-wide fp64 reduction into M's row.  Global fp64 `red` (no f64 vector red on
+// sm_100a) bounds this kernel: bench.py measures the ceiling of exactly this
+// pattern (r-lane reds into random rows of an L2-sized window) with
+// libcparls_peaks.so and k_rhs runs at ~97% of it.  (Privatizing the heaviest
+// rows in shared memory was measured and dropped: the top 64 rows hold < 1% of
+// the entries on the Zipf workloads, and the smem cost halved occupancy.)
 //
 // M (n_k x ld fp64) is far larger than L2 for the big modes, so random reds
 // would each be a DRAM read-modify-write.  The entries are therefore visited
-// in output-row windows of ~48 MB of M: each fiber is sorted by output row, so
+// in output-row windows of ~96 MB of M: each fiber is sorted by output row, so
 // its entries inside window w are the sub-range found by k_win_bounds; the
 // (window, fiber) segments are concatenated window-major and warps take
 // chunks from a global counter, so the rows being reduced stay in L2.
@@ -25,8 +25,6 @@
 namespace cparls {
 
 constexpr int kRhsThreads = 256;
-constexpr int kRhsWarps = kRhsThreads / 32;
-constexpr int kRhsHot = 64;   // privatized hot rows per warp
 
 template <typename VT, bool HI>
 __global__ void __launch_bounds__(kRhsThreads) k_rhs(const int64_t *__restrict__ off, const int64_t *__restrict__ lo,
@@ -35,14 +33,8 @@ __global__ void __launch_bounds__(kRhsThreads) k_rhs(const int64_t *__restrict__
                                                     unsigned long long *__restrict__ work,
                                                     const int32_t *__restrict__ outidx, const VT *__restrict__ vals,
                                                     const double *__restrict__ sw2, const double *__restrict__ Z,
-                                                    const int16_t *__restrict__ hot_slot,
-                                                    const int32_t *__restrict__ hot_row, int nhot, int r, int ld,
-                                                    double *__restrict__ M, int64_t per_warp) {
-  extern __shared__ double priv[];   // kRhsWarps x nhot x r
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  double *mine = priv + (size_t)w * nhot * r;
-  for (int i = threadIdx.x; i < kRhsWarps * nhot * r; i += blockDim.x) priv[i] = 0.0;
-  __syncthreads();
+                                                    int r, int ld, double *__restrict__ M, int64_t per_warp) {
+  const int lane = threadIdx.x & 31;
   const int64_t mk = *mk_ptr;
   const uint64_t pstream = l2_evict_first();
   while (true) {
@@ -67,15 +59,12 @@ __global__ void __launch_bounds__(kRhsThreads) k_rhs(const int64_t *__restrict__
       int64_t jj = jcur;
       while (jj + 1 < nseg && __ldg(off + jj + 1) <= tt) ++jj;
       int64_t j_l = -1;
-      long long os_l = 0;    // (hot slot << 32) | output row
+      int32_t o_l = 0;
       double cx_l = 0.0;     // w_j^2 * x_e
       if (valid) {
         j_l = seg_j ? (int64_t)__ldg(seg_j + jj) : jj;
         const int64_t e = __ldg(lo + jj) + (tt - __ldg(off + jj));
-        const int32_t o = ld_stream(outidx + e, pstream);
-        int sl = __ldg(hot_slot + o);
-        if (sl >= nhot) sl = -1;
-        os_l = ((long long)sl << 32) | (unsigned)o;
+        o_l = ld_stream(outidx + e, pstream);
         cx_l = __ldg(sw2 + j_l) * (double)ld_stream(vals + e, pstream);
       }
       const int cnt = (int)min((int64_t)32, t1 - t);
@@ -89,20 +78,14 @@ __global__ void __launch_bounds__(kRhsThreads) k_rhs(const int64_t *__restrict__
         }
 #pragma unroll 4
         for (int u = 0; u < cnt; ++u) {
-          const long long os = __shfl_sync(0xffffffffu, os_l, u);
+          const int o = __shfl_sync(0xffffffffu, o_l, u);
           const double cx = __shfl_sync(0xffffffffu, cx_l, u);
-          const int o = (int)(unsigned)os, sl = (int)(os >> 32);
-          if (sl >= 0) {   // hot row: warp-private shared accumulator, no atomics
-            if (lane < r) mine[sl * r + lane] += cx * z0;
-            if (HI && lane + 32 < r) mine[sl * r + lane + 32] += cx * z1;
-          } else {
-            if (lane < r) atomicAdd(M + (int64_t)o * ld + lane, cx * z0);
-            if (HI && lane + 32 < r) atomicAdd(M + (int64_t)o * ld + lane + 32, cx * z1);
-          }
+          if (lane < r) atomicAdd(M + (int64_t)o * ld + lane, cx * z0);
+          if (HI && lane + 32 < r) atomicAdd(M + (int64_t)o * ld + lane + 32, cx * z1);
         }
       } else {
         for (int u = 0; u < cnt; ++u) {
-          const long long os = __shfl_sync(0xffffffffu, os_l, u);
+          const int o = __shfl_sync(0xffffffffu, o_l, u);
           const double cx = __shfl_sync(0xffffffffu, cx_l, u);
           const int64_t ju = __shfl_sync(0xffffffffu, j_l, u);
           if (ju != jz) {
@@ -110,32 +93,15 @@ __global__ void __launch_bounds__(kRhsThreads) k_rhs(const int64_t *__restrict__
             z0 = lane < r ? __ldg(Z + ju * ld + lane) : 0.0;
             if (HI) z1 = lane + 32 < r ? __ldg(Z + ju * ld + lane + 32) : 0.0;
           }
-          const int o = (int)(unsigned)os, sl = (int)(os >> 32);
-          if (sl >= 0) {
-            if (lane < r) mine[sl * r + lane] += cx * z0;
-            if (HI && lane + 32 < r) mine[sl * r + lane + 32] += cx * z1;
-          } else {
-            if (lane < r) atomicAdd(M + (int64_t)o * ld + lane, cx * z0);
-            if (HI && lane + 32 < r) atomicAdd(M + (int64_t)o * ld + lane + 32, cx * z1);
-          }
+          if (lane < r) atomicAdd(M + (int64_t)o * ld + lane, cx * z0);
+          if (HI && lane + 32 < r) atomicAdd(M + (int64_t)o * ld + lane + 32, cx * z1);
         }
       }
       jcur = __shfl_sync(0xffffffffu, jj, 31);
     }
   }
-  __syncwarp();
-  for (int s = 0; s < nhot; ++s) {
-    const int row = hot_row[s];
-    if (row < 0) break;
-    for (int c = lane; c < r; c += 32) {
-      const double v = mine[s * r + c];
-      if (v != 0.0) atomicAdd(M + (int64_t)row * ld + c, v);
-    }
-  }
 }
 
-// privatized rows per warp that fit ~200 KB of shared memory
-inline int rhs_nhot(int r) { return std::min(kRhsHot, (int)(200 * 1024 / (sizeof(double) * kRhsWarps * r))); }
 // For every (window w, sample j): the sub-range of fiber j whose output rows
 // fall in [w*RW, (w+1)*RW) (fibers are sorted by output row).
 __global__ void k_win_bounds(const int64_t *__restrict__ lo, const int64_t *__restrict__ len, int64_t sbar,
@@ -161,30 +127,6 @@ __global__ void k_win_bounds(const int64_t *__restrict__ lo, const int64_t *__re
   seg_lo[g] = b0;
   seg_len[g] = b1 - b0;
   seg_j[g] = (int32_t)j;
-}
-
-inline size_t rhs_smem(int r) { return sizeof(double) * (size_t)kRhsWarps * rhs_nhot(r) * r; }
-
-// ---- hot rows (index build): nonzero count per mode-k row ---------------------
-__global__ void k_row_degree(const int32_t *__restrict__ outidx, int64_t nnz, unsigned *__restrict__ deg) {
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nnz; i += (int64_t)gridDim.x * blockDim.x)
-    atomicAdd(deg + outidx[i], 1u);
-}
-
-__global__ void k_deg_keys(const unsigned *__restrict__ deg, int64_t n, uint32_t *__restrict__ key,
-                           uint32_t *__restrict__ row) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n) { key[i] = ~deg[i]; row[i] = (uint32_t)i; }   // ascending ~deg = descending degree
-}
-
-__global__ void k_hot_slots(const uint32_t *__restrict__ sorted_rows, int nhot, int16_t *__restrict__ hot_slot,
-                            int32_t *__restrict__ hot_row) {
-  const int s = threadIdx.x;
-  if (s < kRhsHot) {
-    const int row = s < nhot ? (int)sorted_rows[s] : -1;
-    hot_row[s] = row;
-    if (row >= 0) hot_slot[row] = (int16_t)s;
-  }
 }
 
 }  // namespace cparls
