@@ -258,8 +258,9 @@ enum { KT_RHS = 0, KT_FIT = 1, KT_SOLVE = 2, KT_LEV = 3, KT_N = 4 };
 struct KTimer {
   cparls_ctx *c;
   int id;
+  cudaStream_t st;
   cudaEvent_t a = nullptr, b = nullptr;
-  KTimer(cparls_ctx *c_, int id_);
+  KTimer(cparls_ctx *c_, int id_, cudaStream_t st_ = nullptr);
   void stop();
 };
 
@@ -273,13 +274,13 @@ cudaEvent_t ev_get(cparls_ctx *c) {
   CK(cudaEventCreate(&e));
   return e;
 }
-KTimer::KTimer(cparls_ctx *c_, int id_) : c(c_), id(id_) {
+KTimer::KTimer(cparls_ctx *c_, int id_, cudaStream_t st_) : c(c_), id(id_), st(st_ ? st_ : c_->st) {
   a = ev_get(c);
   b = ev_get(c);
-  CK(cudaEventRecord(a, c->st));
+  CK(cudaEventRecord(a, st));
 }
 void KTimer::stop() {
-  CK(cudaEventRecord(b, c->st));
+  CK(cudaEventRecord(b, st));
   c->ev_pending.push_back({id, {a, b}});
   c->stats.kernel_launches_by_id[id]++;
 }
@@ -1208,8 +1209,12 @@ void solve_impl(cparls_ctx *c, int k, cparls_solve_info *info) {
   c->smode_last_solved = k;
 }
 
-double fit_impl(cparls_ctx *c) {
-  Phase ph(c, &c->stats.ms_fit);
+// Launch the exact fit (eq:fit) on stream st from the factors
+// A[0..D) and the model's lambda: <X,M> partials into part (dd[nb]), then
+// k_fit_final -> out[0] = fit (single GPU), out[1] = <X,M>, out[2] = ||M||^2.
+// blocks_per_sm: CTAs of the persistent fit kernel per SM (2 = all warp slots).
+void fit_launch(cparls_ctx *c, cudaStream_t st, double *const *A, const double *lam, const FitModes &fm,
+                dd *part, unsigned long long *counter, double *out, int blocks_per_sm) {
   const int k = c->fit_mode;
   FitDecode fd{};
   fd.d = c->D - 1;
@@ -1218,20 +1223,19 @@ double fit_impl(cparls_ctx *c) {
     const int m = c->idx[k].order[j];
     fd.n[j] = c->dims[m];
     fd.inv[j] = 1.0 / (double)c->dims[m];
-    fd.A[j] = c->A[m];
+    fd.A[j] = A[m];
     N *= (long double)c->dims[m];
   }
   fd.fast = N < 9007199254740992.0L;   // keys < 2^53
   int nb = 148 * 4;
-  KTimer kt(c, KT_FIT);
+  KTimer kt(c, KT_FIT, st);
   if (fd.d <= 3) {
     // sub-warp per entry, 4 columns per lane (k_fit_sub)
-    nb = 148 * 2;
-    CK(cudaMemsetAsync(&c->dv->counter, 0, sizeof(unsigned long long), c->st));
+    nb = 148 * std::max(1, std::min(2, blocks_per_sm));
+    CK(cudaMemsetAsync(counter, 0, sizeof(unsigned long long), st));
 #define FITS(VT, SW, DM)                                                                                         \
-  k_fit_sub<VT, SW, DM, (SW >= CPARLS_FIT_U ? CPARLS_FIT_U : SW)><<<nb, kFitThreads, 0, c->st>>>(c->idx[k].key, c->idx[k].out, (const VT *)c->idx[k].val, \
-                                                          c->idx[k].nnz, fd, c->A[k], c->lam_model, c->r, c->ld,  \
-                                                          c->ddpart, &c->dv->counter)
+  k_fit_sub<VT, SW, DM, (SW >= CPARLS_FIT_U ? CPARLS_FIT_U : SW)><<<nb, kFitThreads, 0, st>>>(c->idx[k].key, c->idx[k].out, (const VT *)c->idx[k].val, \
+                                                          c->idx[k].nnz, fd, A[k], lam, c->r, c->ld, part, counter)
 #define FITSD(VT, SW)                          \
   do {                                         \
     if (fd.d == 1) FITS(VT, SW, 1);            \
@@ -1251,22 +1255,33 @@ double fit_impl(cparls_ctx *c) {
   } else {
     const size_t smem = sizeof(double) * kFitThreads * (size_t)(c->r | 1);
     if (c->vf32)
-      RSWITCH(c->r, k_fit_thread<float, RM><<<nb, kFitThreads, smem, c->st>>>(
-                        c->idx[k].key, c->idx[k].out, (const float *)c->idx[k].val, c->idx[k].nnz, fd, c->A[k],
-                        c->lam_model, c->r, c->ld, c->ddpart));
+      RSWITCH(c->r, k_fit_thread<float, RM><<<nb, kFitThreads, smem, st>>>(
+                        c->idx[k].key, c->idx[k].out, (const float *)c->idx[k].val, c->idx[k].nnz, fd, A[k],
+                        lam, c->r, c->ld, part));
     else
-      RSWITCH(c->r, k_fit_thread<double, RM><<<nb, kFitThreads, smem, c->st>>>(
-                        c->idx[k].key, c->idx[k].out, (const double *)c->idx[k].val, c->idx[k].nnz, fd, c->A[k],
-                        c->lam_model, c->r, c->ld, c->ddpart));
+      RSWITCH(c->r, k_fit_thread<double, RM><<<nb, kFitThreads, smem, st>>>(
+                        c->idx[k].key, c->idx[k].out, (const double *)c->idx[k].val, c->idx[k].nnz, fd, A[k],
+                        lam, c->r, c->ld, part));
   }
   kt.stop();
   CK_LAUNCH();
-  FitModes fm{};
-  fm.D = c->D;
-  for (int m = 0; m < c->D; ++m) fm.GA[m] = c->md[m]->GA;
-  k_fit_final<<<1, 256, 0, c->st>>>(c->ddpart, nb, fm, c->lam_model, c->r, c->normX2, c->dv->fit);
+  k_fit_final<<<1, 256, 0, st>>>(part, nb, fm, lam, c->r, c->normX2, out);
   CK_LAUNCH();
   LAUNCHED(c, 2);
+  c->stats.fits++;
+  c->stats.bytes_fit += (double)c->idx[k].nnz * (8.0 + 4.0 + (c->vf32 ? 4.0 : 8.0));
+}
+
+FitModes fit_modes(cparls_ctx *c, double *const *GA) {
+  FitModes fm{};
+  fm.D = c->D;
+  for (int m = 0; m < c->D; ++m) fm.GA[m] = GA ? GA[m] : c->md[m]->GA;
+  return fm;
+}
+
+double fit_impl(cparls_ctx *c) {
+  Phase ph(c, &c->stats.ms_fit);
+  fit_launch(c, c->st, c->A, c->lam_model, fit_modes(c, nullptr), c->ddpart, &c->dv->counter, c->dv->fit, 2);
   double f;
   if (c->world > 1) {
     // <X,M> is a sum over the ranks' slices of the fit mode
@@ -1280,8 +1295,6 @@ double fit_impl(cparls_ctx *c) {
   } else {
     f = read_dev(c, &c->dv->fit[0]);
   }
-  c->stats.fits++;
-  c->stats.bytes_fit += (double)c->idx[k].nnz * (8.0 + 4.0 + (c->vf32 ? 4.0 : 8.0));
   ph.end();
   return f;
 }
