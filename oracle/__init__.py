@@ -84,6 +84,10 @@ def _setup(L):
     L.or_run.argtypes = [P, I32, I64, D, U64, I32, P]; L.or_run.restype = I32
     L.or_didx.argtypes = [I32, P, P, D, I64, P, P, P]; L.or_didx.restype = I64
     L.or_didx_brute.argtypes = [I32, P, P, D, I64, P, P, P]; L.or_didx_brute.restype = I64
+    L.or_fit_sample.argtypes = [P, I64, D, U64, P, P]; L.or_fit_sample.restype = I32
+    L.or_get_fit_sample.argtypes = [P, I64, P, P, P]; L.or_get_fit_sample.restype = I64
+    L.or_fit_estimate.argtypes = [P, P]; L.or_fit_estimate.restype = D
+    L.or_run_until.argtypes = [P, I64, D, U64, I32, I32, D, I32, I32, P, P]; L.or_run_until.restype = I32
 
 
 def _p(a: np.ndarray):
@@ -254,6 +258,35 @@ class Oracle:
 
     def als_update(self, k):
         return lib().or_als_update(self._h, k)
+
+    def fit_sample(self, s_fit, alpha=0.5, seed=0):
+        """Draw and freeze the stratified fit sample (AMB-32)."""
+        nn, nz = C.c_int64(), C.c_int64()
+        st = lib().or_fit_sample(self._h, int(s_fit), float(alpha), int(seed), C.byref(nn), C.byref(nz))
+        if st:
+            raise RuntimeError(f"or_fit_sample status {st}")
+        return nn.value, nz.value
+
+    def get_fit_sample(self):
+        n = lib().or_get_fit_sample(self._h, 0, None, None, None)
+        coords = np.zeros((n, self.D), dtype=np.int64); x = np.zeros(n); nz = np.zeros(n, dtype=np.uint8)
+        lib().or_get_fit_sample(self._h, n, _p(coords), _p(x), _p(nz))
+        return coords, x, nz.astype(bool)
+
+    def fit_estimate(self):
+        F = np.zeros(1)
+        f = lib().or_fit_estimate(self._h, _p(F))
+        return float(f), float(F[0])
+
+    def run_until(self, s, tau, seed, eta=5, pi=3, tol=1e-4, max_epochs=50, estimated=False):
+        """Alg. 3 with its stopping rule (AMB-33); returns the per-epoch fit trace."""
+        trace = np.full(max_epochs, np.nan)
+        ep = C.c_int()
+        st = lib().or_run_until(self._h, int(s), float(tau), int(seed), int(eta), int(pi), float(tol),
+                                int(max_epochs), 1 if estimated else 0, _p(trace), C.byref(ep))
+        if st:
+            raise RuntimeError(f"or_run_until status {st}")
+        return trace[:ep.value]
 
     def run(self, iters, s, tau, seed, fit_every=1):
         trace = np.full(iters, np.nan)

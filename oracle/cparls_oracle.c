@@ -228,6 +228,11 @@ struct or_ctx {
   int lmode;
   double G[OR_MAXR * OR_MAXR];
   double *M, *B;
+  /* frozen stratified fit sample */
+  int64_t fs_nnz, fs_zero;   /* stratum sizes */
+  int64_t *fs_coords;        /* (fs_nnz + fs_zero) x D */
+  double *fs_x;
+  double fs_phi_nz, fs_phi_z;
 };
 
 static uint64_t hash64(uint64_t k) { return k * 0x9E3779B97F4A7C15ull; }
@@ -331,6 +336,7 @@ void or_destroy(or_ctx *c) {
   free(c->coords); free(c->vals);
   free(c->skeys); free(c->scnt); free(c->sw2); free(c->sp); free(c->sisdet);
   free(c->M); free(c->B);
+  free(c->fs_coords); free(c->fs_x);
   free(c);
 }
 
@@ -924,5 +930,138 @@ int or_run(or_ctx *c, int iters, int64_t s, double tau, uint64_t seed, int fit_e
       else fit_trace[t] = NAN;
     }
   }
+  return 0;
+}
+
+/* ------------------------------------------------------------------ */
+/* O20: estimated fit by stratified sampling (sec:estimating-fit,       */
+/* P:964-989), AMB-32: ceil(alpha s_fit) nonzeros drawn uniformly WITH   */
+/* replacement from the input COO order, floor((1-alpha) s_fit) zeros by */
+/* rejection of uniform cells that are nonzeros (attempt order); draws   */
+/* from Philox4x32-10 with key = seed, counter = (draw lo, draw hi,      */
+/* 0x46495400, lane): nonzero draw i lane 0 words (0,1) -> e =            */
+/* mulhi(R, nnz); zero attempt a, mode m: lane 1 + m/2, words            */
+/* (2(m%2), 2(m%2)+1) -> i_m = mulhi(R, n_m).                            */
+/* ------------------------------------------------------------------ */
+static uint64_t mulhi64(uint64_t a, uint64_t b) { return (uint64_t)(((unsigned __int128)a * b) >> 64); }
+
+static uint64_t fs_word(uint64_t seed, uint64_t ctr, uint32_t lane, int half) {
+  uint32_t cc[4] = {(uint32_t)ctr, (uint32_t)(ctr >> 32), 0x46495400u, lane};
+  uint32_t kk[2] = {(uint32_t)seed, (uint32_t)(seed >> 32)};
+  uint32_t o[4];
+  or_philox4x32_10(cc, kk, o);
+  return (uint64_t)o[2 * half] | ((uint64_t)o[2 * half + 1] << 32);
+}
+
+/* is (ii[0..D)) a nonzero of X?  (mode-0 fiber of its key, scanned) */
+static int is_nonzero(or_ctx *c, const int64_t *ii) {
+  int64_t *ids = NULL;
+  int64_t n = fiber(c, 0, or_key(c->D, c->dims, 0, ii), &ids);
+  int hit = 0;
+  for (int64_t t = 0; t < n; ++t)
+    if (c->coords[ids[t] * c->D] == ii[0]) { hit = 1; break; }
+  free(ids);
+  return hit;
+}
+
+int or_fit_sample(or_ctx *c, int64_t s_fit, double alpha, uint64_t seed, int64_t *n_nz, int64_t *n_z) {
+  const int D = c->D;
+  if (s_fit < 1 || !(alpha >= 0.0 && alpha <= 1.0)) return 1;
+  int64_t nn = (int64_t)ceil(alpha * (double)s_fit);
+  int64_t nz = (int64_t)floor((1.0 - alpha) * (double)s_fit);
+  if (c->nnz == 0) nn = 0;
+  double Nd = 1.0;
+  for (int k = 0; k < D; ++k) Nd *= (double)c->dims[k];
+  const double Nz = Nd - (double)c->nnz;
+  if (!(Nz > 0.0)) nz = 0;   /* fully dense: no zero stratum */
+  free(c->fs_coords); free(c->fs_x);
+  c->fs_coords = (int64_t *)malloc(sizeof(int64_t) * ((nn + nz) * D + 1));
+  c->fs_x = (double *)malloc(sizeof(double) * (nn + nz + 1));
+  for (int64_t i = 0; i < nn; ++i) {
+    int64_t e = (int64_t)mulhi64(fs_word(seed, (uint64_t)i, 0u, 0), (uint64_t)c->nnz);
+    memcpy(c->fs_coords + i * D, c->coords + e * D, sizeof(int64_t) * D);
+    c->fs_x[i] = c->vals[e];
+  }
+  const int64_t cap = 64 * nz + 65536;
+  int64_t got = 0;
+  for (uint64_t a = 0; got < nz; ++a) {
+    if ((int64_t)a >= cap) return 6;
+    int64_t ii[OR_MAXD];
+    for (int m = 0; m < D; ++m) ii[m] = (int64_t)mulhi64(fs_word(seed, a, 1u + (uint32_t)(m / 2), m % 2),
+                                                         (uint64_t)c->dims[m]);
+    if (is_nonzero(c, ii)) continue;
+    memcpy(c->fs_coords + (nn + got) * D, ii, sizeof(int64_t) * D);
+    c->fs_x[nn + got] = 0.0;
+    ++got;
+  }
+  c->fs_nnz = nn;
+  c->fs_zero = nz;
+  c->fs_phi_nz = nn > 0 ? (double)c->nnz / (double)nn : 0.0;
+  c->fs_phi_z = nz > 0 ? Nz / (double)nz : 0.0;
+  if (n_nz) *n_nz = nn;
+  if (n_z) *n_z = nz;
+  return 0;
+}
+
+int64_t or_get_fit_sample(or_ctx *c, int64_t cap, int64_t *coords, double *x, uint8_t *is_nz) {
+  const int64_t n = c->fs_nnz + c->fs_zero;
+  for (int64_t i = 0; i < n && i < cap; ++i) {
+    if (coords) memcpy(coords + i * c->D, c->fs_coords + i * c->D, sizeof(int64_t) * c->D);
+    if (x) x[i] = c->fs_x[i];
+    if (is_nz) is_nz[i] = i < c->fs_nnz;
+  }
+  return n;
+}
+
+/* F^ = sum_i phi_i (m_i - x_i)^2; returns 1 - sqrt(F^)/||X||. */
+double or_fit_estimate(or_ctx *c, double *Fhat) {
+  const int D = c->D, r = c->r;
+  ksum F = {0, 0};
+  const int64_t n = c->fs_nnz + c->fs_zero;
+  for (int64_t i = 0; i < n; ++i) {
+    const int64_t *ix = c->fs_coords + i * D;
+    double m = 0.0;
+    for (int q = 0; q < r; ++q) {
+      double t = c->lambda[q];
+      for (int k = 0; k < D; ++k) t *= c->A[k][ix[k] * r + q];
+      m += t;
+    }
+    const double dlt = m - c->fs_x[i];
+    const double phi = i < c->fs_nnz ? c->fs_phi_nz : c->fs_phi_z;
+    kadd(&F, phi * (dlt * dlt));
+  }
+  double f = kval(&F);
+  if (Fhat) *Fhat = f;
+  if (f < 0.0) f = 0.0;
+  return 1.0 - sqrt(f) / sqrt(c->normX2);
+}
+
+/* Alg. 3 with its stopping rule, AMB-33: epochs of
+ * eta outer iterations; after each epoch the fit (0 exact, 1 estimated); an
+ * epoch improves if fit > best + tol (best = best fit so far, initially
+ * -inf), else a failure; stop after pi consecutive failures or max_epochs.
+ * trace[e] = fit after epoch e; returns 0 and *epochs, or a status. */
+int or_run_until(or_ctx *c, int64_t s, double tau, uint64_t seed, int eta, int pi, double tol, int max_epochs,
+                 int fit_kind, double *trace, int *epochs) {
+  double best = -INFINITY;
+  int fails = 0, e = 0;
+  for (e = 0; e < max_epochs; ++e) {
+    for (int t = 0; t < eta; ++t) {
+      const int64_t it = (int64_t)e * eta + t;
+      for (int k = 0; k < c->D; ++k) {
+        or_sample_info si;
+        or_solve_info so;
+        int st = or_sample(c, k, s, tau, seed, (uint64_t)it * c->D + k, &si);
+        if (st) return st;
+        st = or_solve_mode(c, k, &so);
+        if (st) return st;
+      }
+    }
+    const double f = fit_kind == 1 ? or_fit_estimate(c, NULL) : or_fit(c);
+    if (trace) trace[e] = f;
+    if (f > best + tol) { best = f; fails = 0; }
+    else if (++fails >= pi) { ++e; break; }
+  }
+  if (epochs) *epochs = e;
   return 0;
 }

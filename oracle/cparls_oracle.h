@@ -100,6 +100,20 @@ int or_als_update(or_ctx *c, int k);
 int or_run(or_ctx *c, int iters, int64_t s, double tau, uint64_t seed, int fit_every,
            double *fit_trace);
 
+/* Estimated fit (sec:estimating-fit; AMB-32): draw and freeze the
+ * stratified sample (ceil(alpha s_fit) nonzeros with replacement in input COO
+ * order, floor((1-alpha) s_fit) zero cells by rejection), Philox key = seed.
+ * Returns 0, 1 (bad argument) or 6 (rejection attempt cap). */
+int or_fit_sample(or_ctx *c, int64_t s_fit, double alpha, uint64_t seed, int64_t *n_nz, int64_t *n_z);
+/* Copy the frozen sample (nonzero stratum first): coords (n x D), x, is_nz. */
+int64_t or_get_fit_sample(or_ctx *c, int64_t cap, int64_t *coords, double *x, uint8_t *is_nz);
+/* 1 - sqrt(F^)/||X||, F^ = sum_i phi_i (m_i - x_i)^2; *Fhat optional. */
+double or_fit_estimate(or_ctx *c, double *Fhat);
+/* Alg. 3 with its stopping rule (AMB-33): fit_kind 0 exact, 1 estimated;
+ * trace per epoch; *epochs = epochs run. */
+int or_run_until(or_ctx *c, int64_t s, double tau, uint64_t seed, int eta, int pi, double tol, int max_epochs,
+                 int fit_kind, double *trace, int *epochs);
+
 /* Standalone DIDX on d given p~ vectors (for pins): writes up to cap keys
  * (ascending) and p; returns s_det (full count) or -1 on cap overflow. */
 int64_t or_didx(int d, const int64_t *n, const double *const *pt, double tau, int64_t cap,
