@@ -68,6 +68,11 @@ typedef struct {
                               memory without atomics (rhs_bucket.cuh; needs r <= 32,
                               s_bar < 2^27, m_k < 2^32).  Same math; B = M G^+ follows
                               in k_solve_rows_t either way.                          */
+  int64_t fit_samples;     /* s_fit > 0: draw the stratified fit sample at create
+                              (sec:estimating-fit, AMB-32); 0 = none.
+                              Single GPU only (EINVAL with world_size > 1).          */
+  double fit_alpha;        /* nonzero fraction alpha of the sample (<= 0 -> 0.5)     */
+  uint64_t fit_seed;       /* Philox key of the fit sample                           */
 } cparls_opts;
 
 typedef struct {
@@ -166,6 +171,21 @@ cparls_status cparls_fit(cparls_ctx *ctx, double *fit);
  * be resumed exactly (counter-based RNG). */
 cparls_status cparls_run(cparls_ctx *ctx, int32_t iters, int64_t s, uint64_t seed, int32_t iter0,
                          int32_t fit_every, double *fit_trace);
+
+/* Estimated fit: 1 - sqrt(F^)/||X|| over the frozen sample drawn
+ * at create (opts.fit_samples > 0, else ESTATE).  Fhat may be NULL. */
+cparls_status cparls_fit_estimate(cparls_ctx *ctx, double *fit, double *Fhat);
+/* The frozen fit sample, nonzero stratum first: coords (cap x D, int64),
+ * x (cap), is_nz (cap); *n = total size.  NULL arrays / cap 0 query n. */
+cparls_status cparls_get_fit_sample(cparls_ctx *ctx, int64_t cap, int64_t *coords, double *x, uint8_t *is_nz,
+                                    int64_t *n);
+/* Alg. 3 with its stopping rule (AMB-33): epochs of eta outer
+ * iterations (steps (e*eta + t)*D + k), a fit after each epoch (fit_kind 0
+ * exact, 1 estimated), stop after pi consecutive epochs without
+ * fit > best + tol, or after max_epochs.  trace: max_epochs host doubles (fit
+ * per epoch); *epochs = epochs run. */
+cparls_status cparls_run_until(cparls_ctx *ctx, int64_t s, uint64_t seed, int32_t eta, int32_t pi, double tol,
+                               int32_t max_epochs, int32_t fit_kind, double *trace, int32_t *epochs);
 
 /* ---- multi-GPU (SURVEY 8(e), P:1797-1801 sketches the distributed variant) ----
  * Row sharding: for every mode k the rows of B (and the nonzeros whose mode-k

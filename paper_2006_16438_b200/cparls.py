@@ -29,7 +29,8 @@ class Opts(C.Structure):
     _fields_ = [("rank", C.c_int32), ("tau", C.c_double), ("value_dtype", C.c_int32),
                 ("index_dtype", C.c_int32), ("stream", C.c_void_p), ("world_size", C.c_int32),
                 ("world_rank", C.c_int32), ("comm", C.c_void_p), ("didx_cap", C.c_int64),
-                ("attempt_cap", C.c_int64), ("rhs_path", C.c_int32)]
+                ("attempt_cap", C.c_int64), ("rhs_path", C.c_int32), ("fit_samples", C.c_int64),
+                ("fit_alpha", C.c_double), ("fit_seed", C.c_uint64)]
 
 
 class SampleInfo(C.Structure):
@@ -88,6 +89,9 @@ def lib():
             "cparls_get_last_solve": [P, P, P],
             "cparls_fit": [P, P],
             "cparls_run": [P, I32, I64, U64, I32, I32, P],
+            "cparls_fit_estimate": [P, P, P],
+            "cparls_get_fit_sample": [P, I64, P, P, P, P],
+            "cparls_run_until": [P, I64, U64, I32, I32, D, I32, I32, P, P],
             "cparls_get_stats": [P, C.POINTER(Stats)],
             "cparls_reset_stats": [P],
             "cparls_set_profiling": [P, I32],
@@ -113,7 +117,8 @@ def lib():
 EXPORTED = ["cparls_create", "cparls_destroy", "cparls_set_factor", "cparls_get_factor",
             "cparls_leverage", "cparls_get_ptilde", "cparls_set_ptilde", "cparls_sample",
             "cparls_set_tau", "cparls_get_sample", "cparls_get_fibers", "cparls_solve_mode",
-            "cparls_get_last_solve", "cparls_fit", "cparls_run", "cparls_get_stats",
+            "cparls_get_last_solve", "cparls_fit", "cparls_run", "cparls_fit_estimate",
+            "cparls_get_fit_sample", "cparls_run_until", "cparls_get_stats",
             "cparls_reset_stats", "cparls_set_profiling", "cparls_last_error", "cparls_version",
             "cparls_comm_nccl_unique_id", "cparls_comm_create_nccl", "cparls_comm_create_local",
             "cparls_comm_destroy", "cparls_plan_rows", "cparls_owned_rows"]
@@ -133,7 +138,8 @@ class Cparls:
     """One CP-ARLS-LEV context (the C ABI's cparls_ctx)."""
 
     def __init__(self, dims, coords, vals, rank, tau=-1.0, init_seed=2, stream=None,
-                 didx_cap=0, attempt_cap=0, comm=None, world_size=1, world_rank=0, rhs_path=0):
+                 didx_cap=0, attempt_cap=0, comm=None, world_size=1, world_rank=0, rhs_path=0,
+                 fit_samples=0, fit_alpha=0.5, fit_seed=0):
         import torch
         if not torch.cuda.is_available():
             raise RuntimeError("cparls needs a CUDA device (B200); no CPU fallback exists")
@@ -161,7 +167,8 @@ class Cparls:
         o = Opts(rank=self.r, tau=float(tau), value_dtype=vdt, index_dtype=idt,
                  stream=C.c_void_p(stream), world_size=int(world_size), world_rank=int(world_rank),
                  comm=(comm.handle if comm is not None else None),
-                 didx_cap=int(didx_cap), attempt_cap=int(attempt_cap), rhs_path=int(rhs_path))
+                 didx_cap=int(didx_cap), attempt_cap=int(attempt_cap), rhs_path=int(rhs_path),
+                 fit_samples=int(fit_samples), fit_alpha=float(fit_alpha), fit_seed=int(fit_seed))
         d = np.array(self.dims, dtype=np.int64)
         h = C.c_void_p()
         st = L.cparls_create(C.byref(h), self.D, d.ctypes.data, nnz, _ptr(coords), _ptr(vals),
@@ -257,6 +264,30 @@ class Cparls:
         f = C.c_double()
         self._check(lib().cparls_fit(self._h, C.byref(f)))
         return f.value
+
+    def fit_estimate(self):
+        """Estimated fit over the frozen stratified sample: (fit, F^)."""
+        f, F = C.c_double(), C.c_double()
+        self._check(lib().cparls_fit_estimate(self._h, C.byref(f), C.byref(F)))
+        return f.value, F.value
+
+    def get_fit_sample(self):
+        n = C.c_int64()
+        self._check(lib().cparls_get_fit_sample(self._h, 0, None, None, None, C.byref(n)))
+        m = n.value
+        coords = np.zeros((m, self.D), dtype=np.int64); x = np.zeros(m); nz = np.zeros(m, dtype=np.uint8)
+        self._check(lib().cparls_get_fit_sample(self._h, m, coords.ctypes.data, x.ctypes.data, nz.ctypes.data,
+                                                C.byref(n)))
+        return coords, x, nz.astype(bool)
+
+    def run_until(self, s, seed, eta=5, pi=3, tol=1e-4, max_epochs=50, estimated=False):
+        """Alg. 3 with its stopping rule (AMB-33): the per-epoch fit trace."""
+        trace = np.full(max(max_epochs, 1), np.nan)
+        ep = C.c_int32()
+        self._check(lib().cparls_run_until(self._h, int(s), int(seed), int(eta), int(pi), float(tol),
+                                           int(max_epochs), 1 if estimated else 0, trace.ctypes.data,
+                                           C.byref(ep)))
+        return trace[:ep.value]
 
     def run(self, iters, s, seed, iter0=0, fit_every=1):
         trace = np.full(max(iters, 1), np.nan)

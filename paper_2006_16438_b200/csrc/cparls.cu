@@ -144,6 +144,12 @@ struct cparls_ctx {
   uint32_t *rec = nullptr;
   double *recc = nullptr;
   bool m_dirty = false;   // M holds rows written by the bucketed RHS (not zero)
+  // frozen stratified fit sample (fitest.cuh, AMB-32)
+  bool have_fs = false;
+  int64_t fs_nnz = 0, fs_zero = 0;
+  double fs_phi_nz = 0.0, fs_phi_z = 0.0;
+  int32_t *fs_idx[kMaxModes] = {nullptr};
+  double *fs_x = nullptr;
   int32_t *seg_j = nullptr;
   // RHS hot rows per mode (warp-private accumulation, see rhs.cuh)
   int64_t nfib[kMaxModes] = {0};
@@ -1209,6 +1215,102 @@ void solve_impl(cparls_ctx *c, int k, cparls_solve_info *info) {
   c->smode_last_solved = k;
 }
 
+// ---------------------------------------------------------------- estimated fit (N1)
+FitSampleDev fs_dev(cparls_ctx *c) {
+  FitSampleDev fs{};
+  fs.D = c->D;
+  for (int m = 0; m < c->D; ++m) { fs.dims[m] = c->dims[m]; fs.idx[m] = c->fs_idx[m]; }
+  fs.x = c->fs_x;
+  return fs;
+}
+
+// Draw and freeze the stratified sample (AMB-32) from the COO
+// input (device pointers) and the mode-0 sorted copy (membership of zeros).
+template <typename IT, typename VT>
+void draw_fit_sample(cparls_ctx *c, const IT *coords, const VT *vals, int64_t s_fit, double alpha, uint64_t seed) {
+  if (!(alpha > 0.0)) alpha = 0.5;
+  if (alpha > 1.0) throw ApiError(CPARLS_EINVAL, "fit_alpha must be in (0, 1]");
+  int64_t nn = (int64_t)std::ceil(alpha * (double)s_fit);
+  int64_t nz = (int64_t)std::floor((1.0 - alpha) * (double)s_fit);
+  if (c->nnz == 0) nn = 0;
+  double Nd = 1.0;
+  for (int m = 0; m < c->D; ++m) Nd *= (double)c->dims[m];
+  const double Nz = Nd - (double)c->nnz;
+  if (!(Nz > 0.0)) nz = 0;
+  const int64_t tot = nn + nz;
+  for (int m = 0; m < c->D; ++m) c->fs_idx[m] = dalloc_t<int32_t>(c, tot);
+  c->fs_x = dalloc_t<double>(c, tot);
+  FitSampleDev fs = fs_dev(c);
+  if (nn > 0) {
+    k_fs_nz<IT, VT><<<(unsigned)ceil_div(nn, 256), 256, 0, c->st>>>(coords, vals, c->nnz, nn, seed, fs);
+    CK_LAUNCH();
+  }
+  if (nz > 0) {
+    MemberIndex mi{};
+    const ModeIndex &ix = c->idx[0];
+    mi.key = ix.key; mi.out = ix.out; mi.dir = ix.dir; mi.shift = ix.shift; mi.nbkt = ix.nbkt;
+    mi.d = c->D - 1;
+    uint64_t mult = 1;
+    for (int j = 0; j < mi.d; ++j) { mi.order[j] = ix.order[j]; mi.mult[j] = mult; mult *= (uint64_t)c->dims[ix.order[j]]; }
+    const int64_t cap = 64 * nz + 65536;
+    const int64_t wmax = std::min<int64_t>(nz + nz / 16 + 4096, int64_t(1) << 26);
+    int64_t *flag = dalloc_t<int64_t>(c, wmax), *pos = dalloc_t<int64_t>(c, wmax);
+    int32_t *cell = dalloc_t<int32_t>(c, wmax * c->D);
+    int64_t *part = dalloc_t<int64_t>(c, ceil_div(wmax, kScanTile) + 16);
+    int64_t have = 0;
+    uint64_t a0 = 0;
+    while (have < nz) {
+      if ((int64_t)a0 >= cap) throw ApiError(CPARLS_ESAMPLE, "fit sample: zero-rejection attempt cap reached");
+      const int64_t win = std::min<int64_t>(wmax, std::min<int64_t>(cap - (int64_t)a0, (nz - have) + (nz - have) / 16 + 4096));
+      const unsigned g = (unsigned)ceil_div(win, 256);
+      k_fs_zero_gen<<<g, 256, 0, c->st>>>(mi, c->D, fs, seed, a0, win, flag, cell);
+      CK_LAUNCH();
+      exclusive_scan_i64(flag, pos, win, part, &c->dv->total, c->st);
+      k_fs_zero_scatter<<<g, 256, 0, c->st>>>(flag, pos, win, cell, c->D, nn + have, nz - have, fs,
+                                               &c->dv->last_attempt, a0);
+      CK_LAUNCH();
+      have += std::min<int64_t>(read_dev(c, &c->dv->total), nz - have);
+      a0 += (uint64_t)win;
+    }
+    sync(c);
+    dfree(c, flag); dfree(c, pos); dfree(c, cell); dfree(c, part);
+  }
+  c->fs_nnz = nn;
+  c->fs_zero = nz;
+  c->fs_phi_nz = nn > 0 ? (double)c->nnz / (double)nn : 0.0;
+  c->fs_phi_z = nz > 0 ? Nz / (double)nz : 0.0;
+  c->have_fs = true;
+}
+
+double fit_estimate_impl(cparls_ctx *c, double *Fhat) {
+  if (!c->have_fs) throw ApiError(CPARLS_ESTATE, "no fit sample (cparls_opts.fit_samples = 0)");
+  Phase ph(c, &c->stats.ms_fit);
+  FitDecode fa{};
+  fa.d = c->D;
+  for (int m = 0; m < c->D; ++m) fa.A[m] = c->A[m];
+  const int64_t tot = c->fs_nnz + c->fs_zero;
+  const int nb = 148 * 8;
+  KTimer kt(c, KT_FIT);
+  if (c->ld <= 8) k_fit_est<2><<<nb, 256, 0, c->st>>>(fs_dev(c), c->fs_nnz, tot, c->fs_phi_nz, c->fs_phi_z, fa,
+                                                      c->lam_model, c->r, c->ld, c->ddpart);
+  else if (c->ld <= 32) k_fit_est<8><<<nb, 256, 0, c->st>>>(fs_dev(c), c->fs_nnz, tot, c->fs_phi_nz, c->fs_phi_z,
+                                                            fa, c->lam_model, c->r, c->ld, c->ddpart);
+  else k_fit_est<16><<<nb, 256, 0, c->st>>>(fs_dev(c), c->fs_nnz, tot, c->fs_phi_nz, c->fs_phi_z, fa,
+                                            c->lam_model, c->r, c->ld, c->ddpart);
+  kt.stop();
+  CK_LAUNCH();
+  k_fit_est_final<<<1, 256, 0, c->st>>>(c->ddpart, nb, c->normX2, c->dv->fit);
+  CK_LAUNCH();
+  LAUNCHED(c, 2);
+  double hv[2];
+  CK(cudaMemcpyAsync(hv, c->dv->fit, sizeof(hv), cudaMemcpyDeviceToHost, c->st));
+  sync(c);
+  if (Fhat) *Fhat = hv[1];
+  c->stats.fits++;
+  ph.end();
+  return hv[0];
+}
+
 // Launch the exact fit (eq:fit) on stream st from the factors
 // A[0..D) and the model's lambda: <X,M> partials into part (dd[nb]), then
 // k_fit_final -> out[0] = fit (single GPU), out[1] = <X,M>, out[2] = ||M||^2.
@@ -1410,6 +1512,21 @@ cparls_status cparls_create(cparls_ctx **out, int32_t nmodes, const int64_t *dim
     else if (vsz == 4) build_all<int64_t, float>(c, (const int64_t *)dco, (const float *)dva);
     else build_all<int64_t, double>(c, (const int64_t *)dco, (const double *)dva);
     sync(c);
+    if (opts->fit_samples > 0) {
+      if (c->world > 1) throw ApiError(CPARLS_EINVAL, "fit_samples needs world_size == 1");
+      if (isz == 4 && vsz == 4)
+        draw_fit_sample<int32_t, float>(c, (const int32_t *)dco, (const float *)dva, opts->fit_samples,
+                                        opts->fit_alpha, opts->fit_seed);
+      else if (isz == 4)
+        draw_fit_sample<int32_t, double>(c, (const int32_t *)dco, (const double *)dva, opts->fit_samples,
+                                         opts->fit_alpha, opts->fit_seed);
+      else if (vsz == 4)
+        draw_fit_sample<int64_t, float>(c, (const int64_t *)dco, (const float *)dva, opts->fit_samples,
+                                        opts->fit_alpha, opts->fit_seed);
+      else
+        draw_fit_sample<int64_t, double>(c, (const int64_t *)dco, (const double *)dva, opts->fit_samples,
+                                         opts->fit_alpha, opts->fit_seed);
+    }
     dfree(c, own_c);
     dfree(c, own_v);
     // factors, p~, CDF
@@ -1743,6 +1860,71 @@ cparls_status cparls_run(cparls_ctx *c, int32_t iters, int64_t s, uint64_t seed,
       }
       if (fit_trace) fit_trace[t] = f;
     }
+  });
+}
+
+cparls_status cparls_fit_estimate(cparls_ctx *c, double *fit, double *Fhat) {
+  if (!c) return CPARLS_EINVAL;
+  return guarded(c, [&] {
+    if (c->normX2 <= 0.0) throw ApiError(CPARLS_ENUMERIC, "||X|| = 0: fit undefined");
+    const double f = fit_estimate_impl(c, Fhat);
+    if (fit) *fit = f;
+  });
+}
+
+cparls_status cparls_get_fit_sample(cparls_ctx *c, int64_t cap, int64_t *coords, double *x, uint8_t *is_nz,
+                                    int64_t *n) {
+  if (!c) return CPARLS_EINVAL;
+  return guarded(c, [&] {
+    if (!c->have_fs) throw ApiError(CPARLS_ESTATE, "no fit sample (cparls_opts.fit_samples = 0)");
+    const int64_t tot = c->fs_nnz + c->fs_zero;
+    if (n) *n = tot;
+    const int64_t m = std::min(cap, tot);
+    if (m <= 0) return;
+    std::vector<int32_t> col(m);
+    for (int d = 0; d < c->D; ++d) {
+      CK(cudaMemcpyAsync(col.data(), c->fs_idx[d], sizeof(int32_t) * m, cudaMemcpyDeviceToHost, c->st));
+      sync(c);
+      if (coords)
+        for (int64_t i = 0; i < m; ++i) coords[i * c->D + d] = col[i];
+    }
+    if (x) {
+      CK(cudaMemcpyAsync(x, c->fs_x, sizeof(double) * m, cudaMemcpyDeviceToHost, c->st));
+      sync(c);
+    }
+    if (is_nz)
+      for (int64_t i = 0; i < m; ++i) is_nz[i] = i < c->fs_nnz;
+  });
+}
+
+cparls_status cparls_run_until(cparls_ctx *c, int64_t s, uint64_t seed, int32_t eta, int32_t pi, double tol,
+                               int32_t max_epochs, int32_t fit_kind, double *trace, int32_t *epochs) {
+  if (!c) return CPARLS_EINVAL;
+  return guarded(c, [&] {
+    if (eta < 1 || pi < 1 || max_epochs < 0) throw ApiError(CPARLS_EINVAL, "eta, pi >= 1; max_epochs >= 0");
+    if (c->normX2 <= 0.0) throw ApiError(CPARLS_ENUMERIC, "||X|| = 0: fit undefined");
+    if (fit_kind == 1 && !c->have_fs) throw ApiError(CPARLS_ESTATE, "estimated fit needs opts.fit_samples > 0");
+    double best = -INFINITY;
+    int fails = 0, e = 0;
+    for (e = 0; e < max_epochs; ++e) {
+      for (int t = 0; t < eta; ++t) {
+        const int64_t it = (int64_t)e * eta + t;
+        for (int k = 0; k < c->D; ++k) {
+          sample_impl(c, k, s, seed, (uint64_t)it * c->D + k, nullptr);   // AMB-10
+          solve_impl(c, k, nullptr);
+        }
+      }
+      const double f = fit_kind == 1 ? fit_estimate_impl(c, nullptr) : fit_impl(c);
+      if (trace) trace[e] = f;
+      if (f > best + tol) {   // AMB-33: improvement over the best fit so far
+        best = f;
+        fails = 0;
+      } else if (++fails >= pi) {
+        ++e;
+        break;
+      }
+    }
+    if (epochs) *epochs = e;
   });
 }
 

@@ -808,3 +808,4 @@ __global__ void k_pack_nz(const IT *__restrict__ coords, const VT *__restrict__ 
 #include "rhs.cuh"
 #include "rhs_bucket.cuh"
 #include "fit.cuh"
+#include "fitest.cuh"
