@@ -24,6 +24,8 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 ETA = 5                       # epoch length
+FIT_SAMPLES = 1 << 27         # s_fit of the paper's estimated fit on Amazon
+FIT_SEED = 17
 METRIC = "CP-ARLS-LEV ALS iterations/sec (r=25, s=2^17) and % of HBM roofline"
 
 
@@ -262,8 +264,12 @@ def run_ours(args):
     torch.cuda.empty_cache()
     stream = torch.cuda.current_stream(dev)
     t0 = time.perf_counter()
+    # the paper's estimated-fit sample for its Amazon runs: s_fit = 2^27,
+    # drawn once at create (single GPU; the exact fit is the headline)
+    fit_samples = FIT_SAMPLES if ws == 1 else 0
     g = Cparls(cfg.dims, coords, vals, cfg.rank, tau=args.tau, init_seed=cfg.init_seed,
-               stream=stream.cuda_stream, comm=comm, world_size=ws, world_rank=rk)
+               stream=stream.cuda_stream, comm=comm, world_size=ws, world_rank=rk,
+               fit_samples=fit_samples, fit_seed=FIT_SEED)
     torch.cuda.synchronize()
     t_build = time.perf_counter() - t0
     del coords, vals, T
@@ -296,6 +302,26 @@ def run_ours(args):
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         ms = float(tt[0])
     st = g.stats()          # resolves the per-kernel event timers of the timed region
+    # secondary: the same K iterations with the paper's estimated fit
+    # per epoch instead of the exact one (Alg. 3 as run on Amazon, s_fit = 2^27)
+    est = None
+    if fit_samples:
+        g.reset_stats()
+        torch.cuda.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for t in range(K):
+            g.run(1, cfg.s, seed, iter0=args.warmup + K + t, fit_every=0)
+            if (t + 1) % ETA == 0:
+                g.fit_estimate()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        st_est = g.stats()
+        nf = st_est["kernel_launches_by_id"]["fit"]
+        est = {"value": K / (e0.elapsed_time(e1) / 1000.0), "unit": "iterations/s", "s_fit": FIT_SAMPLES,
+               "fit_alpha": 0.5, "fit_est_kernel_avg_ms": (st_est["kernel_ms"]["fit"] / nf) if nf else None,
+               "fit_estimate": g.fit_estimate()[0],
+               "what": "same K iterations, estimated fit (stratified sample, frozen at create) per epoch"}
     if st["fits"] == 0:     # K < ETA: time one fit so the fit kernel is still reported
         g.fit()
         st_fit = g.stats()
@@ -411,6 +437,7 @@ def run_ours(args):
         "e2e": e2e,
         "cpu_baseline": cpu,
         "fit": final_fit,
+        "estimated_fit_variant": est,
         "setup": {"generate_s": t_gen, "create_s": t_build},
         "phases_ms": {k[3:]: st[k] for k in st if k.startswith("ms_")} if args.profile_phases else None,
         "counters": {"last_matched_nnz": st["last_matched_nnz"], "last_s_bar": st["last_s_bar"],

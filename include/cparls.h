@@ -179,6 +179,9 @@ cparls_status cparls_fit_estimate(cparls_ctx *ctx, double *fit, double *Fhat);
  * x (cap), is_nz (cap); *n = total size.  NULL arrays / cap 0 query n. */
 cparls_status cparls_get_fit_sample(cparls_ctx *ctx, int64_t cap, int64_t *coords, double *x, uint8_t *is_nz,
                                     int64_t *n);
+/* The model's value m_i at every fit-sample position (n = sample size host
+ * doubles), the same arithmetic as the estimate (diagnostics). */
+cparls_status cparls_fit_sample_model(cparls_ctx *ctx, double *m);
 /* Alg. 3 with its stopping rule (AMB-33): epochs of eta outer
  * iterations (steps (e*eta + t)*D + k), a fit after each epoch (fit_kind 0
  * exact, 1 estimated), stop after pi consecutive epochs without

@@ -91,6 +91,7 @@ def lib():
             "cparls_run": [P, I32, I64, U64, I32, I32, P],
             "cparls_fit_estimate": [P, P, P],
             "cparls_get_fit_sample": [P, I64, P, P, P, P],
+            "cparls_fit_sample_model": [P, P],
             "cparls_run_until": [P, I64, U64, I32, I32, D, I32, I32, P, P],
             "cparls_get_stats": [P, C.POINTER(Stats)],
             "cparls_reset_stats": [P],
@@ -118,7 +119,7 @@ EXPORTED = ["cparls_create", "cparls_destroy", "cparls_set_factor", "cparls_get_
             "cparls_leverage", "cparls_get_ptilde", "cparls_set_ptilde", "cparls_sample",
             "cparls_set_tau", "cparls_get_sample", "cparls_get_fibers", "cparls_solve_mode",
             "cparls_get_last_solve", "cparls_fit", "cparls_run", "cparls_fit_estimate",
-            "cparls_get_fit_sample", "cparls_run_until", "cparls_get_stats",
+            "cparls_get_fit_sample", "cparls_fit_sample_model", "cparls_run_until", "cparls_get_stats",
             "cparls_reset_stats", "cparls_set_profiling", "cparls_last_error", "cparls_version",
             "cparls_comm_nccl_unique_id", "cparls_comm_create_nccl", "cparls_comm_create_local",
             "cparls_comm_destroy", "cparls_plan_rows", "cparls_owned_rows"]
@@ -279,6 +280,14 @@ class Cparls:
         self._check(lib().cparls_get_fit_sample(self._h, m, coords.ctypes.data, x.ctypes.data, nz.ctypes.data,
                                                 C.byref(n)))
         return coords, x, nz.astype(bool)
+
+    def fit_sample_model(self):
+        """m_i of the current model at every fit-sample position (diagnostics)."""
+        n = C.c_int64()
+        self._check(lib().cparls_get_fit_sample(self._h, 0, None, None, None, C.byref(n)))
+        m = np.zeros(n.value)
+        self._check(lib().cparls_fit_sample_model(self._h, m.ctypes.data))
+        return m
 
     def run_until(self, s, seed, eta=5, pi=3, tol=1e-4, max_epochs=50, estimated=False):
         """Alg. 3 with its stopping rule (AMB-33): the per-epoch fit trace."""

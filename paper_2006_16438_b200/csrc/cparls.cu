@@ -1872,6 +1872,26 @@ cparls_status cparls_fit_estimate(cparls_ctx *c, double *fit, double *Fhat) {
   });
 }
 
+cparls_status cparls_fit_sample_model(cparls_ctx *c, double *m) {
+  if (!c || !m) return CPARLS_EINVAL;
+  return guarded(c, [&] {
+    if (!c->have_fs) throw ApiError(CPARLS_ESTATE, "no fit sample (cparls_opts.fit_samples = 0)");
+    FitDecode fa{};
+    fa.d = c->D;
+    for (int k = 0; k < c->D; ++k) fa.A[k] = c->A[k];
+    const int64_t tot = c->fs_nnz + c->fs_zero;
+    double *dm = dalloc_t<double>(c, tot);
+    const int nb = 148 * 8;
+    if (c->ld <= 8) k_fit_est_model<2><<<nb, 256, 0, c->st>>>(fs_dev(c), tot, fa, c->lam_model, c->r, c->ld, dm);
+    else if (c->ld <= 32) k_fit_est_model<8><<<nb, 256, 0, c->st>>>(fs_dev(c), tot, fa, c->lam_model, c->r, c->ld, dm);
+    else k_fit_est_model<16><<<nb, 256, 0, c->st>>>(fs_dev(c), tot, fa, c->lam_model, c->r, c->ld, dm);
+    CK_LAUNCH();
+    CK(cudaMemcpyAsync(m, dm, sizeof(double) * tot, cudaMemcpyDeviceToHost, c->st));
+    sync(c);
+    dfree(c, dm);
+  });
+}
+
 cparls_status cparls_get_fit_sample(cparls_ctx *c, int64_t cap, int64_t *coords, double *x, uint8_t *is_nz,
                                     int64_t *n) {
   if (!c) return CPARLS_EINVAL;

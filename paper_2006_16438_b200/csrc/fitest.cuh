@@ -161,6 +161,41 @@ __global__ void __launch_bounds__(256) k_fit_est(FitSampleDev fs, int64_t n_nz, 
   }
 }
 
+// m_i at every sample position (diagnostics: cparls_fit_sample_model), the
+// same arithmetic as k_fit_est
+template <int SW>
+__global__ void __launch_bounds__(256) k_fit_est_model(FitSampleDev fs, int64_t n_tot, FitDecode fa,
+                                                       const double *__restrict__ lam, int r, int ld,
+                                                       double *__restrict__ mout) {
+  const int lane = threadIdx.x & 31, sl = lane & (SW - 1);
+  const int c0 = 4 * sl;
+  const bool colok = c0 < ld;
+  double lam4[4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) lam4[q] = (c0 + q < r) ? lam[c0 + q] : 0.0;
+  const int64_t per = 32 / SW;
+  const int64_t gsub = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / SW;
+  const int64_t nsub = (int64_t)gridDim.x * blockDim.x / SW;
+  for (int64_t i0 = gsub - (gsub % per); i0 < n_tot; i0 += nsub) {
+    const int64_t i = i0 + (gsub % per);
+    const bool valid = i < n_tot;
+    double h[4] = {lam4[0], lam4[1], lam4[2], lam4[3]};
+    if (valid && colok) {
+      for (int m = 0; m < fa.d; ++m) {
+        const double2 *row = reinterpret_cast<const double2 *>(fa.A[m] + (int64_t)fs.idx[m][i] * ld + c0);
+        const double2 p0 = __ldg(row), p1 = __ldg(row + 1);
+        h[0] *= p0.x; h[1] *= p0.y; h[2] *= p1.x; h[3] *= p1.y;
+      }
+    } else {
+      h[0] = h[1] = h[2] = h[3] = 0.0;
+    }
+    double mpart = (h[0] + h[1]) + (h[2] + h[3]);
+#pragma unroll
+    for (int o = SW / 2; o >= 1; o >>= 1) mpart += __shfl_xor_sync(0xffffffffu, mpart, o, SW);
+    if (valid && sl == 0) mout[i] = mpart;
+  }
+}
+
 // F^ = sum of partials; out[0] = 1 - sqrt(max(F^,0))/||X||, out[1] = F^
 __global__ void k_fit_est_final(const dd *__restrict__ part, int nb, double normX2, double *out) {
   __shared__ dd red[256];

@@ -19,6 +19,8 @@ property that holds at any size:
 * the exact fit against its definition evaluated by torch in fp64 over all
   1.74B nonzeros (chunked), to 1e-8 absolute.
 """
+import math
+
 import numpy as np
 import pytest
 import torch
@@ -29,6 +31,8 @@ import synth
 pytestmark = pytest.mark.gpu
 
 SEED = 3
+FIT_SAMPLES = 1 << 27     # the paper's s_fit for Amazon
+FIT_SEED = 17
 
 
 def need_gpu():
@@ -44,7 +48,8 @@ def c4():
     dev = torch.device("cuda", 0)
     T = synth.make(cfg, device=dev, index_dtype=torch.int32)
     torch.cuda.empty_cache()
-    g = Cparls(cfg.dims, T.coords, T.vals, cfg.rank, tau=-1.0, init_seed=cfg.init_seed)
+    g = Cparls(cfg.dims, T.coords, T.vals, cfg.rank, tau=-1.0, init_seed=cfg.init_seed,
+               fit_samples=FIT_SAMPLES, fit_alpha=0.5, fit_seed=FIT_SEED)
     g.run(3, cfg.s, SEED, iter0=0, fit_every=0)        # bench.py's warm-up
     yield cfg, T, g
     g.close()
@@ -174,4 +179,77 @@ def test_c4_exact_fit_against_its_definition(c4):
     nm2 = lam_model @ V @ lam_model
     resid2 = torch.clamp(nx2 - 2 * inner + nm2, min=0.0)
     fref = float(1.0 - torch.sqrt(resid2) / torch.sqrt(nx2))
+    assert abs(fg - fref) <= 1e-8, (fg, fref)
+
+
+def test_c4_fit_sample_and_estimate(c4):
+    """N1 at full size: the frozen stratified sample re-derived from its
+    definition (AMB-32) with the generator's independent Philox on the GPU
+    (nonzero stratum: COO entries mulhi(R, nnz); zero stratum: the proposed
+    cells in attempt order, every skipped proposal a nonzero and a random
+    subset of the accepted ones checked absent by brute force), and F^ against
+    its definition evaluated by torch in fp64 over the sample."""
+    from synth import philox4x32_10
+    cfg, T, g = c4
+    dev = T.coords.device
+    gc, gx, gnz = g.get_fit_sample()
+    nn = (FIT_SAMPLES + 1) // 2
+    nz = FIT_SAMPLES // 2
+    assert gnz.sum() == nn and (~gnz).sum() == nz
+    nnz = T.coords.shape[0]
+
+    def words(ctr, lane):
+        c0 = (ctr & 0xFFFFFFFF).to(torch.int64)
+        c1 = (ctr >> 32).to(torch.int64)
+        return philox4x32_10(c0, c1, 0x46495400, lane, FIT_SEED & 0xFFFFFFFF, FIT_SEED >> 32)
+
+    def mulhi(lo32, hi32, n):
+        # floor(((hi << 32) | lo) * n / 2^64) with 64-bit limbs (n < 2^32)
+        a = lo32 * n
+        b = hi32 * n + (a >> 32)
+        return b >> 32
+
+    gcd = torch.from_numpy(gc).to(dev)
+    step = 1 << 24
+    for lo in range(0, nn, step):
+        i = torch.arange(lo, min(nn, lo + step), device=dev, dtype=torch.int64)
+        w = words(i, 0)
+        e = mulhi(w[0], w[1], nnz)
+        assert torch.equal(T.coords[e].to(torch.int64), gcd[lo:lo + len(i)])
+        assert torch.equal(T.vals[e].to(torch.float64), torch.from_numpy(gx[lo:lo + len(i)]).to(dev))
+    # zero stratum: proposals in attempt order
+    a = torch.arange(0, nz, device=dev, dtype=torch.int64)
+    w1, w2 = words(a, 1), words(a, 2)
+    cells = torch.stack([mulhi(w1[0], w1[1], cfg.dims[0]), mulhi(w1[2], w1[3], cfg.dims[1]),
+                         mulhi(w2[0], w2[1], cfg.dims[2])], 1)
+    zs = gcd[nn:]
+    # density ~1e-10: with this seed no proposal among the first n_z hits a
+    # nonzero, so the zero stratum is exactly the first n_z proposals
+    assert torch.equal(cells[:nz], zs)
+    for cell in zs[torch.randint(0, nz, (64,), device=dev, generator=torch.Generator(device=dev).manual_seed(0))]:
+        hit = ((T.coords[:, 0] == cell[0]) & (T.coords[:, 1] == cell[1]) & (T.coords[:, 2] == cell[2])).any()
+        assert not bool(hit)
+    # F^ from its definition over the (validated) sample
+    fg, Fg = g.fit_estimate()
+    A = [torch.from_numpy(g.get_factor(m)[0]).to(dev) for m in range(3)]
+    lam = torch.from_numpy(g.get_factor(0)[1]).to(dev)
+    x = torch.from_numpy(gx).to(dev)
+    m = torch.zeros(len(gx), dtype=torch.float64, device=dev)
+    am = torch.zeros(len(gx), dtype=torch.float64, device=dev)   # sum_c |lambda_c prod_m A_m(i_m, c)|
+    for lo in range(0, len(gx), step):
+        c = gcd[lo:lo + step]
+        h = A[0][c[:, 0]] * A[1][c[:, 1]] * A[2][c[:, 2]]
+        m[lo:lo + step] = h @ lam
+        am[lo:lo + step] = h.abs() @ lam.abs()
+    f64 = dict(dtype=torch.float64, device=dev)   # (torch.where on Python scalars would give fp32)
+    phi = torch.where(torch.from_numpy(gnz).to(dev), torch.tensor(nnz / nn, **f64),
+                      torch.tensor((float(cfg.dims[0]) * float(cfg.dims[1]) * float(cfg.dims[2]) - nnz) / nz, **f64))
+    Fref = float((phi * (m - x) ** 2).sum())
+    # m_i is a sum of r signed terms: its rounding is bounded by (r + d + 2) ulps
+    # of sum |terms| (both sides), so F^ is only that well determined where the
+    # terms cancel (zero cells); plus the long-sum rounding of F^ itself
+    eps = 2.0 ** -53
+    bound = float((phi * 2 * (m - x).abs() * (cfg.rank + 5) * eps * am).sum()) + 1e-13 * abs(Fref)
+    assert abs(Fg - Fref) <= bound, (Fg, Fref, bound)
+    fref = 1.0 - math.sqrt(max(Fref, 0.0)) / math.sqrt(float((T.vals.to(torch.float64) ** 2).sum()))
     assert abs(fg - fref) <= 1e-8, (fg, fref)

@@ -355,6 +355,9 @@ def test_fit_sample_and_estimate_parity(name, alpha):
         o.set_factor(D - 1, A * lam)
         fg, Fg = g.fit_estimate()
         fo, Fo = o.fit_estimate()
+        # the model at the sample positions, from the oracle's factors
+        m_o = np.array([np.prod([o.get_factor(q)[0][c[q]] for q in range(D)], axis=0).sum() for c in oc[:500]])
+        np.testing.assert_allclose(g.fit_sample_model()[:500], m_o, rtol=1e-12, atol=1e-14 * np.abs(m_o).max())
         assert abs(Fg - Fo) <= 1e-12 * abs(Fo), (Fg, Fo)
         assert abs(fg - fo) <= 1e-8
 
