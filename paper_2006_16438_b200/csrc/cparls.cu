@@ -1586,6 +1586,7 @@ cparls_status cparls_create(cparls_ctx **out, int32_t nmodes, const int64_t *dim
         const double cost = (double)nnz_global * (double)c->dims[m] + (double)c->nfib[m] * fib;
         if (m == 0 || cost < best) { best = cost; c->fit_mode = m; }
       }
+      if (getenv("CPARLS_FIT_MODE")) c->fit_mode = std::min(nmodes - 1, std::max(0, atoi(getenv("CPARLS_FIT_MODE"))));
     }
     if (getenv("CPARLS_DEBUG")) {
       for (int m = 0; m < nmodes; ++m)
