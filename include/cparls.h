@@ -190,6 +190,14 @@ cparls_status cparls_fit_sample_model(cparls_ctx *ctx, double *m);
 cparls_status cparls_run_until(cparls_ctx *ctx, int64_t s, uint64_t seed, int32_t eta, int32_t pi, double tol,
                                int32_t max_epochs, int32_t fit_kind, double *trace, int32_t *epochs);
 
+/* Exact CP-ALS baseline on the same sorted copies:
+ * one mode update = full sparse MTTKRP, V = *_{m != k} A_m^T A_m, B = M V^+
+ * (AMB-12 pseudo-inverse), normalize (lambda), leverage refresh.  Single GPU,
+ * D <= 4.  cparls_run_als: iters outer iterations over all modes, exact fit
+ * every fit_every (trace as cparls_run). */
+cparls_status cparls_als_update(cparls_ctx *ctx, int32_t mode);
+cparls_status cparls_run_als(cparls_ctx *ctx, int32_t iters, int32_t fit_every, double *fit_trace);
+
 /* ---- multi-GPU (SURVEY 8(e), P:1797-1801 sketches the distributed variant) ----
  * Row sharding: for every mode k the rows of B (and the nonzeros whose mode-k
  * index is one of them) are split into world_size contiguous blocks balanced

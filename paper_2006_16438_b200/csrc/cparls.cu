@@ -31,10 +31,9 @@ struct ModeIndex {
   int shift = 0;
   int64_t nbkt = 0;
   int64_t nnz = 0;           // nonzeros of this rank's slice of mode k
-  // order of the other modes in this copy's keys, fastest first: ascending
-  // n_m, so the largest factor is the slowest (sequentially swept) key mode of
-  // the exact fit and the per-fiber random gathers hit the smallest factors.
-  // Sample keys stay canonical (AMB-1) and are re-encoded by the lookup.
+  // order of the other modes in this copy's keys, fastest first (copy_order):
+  // the slowest is mode (k+1) mod D, the rest by ascending n_m.  Sample keys
+  // stay canonical (AMB-1) and are re-encoded by the lookup.
   int order[kMaxModes] = {};
 };
 
@@ -449,10 +448,15 @@ OtherModes other_modes(cparls_ctx *c, int k, bool need_alpha) {
 }
 
 void copy_order(const cparls_ctx *c, int k, int *order) {
+  // slowest: mode (k+1) mod D, so every mode is the slowest key mode of exactly
+  // one copy (the exact CP-ALS MTTKRP streams that copy, als.cuh); the others
+  // by ascending n_m, fastest first
+  const int slow = (k + 1) % c->D;
   int d = 0;
   for (int m = 0; m < c->D; ++m)
-    if (m != k) order[d++] = m;
+    if (m != k && m != slow) order[d++] = m;
   std::stable_sort(order, order + d, [&](int a, int b) { return c->dims[a] < c->dims[b]; });
+  order[d] = slow;
 }
 
 KeyRemap key_remap(const cparls_ctx *c, int k) {
@@ -1215,6 +1219,93 @@ void solve_impl(cparls_ctx *c, int k, cparls_solve_info *info) {
   c->smode_last_solved = k;
 }
 
+// ---------------------------------------------------------------- exact CP-ALS (N2)
+// One exact ALS mode update: full MTTKRP from the copy whose slowest
+// key mode is k (als.cuh), V = *_{m != k} G_m, B = M V^+ (the same solve and
+// AMB-12 pseudo-inverse as the sketched path), normalize, leverage refresh.
+void als_update_impl(cparls_ctx *c, int k) {
+  if (c->world > 1) throw ApiError(CPARLS_EINVAL, "exact CP-ALS update: single GPU only");
+  const int r = c->r, ld = c->ld;
+  const int64_t nk = c->dims[k];
+  int cm = -1;
+  for (int m = 0; m < c->D; ++m)
+    if (m != k && c->idx[m].order[c->D - 2] == k) cm = m;
+  if (cm < 0) throw ApiError(CPARLS_ESTATE, "no copy with slowest key mode k");
+  Phase ph(c, &c->stats.ms_rhs);
+  if (c->m_dirty) {
+    CK(cudaMemsetAsync(c->M, 0, sizeof(double) * c->nmax * c->ld, c->st));
+    c->m_dirty = false;
+  }
+  FitDecode fd{};
+  fd.d = c->D - 1;
+  long double N = 1;
+  for (int j = 0; j < fd.d; ++j) {
+    const int m = c->idx[cm].order[j];
+    fd.n[j] = c->dims[m];
+    fd.inv[j] = 1.0 / (double)c->dims[m];
+    fd.A[j] = c->A[m];
+    N *= (long double)c->dims[m];
+  }
+  fd.fast = N < 9007199254740992.0L;
+  const ModeIndex &ix = c->idx[cm];
+  if (ix.nnz > 0) {
+    CK(cudaMemsetAsync(&c->dv->counter, 0, sizeof(unsigned long long), c->st));
+    const int nb = 148 * 2;
+    KTimer kt(c, KT_RHS);
+#define MTT(VT, SW, DM)                                                                                        \
+  k_mttkrp<VT, SW, DM, (SW >= CPARLS_FIT_U ? CPARLS_FIT_U : SW)><<<nb, kFitThreads, 0, c->st>>>(                \
+      ix.key, ix.out, (const VT *)ix.val, ix.nnz, fd, c->A[cm], ld, c->M, &c->dv->counter)
+#define MTTD(VT, SW)                        \
+  do {                                      \
+    if (fd.d == 1) MTT(VT, SW, 1);          \
+    else if (fd.d == 2) MTT(VT, SW, 2);     \
+    else if (fd.d == 3) MTT(VT, SW, 3);     \
+    else throw ApiError(CPARLS_EINVAL, "exact CP-ALS update: D <= 4"); \
+  } while (0)
+#define MTTV(VT)                            \
+  do {                                      \
+    if (ld <= 8) MTTD(VT, 2);               \
+    else if (ld <= 32) MTTD(VT, 8);         \
+    else MTTD(VT, 16);                      \
+  } while (0)
+    if (c->vf32) MTTV(float); else MTTV(double);
+#undef MTTV
+#undef MTTD
+#undef MTT
+    kt.stop();
+    CK_LAUNCH();
+  }
+  GramList gl{};
+  gl.D = c->D;
+  gl.k = k;
+  for (int m = 0; m < c->D; ++m) gl.GA[m] = c->md[m]->GA;
+  k_hadamard_grams<<<1, 256, 0, c->st>>>(r, gl, c->sd->G);
+  CK_LAUNCH();
+  ph.end();
+  Phase ph2(c, &c->stats.ms_solve);
+  k_solve_prep<<<1, 128, prep_smem(r), c->st>>>(r, c->sd);
+  CK_LAUNCH();
+  const int64_t grid = row_grid(c, ceil_div(std::max<int64_t>(nk, 1), kRowThreads));
+  CK(cudaMemsetAsync(&c->dv->touched, 0, sizeof(unsigned long long), c->st));
+  KTimer kts(c, KT_SOLVE);
+  RSWITCH(r, k_solve_rows_t<RM><<<(unsigned)grid, kRowThreads, solve_smem(r, ld), c->st>>>(
+                 c->M, nk, r, ld, c->sd, c->A[k], c->gpart, &c->dv->touched, 1));
+  kts.stop();
+  CK_LAUNCH();
+  k_pairs_reduce<<<pairs_reduce_grid(r), 256, 0, c->st>>>(c->gpart, grid, r, c->sd->BtB);
+  CK_LAUNCH();
+  k_norm_prep<<<1, 128, prep_smem(r), c->st>>>(r, c->sd, c->md[k]);
+  CK_LAUNCH();
+  LAUNCHED(c, 8);
+  lev_rows_and_cdf(c, k, c->sd->lambda);
+  CK(cudaMemcpyAsync(c->lam_model, c->sd->lambda, sizeof(double) * r, cudaMemcpyDeviceToDevice, c->st));
+  sync(c);
+  c->have_sample = false;
+  c->smode_last_solved = k;
+  c->stats.mode_steps++;
+  ph2.end();
+}
+
 // ---------------------------------------------------------------- estimated fit (N1)
 FitSampleDev fs_dev(cparls_ctx *c) {
   FitSampleDev fs{};
@@ -1946,6 +2037,30 @@ cparls_status cparls_run_until(cparls_ctx *c, int64_t s, uint64_t seed, int32_t 
       }
     }
     if (epochs) *epochs = e;
+  });
+}
+
+cparls_status cparls_als_update(cparls_ctx *c, int32_t mode) {
+  if (!c) return CPARLS_EINVAL;
+  return guarded(c, [&] {
+    check_mode(c, mode);
+    als_update_impl(c, mode);
+  });
+}
+
+cparls_status cparls_run_als(cparls_ctx *c, int32_t iters, int32_t fit_every, double *fit_trace) {
+  if (!c) return CPARLS_EINVAL;
+  return guarded(c, [&] {
+    if (iters < 0) throw ApiError(CPARLS_EINVAL, "iters < 0");
+    for (int t = 0; t < iters; ++t) {
+      for (int k = 0; k < c->D; ++k) als_update_impl(c, k);
+      double f = NAN;
+      if (fit_every > 0 && (t + 1) % fit_every == 0) {
+        if (c->normX2 <= 0.0) throw ApiError(CPARLS_ENUMERIC, "||X|| = 0: fit undefined");
+        f = fit_impl(c);
+      }
+      if (fit_trace) fit_trace[t] = f;
+    }
   });
 }
 

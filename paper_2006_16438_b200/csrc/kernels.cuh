@@ -809,3 +809,4 @@ __global__ void k_pack_nz(const IT *__restrict__ coords, const VT *__restrict__ 
 #include "rhs_bucket.cuh"
 #include "fit.cuh"
 #include "fitest.cuh"
+#include "als.cuh"

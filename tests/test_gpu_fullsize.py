@@ -253,3 +253,34 @@ def test_c4_fit_sample_and_estimate(c4):
     assert abs(Fg - Fref) <= bound, (Fg, Fref, bound)
     fref = 1.0 - math.sqrt(max(Fref, 0.0)) / math.sqrt(float((T.vals.to(torch.float64) ** 2).sum()))
     assert abs(fg - fref) <= 1e-8, (fg, fref)
+
+
+def test_c4_als_update_sampled_rows(c4):
+    """N2 at full size: one exact CP-ALS update of mode 0; B rows of sampled
+    output rows (random + the heaviest) against B_i = M_i V^+ from their
+    definitions: M_i = sum over the nonzeros of row i of x * (A_1 * A_2) rows
+    (brute-force row selection over the COO, fp64), V = (A_1^T A_1) * (A_2^T A_2),
+    V^+ with the oracle's Jacobi eigen-solver and the AMB-11/12 cutoff."""
+    cfg, T, g = c4
+    dev = T.coords.device
+    k = 0
+    A = [g.get_factor(m)[0] for m in range(3)]
+    g.als_update(k)
+    _, Bg = g.last_solve(k)
+    V = (A[1].T @ A[1]) * (A[2].T @ A[2])
+    w, Q = oracle.jacobi_eig(V)
+    keep = w > cfg.rank * np.finfo(float).eps * w.max()
+    Vp = (Q[:, keep] / w[keep]) @ Q[:, keep].T
+    deg = torch.bincount(T.coords[:, 0].to(torch.int64), minlength=cfg.dims[0])
+    rows = torch.cat([torch.topk(deg, 4).indices,
+                      torch.randint(0, cfg.dims[0], (12,), device=dev,
+                                    generator=torch.Generator(device=dev).manual_seed(1))]).tolist()
+    A1, A2 = torch.from_numpy(A[1]).to(dev), torch.from_numpy(A[2]).to(dev)
+    for i in rows:
+        sel = torch.nonzero(T.coords[:, 0] == i).squeeze(1)
+        c = T.coords[sel].to(torch.int64)
+        x = T.vals[sel].to(torch.float64)
+        Mi = (x[:, None] * A1[c[:, 1]] * A2[c[:, 2]]).sum(0).cpu().numpy()
+        Bi = Mi @ Vp
+        nb = np.linalg.norm(Bi)
+        assert np.linalg.norm(Bg[i] - Bi) <= 1e-9 * max(nb, 1e-300), (i, np.linalg.norm(Bg[i] - Bi), nb)

@@ -380,3 +380,47 @@ def test_run_until_matches_oracle():
         to = o.run_until(256, -1.0, 3, eta=5, pi=3, tol=1e-4, max_epochs=12, estimated=estimated)
         assert len(tg) == len(to) and len(tg) >= 3
         np.testing.assert_allclose(tg, to, atol=1e-8)
+
+
+# ---------------------------------------------------------------- exact CP-ALS baseline (N2)
+@pytest.mark.parametrize("name", ["C1", "C2"])
+def test_als_update_parity(name):
+    """One exact CP-ALS mode update per mode against the oracle's
+    or_als_update from the same factors: V, B (<= 1e-9), lambda, leverage."""
+    need_gpu()
+    T = synth.make(name, device="cpu" if name == "C1" else "cuda")
+    T = synth.Tensor(T.cfg, T.dims, T.coords.cpu(), T.vals.cpu())
+    r = T.cfg.rank
+    g = make_ctx(T, r)
+    o = make_oracle(T, r)
+    for t in range(2):
+        for k in range(len(T.dims)):
+            sync_oracle_from_gpu(g, o)
+            g.als_update(k)
+            o.als_update(k)
+            Gg, Bg = g.last_solve(k)
+            Go, _, Bo = o.last_solve(k)
+            np.testing.assert_allclose(Gg, Go, rtol=1e-12, atol=1e-14 * np.abs(Go).max())
+            assert np.linalg.norm(Bg - Bo) <= solve_tol(Go) * np.linalg.norm(Bo), (t, k)
+            np.testing.assert_allclose(g.get_factor(k)[1], o.get_factor(k)[1], rtol=1e-9)
+            assert_leverage_close(g, o, k)
+
+
+def test_run_als_trace_and_monotone():
+    """CP-ALS free running on the planted C1 variant: the exact fit trace
+    matches the oracle's ALS to 1e-8 and never decreases (ALS property)."""
+    need_gpu()
+    T = synth.make("C1", dense_planted=True)
+    g = make_ctx(T, 3)
+    o = make_oracle(T, 3)
+    init = synth.uniform_init(T.dims, 3, 2)
+    for m in range(3):
+        o.set_factor(m, init[m].numpy())
+    tg = g.run_als(12, fit_every=1)
+    to = []
+    for t in range(12):
+        for k in range(3):
+            o.als_update(k)
+        to.append(o.fit())
+    np.testing.assert_allclose(tg, to, atol=1e-8)
+    assert (np.diff(tg) >= -1e-10).all()
