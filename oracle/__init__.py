@@ -85,6 +85,9 @@ def _setup(L):
     L.or_didx.argtypes = [I32, P, P, D, I64, P, P, P]; L.or_didx.restype = I64
     L.or_didx_brute.argtypes = [I32, P, P, D, I64, P, P, P]; L.or_didx_brute.restype = I64
     L.or_fit_sample.argtypes = [P, I64, D, U64, P, P]; L.or_fit_sample.restype = I32
+    L.or_init_rrf.argtypes = [P, I64, U64]; L.or_init_rrf.restype = I32
+    L.or_rrf_omega.argtypes = [U64, I32, U64, I32]; L.or_rrf_omega.restype = D
+    L.or_rrf_fiber.argtypes = [U64, I32, U64, I64]; L.or_rrf_fiber.restype = I64
     L.or_get_fit_sample.argtypes = [P, I64, P, P, P]; L.or_get_fit_sample.restype = I64
     L.or_fit_estimate.argtypes = [P, P]; L.or_fit_estimate.restype = D
     L.or_run_until.argtypes = [P, I64, D, U64, I32, I32, D, I32, I32, P, P]; L.or_run_until.restype = I32
@@ -258,6 +261,12 @@ class Oracle:
 
     def als_update(self, k):
         return lib().or_als_update(self._h, k)
+
+    def init_rrf(self, s_init, seed=0):
+        """Randomized range finder initialization of every factor (AMB-34)."""
+        st = lib().or_init_rrf(self._h, int(s_init), int(seed))
+        if st:
+            raise RuntimeError(f"or_init_rrf status {st}")
 
     def fit_sample(self, s_fit, alpha=0.5, seed=0):
         """Draw and freeze the stratified fit sample (AMB-32)."""

@@ -1065,3 +1065,75 @@ int or_run_until(or_ctx *c, int64_t s, double tau, uint64_t seed, int eta, int p
   if (epochs) *epochs = e;
   return 0;
 }
+
+/* ------------------------------------------------------------------ */
+/* O21: randomized range finder initialization (sec:enron), */
+/* AMB-34: for every mode k, A_k = X_(k)(:, S) Omega with S = s_init     */
+/* fibers drawn uniformly WITH replacement from the nonempty mode-k      */
+/* fibers ordered by canonical key (AMB-1), Omega(j, c) standard normal. */
+/* Draw j of mode k: Philox key = seed, counter = (j lo, j hi,           */
+/* 0x52524600 + k, lane); fiber u = mulhi(R, nfib) from lane 0xFFFF      */
+/* words (0,1); Omega(j, c) from lane c/2: u1 = (w0|w1<<32 >> 11 + 1)    */
+/* 2^-53, u2 = (w2|w3<<32 >> 11) 2^-53, rho = sqrt(-2 ln u1), c even ->   */
+/* rho cos(2 pi u2), odd -> rho sin(2 pi u2) (Box-Muller).  lambda = 1.  */
+/* ------------------------------------------------------------------ */
+static void rrf_words(uint64_t seed, uint64_t j, int k, uint32_t lane, uint32_t o[4]) {
+  uint32_t cc[4] = {(uint32_t)j, (uint32_t)(j >> 32), 0x52524600u + (uint32_t)k, lane};
+  uint32_t kk[2] = {(uint32_t)seed, (uint32_t)(seed >> 32)};
+  or_philox4x32_10(cc, kk, o);
+}
+
+double or_rrf_omega(uint64_t seed, int k, uint64_t j, int c) {
+  uint32_t o[4];
+  rrf_words(seed, j, k, (uint32_t)(c / 2), o);
+  const uint64_t a = (uint64_t)o[0] | ((uint64_t)o[1] << 32), b = (uint64_t)o[2] | ((uint64_t)o[3] << 32);
+  const double u1 = (double)((a >> 11) + 1) * 0x1p-53, u2 = (double)(b >> 11) * 0x1p-53;
+  const double rho = sqrt(-2.0 * log(u1));
+  const double th = 2.0 * 3.14159265358979323846 * u2;
+  return (c % 2 == 0) ? rho * cos(th) : rho * sin(th);
+}
+
+int64_t or_rrf_fiber(uint64_t seed, int k, uint64_t j, int64_t nfib) {
+  uint32_t o[4];
+  rrf_words(seed, j, k, 0xFFFFu, o);
+  return (int64_t)mulhi64((uint64_t)o[0] | ((uint64_t)o[1] << 32), (uint64_t)nfib);
+}
+
+static int cmp_u64_rrf(const void *a, const void *b) {
+  uint64_t x = *(const uint64_t *)a, y = *(const uint64_t *)b;
+  return (x > y) - (x < y);
+}
+
+int or_init_rrf(or_ctx *c, int64_t s_init, uint64_t seed) {
+  const int D = c->D, r = c->r;
+  if (s_init < 1) return 1;
+  for (int k = 0; k < D; ++k) {
+    /* nonempty fibers of X_(k): distinct canonical keys, ascending */
+    uint64_t *keys = (uint64_t *)malloc(sizeof(uint64_t) * (c->nnz + 1));
+    for (int64_t e = 0; e < c->nnz; ++e) keys[e] = c->idx[k].key[e];
+    qsort(keys, (size_t)c->nnz, sizeof(uint64_t), cmp_u64_rrf);
+    int64_t nf = 0;
+    for (int64_t e = 0; e < c->nnz; ++e)
+      if (e == 0 || keys[e] != keys[e - 1]) keys[nf++] = keys[e];
+    const int64_t n = c->dims[k];
+    ksum *acc = (ksum *)calloc((size_t)n * r + 1, sizeof(ksum));
+    for (int64_t j = 0; j < s_init && nf > 0; ++j) {
+      const uint64_t key = keys[or_rrf_fiber(seed, k, (uint64_t)j, nf)];
+      int64_t *ids = NULL;
+      const int64_t len = fiber(c, k, key, &ids);
+      double om[OR_MAXR];
+      for (int q = 0; q < r; ++q) om[q] = or_rrf_omega(seed, k, (uint64_t)j, q);
+      for (int64_t t = 0; t < len; ++t) {
+        const int64_t e = ids[t], i = c->coords[e * D + k];
+        for (int q = 0; q < r; ++q) kadd(&acc[i * r + q], c->vals[e] * om[q]);
+      }
+      free(ids);
+    }
+    for (int64_t i = 0; i < n * r; ++i) c->A[k][i] = kval(&acc[i]);
+    free(acc);
+    free(keys);
+    refresh_mode(c, k, NULL);
+  }
+  for (int q = 0; q < r; ++q) c->lambda[q] = 1.0;
+  return 0;
+}

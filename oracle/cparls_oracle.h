@@ -114,6 +114,14 @@ double or_fit_estimate(or_ctx *c, double *Fhat);
 int or_run_until(or_ctx *c, int64_t s, double tau, uint64_t seed, int eta, int pi, double tol, int max_epochs,
                  int fit_kind, double *trace, int *epochs);
 
+/* Randomized range finder initialization (sec:enron; AMB-34):
+ * A_k = X_(k)(:, S) Omega for every mode, S = s_init fibers drawn uniformly
+ * with replacement from the nonempty fibers (ascending canonical key),
+ * Omega standard normal (Box-Muller on Philox).  lambda = 1. */
+int or_init_rrf(or_ctx *c, int64_t s_init, uint64_t seed);
+double or_rrf_omega(uint64_t seed, int k, uint64_t j, int c);
+int64_t or_rrf_fiber(uint64_t seed, int k, uint64_t j, int64_t nfib);
+
 /* Standalone DIDX on d given p~ vectors (for pins): writes up to cap keys
  * (ascending) and p; returns s_det (full count) or -1 on cap overflow. */
 int64_t or_didx(int d, const int64_t *n, const double *const *pt, double tau, int64_t cap,
