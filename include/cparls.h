@@ -190,6 +190,13 @@ cparls_status cparls_fit_sample_model(cparls_ctx *ctx, double *m);
 cparls_status cparls_run_until(cparls_ctx *ctx, int64_t s, uint64_t seed, int32_t eta, int32_t pi, double tol,
                                int32_t max_epochs, int32_t fit_kind, double *trace, int32_t *epochs);
 
+/* Randomized range finder initialization (SURVEY 8(f) N4, sec:enron
+ * P:1668-1701, AMB-34): every factor A_k = X_(k)(:, S) Omega, S = s_init
+ * nonempty fibers drawn uniformly with replacement (ranked by canonical key),
+ * Omega standard normal (Box-Muller on Philox, key = seed); lambda = 1, p~
+ * refreshed.  Single GPU. */
+cparls_status cparls_init_rrf(cparls_ctx *ctx, int64_t s_init, uint64_t seed);
+
 /* Exact CP-ALS baseline on the same sorted copies:
  * one mode update = full sparse MTTKRP, V = *_{m != k} A_m^T A_m, B = M V^+
  * (AMB-12 pseudo-inverse), normalize (lambda), leverage refresh.  Single GPU,

@@ -94,6 +94,7 @@ def lib():
             "cparls_fit_sample_model": [P, P],
             "cparls_run_until": [P, I64, U64, I32, I32, D, I32, I32, P, P],
             "cparls_als_update": [P, I32],
+            "cparls_init_rrf": [P, I64, U64],
             "cparls_run_als": [P, I32, I32, P],
             "cparls_get_stats": [P, C.POINTER(Stats)],
             "cparls_reset_stats": [P],
@@ -121,7 +122,7 @@ EXPORTED = ["cparls_create", "cparls_destroy", "cparls_set_factor", "cparls_get_
             "cparls_leverage", "cparls_get_ptilde", "cparls_set_ptilde", "cparls_sample",
             "cparls_set_tau", "cparls_get_sample", "cparls_get_fibers", "cparls_solve_mode",
             "cparls_get_last_solve", "cparls_fit", "cparls_run", "cparls_fit_estimate",
-            "cparls_get_fit_sample", "cparls_fit_sample_model", "cparls_run_until", "cparls_als_update",
+            "cparls_get_fit_sample", "cparls_fit_sample_model", "cparls_run_until", "cparls_init_rrf", "cparls_als_update",
             "cparls_run_als", "cparls_get_stats",
             "cparls_reset_stats", "cparls_set_profiling", "cparls_last_error", "cparls_version",
             "cparls_comm_nccl_unique_id", "cparls_comm_create_nccl", "cparls_comm_create_local",
@@ -300,6 +301,10 @@ class Cparls:
                                            int(max_epochs), 1 if estimated else 0, trace.ctypes.data,
                                            C.byref(ep)))
         return trace[:ep.value]
+
+    def init_rrf(self, s_init, seed=0):
+        """Randomized range finder initialization of every factor (AMB-34)."""
+        self._check(lib().cparls_init_rrf(self._h, int(s_init), int(seed)))
 
     def als_update(self, k):
         """One exact CP-ALS mode update."""

@@ -1306,6 +1306,84 @@ void als_update_impl(cparls_ctx *c, int k) {
   ph2.end();
 }
 
+// ---------------------------------------------------------------- RRF initialization (N4)
+void init_rrf_impl(cparls_ctx *c, int64_t s_init, uint64_t seed) {
+  if (c->world > 1) throw ApiError(CPARLS_EINVAL, "RRF initialization: single GPU only");
+  if (s_init < 1) throw ApiError(CPARLS_EINVAL, "s_init >= 1");
+  const int r = c->r, ld = c->ld;
+  if (c->m_dirty) {
+    CK(cudaMemsetAsync(c->M, 0, sizeof(double) * c->nmax * ld, c->st));
+    c->m_dirty = false;
+  }
+  for (int k = 0; k < c->D; ++k) {
+    const ModeIndex &ix = c->idx[k];
+    const int64_t nnz = ix.nnz, nk = c->dims[k];
+    CK(cudaMemsetAsync(c->M, 0, sizeof(double) * nk * ld, c->st));
+    if (nnz > 0) {
+      int64_t *flag = dalloc_t<int64_t>(c, nnz), *pos = dalloc_t<int64_t>(c, nnz);
+      int64_t *part = dalloc_t<int64_t>(c, ceil_div(nnz, kScanTile) + 16);
+      k_fiber_flags<<<1184, 256, 0, c->st>>>(ix.key, nnz, flag);
+      CK_LAUNCH();
+      exclusive_scan_i64(flag, pos, nnz, part, &c->dv->total, c->st);
+      const int64_t nfib = read_dev(c, &c->dv->total);
+      dfree(c, part);
+      int64_t *fstart = dalloc_t<int64_t>(c, nfib);
+      uint64_t *fkey = dalloc_t<uint64_t>(c, nfib);
+      KeyToCanon kc{};
+      kc.d = c->D - 1;
+      bool identity = true;
+      for (int j = 0; j < kc.d; ++j) {
+        const int m = ix.order[j];
+        kc.n[j] = c->dims[m];
+        uint64_t mult = 1;   // canonical: other modes ascending, first fastest
+        for (int q = 0; q < m; ++q)
+          if (q != k) mult *= (uint64_t)c->dims[q];
+        kc.cmult[j] = mult;
+      }
+      {
+        int jj = 0;
+        for (int m = 0; m < c->D; ++m)
+          if (m != k) identity &= (ix.order[jj++] == m);
+      }
+      k_fiber_list<<<1184, 256, 0, c->st>>>(ix.key, nnz, flag, pos, kc, fstart, fkey);
+      CK_LAUNCH();
+      dfree(c, flag);
+      dfree(c, pos);
+      uint32_t *perm = nullptr;
+      if (!identity && nfib > 1) {   // rank the fibers by canonical key
+        uint64_t *k2 = dalloc_t<uint64_t>(c, nfib);
+        uint32_t *v1 = dalloc_t<uint32_t>(c, nfib), *v2 = dalloc_t<uint32_t>(c, nfib);
+        k_iota_u32<<<(unsigned)ceil_div(nfib, 256), 256, 0, c->st>>>(v1, nfib);
+        CK_LAUNCH();
+        cub::DoubleBuffer<uint64_t> kb(fkey, k2);
+        cub::DoubleBuffer<uint32_t> vb(v1, v2);
+        size_t tb = 0;
+        CK(cub::DeviceRadixSort::SortPairs(nullptr, tb, kb, vb, nfib, 0, 64, c->st));
+        void *tmp = dalloc(c, tb);
+        CK(cub::DeviceRadixSort::SortPairs(tmp, tb, kb, vb, nfib, 0, 64, c->st));
+        sync(c);
+        dfree(c, tmp);
+        perm = vb.Current();
+        dfree(c, vb.Alternate());
+        dfree(c, k2);
+      }
+      k_rrf_scatter<<<(unsigned)std::min<int64_t>(ceil_div(s_init * 32, 256), 148 * 64), 256, 0, c->st>>>(
+          s_init, seed, k, nfib, perm, fstart, nnz, ix.out, ix.val, c->vf32 ? 1 : 0, r, ld, c->M);
+      CK_LAUNCH();
+      sync(c);
+      dfree(c, fstart);
+      dfree(c, fkey);
+      if (perm) dfree(c, perm);
+    }
+    CK(cudaMemcpyAsync(c->A[k], c->M, sizeof(double) * nk * ld, cudaMemcpyDeviceToDevice, c->st));
+    CK(cudaMemsetAsync(c->M, 0, sizeof(double) * nk * ld, c->st));
+  }
+  c->have_sample = false;
+  reset_lambda(c);
+  for (int k = 0; k < c->D; ++k) leverage_full(c, k);
+  sync(c);
+}
+
 // ---------------------------------------------------------------- estimated fit (N1)
 FitSampleDev fs_dev(cparls_ctx *c) {
   FitSampleDev fs{};
@@ -2038,6 +2116,11 @@ cparls_status cparls_run_until(cparls_ctx *c, int64_t s, uint64_t seed, int32_t 
     }
     if (epochs) *epochs = e;
   });
+}
+
+cparls_status cparls_init_rrf(cparls_ctx *c, int64_t s_init, uint64_t seed) {
+  if (!c) return CPARLS_EINVAL;
+  return guarded(c, [&] { init_rrf_impl(c, s_init, seed); });
 }
 
 cparls_status cparls_als_update(cparls_ctx *c, int32_t mode) {

@@ -810,3 +810,4 @@ __global__ void k_pack_nz(const IT *__restrict__ coords, const VT *__restrict__ 
 #include "fit.cuh"
 #include "fitest.cuh"
 #include "als.cuh"
+#include "rrf.cuh"

@@ -424,3 +424,25 @@ def test_run_als_trace_and_monotone():
         to.append(o.fit())
     np.testing.assert_allclose(tg, to, atol=1e-8)
     assert (np.diff(tg) >= -1e-10).all()
+
+
+# ---------------------------------------------------------------- RRF initialization (N4)
+@pytest.mark.parametrize("name", ["C1", "C2"])
+def test_rrf_init_parity(name):
+    """cparls_init_rrf vs the oracle's RRF (AMB-34): every factor to 1e-12
+    (Box-Muller's libm differs by ulps between host and device), lambda = 1,
+    and the leverage refresh of the new factors; then one lockstep iteration."""
+    need_gpu()
+    T = synth.make(name, device="cpu" if name == "C1" else "cuda")
+    T = synth.Tensor(T.cfg, T.dims, T.coords.cpu(), T.vals.cpu())
+    r = T.cfg.rank
+    g = make_ctx(T, r)
+    o = make_oracle(T, r)
+    g.init_rrf(1000, 42)
+    o.init_rrf(1000, 42)
+    for k in range(len(T.dims)):
+        Ag, lg = g.get_factor(k)
+        Ao, lo = o.get_factor(k)
+        np.testing.assert_allclose(Ag, Ao, rtol=1e-12, atol=1e-12 * np.abs(Ao).max())
+        assert (lg == 1).all()
+        assert_leverage_close(g, o, k)
