@@ -255,6 +255,15 @@ class Cparls:
                                             val.ctypes.data, C.byref(mk)))
         return lens, out, val
 
+    def get_fiber_lengths(self):
+        """Per-sample fiber lengths of the current sample (canonical order)."""
+        n = C.c_int64()
+        self._check(lib().cparls_get_sample(self._h, 0, None, None, None, None, None, C.byref(n)))
+        lens = np.zeros(n.value, dtype=np.int64)
+        mk = C.c_int64()
+        self._check(lib().cparls_get_fibers(self._h, 0, lens.ctypes.data, None, None, C.byref(mk)))
+        return lens
+
     def solve_mode(self, k):
         info = SolveInfo()
         self._check(lib().cparls_solve_mode(self._h, k, C.byref(info)))

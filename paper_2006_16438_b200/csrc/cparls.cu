@@ -124,6 +124,7 @@ struct cparls_ctx {
   std::vector<void *> allocs;
   cparls_stats stats{};
   bool profiling = false;
+  bool debug_sync = getenv("CPARLS_DEBUG_SYNC") != nullptr;   // sync + report inside the sampler
   std::vector<cudaEvent_t> ev_pool;                             // free events
   std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> ev_pending;
   int fit_mode = 0;
@@ -757,6 +758,10 @@ int64_t run_didx(cparls_ctx *c, const OtherModes &om, double tau, int *which) {
     }
     c->stats.bytes_sample += (double)n * 8.0;
     ncand[j] = nc;
+    if (c->debug_sync) {
+      sync(c);
+      fprintf(stderr, "[didx] mode j=%d n=%lld ncand=%lld alpha=%g\n", j, (long long)n, (long long)nc, om.alpha[j]);
+    }
   }
   // level expansion (DetSet is a subset of the product of the
   // candidate sets); the exact canonical predicate decides membership.
@@ -783,6 +788,7 @@ int64_t run_didx(cparls_ctx *c, const OtherModes &om, double tau, int *which) {
     exclusive_scan_i64(c->lcnt, c->loff, nlist, c->i64part, &c->dv->total, c->st);
     LAUNCHED(c, 4);
     const int64_t nn = read_dev(c, &c->dv->total);
+    if (c->debug_sync) fprintf(stderr, "[didx] level %d nlist=%lld -> %lld (lcap %lld)\n", l, (long long)nlist, (long long)nn, (long long)c->lcap);
     if (nn > cap) throw ApiError(CPARLS_ESAMPLE, "DIDX list exceeds didx_cap (" + std::to_string(nn) + ")");
     if (nn > c->lcap) {
       // grow, keeping the current level
@@ -1712,11 +1718,12 @@ cparls_status cparls_create(cparls_ctx **out, int32_t nmodes, const int64_t *dim
     }
     c->M = dalloc_t<double>(c, c->nmax * c->ld);
     CK(cudaMemsetAsync(c->M, 0, sizeof(double) * c->nmax * c->ld, c->st));
-    // DIDX candidate buffers (n_m each, worst case)
+    // DIDX candidate buffers: slot j holds the candidates of the j-th OTHER
+    // mode of whichever mode is being sampled, so every slot takes max n_m
     int64_t cc = c->nmax;
     for (int m = 0; m < nmodes; ++m) {
-      c->ckey[m] = dalloc_t<uint64_t>(c, c->dims[m]);
-      c->cidx[m] = dalloc_t<uint32_t>(c, c->dims[m]);
+      c->ckey[m] = dalloc_t<uint64_t>(c, cc);
+      c->cidx[m] = dalloc_t<uint32_t>(c, cc);
     }
     c->ckey_tmp = dalloc_t<uint64_t>(c, cc);
     c->cidx_tmp = dalloc_t<uint32_t>(c, cc);
@@ -1935,15 +1942,16 @@ cparls_status cparls_get_fibers(cparls_ctx *c, int64_t cap, int64_t *len, int64_
     std::vector<uint64_t> hk(n);
     std::vector<uint8_t> hd(n);
     std::vector<int64_t> hl(n), ho(n);
-    std::vector<int64_t> go(mk);
-    std::vector<double> gv(mk);
+    const bool entries = (out || val) && cap > 0;   // lengths only otherwise
+    std::vector<int64_t> go(entries ? mk : 0);
+    std::vector<double> gv(entries ? mk : 0);
     if (n > 0) {
       CK(cudaMemcpyAsync(hk.data(), c->skey, 8 * n, cudaMemcpyDeviceToHost, c->st));
       CK(cudaMemcpyAsync(hd.data(), c->sisdet, n, cudaMemcpyDeviceToHost, c->st));
       CK(cudaMemcpyAsync(hl.data(), c->len, 8 * n, cudaMemcpyDeviceToHost, c->st));
       CK(cudaMemcpyAsync(ho.data(), c->off, 8 * n, cudaMemcpyDeviceToHost, c->st));
     }
-    if (mk > 0) {
+    if (mk > 0 && entries) {
       int64_t *dO = dalloc_t<int64_t>(c, mk);
       double *dV = dalloc_t<double>(c, mk);
       if (c->vf32)
@@ -1965,6 +1973,7 @@ cparls_status cparls_get_fibers(cparls_ctx *c, int64_t cap, int64_t *len, int64_
     for (int64_t i = 0; i < n; ++i) {
       int64_t j = o[i];
       if (len) len[i] = hl[j];
+      if (!entries) continue;
       for (int64_t t = 0; t < hl[j]; ++t, ++w) {
         if (w < cap) {
           if (out) out[w] = go[ho[j] + t];

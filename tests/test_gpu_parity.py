@@ -446,3 +446,30 @@ def test_rrf_init_parity(name):
         np.testing.assert_allclose(Ag, Ao, rtol=1e-12, atol=1e-12 * np.abs(Ao).max())
         assert (lg == 1).all()
         assert_leverage_close(g, o, k)
+
+
+def test_c2_hybrid_concentrated_leverage_lockstep():
+    """Regression: an exact-ALS (rank 10) solution concentrates the leverage, so
+    the DIDX candidate list of a small mode's neighbour exceeds that small
+    mode's length (candidate slot j holds the j-th OTHER mode: it must take
+    max n_m).  Bit-exact sample vs the oracle at s = 2^17, hybrid."""
+    need_gpu()
+    T = synth.make("C2", device="cuda")
+    from paper_2006_16438_b200 import Cparls
+    r = 10
+    g = Cparls(T.dims, T.coords, T.vals, r)
+    g.run_als(5, fit_every=0)
+    A = [g.get_factor(m)[0] for m in range(4)]
+    A[3] = A[3] * g.get_factor(0)[1]
+    o = oracle.Oracle(T.dims, T.coords.cpu().numpy().astype(np.int64), T.vals.cpu().numpy(), r)
+    for k in range(4):
+        for m in range(4):
+            g.set_factor(m, A[m])
+            o.set_factor(m, A[m])
+            o.set_ptilde(m, g.get_ptilde(m))
+        gi = g.sample(k, 1 << 17, 1000, k)
+        oi = o.sample(k, 1 << 17, -1.0, 1000, k)
+        assert (gi.s_det, gi.s_bar, gi.attempts) == (oi.s_det, oi.s_bar, oi.attempts)
+        assert oi.s_det > 0
+        a, b = g.get_sample(), o.get_sample()
+        assert (a["keys"] == b["keys"]).all() and (a["counts"] == b["counts"]).all()
