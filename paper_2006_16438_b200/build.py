@@ -47,8 +47,12 @@ def _nvcc(out, src, libs, verbose):
     os.replace(out + ".tmp", out)
 
 
-def build(force=False, verbose=False):
-    """libcparls.so (the product) and libcparls_peaks.so (bench-only microbenchmarks)."""
+def build(force=False, verbose=False, lib=None, extra=()):
+    """libcparls.so (the product) and libcparls_peaks.so (bench-only microbenchmarks).
+    lib/extra: build a variant library (e.g. -D flags) at another path (experiments)."""
+    if lib is not None:
+        _nvcc(lib, SRC, ["-lcudart", "-l:libnccl.so.2"] + list(extra), verbose)
+        return lib
     if force or not os.path.exists(PEAKS_LIB) or os.path.getmtime(PEAKS_LIB) < os.path.getmtime(PEAKS_SRC):
         _nvcc(PEAKS_LIB, PEAKS_SRC, ["-lcudart"], verbose)
     srcs = [s for s in sources() if s != PEAKS_SRC]

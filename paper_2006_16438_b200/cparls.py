@@ -13,7 +13,8 @@ from typing import Optional
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libcparls.so")
+# CPARLS_LIB: an alternative in-tree build of the same library (A/B experiments)
+LIB_PATH = os.environ.get("CPARLS_LIB") or os.path.join(_HERE, "libcparls.so")
 
 OK, EINVAL, EOOM, ECUDA, ENCCL, ENUMERIC, ESAMPLE, ERANGE, ESTATE = range(9)
 _NAMES = ["OK", "EINVAL", "EOOM", "ECUDA", "ENCCL", "ENUMERIC", "ESAMPLE", "ERANGE", "ESTATE"]
