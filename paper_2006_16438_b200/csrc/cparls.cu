@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -1617,6 +1618,7 @@ static thread_local std::string g_create_err;
 
 cparls_status cparls_create(cparls_ctx **out, int32_t nmodes, const int64_t *dims, int64_t nnz_local,
                             const void *coords, const void *vals, const cparls_opts *opts, uint64_t init_seed) {
+  const auto t_create0 = std::chrono::steady_clock::now();
   if (!out || !dims || !opts) return CPARLS_EINVAL;
   *out = nullptr;
   cparls_ctx *c = new (std::nothrow) cparls_ctx();
@@ -1682,11 +1684,24 @@ cparls_status cparls_create(cparls_ctx **out, int32_t nmodes, const int64_t *dim
       CK(cudaMemcpyAsync(own_v, vals, vsz * nnz_local, cudaMemcpyHostToDevice, c->st));
       dva = own_v;
     }
+    const bool tdbg = getenv("CPARLS_DEBUG") != nullptr;
+    auto now = [] { return std::chrono::steady_clock::now(); };
+    auto t_h2d_end = now();
+    if (tdbg) {
+      sync(c);
+      t_h2d_end = now();
+    }
     if (isz == 4 && vsz == 4) build_all<int32_t, float>(c, (const int32_t *)dco, (const float *)dva);
     else if (isz == 4) build_all<int32_t, double>(c, (const int32_t *)dco, (const double *)dva);
     else if (vsz == 4) build_all<int64_t, float>(c, (const int64_t *)dco, (const float *)dva);
     else build_all<int64_t, double>(c, (const int64_t *)dco, (const double *)dva);
     sync(c);
+    if (tdbg) {
+      sync(c);
+      fprintf(stderr, "[cparls] create: setup+H2D %.3f s, build %.3f s\n",
+              std::chrono::duration<double>(t_h2d_end - t_create0).count(),
+              std::chrono::duration<double>(now() - t_h2d_end).count());
+    }
     if (opts->fit_samples > 0) {
       if (c->world > 1) throw ApiError(CPARLS_EINVAL, "fit_samples needs world_size == 1");
       if (isz == 4 && vsz == 4)
