@@ -27,6 +27,19 @@ __global__ void k_peak_red(double *M, int64_t rows, int r, int ld, int64_t ops_p
   }
 }
 
+// same pattern with 64-bit integer and 32-bit float reductions (what a
+// fixed-point or single-precision accumulation would cost)
+template <typename T>
+__global__ void k_peak_red_t(T *M, int64_t rows, int r, int ld, int64_t ops_per_warp, uint32_t salt) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  for (int64_t i = 0; i < ops_per_warp; ++i) {
+    const uint32_t h = mix32(wid * 0x9E3779B9u + (uint32_t)i * 0x85EBCA6Bu + salt);
+    const int64_t row = (int64_t)(((uint64_t)h * (uint64_t)rows) >> 32);
+    if (lane < r) atomicAdd(M + row * ld + lane, (T)3);
+  }
+}
+
 template <int SW>
 __global__ void k_peak_gather(const double *__restrict__ A, int64_t rows, int ld, int64_t rows_per_warp,
                               double *out) {
@@ -72,6 +85,31 @@ double cparls_peak_red_f64(double *M, int64_t rows, int r, int ld, int64_t ops_p
   if (cudaGetLastError() != cudaSuccess || ms <= 0.f) return -1.0;
   const double ops = (double)reps * blocks * (256 / 32) * (double)ops_per_warp * r;
   return ops / (ms * 1e-3);
+}
+
+// kind 0: unsigned long long, 1: float.  Returns lane-ops per second.
+double cparls_peak_red_kind(void *M, int64_t rows, int r, int ld, int64_t ops_per_warp, int blocks, int reps,
+                            int kind) {
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  auto launch = [&](uint32_t salt) {
+    if (kind == 0)
+      k_peak_red_t<unsigned long long><<<blocks, 256>>>((unsigned long long *)M, rows, r, ld, ops_per_warp, salt);
+    else
+      k_peak_red_t<float><<<blocks, 256>>>((float *)M, rows, r, ld, ops_per_warp, salt);
+  };
+  launch(1u);
+  cudaEventRecord(a);
+  for (int i = 0; i < reps; ++i) launch(7u + i);
+  cudaEventRecord(b);
+  cudaEventSynchronize(b);
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, a, b);
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  if (cudaGetLastError() != cudaSuccess || ms <= 0.f) return -1.0;
+  return (double)reps * blocks * 8 * (double)ops_per_warp * r / (ms * 1e-3);
 }
 
 // Returns bytes per second of row data gathered (rows gathered * ld * 8 / time).
