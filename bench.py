@@ -111,10 +111,34 @@ class Clocks:
 KERNEL_NAMES = {"rhs": "k_rhs", "fit": "k_fit_sub", "solve_rows": "k_solve_rows_t", "lev_rows": "k_lev_rows_w"}
 
 
-def measure_peaks(cfg, dev, window_rows, fit_rows):
+def rhs_fixed_point():
+    """k_rhs accumulates in int64 fixed point (rhs_path 0/1, AMB-35) unless
+    CPARLS_RHS_FIXED=0 selects the fp64 reductions."""
+    return os.environ.get("CPARLS_RHS_FIXED", "1") != "0"
+
+
+def rhs_row_stream(g, cfg, seed, window_rows, per_mode=1 << 25):
+    """The output rows k_rhs reduces into, taken from the library itself: for
+    every mode k a fresh sample (same s and tau as the run), its matched
+    fiber entries in the sample's canonical order (cparls_get_fibers), those
+    in the first output-row window, first `per_mode` of them."""
+    import numpy as np
+    import torch
+    parts = []
+    for k in range(len(cfg.dims)):
+        g.sample(k, cfg.s, seed, 1_000_000 + k)
+        _, out, _ = g.get_fibers()
+        out = out[out < min(window_rows, cfg.dims[k])][:per_mode]
+        parts.append(torch.from_numpy(out.astype(np.int32)))
+        del out
+    return torch.cat(parts).contiguous()
+
+
+def measure_peaks(cfg, dev, window_rows, fit_rows, row_stream=None):
     """Ceilings of the hot kernels' own access patterns on this GPU, measured
-    here (libcparls_peaks.so, not part of the method): fp64 r-lane reductions
-    into random rows of an L2-sized window (k_rhs) and r-wide fp64 row gathers
+    here (libcparls_peaks.so, not part of the method): r-lane reductions (fp64,
+    and int64 for the fixed-point RHS) into random rows of an L2-sized window
+    and into the tensor's own row stream (k_rhs), and r-wide fp64 row gathers
     from random rows of a factor-sized matrix (k_fit_sub)."""
     import ctypes as C
     import torch
@@ -128,6 +152,18 @@ def measure_peaks(cfg, dev, window_rows, fit_rows):
     torch.cuda.synchronize()
     M = torch.zeros(window_rows * ld, dtype=torch.float64, device=dev)
     red = lib.cparls_peak_red_f64(M.data_ptr(), window_rows, r, ld, 8192, 148 * 8, 5)
+    lib.cparls_peak_red_kind.restype = C.c_double
+    lib.cparls_peak_red_kind.argtypes = [C.c_void_p, C.c_int64, C.c_int, C.c_int, C.c_int64, C.c_int, C.c_int,
+                                         C.c_int]
+    red_u64 = lib.cparls_peak_red_kind(M.data_ptr(), window_rows, r, ld, 8192, 148 * 8, 5, 0)
+    red_idx = {}
+    if row_stream is not None and row_stream.numel() > 0:
+        lib.cparls_peak_red_idx.restype = C.c_double
+        lib.cparls_peak_red_idx.argtypes = [C.c_void_p, C.c_void_p, C.c_int64, C.c_int, C.c_int, C.c_int, C.c_int,
+                                            C.c_int]
+        for name, kind in (("u64", 0), ("f64", 2)):
+            red_idx[name] = lib.cparls_peak_red_idx(M.data_ptr(), row_stream.data_ptr(), row_stream.numel(), r, ld,
+                                                    148 * 8, 5, kind)
     del M
     A = torch.rand(fit_rows * ld, dtype=torch.float64, device=dev)
     scr = torch.zeros(1, dtype=torch.float64, device=dev)
@@ -135,7 +171,10 @@ def measure_peaks(cfg, dev, window_rows, fit_rows):
     del A, scr
     torch.cuda.synchronize()
     torch.cuda.empty_cache()
-    return {"red_f64_lane_ops_per_s": red, "red_window_rows": window_rows,
+    return {"red_f64_lane_ops_per_s": red, "red_u64_lane_ops_per_s": red_u64,
+            "red_stream_u64_lane_ops_per_s": red_idx.get("u64"), "red_stream_f64_lane_ops_per_s": red_idx.get("f64"),
+            "red_stream_len": int(row_stream.numel()) if row_stream is not None else 0,
+            "red_window_rows": window_rows,
             "gather_bytes_per_s": gat, "gather_rows": fit_rows, "rank": r, "ld": ld}
 
 
@@ -302,6 +341,11 @@ def run_ours(args):
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         ms = float(tt[0])
     st = g.stats()          # resolves the per-kernel event timers of the timed region
+    # k_rhs's own row stream at the state the timed run left (for its ceiling)
+    row_stream = None
+    if ws == 1:
+        ld_ = (cfg.rank + 3) // 4 * 4
+        row_stream = rhs_row_stream(g, cfg, seed, min(max(cfg.dims), (96 << 20) // (ld_ * 8)))
     # secondary: the same K iterations with the paper's estimated fit
     # per epoch instead of the exact one (Alg. 3 as run on Amazon, s_fit = 2^27)
     est = None
@@ -373,7 +417,9 @@ def run_ours(args):
     # measured ceilings of the hot kernels' access patterns (same GPU, same run)
     ld = (cfg.rank + 3) // 4 * 4
     window_rows = min(max(cfg.dims), (96 << 20) // (ld * 8))
-    peaks = measure_peaks(cfg, dev, window_rows, int(sorted(cfg.dims)[len(cfg.dims) // 2]))
+    row_stream = row_stream.to(dev) if row_stream is not None else None
+    peaks = measure_peaks(cfg, dev, window_rows, int(sorted(cfg.dims)[len(cfg.dims) // 2]), row_stream)
+    del row_stream
     hbm_peak, peak_src = measured_peaks()
     # k_rhs: algorithmic work = m_k * r fp64 reductions per launch (SURVEY 8(d):
     # every matched nonzero adds w^2 x z_j to its output row); bytes = matched
@@ -388,12 +434,19 @@ def run_ours(args):
     fit_avg_s = (kms["fit"] / max(1, kn["fit"])) / 1000.0 if kn["fit"] else None
     rl = {}
     if rhs_avg_s:
+        fx = rhs_fixed_point()
+        kind = "u64" if fx else "f64"
+        pk = peaks[f"red_stream_{kind}_lane_ops_per_s"] or peaks[f"red_{kind}_lane_ops_per_s"]
         rl["rhs"] = {"bound": "l2_atomic", "kernel": "k_rhs (sampled RHS, P:949-958)",
-                     "achieved": rhs_red / rhs_avg_s / 1e9, "peak": peaks["red_f64_lane_ops_per_s"] / 1e9,
-                     "unit": "G fp64 reductions/s", "frac": (rhs_red / rhs_avg_s) / peaks["red_f64_lane_ops_per_s"],
+                     "achieved": rhs_red / rhs_avg_s / 1e9, "peak": pk / 1e9,
+                     "unit": f"G {'int64 fixed-point' if fx else 'fp64'} reductions/s",
+                     "frac": (rhs_red / rhs_avg_s) / pk,
                      "traffic": traffic_for("k_rhs", args.config),
-                     "peak_source": "measured here: cparls_peak_red_f64, r-lane fp64 red into random rows of a "
-                                    f"{window_rows}-row window (the k_rhs pattern)",
+                     "peak_source": f"measured here: cparls_peak_red_idx, r-lane {kind} red (nothing else) into the "
+                                    f"rows of {peaks['red_stream_len']} matched fiber entries of fresh samples (every "
+                                    f"mode) that fall in the first {window_rows}-row output window (the k_rhs "
+                                    f"row stream; "
+                                    f"uniform-row rate {peaks[f'red_{kind}_lane_ops_per_s'] / 1e9:.0f} G/s)",
                      "alg_bytes_per_launch": rhs_bytes, "avg_launch_ms": rhs_avg_s * 1e3,
                      "hbm_view": {"achieved": rhs_bytes / rhs_avg_s / 1e9, "peak": hbm_peak, "unit": "GB/s",
                                   "frac": rhs_bytes / rhs_avg_s / 1e9 / hbm_peak}}

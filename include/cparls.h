@@ -63,11 +63,14 @@ typedef struct {
   int64_t didx_cap;        /* max DIDX list length per level (0 -> default 1<<22)     */
   int64_t attempt_cap;     /* max SIDX attempts (0 -> 1024*s_rnd + 65536, AMB-7)      */
   int32_t rhs_path;        /* sampled RHS kernels: 0 auto (= 1, the faster on B200),
-                              1 fp64 reductions into M (rhs.cuh), 2 bucketed: entries
-                              placed into 32-row buckets, accumulated in shared
-                              memory without atomics (rhs_bucket.cuh; needs r <= 32,
-                              s_bar < 2^27, m_k < 2^32).  Same math; B = M G^+ follows
-                              in k_solve_rows_t either way.                          */
+                              1 fixed-point int64 reductions into M (rhs.cuh, AMB-35:
+                              deterministic, per-column scale 2^e_c from a bound on
+                              |M|), 2 bucketed: entries placed into 32-row buckets,
+                              accumulated in shared memory without atomics
+                              (rhs_bucket.cuh; needs r <= 32, s_bar < 2^27,
+                              m_k < 2^32), 3 fp64 reductions into M (rhs.cuh; order
+                              of the additions not fixed).  Same math; B = M G^+
+                              follows in k_solve_rows_t.  Other values: EINVAL.     */
   int64_t fit_samples;     /* s_fit > 0: draw the stratified fit sample at create
                               (sec:estimating-fit, AMB-32); 0 = none.
                               Single GPU only (EINVAL with world_size > 1).          */

@@ -52,6 +52,8 @@ struct DevScalars {
   unsigned long long det_drawable;
   double fit[3];
   double normX2;
+  double maxabs;                    // max |x| over the nonzeros (fixed-point RHS bound)
+  unsigned long long dupmax;        // longest run of duplicate coordinates in a copy
 };
 
 }  // namespace
@@ -96,6 +98,12 @@ struct cparls_ctx {
   double *sw2 = nullptr, *sp = nullptr;
   int32_t *scnt = nullptr;
   uint8_t *sisdet = nullptr;
+  // canonical-order sort of the combined sample (second copies, swapped in)
+  uint64_t *skey2 = nullptr;
+  double *sw2_2 = nullptr, *sp2 = nullptr;
+  int32_t *scnt2 = nullptr;
+  uint8_t *sisdet2 = nullptr;
+  uint32_t *sperm = nullptr, *sperm2 = nullptr, *shist = nullptr;
   double *Z = nullptr;
   int64_t *lo = nullptr, *len = nullptr, *off = nullptr;
   int64_t mk = 0;
@@ -145,6 +153,10 @@ struct cparls_ctx {
   uint32_t *rec = nullptr;
   double *recc = nullptr;
   bool m_dirty = false;   // M holds rows written by the bucketed RHS (not zero)
+  double *fx_scale = nullptr;   // fixed-point RHS scales 2^e_c, 2^-e_c (kernels.cuh)
+  double dupmax = 1.0;
+  bool rhs_fixed = !(getenv("CPARLS_RHS_FIXED") && atoi(getenv("CPARLS_RHS_FIXED")) == 0);
+  bool fx_on = false;           // this solve's RHS is fixed point (M holds int64)
   // frozen stratified fit sample (fitest.cuh, AMB-32)
   bool have_fs = false;
   int64_t fs_nnz = 0, fs_zero = 0;
@@ -666,11 +678,14 @@ void build_all(cparls_ctx *c, const IT *coords, const VT *vals) {
   if (read_dev(c, &c->dv->bad) != 0) throw ApiError(CPARLS_ERANGE, "coordinate out of range [0, n_k)");
   // ||X||^2 (compensated; summed over ranks)
   const int nb = 296;
-  k_sumsq<VT><<<nb, 256, 0, c->st>>>(vals, c->nnz, c->ddpart);
+  k_sumsq<VT><<<nb, 256, 0, c->st>>>(vals, c->nnz, c->ddpart, &c->dv->maxabs);
   CK_LAUNCH();
   k_sum_dd_final<<<1, 32, 0, c->st>>>(c->ddpart, nb, &c->dv->normX2);
   CK_LAUNCH();
-  if (c->world > 1) c->comm->allreduce_f64(&c->dv->normX2, 1, c->st);
+  if (c->world > 1) {
+    c->comm->allreduce_f64(&c->dv->normX2, 1, c->st);
+    c->comm->allreduce_f64(&c->dv->maxabs, 1, c->st);   // sum of the ranks' maxima: a common upper bound
+  }
   c->normX2 = read_dev(c, &c->dv->normX2);
   for (int k = 0; k < c->D; ++k) {
     if (c->world == 1) {
@@ -688,7 +703,8 @@ void alloc_sample_buffers(cparls_ctx *c, int64_t s) {
   int64_t cap = std::max<int64_t>(s, 1024);
   for (void *p : {(void *)c->skey, (void *)c->sw2, (void *)c->sp, (void *)c->scnt, (void *)c->sisdet, (void *)c->Z,
                   (void *)c->lo, (void *)c->len, (void *)c->off, (void *)c->rkey, (void *)c->rp, (void *)c->hkey,
-                  (void *)c->hcnt, (void *)c->hp})
+                  (void *)c->hcnt, (void *)c->hp, (void *)c->skey2, (void *)c->sw2_2, (void *)c->sp2,
+                  (void *)c->scnt2, (void *)c->sisdet2, (void *)c->sperm, (void *)c->sperm2, (void *)c->shist})
     dfree(c, p);
   c->skey = dalloc_t<uint64_t>(c, cap);
   c->sw2 = dalloc_t<double>(c, cap);
@@ -701,6 +717,14 @@ void alloc_sample_buffers(cparls_ctx *c, int64_t s) {
   c->off = dalloc_t<int64_t>(c, cap);
   c->rkey = dalloc_t<uint64_t>(c, cap);
   c->rp = dalloc_t<double>(c, cap);
+  c->skey2 = dalloc_t<uint64_t>(c, cap);
+  c->sw2_2 = dalloc_t<double>(c, cap);
+  c->sp2 = dalloc_t<double>(c, cap);
+  c->scnt2 = dalloc_t<int32_t>(c, cap);
+  c->sisdet2 = dalloc_t<uint8_t>(c, cap);
+  c->sperm = dalloc_t<uint32_t>(c, cap);
+  c->sperm2 = dalloc_t<uint32_t>(c, cap);
+  c->shist = dalloc_t<uint32_t>(c, 256 * (ceil_div(cap, kScanTile) + 1));
   uint64_t hs = 1;
   while (hs < (uint64_t)(2 * cap)) hs <<= 1;
   c->hsize = hs;
@@ -962,6 +986,34 @@ void sample_impl(cparls_ctx *c, int k, int64_t s, uint64_t seed, uint64_t step, 
     LAUNCHED(c, 2);
     nuniq = (int64_t)read_dev(c, &c->dv->counter);
   }
+  // canonical order: the DIDX list and the CIDX hash emit in an order that
+  // depends on thread timing; sorting by the (unique) key makes Z, the sampled
+  // Gram and the solve bit-reproducible (AMB-35) and walks the factor rows and
+  // the fiber directory in key order
+  if (sdet + nuniq > 1) {
+    const int64_t n = sdet + nuniq;
+    int end_bit = 0;
+    {
+      unsigned __int128 prod = 1;
+      for (int j = 0; j < d; ++j) prod *= (unsigned __int128)om.n[j];
+      while (end_bit < 64 && (((unsigned __int128)1) << end_bit) < prod) ++end_bit;
+    }
+    const unsigned g = (unsigned)ceil_div(n, 256);
+    k_iota_u32<<<g, 256, 0, c->st>>>(c->sperm, n);
+    CK_LAUNCH();
+    int res = radix_sort_pairs(c->skey, c->sperm, c->skey2, c->sperm2, n, end_bit, c->shist, c->st,
+                               &c->stats.kernel_launches);
+    if (res) std::swap(c->skey, c->skey2);   // sorted keys
+    const uint32_t *perm = res ? c->sperm2 : c->sperm;
+    k_sample_permute<<<g, 256, 0, c->st>>>(perm, n, c->sw2, c->sp, c->scnt, c->sisdet, c->sw2_2, c->sp2, c->scnt2,
+                                           c->sisdet2);
+    CK_LAUNCH();
+    std::swap(c->sw2, c->sw2_2);
+    std::swap(c->sp, c->sp2);
+    std::swap(c->scnt, c->scnt2);
+    std::swap(c->sisdet, c->sisdet2);
+    LAUNCHED(c, 2);
+  }
   c->smode = k;
   c->sdet = sdet;
   c->s_rnd = s_rnd;
@@ -1037,6 +1089,7 @@ void solve_impl(cparls_ctx *c, int k, cparls_solve_info *info) {
   bool use_bkt = false;
   {
     const int path = c->opts.rhs_path;
+    c->fx_on = c->rhs_fixed && path != 3;
     const bool ok = r <= 32 && sbar < kBktMaxSbar;
     // auto = atomic: on C4 the bucketed path measured 14.8 ms per mode step
     // (count 0.6 + place 2.2 + accumulate 7.2 + solve 1.3) against 7.0 + 0.8
@@ -1105,7 +1158,7 @@ void solve_impl(cparls_ctx *c, int k, cparls_solve_info *info) {
     CK(cudaMemsetAsync(&c->dv->touched, 0, sizeof(unsigned long long), c->st));
     const int64_t bgrid = row_grid(c, ceil_div(std::max<int64_t>(nown, 1), kRowThreads));
     RSWITCH(r, k_solve_rows_t<RM><<<(unsigned)bgrid, kRowThreads, solve_smem(r, ld), c->st>>>(
-                   c->M + r0 * ld, nown, r, ld, c->sd, c->A[k] + r0 * ld, c->gpart, &c->dv->touched, 0));
+                   c->M + r0 * ld, nown, r, ld, c->sd, c->A[k] + r0 * ld, c->gpart, &c->dv->touched, 0, nullptr));
     CK_LAUNCH();
     c->m_dirty = true;   // M holds this mode's rows (no zeroing pass)
     kt.stop();
@@ -1149,17 +1202,28 @@ void solve_impl(cparls_ctx *c, int k, cparls_solve_info *info) {
         exclusive_scan_i64(c->seg_len, c->seg_off, nseg, c->i64part_seg, nullptr, c->st);
         LAUNCHED(c, 4);
       }
+      if (c->fx_on) {   // per-column fixed-point scales from the sample (kernels.cuh)
+        const int nbc = 148;
+        k_colabs_part<<<nbc, 256, 0, c->st>>>(c->Z, c->sw2, sbar, r, ld, c->gpart);
+        CK_LAUNCH();
+        k_fixed_scales<<<1, 64, 0, c->st>>>(c->gpart, nbc, r, &c->dv->maxabs, c->dupmax, c->fx_scale);
+        CK_LAUNCH();
+        LAUNCHED(c, 2);
+      }
       CK(cudaMemsetAsync(&c->dv->counter, 0, sizeof(unsigned long long), c->st));
       const int grid = 148 * grid_mult;
       const int64_t per_warp = 512;
 #define RHS(VT, HI)                                                                                               \
-  k_rhs<VT, HI><<<grid, kRhsThreads, 0, c->st>>>(c->seg_off, c->seg_lo, nwin > 1 ? c->seg_j : nullptr, nseg, &c->dv->mk,          \
+  if (c->fx_on) RHS2(VT, HI, true); else RHS2(VT, HI, false)
+#define RHS2(VT, HI, FX)                                                                                           \
+  k_rhs<VT, HI, FX><<<grid, kRhsThreads, 0, c->st>>>(c->seg_off, c->seg_lo, nwin > 1 ? c->seg_j : nullptr, nseg, &c->dv->mk,          \
                                                            &c->dv->counter, c->idx[k].out, (const VT *)c->idx[k].val, \
-                                                           c->sw2, c->Z, r, ld, c->M, per_warp)
+                                                           c->sw2, c->Z, r, ld, c->M, per_warp, c->fx_scale)
       KTimer kt(c, KT_RHS);
       if (c->vf32) { if (r > 32) RHS(float, true); else RHS(float, false); }
       else { if (r > 32) RHS(double, true); else RHS(double, false); }
       kt.stop();
+#undef RHS2
 #undef RHS
       CK_LAUNCH();
       LAUNCHED(c, 1);
@@ -1176,7 +1240,8 @@ void solve_impl(cparls_ctx *c, int k, cparls_solve_info *info) {
     CK(cudaMemsetAsync(&c->dv->touched, 0, sizeof(unsigned long long), c->st));
     KTimer kts(c, KT_SOLVE);
     RSWITCH(r, k_solve_rows_t<RM><<<(unsigned)grid, kRowThreads, solve_smem(r, ld), c->st>>>(
-                   c->M + r0 * ld, nown, r, ld, c->sd, c->A[k] + r0 * ld, c->gpart, &c->dv->touched, 1));
+                   c->M + r0 * ld, nown, r, ld, c->sd, c->A[k] + r0 * ld, c->gpart, &c->dv->touched, 1,
+                   c->fx_on ? c->fx_scale : nullptr));
     kts.stop();
     CK_LAUNCH();
     k_pairs_reduce<<<pairs_reduce_grid(r), 256, 0, c->st>>>(c->gpart, grid, r, c->sd->BtB);
@@ -1296,7 +1361,7 @@ void als_update_impl(cparls_ctx *c, int k) {
   CK(cudaMemsetAsync(&c->dv->touched, 0, sizeof(unsigned long long), c->st));
   KTimer kts(c, KT_SOLVE);
   RSWITCH(r, k_solve_rows_t<RM><<<(unsigned)grid, kRowThreads, solve_smem(r, ld), c->st>>>(
-                 c->M, nk, r, ld, c->sd, c->A[k], c->gpart, &c->dv->touched, 1));
+                 c->M, nk, r, ld, c->sd, c->A[k], c->gpart, &c->dv->touched, 1, nullptr));
   kts.stop();
   CK_LAUNCH();
   k_pairs_reduce<<<pairs_reduce_grid(r), 256, 0, c->st>>>(c->gpart, grid, r, c->sd->BtB);
@@ -1626,6 +1691,7 @@ cparls_status cparls_create(cparls_ctx **out, int32_t nmodes, const int64_t *dim
   cparls_status st = guarded(c, [&] {
     if (nmodes < 2 || nmodes > kMaxModes) throw ApiError(CPARLS_EINVAL, "nmodes must be in [2, 8]");
     if (opts->rank < 1 || opts->rank > kMaxRank) throw ApiError(CPARLS_EINVAL, "rank must be in [1, 64]");
+    if (opts->rhs_path < 0 || opts->rhs_path > 3) throw ApiError(CPARLS_EINVAL, "rhs_path must be in [0, 3]");
     if (nnz_local < 0) throw ApiError(CPARLS_EINVAL, "nnz < 0");
     if (nnz_local >= (int64_t(1) << 32)) throw ApiError(CPARLS_ERANGE, "nnz_local must be < 2^32 per GPU");
     if (nnz_local > 0 && (!coords || !vals)) throw ApiError(CPARLS_EINVAL, "null coords/vals");
@@ -1696,6 +1762,17 @@ cparls_status cparls_create(cparls_ctx **out, int32_t nmodes, const int64_t *dim
     else if (vsz == 4) build_all<int64_t, float>(c, (const int64_t *)dco, (const float *)dva);
     else build_all<int64_t, double>(c, (const int64_t *)dco, (const double *)dva);
     sync(c);
+    {   // duplicate coordinates bound the fixed-point RHS scale (kernels.cuh)
+      CK(cudaMemsetAsync(&c->dv->dupmax, 0, sizeof(unsigned long long), c->st));
+      for (int k = 0; k < nmodes; ++k)
+        if (c->idx[k].nnz > 0) {
+          k_dup_runs<<<1184, 256, 0, c->st>>>(c->idx[k].key, c->idx[k].out, c->idx[k].nnz, &c->dv->dupmax);
+          CK_LAUNCH();
+        }
+      if (c->world > 1) c->comm->allreduce_u64(&c->dv->dupmax, 1, c->st);   // (sum: an upper bound)
+      c->dupmax = std::max<double>(1.0, (double)read_dev(c, &c->dv->dupmax));
+      c->fx_scale = dalloc_t<double>(c, 2 * kMaxRank);
+    }
     if (tdbg) {
       sync(c);
       fprintf(stderr, "[cparls] create: setup+H2D %.3f s, build %.3f s\n",

@@ -40,6 +40,20 @@ __global__ void k_peak_red_t(T *M, int64_t rows, int r, int ld, int64_t ops_per_
   }
 }
 
+// reductions into the rows of a given index stream (e.g. the tensor's own
+// mode coordinates): warp w walks idx[w*per_warp ...), lane c adds to column c
+template <typename T>
+__global__ void k_peak_red_idx(T *M, const int32_t *__restrict__ idx, int64_t n, int r, int ld,
+                               int64_t per_warp) {
+  const int lane = threadIdx.x & 31;
+  const int64_t wid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t b = wid * per_warp, e = min(n, b + per_warp);
+  for (int64_t i = b; i < e; ++i) {
+    const int64_t row = __ldg(idx + i);
+    if (lane < r) atomicAdd(M + row * ld + lane, (T)3);
+  }
+}
+
 template <int SW>
 __global__ void k_peak_gather(const double *__restrict__ A, int64_t rows, int ld, int64_t rows_per_warp,
                               double *out) {
@@ -110,6 +124,33 @@ double cparls_peak_red_kind(void *M, int64_t rows, int r, int ld, int64_t ops_pe
   cudaEventDestroy(b);
   if (cudaGetLastError() != cudaSuccess || ms <= 0.f) return -1.0;
   return (double)reps * blocks * 8 * (double)ops_per_warp * r / (ms * 1e-3);
+}
+
+// kind 0: unsigned long long, 2: double.  idx: n device row ids (< rows of M).
+// Returns lane-ops per second (n * r / time).
+double cparls_peak_red_idx(void *M, const int32_t *idx, int64_t n, int r, int ld, int blocks, int reps, int kind) {
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  const int64_t warps = (int64_t)blocks * 8;
+  const int64_t per_warp = (n + warps - 1) / warps;
+  auto launch = [&]() {
+    if (kind == 0)
+      k_peak_red_idx<unsigned long long><<<blocks, 256>>>((unsigned long long *)M, idx, n, r, ld, per_warp);
+    else
+      k_peak_red_idx<double><<<blocks, 256>>>((double *)M, idx, n, r, ld, per_warp);
+  };
+  launch();
+  cudaEventRecord(a);
+  for (int i = 0; i < reps; ++i) launch();
+  cudaEventRecord(b);
+  cudaEventSynchronize(b);
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, a, b);
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  if (cudaGetLastError() != cudaSuccess || ms <= 0.f) return -1.0;
+  return (double)reps * (double)n * r / (ms * 1e-3);
 }
 
 // Returns bytes per second of row data gathered (rows gathered * ld * 8 / time).

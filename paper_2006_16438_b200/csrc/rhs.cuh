@@ -26,15 +26,23 @@ namespace cparls {
 
 constexpr int kRhsThreads = 256;
 
-template <typename VT, bool HI>
+__device__ __forceinline__ void red_fixed(double *addr, double v, double sc) {
+  const long long q = __double2ll_rn(v * sc);   // v * 2^e exact; the only rounding is to the integer
+  if (q != 0) atomicAdd(reinterpret_cast<unsigned long long *>(addr), (unsigned long long)q);
+}
+
+template <typename VT, bool HI, bool FIXED>
 __global__ void __launch_bounds__(kRhsThreads) k_rhs(const int64_t *__restrict__ off, const int64_t *__restrict__ lo,
                                                     const int32_t *__restrict__ seg_j, int64_t nseg,
                                                     const int64_t *__restrict__ mk_ptr,
                                                     unsigned long long *__restrict__ work,
                                                     const int32_t *__restrict__ outidx, const VT *__restrict__ vals,
                                                     const double *__restrict__ sw2, const double *__restrict__ Z,
-                                                    int r, int ld, double *__restrict__ M, int64_t per_warp) {
+                                                    int r, int ld, double *__restrict__ M, int64_t per_warp,
+                                                    const double *__restrict__ fscale) {
   const int lane = threadIdx.x & 31;
+  const double sc0 = FIXED && lane < r ? fscale[lane] : 0.0;
+  const double sc1 = FIXED && HI && lane + 32 < r ? fscale[lane + 32] : 0.0;
   const int64_t mk = *mk_ptr;
   const uint64_t pstream = l2_evict_first();
   while (true) {
@@ -80,8 +88,14 @@ __global__ void __launch_bounds__(kRhsThreads) k_rhs(const int64_t *__restrict__
         for (int u = 0; u < cnt; ++u) {
           const int o = __shfl_sync(0xffffffffu, o_l, u);
           const double cx = __shfl_sync(0xffffffffu, cx_l, u);
-          if (lane < r) atomicAdd(M + (int64_t)o * ld + lane, cx * z0);
-          if (HI && lane + 32 < r) atomicAdd(M + (int64_t)o * ld + lane + 32, cx * z1);
+          if (lane < r) {
+            if (FIXED) red_fixed(M + (int64_t)o * ld + lane, cx * z0, sc0);
+            else atomicAdd(M + (int64_t)o * ld + lane, cx * z0);
+          }
+          if (HI && lane + 32 < r) {
+            if (FIXED) red_fixed(M + (int64_t)o * ld + lane + 32, cx * z1, sc1);
+            else atomicAdd(M + (int64_t)o * ld + lane + 32, cx * z1);
+          }
         }
       } else {
         for (int u = 0; u < cnt; ++u) {
@@ -93,8 +107,14 @@ __global__ void __launch_bounds__(kRhsThreads) k_rhs(const int64_t *__restrict__
             z0 = lane < r ? __ldg(Z + ju * ld + lane) : 0.0;
             if (HI) z1 = lane + 32 < r ? __ldg(Z + ju * ld + lane + 32) : 0.0;
           }
-          if (lane < r) atomicAdd(M + (int64_t)o * ld + lane, cx * z0);
-          if (HI && lane + 32 < r) atomicAdd(M + (int64_t)o * ld + lane + 32, cx * z1);
+          if (lane < r) {
+            if (FIXED) red_fixed(M + (int64_t)o * ld + lane, cx * z0, sc0);
+            else atomicAdd(M + (int64_t)o * ld + lane, cx * z0);
+          }
+          if (HI && lane + 32 < r) {
+            if (FIXED) red_fixed(M + (int64_t)o * ld + lane + 32, cx * z1, sc1);
+            else atomicAdd(M + (int64_t)o * ld + lane + 32, cx * z1);
+          }
         }
       }
       jcur = __shfl_sync(0xffffffffu, jj, 31);

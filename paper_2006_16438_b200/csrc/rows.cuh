@@ -77,7 +77,7 @@ __global__ void __launch_bounds__(kRowThreads) k_solve_rows_t(double *__restrict
                                                              const SolveDev *__restrict__ sd, double *__restrict__ B,
                                                              double *__restrict__ part,
                                                              unsigned long long *__restrict__ touched,
-                                                             int zero_m) {
+                                                             int zero_m, const double *__restrict__ fscale) {
   extern __shared__ double smem[];
   const int S = ld + 1;
   double *Gi = smem;
@@ -103,7 +103,10 @@ __global__ void __launch_bounds__(kRowThreads) k_solve_rows_t(double *__restrict
       bool nz = false;
 #pragma unroll
       for (int c = 0; c < RMAX; ++c) {
-        m[c] = (c < r) ? x[c] : 0.0;
+        double v = (c < r) ? x[c] : 0.0;
+        if (fscale != nullptr && c < r)   // fixed-point RHS: int64 count of 2^-e_c
+          v = (double)__double_as_longlong(v) * fscale[kMaxRank + c];
+        m[c] = v;
         nz |= (m[c] != 0.0);
       }
       if (nz) {

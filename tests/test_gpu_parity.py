@@ -130,10 +130,11 @@ def test_c1_lockstep_20_iterations():
     lockstep(T, cfg.rank, cfg.iters, cfg.s, cfg.sample_seed)
 
 
-@pytest.mark.parametrize("rhs_path", [1, 2])
+@pytest.mark.parametrize("rhs_path", [1, 2, 3])
 def test_c1_lockstep_rhs_paths(rhs_path):
-    """Both RHS + solve implementations (atomic reductions into M, and the
-    bucketed RHS with the fused solve) against the oracle."""
+    """Every RHS + solve implementation (fixed-point int64 reductions into M,
+    the bucketed RHS with the fused solve, fp64 reductions into M) against the
+    oracle."""
     T = synth.make("C1")
     cfg = T.cfg
     lockstep(T, cfg.rank, 6, cfg.s, cfg.sample_seed, rhs_path=rhs_path)
@@ -473,3 +474,32 @@ def test_c2_hybrid_concentrated_leverage_lockstep():
         assert oi.s_det > 0
         a, b = g.get_sample(), o.get_sample()
         assert (a["keys"] == b["keys"]).all() and (a["counts"] == b["counts"]).all()
+
+
+@pytest.mark.parametrize("rank", [10, 25, 40])
+def test_rhs_fixed_point_deterministic_and_close(rank):
+    """AMB-35: the fixed-point RHS (rhs_path 1) is bit-reproducible run to run,
+    and agrees with the fp64-reduction path (rhs_path 3) to the quantisation
+    bound (<= 1e-11 relative Frobenius on B; HI lanes covered by rank 40)."""
+    need_gpu()
+    T = synth.make("C2", device="cuda")
+    from paper_2006_16438_b200 import Cparls
+    gs = {p: Cparls(T.dims, T.coords, T.vals, rank, rhs_path=p, init_seed=5) for p in (1, 3)}
+    A = [gs[1].get_factor(m)[0] for m in range(4)]
+    for k in range(4):
+        out = {}
+        for p, g in gs.items():
+            Bs = []
+            for rep in range(2):
+                for m in range(4):
+                    g.set_factor(m, A[m])
+                g.sample(k, 1 << 16, 77, k)
+                g.solve_mode(k)
+                Bs.append(g.last_solve(k)[1].copy())
+            out[p] = Bs
+        assert np.array_equal(out[1][0].view(np.uint64), out[1][1].view(np.uint64)), k
+        nb = np.linalg.norm(out[3][0])
+        rel = np.linalg.norm(out[1][0] - out[3][0]) / nb
+        assert rel <= 1e-11, (k, rel)
+    for g in gs.values():
+        g.close()
