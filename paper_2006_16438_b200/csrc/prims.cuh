@@ -133,15 +133,26 @@ __global__ void k_radix_hist(const uint64_t *__restrict__ keys, int64_t n, int s
   for (int i = threadIdx.x; i < kRadixBins; i += blockDim.x) hist[(int64_t)i * gridDim.x + blockIdx.x] = h[i];
 }
 
-// single block: exclusive scan over hist (bins-major) in place
+// single block: exclusive scan over hist (bins-major) in place; each thread
+// scans kScanItems consecutive entries serially, one block scan per 2048
 __global__ void k_radix_scan(uint32_t *hist, int64_t len) {
   uint32_t carry = 0;
-  for (int64_t base = 0; base < len; base += kScanThreads) {
-    int64_t idx = base + threadIdx.x;
-    uint32_t v = idx < len ? hist[idx] : 0u;
+  for (int64_t base = 0; base < len; base += kScanTile) {
+    const int64_t b0 = base + (int64_t)threadIdx.x * kScanItems;
+    uint32_t v[kScanItems];
+    uint32_t sum = 0;
+#pragma unroll
+    for (int i = 0; i < kScanItems; ++i) {
+      v[i] = b0 + i < len ? hist[b0 + i] : 0u;
+      sum += v[i];
+    }
     uint32_t tot;
-    uint32_t ex = block_excl_scan<uint32_t>(v, &tot);
-    if (idx < len) hist[idx] = carry + ex;
+    uint32_t ex = carry + block_excl_scan<uint32_t>(sum, &tot);
+#pragma unroll
+    for (int i = 0; i < kScanItems; ++i) {
+      if (b0 + i < len) hist[b0 + i] = ex;
+      ex += v[i];
+    }
     carry += tot;
     __syncthreads();
   }
@@ -204,9 +215,56 @@ __global__ void k_radix_scatter(const uint64_t *__restrict__ kin, const uint32_t
 // Sorts (keys, vals) by key bits [0, end_bit) stably.  Ping-pongs between the
 // given buffers; returns the index (0 = keys/vals, 1 = ktmp/vtmp) holding the
 // result.  hist needs 256*ceil(n/2048) entries.  n must be < 2^32.
+// Small lists: one CTA sorts (key, val) pairs in shared memory by the
+// composite (key, val) -- a bitonic network over the next power of two, padded
+// with (max, max).  With distinct vals (row indices, sample positions) the
+// order equals the stable radix order by key.
+constexpr int kSmallSortMax = 4096;   // 48 KB of static shared memory
+constexpr int kSmallSortThreads = 1024;
+
+__global__ void __launch_bounds__(kSmallSortThreads) k_small_sort_pairs(uint64_t *__restrict__ keys,
+                                                                        uint32_t *__restrict__ vals, int n) {
+  __shared__ uint64_t sk[kSmallSortMax];
+  __shared__ uint32_t sv[kSmallSortMax];
+  int np = 1;
+  while (np < n) np <<= 1;
+  for (int i = threadIdx.x; i < np; i += blockDim.x) {
+    sk[i] = i < n ? keys[i] : ~0ull;
+    sv[i] = i < n ? vals[i] : 0xFFFFFFFFu;
+  }
+  __syncthreads();
+  for (int size = 2; size <= np; size <<= 1) {
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      for (int t = threadIdx.x; t < (np >> 1); t += blockDim.x) {
+        const int lo = 2 * t - (t & (stride - 1));
+        const int hi = lo + stride;
+        const bool up = (lo & size) == 0;
+        const uint64_t a = sk[lo], b = sk[hi];
+        const uint32_t va = sv[lo], vb = sv[hi];
+        const bool gt = (a > b) || (a == b && va > vb);
+        if (gt == up) {
+          sk[lo] = b; sk[hi] = a;
+          sv[lo] = vb; sv[hi] = va;
+        }
+      }
+      __syncthreads();
+    }
+  }
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    keys[i] = sk[i];
+    vals[i] = sv[i];
+  }
+}
+
 inline int radix_sort_pairs(uint64_t *keys, uint32_t *vals, uint64_t *ktmp, uint32_t *vtmp, int64_t n,
                             int end_bit, uint32_t *hist, cudaStream_t st, int64_t *launches) {
   if (n <= 1) return 0;
+  if (n <= kSmallSortMax) {   // in place, one launch (requires distinct vals; callers pass indices)
+    k_small_sort_pairs<<<1, kSmallSortThreads, 0, st>>>(keys, vals, (int)n);
+    CK_LAUNCH();
+    if (launches) *launches += 1;
+    return 0;
+  }
   int64_t nb = ceil_div(n, kScanTile);
   uint64_t *kb[2] = {keys, ktmp};
   uint32_t *vb[2] = {vals, vtmp};

@@ -32,12 +32,18 @@ def launches(path, out, steps):
     ks = [(short(r[ki]), float(r[vi].replace(",", ""))) for r in data]
     base = [re.sub(r"<.*", "", n) for n, _ in ks]
     rhs = [i for i, n in enumerate(base) if n == "k_rhs"]
-    per = len(rhs) // 3 // 1
-    # timed region: from the first kernel after the warm-up's last k_rhs to the last k_rhs + its mode step
-    start = rhs[len(rhs) - 3 * steps - 1] + 1 if len(rhs) > 3 * steps else 0
+    # timed region of bench.py: mode steps 3W .. 3W+3K-1 (W = 3 warm-up
+    # iterations, 3 modes) from the kernel after the previous mode step's
+    # leverage pass, through the epoch fit, up to the next sample that
+    # bench.py draws after the timed region (its first k_cand_count)
+    W = 3
+    first = rhs[3 * W]
+    start = max(i for i in range(first) if base[i] == "k_lev_rows_w") + 1
+    last = rhs[3 * W + 3 * steps - 1]
+    end = next(i for i in range(last, len(base)) if base[i] == "k_cand_count")
     tot, cnt = collections.Counter(), collections.Counter()
     peaks = {"k_peak_red", "k_peak_gather"}
-    for i in range(start, len(ks)):
+    for i in range(start, end):
         n, t = ks[i]
         if any(p in n for p in peaks) or n.startswith("<unnamed>"):
             continue
@@ -46,8 +52,8 @@ def launches(path, out, steps):
     s = sum(tot.values())
     with open(out, "w") as f:
         f.write(f"# C4 kernel launch list (ncu gpu__time_duration.sum, --clock-control none)\n\n")
-        f.write(f"Source: `{path}`; {steps} timed iterations after 3 warm-up iterations (includes one exact "
-                f"fit per epoch plus the bench's final fit; ncu serialises launches and flushes caches, so "
+        f.write(f"Source: `{path}`; the {steps} timed iterations after 3 warm-up iterations (launches "
+                f"{start}..{end - 1}: every mode step and the epoch's exact fit; ncu serialises launches and flushes caches, so "
                 f"compare shares, not absolute times).\n\n")
         f.write("| kernel | launches | total ms | avg ms | share |\n|---|---|---|---|---|\n")
         for n, t in tot.most_common():
