@@ -336,7 +336,7 @@ inline int rmax_bucket(int r) { return r <= 4 ? 4 : r <= 8 ? 8 : r <= 16 ? 16 : 
 // unconditional register loads of padded columns
 size_t tile_d(int ld) { return (size_t)kRowThreads * (ld + 1); }
 size_t gram_smem(int r, int ld) { return sizeof(double) * (tile_d(ld) + 64); }
-size_t solve_smem(int r, int ld) { return sizeof(double) * ((size_t)r * r + tile_d(ld) + 64); }
+size_t solve_smem(int r, int ld) { return sizeof(double) * ((size_t)r * ld + tile_d(ld) + 64); }
 size_t krp_smem(int r, int ld) { return sizeof(double) * (tile_d(ld) + kRowThreads + 64); }
 size_t prep_smem(int r) { return sizeof(double) * 4 * (size_t)r * r; }
 size_t warp_tiles_d(int ld) { return (size_t)(kRowThreads / 32) * kWarpRows * warp_tile_stride(ld); }
