@@ -1771,7 +1771,7 @@ cparls_status cparls_create(cparls_ctx **out, int32_t nmodes, const int64_t *dim
         }
       if (c->world > 1) c->comm->allreduce_u64(&c->dv->dupmax, 1, c->st);   // (sum: an upper bound)
       c->dupmax = std::max<double>(1.0, (double)read_dev(c, &c->dv->dupmax));
-      c->fx_scale = dalloc_t<double>(c, 2 * kMaxRank);
+      c->fx_scale = dalloc_t<double>(c, 2 * kMaxRank + 1);
     }
     if (tdbg) {
       sync(c);

@@ -853,19 +853,28 @@ __global__ void k_colabs_part(const double *__restrict__ Z, const double *__rest
 __global__ void k_fixed_scales(const double *__restrict__ part, int nb, int r, const double *maxabs, double dupmax,
                                double *__restrict__ scale) {
   const int c = threadIdx.x;
-  if (c >= r) return;
-  double u = 0.0;
-  for (int b = 0; b < nb; ++b) u += part[(int64_t)b * r + c];
-  u *= *maxabs * dupmax;
   int e = 0;
-  if (u > 0.0) {
-    int ex;
-    frexp(u, &ex);              // u < 2^ex
-    e = 60 - ex;
-    e = max(-1000, min(1000, e));
+  bool ok = true;
+  if (c < r) {
+    double u = 0.0;
+    for (int b = 0; b < nb; ++b) u += part[(int64_t)b * r + c];
+    u *= *maxabs * dupmax;
+    if (!(u < INFINITY)) ok = false;   // inf / NaN bound
+    else if (u > 0.0) {
+      int ex;
+      frexp(u, &ex);              // u < 2^ex
+      e = 60 - ex;
+      if (e < -960 || e > 960) ok = false;   // 2^e_c or the terms' quanta out of range
+    }
   }
-  scale[c] = ldexp(1.0, e);
-  scale[kMaxRank + c] = ldexp(1.0, -e);
+  ok = __syncthreads_and(ok);
+  if (c < r) {
+    scale[c] = ok ? ldexp(1.0, e) : 1.0;
+    scale[kMaxRank + c] = ok ? ldexp(1.0, -e) : 1.0;
+  }
+  // scale[2 kMaxRank]: 1 = fixed point, 0 = this step falls back to fp64
+  // reductions (k_rhs and k_solve_rows_t read the flag)
+  if (c == 0) scale[2 * kMaxRank] = ok ? 1.0 : 0.0;
 }
 
 // longest run of equal (key, out) in a sorted copy (duplicate coordinates)

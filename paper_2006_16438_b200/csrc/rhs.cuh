@@ -41,6 +41,7 @@ __global__ void __launch_bounds__(kRhsThreads) k_rhs(const int64_t *__restrict__
                                                     int r, int ld, double *__restrict__ M, int64_t per_warp,
                                                     const double *__restrict__ fscale) {
   const int lane = threadIdx.x & 31;
+  const bool fx = FIXED && fscale[2 * kMaxRank] != 0.0;   // else: out-of-range bound, fp64 reductions
   const double sc0 = FIXED && lane < r ? fscale[lane] : 0.0;
   const double sc1 = FIXED && HI && lane + 32 < r ? fscale[lane + 32] : 0.0;
   const int64_t mk = *mk_ptr;
@@ -89,11 +90,11 @@ __global__ void __launch_bounds__(kRhsThreads) k_rhs(const int64_t *__restrict__
           const int o = __shfl_sync(0xffffffffu, o_l, u);
           const double cx = __shfl_sync(0xffffffffu, cx_l, u);
           if (lane < r) {
-            if (FIXED) red_fixed(M + (int64_t)o * ld + lane, cx * z0, sc0);
+            if (fx) red_fixed(M + (int64_t)o * ld + lane, cx * z0, sc0);
             else atomicAdd(M + (int64_t)o * ld + lane, cx * z0);
           }
           if (HI && lane + 32 < r) {
-            if (FIXED) red_fixed(M + (int64_t)o * ld + lane + 32, cx * z1, sc1);
+            if (fx) red_fixed(M + (int64_t)o * ld + lane + 32, cx * z1, sc1);
             else atomicAdd(M + (int64_t)o * ld + lane + 32, cx * z1);
           }
         }
@@ -108,11 +109,11 @@ __global__ void __launch_bounds__(kRhsThreads) k_rhs(const int64_t *__restrict__
             if (HI) z1 = lane + 32 < r ? __ldg(Z + ju * ld + lane + 32) : 0.0;
           }
           if (lane < r) {
-            if (FIXED) red_fixed(M + (int64_t)o * ld + lane, cx * z0, sc0);
+            if (fx) red_fixed(M + (int64_t)o * ld + lane, cx * z0, sc0);
             else atomicAdd(M + (int64_t)o * ld + lane, cx * z0);
           }
           if (HI && lane + 32 < r) {
-            if (FIXED) red_fixed(M + (int64_t)o * ld + lane + 32, cx * z1, sc1);
+            if (fx) red_fixed(M + (int64_t)o * ld + lane + 32, cx * z1, sc1);
             else atomicAdd(M + (int64_t)o * ld + lane + 32, cx * z1);
           }
         }

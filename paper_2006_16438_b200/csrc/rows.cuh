@@ -86,6 +86,7 @@ __global__ void __launch_bounds__(kRowThreads) k_solve_rows_t(double *__restrict
     const int p = i / ld, c = i - p * ld;
     Gi[i] = c < r ? sd->Ginv[p * r + c] : 0.0;
   }
+  const bool fixed = fscale != nullptr && fscale[2 * kMaxRank] != 0.0;
   Syrk<RMAX> sy;
   sy.init(r);
   unsigned long long ntouch = 0;
@@ -107,7 +108,7 @@ __global__ void __launch_bounds__(kRowThreads) k_solve_rows_t(double *__restrict
 #pragma unroll
       for (int c = 0; c < RMAX; ++c) {
         double v = (c < r) ? x[c] : 0.0;
-        if (fscale != nullptr && c < r)   // fixed-point RHS: int64 count of 2^-e_c
+        if (fixed && c < r)   // fixed-point RHS: int64 count of 2^-e_c
           v = (double)__double_as_longlong(v) * fscale[kMaxRank + c];
         m[c] = v;
         nz |= (m[c] != 0.0);

@@ -77,10 +77,18 @@ def compare_sample(g, o):
     assert (a["is_det"] == b["is_det"]).all()
     assert (a["p"] == b["p"]).all()               # same canonical product bits
     np.testing.assert_allclose(a["w2"], b["w2"], rtol=1e-14, atol=0)
-    la, oa, va = g.get_fibers()
-    lb, ob, vb = o.get_fibers()
+    la, oa, va = canonical_fibers(*g.get_fibers())
+    lb, ob, vb = canonical_fibers(*o.get_fibers())
     assert (la == lb).all() and (oa == ob).all() and (va == vb).all()
     return a
+
+
+def canonical_fibers(lens, out, val):
+    """Entries of each fiber ordered by (row, value): duplicate coordinates
+    (equal key and row) may come in any order; everything else is unique."""
+    fid = np.repeat(np.arange(len(lens)), lens)
+    o = np.lexsort((val, out, fid))
+    return lens, out[o], val[o]
 
 
 def lockstep(T, rank, iters, s, seed, tau=-1.0, check_fit=True, rhs_path=0):
@@ -503,3 +511,22 @@ def test_rhs_fixed_point_deterministic_and_close(rank):
         assert rel <= 1e-11, (k, rel)
     for g in gs.values():
         g.close()
+
+
+@pytest.mark.parametrize("scale", [1.0, 1e150, 1e-290])
+def test_rhs_fixed_point_duplicates_and_range(scale):
+    """AMB-35 bound with duplicate coordinates (dupmax = 4) and value ranges
+    that keep the fixed-point path (1, 1e150) or push 2^e_c out of range so
+    the step falls back to fp64 reductions (1e-290): lockstep vs the oracle."""
+    import types
+    rng = np.random.default_rng(11)
+    dims = (30, 20, 25)
+    base = np.stack([rng.integers(0, n, 300) for n in dims], 1)
+    reps = rng.integers(1, 5, len(base))
+    reps[0] = 4
+    coords = np.repeat(base, reps, axis=0)
+    vals = rng.uniform(0.5, 2.0, len(coords)) * scale
+    perm = rng.permutation(len(coords))
+    T = types.SimpleNamespace(dims=dims, coords=torch.from_numpy(coords[perm].astype(np.int64)),
+                              vals=torch.from_numpy(vals[perm]))
+    lockstep(T, 4, 2, 64, 5, check_fit=(scale == 1.0), rhs_path=1)
