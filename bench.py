@@ -472,16 +472,20 @@ def run_ours(args):
         hc, hv = host
         e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
         e0.record(stream)
+        w0 = time.perf_counter()
         g2 = Cparls(cfg.dims, hc.numpy(), hv.numpy(), cfg.rank, tau=args.tau, init_seed=cfg.init_seed,
                     stream=stream.cuda_stream, comm=comm, world_size=ws, world_rank=rk)
+        w1 = time.perf_counter()
         d2h = 0
         g2.run(K, cfg.s, seed, iter0=0, fit_every=ETA)
         d2h += 8 * (K // ETA)
+        w2 = time.perf_counter()
         for m in range(D):
             A, lam = g2.get_factor(m)
             d2h += A.nbytes + lam.nbytes
         e1.record(stream)
         torch.cuda.synchronize()
+        w3 = time.perf_counter()
         ems = e0.elapsed_time(e1)
         if ws > 1:
             tt = torch.tensor([ems], dtype=torch.float64)
@@ -491,6 +495,7 @@ def run_ours(args):
         h2d = hc.numel() * hc.element_size() + hv.numel() * hv.element_size()
         e2e = {"value": K / (ems / 1000.0), "unit": "iterations/s", "h2d_bytes_per_step": h2d // K,
                "d2h_bytes_per_step": d2h // K,
+               "wall_s": {"create_from_host": w1 - w0, "run": w2 - w1, "factors_to_host": w3 - w2},
                "includes": "cparls_create from pinned host COO (H2D + per-mode index build) + K iterations + "
                            "fits every 5 + factors back to host"}
 
