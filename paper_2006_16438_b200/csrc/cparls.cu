@@ -1623,7 +1623,7 @@ void fit_launch(cparls_ctx *c, cudaStream_t st, double *const *A, const double *
   KTimer kt(c, KT_FIT, st);
   if (fd.d <= 3) {
     // sub-warp per entry, 4 columns per lane (k_fit_sub)
-    nb = 148 * std::max(1, std::min(2, blocks_per_sm));
+    nb = 148 * std::max(1, std::min(CPARLS_FIT_MINB, blocks_per_sm));
     CK(cudaMemsetAsync(counter, 0, sizeof(unsigned long long), st));
 #define FITS(VT, SW, DM)                                                                                         \
   k_fit_sub<VT, SW, DM, (SW >= CPARLS_FIT_U ? CPARLS_FIT_U : SW)><<<nb, kFitThreads, 0, st>>>(c->idx[k].key, c->idx[k].out, (const VT *)c->idx[k].val, \
@@ -1673,7 +1673,7 @@ FitModes fit_modes(cparls_ctx *c, double *const *GA) {
 
 double fit_impl(cparls_ctx *c) {
   Phase ph(c, &c->stats.ms_fit);
-  fit_launch(c, c->st, c->A, c->lam_model, fit_modes(c, nullptr), c->ddpart, &c->dv->counter, c->dv->fit, 2);
+  fit_launch(c, c->st, c->A, c->lam_model, fit_modes(c, nullptr), c->ddpart, &c->dv->counter, c->dv->fit, 8);
   double f;
   if (c->world > 1) {
     // <X,M> is a sum over the ranks' slices of the fit mode

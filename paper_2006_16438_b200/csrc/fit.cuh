@@ -122,6 +122,12 @@ constexpr int kFitChunk = 2048;
 #ifndef CPARLS_FIT_U
 #define CPARLS_FIT_U 4   // entries per sub-warp issued before any is consumed
 #endif
+// Resident CTAs per SM the register budget is sized for.  Measured on C4
+// (r = 25): U4/2 CTAs 69.1 ms, U2/3 83.1, U2/4 79.9, U4/3 85.0 (spills), U8/2
+// 75.6; 256-bit row loads (LDG.E.ENL2.256) instead of 2 x 16 B: 71.0.
+#ifndef CPARLS_FIT_MINB
+#define CPARLS_FIT_MINB 2
+#endif
 
 // Sub-warp fit: SW lanes per entry, 4 columns per lane (two 16-byte loads; ld
 // is a multiple of 4, so a row is ld/4 lanes), NS = 32/SW entries per warp
@@ -135,7 +141,7 @@ constexpr int kFitChunk = 2048;
 // acc_c += x_e * A_{k*}(out_e,c) * h_c per lane: plain fp64 within a chunk,
 // folded into a double-double per chunk (AMB-16).
 template <typename VT, int SW, int DM, int U>
-__global__ void __launch_bounds__(kFitThreads, 2) k_fit_sub(const uint64_t *__restrict__ keys,
+__global__ void __launch_bounds__(kFitThreads, CPARLS_FIT_MINB) k_fit_sub(const uint64_t *__restrict__ keys,
                                                           const int32_t *__restrict__ outidx,
                                                           const VT *__restrict__ vals, int64_t nnz, FitDecode fd,
                                                           const double *__restrict__ Ak,
