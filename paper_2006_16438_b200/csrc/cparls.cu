@@ -159,6 +159,7 @@ struct cparls_ctx {
   bool fx_on = false;           // this solve's RHS is fixed point (M holds int64)
   // pinned double buffer for copies into pageable host memory (rows_to_host)
   void *stage[2] = {nullptr, nullptr};
+  long long *hscr = nullptr;    // small pinned scratch: async scalar reads folded into later syncs
   cudaEvent_t stage_ev[2] = {nullptr, nullptr};
   // frozen stratified fit sample (fitest.cuh, AMB-32)
   bool have_fs = false;
@@ -385,7 +386,7 @@ inline int rmax_bucket(int r) { return r <= 4 ? 4 : r <= 8 ? 8 : r <= 16 ? 16 : 
 // unconditional register loads of padded columns
 size_t tile_d(int ld) { return (size_t)kRowThreads * (ld + 1); }
 size_t gram_smem(int r, int ld) { return sizeof(double) * (tile_d(ld) + 64); }
-size_t solve_smem(int r, int ld) { return sizeof(double) * ((size_t)r * ld + tile_d(ld) + 64); }
+size_t solve_smem(int r, int ld) { return sizeof(double) * ((size_t)r * ld + (size_t)kRowThreads * (ld + 2) + 64); }
 size_t krp_smem(int r, int ld) { return sizeof(double) * (tile_d(ld) + kRowThreads + 64); }
 size_t prep_smem(int r) { return sizeof(double) * 4 * (size_t)r * r; }
 size_t warp_tiles_d(int ld) { return (size_t)(kRowThreads / 32) * kWarpRows * warp_tile_stride(ld); }
@@ -909,12 +910,12 @@ void sample_impl(cparls_ctx *c, int k, int64_t s, uint64_t seed, uint64_t step, 
   if (tau < 0) tau = 1.0 / (double)s;   // tau = 1/s
   OtherModes om = other_modes(c, k, true);
   const int d = om.d;
-  // drawable counts (rows with q > 0)
-  long long drawable[kMaxModes];
+  // drawable counts (rows with q > 0): copied into pinned scratch now, read
+  // after the p_det sync below (stream order), no sync of their own
+  long long *drawable = c->hscr;
   for (int j = 0; j < d; ++j)
     CK(cudaMemcpyAsync(&drawable[j], &c->md[om.mode[j]]->drawable, sizeof(long long), cudaMemcpyDeviceToHost,
                        c->st));
-  sync(c);
   // ---- DIDX
   int which = 0;
   int64_t sdet = run_didx(c, om, tau, &which);
@@ -1013,12 +1014,16 @@ void sample_impl(cparls_ctx *c, int k, int64_t s, uint64_t seed, uint64_t step, 
                                                                  c->rkey, c->rp, &c->dv->last_attempt);
         CK_LAUNCH();
         LAUNCHED(c, 3);
-        int64_t got = read_dev(c, &c->dv->total);
+        // total and last_attempt (adjacent) in one read
+        static_assert(offsetof(DevScalars, last_attempt) == offsetof(DevScalars, total) + 8, "layout");
+        CK(cudaMemcpyAsync(c->hscr + 32, &c->dv->total, 16, cudaMemcpyDeviceToHost, c->st));
+        sync(c);
+        const int64_t got = c->hscr[32];
         have += std::min<int64_t>(got, s_rnd - have);
         a0 += (uint64_t)win;
         c->stats.bytes_sample += (double)win * d * 8.0;
+        if (have >= s_rnd) attempts = (int64_t)(unsigned long long)c->hscr[33] + 1;
       }
-      attempts = (int64_t)read_dev(c, &c->dv->last_attempt) + 1;
     }
   }
   // ---- CIDX (combine repeats)
@@ -1774,6 +1779,7 @@ cparls_status cparls_create(cparls_ctx **out, int32_t nmodes, const int64_t *dim
       if (Nk >= 9223372036854775808.0L) throw ApiError(CPARLS_ERANGE, "prod_{m!=k} n_m >= 2^63");
     }
     set_kernel_attrs(c->r, c->ld);
+    CK(cudaHostAlloc(reinterpret_cast<void **>(&c->hscr), 64 * sizeof(long long), cudaHostAllocDefault));
     c->dv = dalloc_t<DevScalars>(c, 1);
     CK(cudaMemsetAsync(c->dv, 0, sizeof(DevScalars), c->st));
     c->sd = dalloc_t<SolveDev>(c, 1);
@@ -1933,6 +1939,7 @@ cparls_status cparls_destroy(cparls_ctx *c) {
   for (auto &p : c->ev_pending) { cudaEventDestroy(p.second.first); cudaEventDestroy(p.second.second); }
   for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
   for (void *p : c->allocs) cudaFree(p);
+  if (c->hscr) cudaFreeHost(c->hscr);
   for (int b = 0; b < 2; ++b) {
     if (c->stage[b]) cudaFreeHost(c->stage[b]);
     if (c->stage_ev[b]) cudaEventDestroy(c->stage_ev[b]);

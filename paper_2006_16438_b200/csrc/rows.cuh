@@ -46,6 +46,39 @@ __device__ __forceinline__ void store_rows(double *__restrict__ dst, int rows, i
   }
 }
 
+// 16-byte variants for an even tile stride S (rows 16-byte aligned; ld is a
+// multiple of 4): one 16-byte shared store / load per 16-byte global access
+__device__ __forceinline__ void stage_rows_v(const double *__restrict__ src, int rows, int ld, double *tile, int S) {
+  const double2 *s2 = reinterpret_cast<const double2 *>(src);
+  const int n2 = rows * ld / 2;
+  const int B = blockDim.x;
+  for (int i0 = threadIdx.x; i0 < n2; i0 += 4 * B) {
+    double2 v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int i = i0 + u * B;
+      v[u] = i < n2 ? __ldg(s2 + i) : make_double2(0.0, 0.0);
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int i = i0 + u * B;
+      if (i < n2) {
+        const int e = 2 * i, row = e / ld, c = e - row * ld;
+        *reinterpret_cast<double2 *>(tile + row * S + c) = v[u];
+      }
+    }
+  }
+}
+
+__device__ __forceinline__ void store_rows_v(double *__restrict__ dst, int rows, int ld, const double *tile, int S) {
+  double2 *d2 = reinterpret_cast<double2 *>(dst);
+  const int n2 = rows * ld / 2;
+  for (int i = threadIdx.x; i < n2; i += blockDim.x) {
+    const int e = 2 * i, row = e / ld, c = e - row * ld;
+    d2[i] = *reinterpret_cast<const double2 *>(tile + row * S + c);
+  }
+}
+
 // ---------------------------------------------------------------- factor Gram
 template <int RMAX>
 __global__ void __launch_bounds__(kRowThreads) k_gram_rows_t(const double *__restrict__ A, int64_t n, int r, int ld,
@@ -78,8 +111,8 @@ __global__ void __launch_bounds__(kRowThreads) k_solve_rows_t(double *__restrict
                                                              double *__restrict__ part,
                                                              unsigned long long *__restrict__ touched,
                                                              int zero_m, const double *__restrict__ fscale) {
-  extern __shared__ double smem[];
-  const int S = ld + 1;
+  extern __shared__ __align__(16) double smem[];
+  const int S = ld + 2;              // even: 16-byte aligned rows, conflict-free 16-byte row accesses
   double *Gi = smem;                 // G^+ with row stride ld (zero padded): 16-byte operand loads
   double *tile = smem + r * ld;
   for (int i = threadIdx.x; i < r * ld; i += blockDim.x) {
@@ -95,7 +128,7 @@ __global__ void __launch_bounds__(kRowThreads) k_solve_rows_t(double *__restrict
     const int64_t base = t * kRowThreads;
     const int rows = (int)min((int64_t)kRowThreads, n - base);
     __syncthreads();
-    stage_rows(M + base * ld, rows, ld, tile, S);
+    stage_rows_v(M + base * ld, rows, ld, tile, S);
     if (zero_m) {   // keep M zero for the next atomic RHS (the bucketed RHS overwrites every row)
       double2 *d2 = reinterpret_cast<double2 *>(M + base * ld);
       for (int i = threadIdx.x; i < rows * ld / 2; i += blockDim.x) d2[i] = make_double2(0.0, 0.0);
@@ -106,12 +139,16 @@ __global__ void __launch_bounds__(kRowThreads) k_solve_rows_t(double *__restrict
       double m[RMAX];
       bool nz = false;
 #pragma unroll
-      for (int c = 0; c < RMAX; ++c) {
-        double v = (c < r) ? x[c] : 0.0;
-        if (fixed && c < r)   // fixed-point RHS: int64 count of 2^-e_c
-          v = (double)__double_as_longlong(v) * fscale[kMaxRank + c];
-        m[c] = v;
-        nz |= (m[c] != 0.0);
+      for (int c = 0; c < RMAX; c += 2) {
+        const double2 v2 = *reinterpret_cast<const double2 *>(x + c);
+        double v0 = (c < r) ? v2.x : 0.0, v1 = (c + 1 < r) ? v2.y : 0.0;
+        if (fixed) {   // fixed-point RHS: int64 count of 2^-e_c
+          if (c < r) v0 = (double)__double_as_longlong(v0) * fscale[kMaxRank + c];
+          if (c + 1 < r) v1 = (double)__double_as_longlong(v1) * fscale[kMaxRank + c + 1];
+        }
+        m[c] = v0;
+        if (c + 1 < RMAX) m[c + 1] = v1;
+        nz |= (v0 != 0.0) | (v1 != 0.0);
       }
       if (nz) {
         ++ntouch;
@@ -128,16 +165,15 @@ __global__ void __launch_bounds__(kRowThreads) k_solve_rows_t(double *__restrict
               s2 += m[p] * g23.x;
               s3 += m[p] * g23.y;
             }
-          x[c] = s0;
-          if (c + 1 < r) x[c + 1] = s1;
-          if (c + 2 < r) x[c + 2] = s2;
-          if (c + 3 < r) x[c + 3] = s3;
+          // columns >= r come out 0 (zero-padded G^+): the padding stays zero
+          *reinterpret_cast<double2 *>(x + c) = make_double2(s0, s1);
+          *reinterpret_cast<double2 *>(x + c + 2) = make_double2(s2, s3);
         }
       }
     }
     __syncthreads();
-    store_rows(B + base * ld, rows, ld, tile, S);
-    sy.accumulate(tile, rows, S, nullptr);
+    store_rows_v(B + base * ld, rows, ld, tile, S);
+    sy.accumulate_v(tile, rows, S);
   }
   unsigned long long nt = warp_sum<unsigned long long>(ntouch);
   if ((threadIdx.x & 31) == 0 && nt) atomicAdd(touched, nt);

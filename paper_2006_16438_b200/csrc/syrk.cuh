@@ -61,6 +61,29 @@ struct Syrk {
     }
   }
 
+  // Unit weights, even S (16-byte aligned rows): the 4+4 operands of a lane's
+  // block as four 16-byte loads per row.
+  __device__ __forceinline__ void accumulate_v(const double *tile, int rows, int S) {
+    const int g = threadIdx.x >> 5;
+#pragma unroll
+    for (int k = 0; k < PER; ++k) {
+      if (bp[k] < 0) continue;
+      const int p0 = 4 * bp[k], q0 = 4 * bq[k];
+      for (int row = g; row < rows; row += kSyrkThreads / 32) {
+        const double *x = tile + row * S;
+        const double2 a01 = *reinterpret_cast<const double2 *>(x + p0);
+        const double2 a23 = *reinterpret_cast<const double2 *>(x + p0 + 2);
+        const double2 b01 = *reinterpret_cast<const double2 *>(x + q0);
+        const double2 b23 = *reinterpret_cast<const double2 *>(x + q0 + 2);
+        const double xp[4] = {a01.x, a01.y, a23.x, a23.y}, xq[4] = {b01.x, b01.y, b23.x, b23.y};
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) acc[k][4 * i + j] += xp[i] * xq[j];
+      }
+    }
+  }
+
   // Warp-private variant: this warp's lanes walk every row of a tile the warp
   // owns (rows [0, rows), stride S); finish() still sums the 8 warps.
   __device__ __forceinline__ void accumulate_warp(const double *tile, int rows, int S) {
