@@ -230,11 +230,28 @@ def oracle_sample(cfg_name, frac, steps, tau):
     tf0 = time.perf_counter(); o.fit(); tfit = time.perf_counter() - tf0
     nfits = steps // ETA
     total = sum(times) + (steps / ETA - nfits) * tfit
-    return {"value": steps / total, "unit": "iterations/s", "cores": 1, "kind": "oracle",
+    return {"value": steps / total, "unit": "iterations/s", "cores": 1, "kind": "oracle", "host": host_info(),
             "sample": f"{steps} outer iteration(s) of the plain-C oracle (1 thread) on the first {nnz} "
                       f"nonzeros ({frac:.4%}) of {cfg_name}'s seeded draw sequence, full dims "
                       f"{cfg.dims}, r={cfg.rank}, s={cfg.s}, tau={'1/s' if tau < 0 else tau}, "
                       f"exact fit amortized 1/{ETA}"}
+
+
+def host_info():
+    """nproc, CPU model and host RAM (SURVEY 8(d) oracle timing)."""
+    info = {"nproc": os.cpu_count()}
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                info["cpu_model"] = line.split(":", 1)[1].strip()
+                break
+        for line in open("/proc/meminfo"):
+            if line.startswith("MemTotal"):
+                info["ram_gb"] = round(int(line.split()[1]) / 2 ** 20, 1)
+                break
+    except OSError:
+        pass
+    return info
 
 
 def run_reference(args):
@@ -346,6 +363,36 @@ def run_ours(args):
     if ws == 1:
         ld_ = (cfg.rank + 3) // 4 * 4
         row_stream = rhs_row_stream(g, cfg, seed, min(max(cfg.dims), (96 << 20) // (ld_ * 8)))
+    # SURVEY 8(d) byte model of the timed region (cparls_stats counters: what
+    # the method must touch, not the traffic) per iteration, against HBM
+    model_bytes = sum(st[k] for k in st if k.startswith("bytes_")) / K
+    iter_roofline = {"bytes_per_iteration": model_bytes, "achieved_GBps": model_bytes / (ms / K / 1e3) / 1e9,
+                     "what": "SURVEY 8(d) algorithmic bytes per outer iteration (sample, Gram, lookup, RHS, "
+                             "solve, leverage, exact fit / eta) over the measured ms per iteration"}
+    # per-iteration CUDA-event times (no fit), mean and median over iterations 2..K
+    per_it = []
+    if ws == 1:
+        for t in range(K):
+            a = torch.cuda.Event(enable_timing=True); b = torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            g.run(1, cfg.s, seed, iter0=args.warmup + t, fit_every=0)
+            b.record(stream)
+            b.synchronize()
+            per_it.append(a.elapsed_time(b))
+    tail = sorted(per_it[1:]) if len(per_it) > 1 else per_it
+    per_iteration = {"mean_ms": sum(tail) / len(tail), "median_ms": tail[len(tail) // 2],
+                     "what": "one outer iteration without the fit, iterations 2..K"} if tail else None
+    # iterations/s with the exact fit every iteration (fit_every = 1)
+    fe1 = None
+    if ws == 1:
+        K1 = min(K, 5)
+        a = torch.cuda.Event(enable_timing=True); b = torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        a.record(stream)
+        g.run(K1, cfg.s, seed, iter0=args.warmup, fit_every=1)
+        b.record(stream)
+        torch.cuda.synchronize()
+        fe1 = {"value": K1 / (a.elapsed_time(b) / 1e3), "unit": "iterations/s", "iterations": K1}
     # secondary: the same K iterations with the paper's estimated fit
     # per epoch instead of the exact one (Alg. 3 as run on Amazon, s_fit = 2^27)
     est = None
@@ -421,6 +468,8 @@ def run_ours(args):
     peaks = measure_peaks(cfg, dev, window_rows, int(sorted(cfg.dims)[len(cfg.dims) // 2]), row_stream)
     del row_stream
     hbm_peak, peak_src = measured_peaks()
+    iter_roofline.update({"peak_GBps": hbm_peak, "frac": iter_roofline["achieved_GBps"] / hbm_peak,
+                          "frac_nominal_8TBps": iter_roofline["achieved_GBps"] / 8000.0})
     # k_rhs: algorithmic work = m_k * r fp64 reductions per launch (SURVEY 8(d):
     # every matched nonzero adds w^2 x z_j to its output row); bytes = matched
     # entries (out + value) + touched output rows read and written once
@@ -525,6 +574,9 @@ def run_ours(args):
         "estimated_fit_variant": est,
         "cp_als_baseline": als,
         "setup": {"generate_s": t_gen, "create_s": t_build, "rrf_init_ms": rrf_ms},
+        "iteration_roofline": iter_roofline,
+        "per_iteration": per_iteration,
+        "fit_every_1": fe1,
         "phases_ms": {k[3:]: st[k] for k in st if k.startswith("ms_")} if args.profile_phases else None,
         "counters": {"last_matched_nnz": st["last_matched_nnz"], "last_s_bar": st["last_s_bar"],
                      "last_attempts": st["last_attempts"], "touched_rows": st["touched_rows"][:D]},
