@@ -530,3 +530,20 @@ def test_rhs_fixed_point_duplicates_and_range(scale):
     T = types.SimpleNamespace(dims=dims, coords=torch.from_numpy(coords[perm].astype(np.int64)),
                               vals=torch.from_numpy(vals[perm]))
     lockstep(T, 4, 2, 64, 5, check_fit=(scale == 1.0), rhs_path=1)
+
+
+@pytest.mark.parametrize("dims,r", [((5, 6, 7, 4, 3), 3), ((3, 4, 3, 5, 2, 4), 2), ((20, 30, 25), 32),
+                                    ((20, 30, 25), 33)])
+def test_higher_order_and_rank_boundaries(dims, r):
+    """D = 5, 6 (DIDX over 4-5 levels, the thread-per-nonzero fit k_fit_thread)
+    and ranks at the 32-lane boundary of k_rhs (r = 32 one lane pass, r = 33
+    the second pass, RMAX 32 -> 64 row kernels): lockstep vs the oracle."""
+    need_gpu()
+    rng = np.random.default_rng(sum(dims) + r)
+    N = int(np.prod(dims))
+    nnz = min(N, 500)
+    lin = rng.choice(N, nnz, replace=False)
+    coords = np.stack(np.unravel_index(lin, dims, order="F"), 1).astype(np.int32)
+    vals = rng.uniform(0.5, 2.0, nnz)
+    T = synth.Tensor(synth.CONFIGS["C1"], dims, torch.from_numpy(coords), torch.from_numpy(vals))
+    lockstep(T, r, 2, 96, 13)
