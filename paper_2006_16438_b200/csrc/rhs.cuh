@@ -2,16 +2,20 @@
 // AMB-14): M(out_e,:) += w_j^2 x_e z_j for every matched nonzero e of every
 // sampled fiber j.
 //
-// Warps walk the concatenated matched entries (fiber after fiber, so z_j and
-// w_j^2 stay in registers across a fiber); lanes = columns, so one entry is one
-// r-wide fp64 reduction into M's row.  Global fp64 `red` (no f64 vector red on
-// sm_100a) bounds this kernel: bench.py measures the ceiling of exactly this
-// pattern (r-lane reds into random rows of an L2-sized window) with
-// libcparls_peaks.so and k_rhs runs at ~97% of it.  (Privatizing the heaviest
-// rows in shared memory was measured and dropped: the top 64 rows hold < 1% of
-// the entries on the Zipf workloads, and the smem cost halved occupancy.)
+// Warps walk the concatenated matched entries (fiber after fiber, so z_j stays
+// in registers across a fiber); lanes = columns, so one entry is one r-wide
+// reduction into M's row: int64 fixed point by default (AMB-35: z_j is
+// pre-scaled by 2^e_c, one rounding per term, order-free sums), fp64 `red`
+// with rhs_path 3 or when the scales are out of range.  The L2's reduction
+// rate bounds this kernel: bench.py measures it for k_rhs's own row stream
+// (cparls_peak_red_idx) and k_rhs runs at ~100% of it.  Entries reach the
+// lanes through a per-warp shared buffer (one 16-byte broadcast load per
+// entry); addresses are one IMAD.WIDE.U32 from a per-lane column base.
+// (Privatizing the heaviest rows in shared memory was measured and dropped:
+// the top 64 rows hold < 1% of the entries on the Zipf workloads, and shared
+// atomics on spread addresses are no faster than L2 reductions.)
 //
-// M (n_k x ld fp64) is far larger than L2 for the big modes, so random reds
+// M (n_k x ld) is far larger than L2 for the big modes, so random reductions
 // would each be a DRAM read-modify-write.  The entries are therefore visited
 // in output-row windows of ~96 MB of M: each fiber is sorted by output row, so
 // its entries inside window w are the sub-range found by k_win_bounds; the
@@ -26,26 +30,47 @@ namespace cparls {
 
 constexpr int kRhsThreads = 256;
 
-__device__ __forceinline__ void red_fixed(double *addr, double v, double sc) {
-  const long long q = __double2ll_rn(v * sc);   // v * 2^e exact; the only rounding is to the integer
-  if (q != 0) atomicAdd(reinterpret_cast<unsigned long long *>(addr), (unsigned long long)q);
+// One matched entry as the warp shares it: w_j^2 x_e, its output row and its
+// sample.  Lanes publish their entries to a per-warp shared buffer once per
+// 32-entry group and every lane reads entry u with one 16-byte broadcast load
+// (three shuffles per entry before).
+struct RhsEnt {
+  double cx;
+  int32_t o;
+  int32_t j;
+};
+
+// FX: int64 fixed point, zs = z * 2^e_c (exact power-of-two scaling), one
+// rounding to the integer per term; else fp64 reductions of cx * z.  The
+// reduction is predicated (no branch per lane); addr already holds the lane's
+// column.
+template <bool FX>
+__device__ __forceinline__ void rhs_red(char *addr, double cx, double zs, unsigned on) {
+  if (FX) {
+    const long long q = __double2ll_rn(cx * zs);
+    asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %2, 0;\n\t@p red.global.add.u64 [%0], %1;\n\t}"
+                 :: "l"(addr), "l"(q), "r"(on) : "memory");
+  } else {
+    const double v = cx * zs;
+    asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %2, 0;\n\t@p red.global.add.f64 [%0], %1;\n\t}"
+                 :: "l"(addr), "d"(v), "r"(on) : "memory");
+  }
 }
 
-template <typename VT, bool HI, bool FIXED>
-__global__ void __launch_bounds__(kRhsThreads) k_rhs(const int64_t *__restrict__ off, const int64_t *__restrict__ lo,
-                                                    const int32_t *__restrict__ seg_j, int64_t nseg,
-                                                    const int64_t *__restrict__ mk_ptr,
-                                                    unsigned long long *__restrict__ work,
-                                                    const int32_t *__restrict__ outidx, const VT *__restrict__ vals,
-                                                    const double *__restrict__ sw2, const double *__restrict__ Z,
-                                                    int r, int ld, double *__restrict__ M, int64_t per_warp,
-                                                    const double *__restrict__ fscale) {
+template <typename VT, bool HI, bool FX>
+__device__ __forceinline__ void rhs_body(const int64_t *__restrict__ off, const int64_t *__restrict__ lo,
+                                         const int32_t *__restrict__ seg_j, int64_t nseg, int64_t mk,
+                                         unsigned long long *__restrict__ work, const int32_t *__restrict__ outidx,
+                                         const VT *__restrict__ vals, const double *__restrict__ sw2,
+                                         const double *__restrict__ Z, int r, int ld, double *__restrict__ M,
+                                         int64_t per_warp, double sc0, double sc1, RhsEnt *we) {
   const int lane = threadIdx.x & 31;
-  const bool fx = FIXED && fscale[2 * kMaxRank] != 0.0;   // else: out-of-range bound, fp64 reductions
-  const double sc0 = FIXED && lane < r ? fscale[lane] : 0.0;
-  const double sc1 = FIXED && HI && lane + 32 < r ? fscale[lane + 32] : 0.0;
-  const int64_t mk = *mk_ptr;
   const uint64_t pstream = l2_evict_first();
+  // row address = lane's column base + out * row bytes (one IMAD.WIDE.U32)
+  char *const Mb0 = reinterpret_cast<char *>(M + lane);
+  char *const Mb1 = reinterpret_cast<char *>(M + lane + 32);
+  const uint32_t rowb = (uint32_t)ld * 8u;
+  const unsigned on0 = lane < r, on1 = HI && lane + 32 < r;
   while (true) {
     int64_t t0 = 0;
     if (lane == 0) t0 = (int64_t)atomicAdd(work, (unsigned long long)per_warp);
@@ -60,66 +85,78 @@ __global__ void __launch_bounds__(kRhsThreads) k_rhs(const int64_t *__restrict__
       else len = half;
     }
     int64_t jcur = a - 1;   // segment of the first entry of the current 32-group
-    int64_t jz = -1;        // sample whose z row is loaded
+    int32_t jz = -1;        // sample whose (scaled) z row is loaded
     double z0 = 0.0, z1 = 0.0;
     for (int64_t t = t0; t < t1; t += 32) {
       const int64_t tt = t + lane;
       const bool valid = tt < t1;
       int64_t jj = jcur;
       while (jj + 1 < nseg && __ldg(off + jj + 1) <= tt) ++jj;
-      int64_t j_l = -1;
-      int32_t o_l = 0;
-      double cx_l = 0.0;     // w_j^2 * x_e
+      RhsEnt me = {0.0, 0, -1};
       if (valid) {
-        j_l = seg_j ? (int64_t)__ldg(seg_j + jj) : jj;
+        me.j = seg_j ? __ldg(seg_j + jj) : (int32_t)jj;
         const int64_t e = __ldg(lo + jj) + (tt - __ldg(off + jj));
-        o_l = ld_stream(outidx + e, pstream);
-        cx_l = __ldg(sw2 + j_l) * (double)ld_stream(vals + e, pstream);
+        me.o = ld_stream(outidx + e, pstream);
+        me.cx = __ldg(sw2 + me.j) * (double)ld_stream(vals + e, pstream);
       }
       const int cnt = (int)min((int64_t)32, t1 - t);
-      const int64_t j0 = __shfl_sync(0xffffffffu, j_l, 0);
-      if (__all_sync(0xffffffffu, !valid || j_l == j0)) {
-        // whole group inside one fiber: one z row for all 32 entries
-        if (j0 != jz) {
-          jz = j0;
-          z0 = lane < r ? __ldg(Z + j0 * ld + lane) : 0.0;
-          if (HI) z1 = lane + 32 < r ? __ldg(Z + j0 * ld + lane + 32) : 0.0;
-        }
+      __syncwarp();   // the previous group's reads of we[] are done
+      *reinterpret_cast<double2 *>(we + lane) =
+          make_double2(me.cx, __longlong_as_double(((long long)me.j << 32) | (uint32_t)me.o));
+      __syncwarp();
+      const int32_t j0 = __shfl_sync(0xffffffffu, me.j, 0);
+      auto load_z = [&](int32_t j) {
+        jz = j;
+        z0 = lane < r ? __ldg(Z + (int64_t)j * ld + lane) * sc0 : 0.0;
+        if (HI) z1 = lane + 32 < r ? __ldg(Z + (int64_t)j * ld + lane + 32) * sc1 : 0.0;
+      };
+      if (__all_sync(0xffffffffu, !valid || me.j == j0)) {
+        // whole group inside one fiber: one z row for all of its entries
+        if (j0 != jz) load_z(j0);
 #pragma unroll 4
         for (int u = 0; u < cnt; ++u) {
-          const int o = __shfl_sync(0xffffffffu, o_l, u);
-          const double cx = __shfl_sync(0xffffffffu, cx_l, u);
-          if (lane < r) {
-            if (fx) red_fixed(M + (int64_t)o * ld + lane, cx * z0, sc0);
-            else atomicAdd(M + (int64_t)o * ld + lane, cx * z0);
-          }
-          if (HI && lane + 32 < r) {
-            if (fx) red_fixed(M + (int64_t)o * ld + lane + 32, cx * z1, sc1);
-            else atomicAdd(M + (int64_t)o * ld + lane + 32, cx * z1);
-          }
+          const double2 ev = *reinterpret_cast<const double2 *>(we + u);
+          const uint64_t rb = (uint64_t)(uint32_t)__double_as_longlong(ev.y) * rowb;
+          rhs_red<FX>(Mb0 + rb, ev.x, z0, on0);
+          if (HI) rhs_red<FX>(Mb1 + rb, ev.x, z1, on1);
         }
       } else {
         for (int u = 0; u < cnt; ++u) {
-          const int o = __shfl_sync(0xffffffffu, o_l, u);
-          const double cx = __shfl_sync(0xffffffffu, cx_l, u);
-          const int64_t ju = __shfl_sync(0xffffffffu, j_l, u);
-          if (ju != jz) {
-            jz = ju;
-            z0 = lane < r ? __ldg(Z + ju * ld + lane) : 0.0;
-            if (HI) z1 = lane + 32 < r ? __ldg(Z + ju * ld + lane + 32) : 0.0;
-          }
-          if (lane < r) {
-            if (fx) red_fixed(M + (int64_t)o * ld + lane, cx * z0, sc0);
-            else atomicAdd(M + (int64_t)o * ld + lane, cx * z0);
-          }
-          if (HI && lane + 32 < r) {
-            if (fx) red_fixed(M + (int64_t)o * ld + lane + 32, cx * z1, sc1);
-            else atomicAdd(M + (int64_t)o * ld + lane + 32, cx * z1);
-          }
+          const double2 ev = *reinterpret_cast<const double2 *>(we + u);
+          const long long bits = __double_as_longlong(ev.y);
+          const int32_t ju = (int32_t)(bits >> 32);
+          if (ju != jz) load_z(ju);
+          const uint64_t rb = (uint64_t)(uint32_t)bits * rowb;
+          rhs_red<FX>(Mb0 + rb, ev.x, z0, on0);
+          if (HI) rhs_red<FX>(Mb1 + rb, ev.x, z1, on1);
         }
       }
       jcur = __shfl_sync(0xffffffffu, jj, 31);
     }
+  }
+}
+
+template <typename VT, bool HI, bool FIXED>
+__global__ void __launch_bounds__(kRhsThreads) k_rhs(const int64_t *__restrict__ off, const int64_t *__restrict__ lo,
+                                                    const int32_t *__restrict__ seg_j, int64_t nseg,
+                                                    const int64_t *__restrict__ mk_ptr,
+                                                    unsigned long long *__restrict__ work,
+                                                    const int32_t *__restrict__ outidx, const VT *__restrict__ vals,
+                                                    const double *__restrict__ sw2, const double *__restrict__ Z,
+                                                    int r, int ld, double *__restrict__ M, int64_t per_warp,
+                                                    const double *__restrict__ fscale) {
+  __shared__ __align__(16) RhsEnt ents[kRhsThreads];
+  RhsEnt *we = ents + (threadIdx.x & ~31);
+  const int lane = threadIdx.x & 31;
+  const int64_t mk = *mk_ptr;
+  // FIXED: the scales' flag (k_fixed_scales) picks the loop once per warp;
+  // an out-of-range bound falls back to fp64 reductions
+  if (FIXED && fscale[2 * kMaxRank] != 0.0) {
+    const double sc0 = lane < r ? fscale[lane] : 0.0;
+    const double sc1 = HI && lane + 32 < r ? fscale[lane + 32] : 0.0;
+    rhs_body<VT, HI, true>(off, lo, seg_j, nseg, mk, work, outidx, vals, sw2, Z, r, ld, M, per_warp, sc0, sc1, we);
+  } else {
+    rhs_body<VT, HI, false>(off, lo, seg_j, nseg, mk, work, outidx, vals, sw2, Z, r, ld, M, per_warp, 1.0, 1.0, we);
   }
 }
 
