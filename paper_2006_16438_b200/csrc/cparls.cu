@@ -424,6 +424,8 @@ void set_attrs_rm() {
 
 void set_kernel_attrs(int r, int ld) {
   max_dyn_smem(k_bkt_accum<4>);
+  max_dyn_smem(k_fit_tma<float, 1>); max_dyn_smem(k_fit_tma<float, 2>); max_dyn_smem(k_fit_tma<float, 3>);
+  max_dyn_smem(k_fit_tma<double, 1>); max_dyn_smem(k_fit_tma<double, 2>); max_dyn_smem(k_fit_tma<double, 3>);
   set_attrs_rm<4>(); set_attrs_rm<8>(); set_attrs_rm<16>(); set_attrs_rm<28>(); set_attrs_rm<32>();
   set_attrs_rm<64>();
   int prep = (int)prep_smem(r);
@@ -1626,7 +1628,28 @@ void fit_launch(cparls_ctx *c, cudaStream_t st, double *const *A, const double *
   fd.fast = N < 9007199254740992.0L;   // keys < 2^53
   int nb = 148 * 4;
   KTimer kt(c, KT_FIT, st);
-  if (fd.d <= 3) {
+  // opt-in (CPARLS_FIT_TMA=1): bulk-copy gathers measured 146 ms against 69 for
+  // k_fit_sub on C4 -- ~18 SM cycles per 224-byte cp.async.bulk (fit_tma.cuh)
+  const bool use_tma = getenv("CPARLS_FIT_TMA") && atoi(getenv("CPARLS_FIT_TMA")) == 1;
+  int optin = 0;
+  CK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, 0));
+  const size_t tma_warp = (size_t)kFtStages * kFtE * std::max(1, fd.d) * c->ld * 8;
+  const int tma_wpb = (int)std::min<size_t>(8, (size_t)(optin - 1024) / tma_warp);
+  if (use_tma && fd.d <= 3 && c->ld > 8 && c->ld <= 32 && tma_wpb >= 2) {
+    // bulk-copy row gathers (fit_tma.cuh), one CTA of tma_wpb warps per SM
+    nb = 148;
+    CK(cudaMemsetAsync(counter, 0, sizeof(unsigned long long), st));
+#define FITT(VT, DM)                                                                                   \
+  k_fit_tma<VT, DM><<<nb, 32 * tma_wpb, tma_warp * tma_wpb, st>>>(c->idx[k].key, c->idx[k].out,       \
+                                                                  (const VT *)c->idx[k].val, c->idx[k].nnz, fd, \
+                                                                  A[k], lam, c->r, c->ld, part, counter)
+    if (c->vf32) {
+      if (fd.d == 1) FITT(float, 1); else if (fd.d == 2) FITT(float, 2); else FITT(float, 3);
+    } else {
+      if (fd.d == 1) FITT(double, 1); else if (fd.d == 2) FITT(double, 2); else FITT(double, 3);
+    }
+#undef FITT
+  } else if (fd.d <= 3) {
     // sub-warp per entry, 4 columns per lane (k_fit_sub)
     nb = 148 * std::max(1, std::min(CPARLS_FIT_MINB, blocks_per_sm));
     CK(cudaMemsetAsync(counter, 0, sizeof(unsigned long long), st));

@@ -894,6 +894,7 @@ __global__ void k_dup_runs(const uint64_t *__restrict__ key, const int32_t *__re
 #include "rhs.cuh"
 #include "rhs_bucket.cuh"
 #include "fit.cuh"
+#include "fit_tma.cuh"
 #include "fitest.cuh"
 #include "als.cuh"
 #include "rrf.cuh"

@@ -547,3 +547,23 @@ def test_higher_order_and_rank_boundaries(dims, r):
     vals = rng.uniform(0.5, 2.0, nnz)
     T = synth.Tensor(synth.CONFIGS["C1"], dims, torch.from_numpy(coords), torch.from_numpy(vals))
     lockstep(T, r, 2, 96, 13)
+
+
+@pytest.mark.parametrize("name", ["C1", "C2"])
+def test_fit_bulk_copy_kernel_matches(name, monkeypatch):
+    """The opt-in bulk-copy fit kernel (fit_tma.cuh, CPARLS_FIT_TMA=1) computes
+    the same fit as the default k_fit_sub (same entry order and arithmetic:
+    bit-identical; the default is checked against the oracle by the lockstep
+    tests)."""
+    need_gpu()
+    T = synth.make(name) if name == "C1" else synth.make(name, device="cuda")
+    if name == "C2":
+        T = synth.Tensor(T.cfg, T.dims, T.coords.cpu(), T.vals.cpu())
+    r = T.cfg.rank
+    g = make_ctx(T, r)
+    g.run(2, 1 << 10, 5, fit_every=0)
+    monkeypatch.setenv("CPARLS_FIT_TMA", "0")
+    f0 = g.fit()
+    monkeypatch.setenv("CPARLS_FIT_TMA", "1")
+    f1 = g.fit()
+    assert f0 == f1
