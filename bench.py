@@ -111,6 +111,13 @@ class Clocks:
 KERNEL_NAMES = {"rhs": "k_rhs", "fit": "k_fit_sub", "solve_rows": "k_solve_rows_t", "lev_rows": "k_lev_rows_w"}
 
 
+def row_ld(r):
+    """Row stride libcparls uses for r columns (cparls_create: r rounded up to 8, r <= 4: 4)."""
+    if os.environ.get("CPARLS_LD_ALIGN") == "4" or r <= 4:
+        return (r + 3) // 4 * 4
+    return (r + 7) // 8 * 8
+
+
 def rhs_fixed_point():
     """k_rhs accumulates in int64 fixed point (rhs_path 0/1, AMB-35) unless
     CPARLS_RHS_FIXED=0 selects the fp64 reductions."""
@@ -148,7 +155,7 @@ def measure_peaks(cfg, dev, window_rows, fit_rows, row_stream=None):
     lib.cparls_peak_gather.restype = C.c_double
     lib.cparls_peak_gather.argtypes = [C.c_void_p, C.c_int64, C.c_int, C.c_int64, C.c_int, C.c_int, C.c_void_p]
     r = cfg.rank
-    ld = (r + 3) // 4 * 4
+    ld = row_ld(r)
     torch.cuda.synchronize()
     M = torch.zeros(window_rows * ld, dtype=torch.float64, device=dev)
     red = lib.cparls_peak_red_f64(M.data_ptr(), window_rows, r, ld, 8192, 148 * 8, 5)
@@ -361,7 +368,7 @@ def run_ours(args):
     # k_rhs's own row stream at the state the timed run left (for its ceiling)
     row_stream = None
     if ws == 1:
-        ld_ = (cfg.rank + 3) // 4 * 4
+        ld_ = row_ld(cfg.rank)
         row_stream = rhs_row_stream(g, cfg, seed, min(max(cfg.dims), (96 << 20) // (ld_ * 8)))
     # SURVEY 8(d) byte model of the timed region (cparls_stats counters: what
     # the method must touch, not the traffic) per iteration, against HBM
@@ -462,7 +469,7 @@ def run_ours(args):
                                  "share_of_step": share[k]} for k in kms}
     dominant = max(share, key=lambda k: share[k])
     # measured ceilings of the hot kernels' access patterns (same GPU, same run)
-    ld = (cfg.rank + 3) // 4 * 4
+    ld = row_ld(cfg.rank)
     window_rows = min(max(cfg.dims), (96 << 20) // (ld * 8))
     row_stream = row_stream.to(dev) if row_stream is not None else None
     peaks = measure_peaks(cfg, dev, window_rows, int(sorted(cfg.dims)[len(cfg.dims) // 2]), row_stream)
