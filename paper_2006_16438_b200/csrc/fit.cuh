@@ -125,6 +125,9 @@ constexpr int kFitChunk = 2048;
 // Resident CTAs per SM the register budget is sized for.  Measured on C4
 // (r = 25): U4/2 CTAs 69.1 ms, U2/3 83.1, U2/4 79.9, U4/3 85.0 (spills), U8/2
 // 75.6; 256-bit row loads (LDG.E.ENL2.256) instead of 2 x 16 B: 71.0.
+#ifndef CPARLS_FIT_LD256
+#define CPARLS_FIT_LD256 1   // one 256-bit load per lane per row (C4: 65.7 -> 64.5 ms with 256-byte rows)
+#endif
 #ifndef CPARLS_FIT_MINB
 #define CPARLS_FIT_MINB 2
 #endif
@@ -227,14 +230,26 @@ __global__ void __launch_bounds__(kFitThreads, CPARLS_FIT_MINB) k_fit_sub(const 
           xv[u] = __shfl_sync(0xffffffffu, x, src);
           const double2 *row = reinterpret_cast<const double2 *>(Ak + (int64_t)ou * ld + c0);
           double2 p0 = make_double2(0.0, 0.0), p1 = make_double2(0.0, 0.0);
+#if CPARLS_FIT_LD256
+          if (ok && colok)
+            asm("ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%4];"
+                : "=d"(p0.x), "=d"(p0.y), "=d"(p1.x), "=d"(p1.y) : "l"(row));
+#else
           if (ok && colok) { p0 = __ldg(row); p1 = __ldg(row + 1); }
+#endif
           av[u][0] = p0.x; av[u][1] = p0.y; av[u][2] = p1.x; av[u][3] = p1.y;
 #pragma unroll
           for (int m = 0; m + 1 < DM; ++m) {
             const uint32_t im = __shfl_sync(0xffffffffu, id[m], src);
             const double2 *hr = reinterpret_cast<const double2 *>(fd.A[m] + (int64_t)im * ld + c0);
             double2 q0 = make_double2(0.0, 0.0), q1 = make_double2(0.0, 0.0);
+#if CPARLS_FIT_LD256
+            if (lead_[u] && colok)
+              asm("ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%4];"
+                  : "=d"(q0.x), "=d"(q0.y), "=d"(q1.x), "=d"(q1.y) : "l"(hr));
+#else
             if (lead_[u] && colok) { q0 = __ldg(hr); q1 = __ldg(hr + 1); }
+#endif
             hv[u][m][0] = q0.x; hv[u][m][1] = q0.y; hv[u][m][2] = q1.x; hv[u][m][3] = q1.y;
           }
           sid[u] = __shfl_sync(0xffffffffu, id[DM - 1], src);
