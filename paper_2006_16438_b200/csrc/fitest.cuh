@@ -135,9 +135,11 @@ __global__ void __launch_bounds__(256) k_fit_est(FitSampleDev fs, int64_t n_nz, 
     double h[4] = {lam4[0], lam4[1], lam4[2], lam4[3]};
     if (valid && colok) {
       for (int m = 0; m < fa.d; ++m) {
-        const double2 *row = reinterpret_cast<const double2 *>(fa.A[m] + (int64_t)fs.idx[m][i] * ld + c0);
-        const double2 p0 = __ldg(row), p1 = __ldg(row + 1);
-        h[0] *= p0.x; h[1] *= p0.y; h[2] *= p1.x; h[3] *= p1.y;
+        double p0x, p0y, p1x, p1y;   // one 256-bit load (rows are 32-byte aligned)
+        asm("ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%4];"
+            : "=d"(p0x), "=d"(p0y), "=d"(p1x), "=d"(p1y)
+            : "l"(fa.A[m] + (int64_t)fs.idx[m][i] * ld + c0));
+        h[0] *= p0x; h[1] *= p0y; h[2] *= p1x; h[3] *= p1y;
       }
     } else {
       h[0] = h[1] = h[2] = h[3] = 0.0;
@@ -182,9 +184,11 @@ __global__ void __launch_bounds__(256) k_fit_est_model(FitSampleDev fs, int64_t 
     double h[4] = {lam4[0], lam4[1], lam4[2], lam4[3]};
     if (valid && colok) {
       for (int m = 0; m < fa.d; ++m) {
-        const double2 *row = reinterpret_cast<const double2 *>(fa.A[m] + (int64_t)fs.idx[m][i] * ld + c0);
-        const double2 p0 = __ldg(row), p1 = __ldg(row + 1);
-        h[0] *= p0.x; h[1] *= p0.y; h[2] *= p1.x; h[3] *= p1.y;
+        double p0x, p0y, p1x, p1y;   // one 256-bit load (rows are 32-byte aligned)
+        asm("ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%4];"
+            : "=d"(p0x), "=d"(p0y), "=d"(p1x), "=d"(p1y)
+            : "l"(fa.A[m] + (int64_t)fs.idx[m][i] * ld + c0));
+        h[0] *= p0x; h[1] *= p0y; h[2] *= p1x; h[3] *= p1y;
       }
     } else {
       h[0] = h[1] = h[2] = h[3] = 0.0;
