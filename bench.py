@@ -108,7 +108,16 @@ class Clocks:
                 "samples": len(sm)}
 
 
-KERNEL_NAMES = {"rhs": "k_rhs", "fit": "k_fit_sub", "solve_rows": "k_solve_rows_t", "lev_rows": "k_lev_rows_w"}
+KERNEL_NAMES = {"rhs": "k_rhs", "fit": "k_fit_sub", "solve_rows": "k_solve_dmma", "lev_rows": "k_lev_rows_w"}
+
+
+def kernel_names(r):
+    """Timer labels (cparls_stats.kernel_ms ids) -> kernel names; the solve
+    runs on FP64 tensor cores (k_solve_dmma) for r in 5..32."""
+    names = dict(KERNEL_NAMES)
+    if not (4 < r <= 32) or os.environ.get("CPARLS_SOLVE_DMMA") == "0":
+        names["solve_rows"] = "k_solve_rows_t"
+    return names
 
 
 def row_ld(r):
@@ -465,7 +474,8 @@ def run_ours(args):
     share = {k: kms[k] / ms for k in kms}
     if st["fits"] == 0 and kn["fit"]:
         share["fit"] = kms["fit"] / kn["fit"] / ETA / (ms / K)
-    kernels = {KERNEL_NAMES[k]: {"launches": int(kn[k]), "avg_ms": (kms[k] / kn[k]) if kn[k] else None,
+    KN = kernel_names(cfg.rank)
+    kernels = {KN[k]: {"launches": int(kn[k]), "avg_ms": (kms[k] / kn[k]) if kn[k] else None,
                                  "share_of_step": share[k]} for k in kms}
     dominant = max(share, key=lambda k: share[k])
     # measured ceilings of the hot kernels' access patterns (same GPU, same run)
@@ -518,8 +528,8 @@ def run_ours(args):
                                      "frac": gather_bytes / fit_avg_s / peaks["gather_bytes_per_s"],
                                      "what": "per-nonzero A_k* row gathers vs measured random-row gather rate"}}
     roofline = dict(rl.get(dominant, rl.get("rhs") or rl.get("fit") or {}))
-    roofline["dominant"] = KERNEL_NAMES[dominant]
-    roofline["others"] = {KERNEL_NAMES[k]: v for k, v in rl.items() if k != dominant}
+    roofline["dominant"] = KN[dominant]
+    roofline["others"] = {KN[k]: v for k, v in rl.items() if k != dominant}
 
     # e2e: public API from pinned host buffers (create + K iterations + fits + factors back)
     e2e = None

@@ -387,6 +387,26 @@ inline int rmax_bucket(int r) { return r <= 4 ? 4 : r <= 8 ? 8 : r <= 16 ? 16 : 
 size_t tile_d(int ld) { return (size_t)kRowThreads * (ld + 1); }
 size_t gram_smem(int r, int ld) { return sizeof(double) * (tile_d(ld) + 64); }
 size_t solve_smem(int r, int ld) { return sizeof(double) * ((size_t)r * ld + (size_t)kRowThreads * (ld + 2) + 64); }
+// B = M G^+ and B^T B block partials: FP64 tensor-core kernel for r in 5..32
+// (ld = 8..32), CUDA-core k_solve_rows_t otherwise or with CPARLS_SOLVE_DMMA=0
+void launch_solve_rows(cparls_ctx *c, double *M, int64_t n, double *B, int64_t grid, int zero_m,
+                       const double *fscale) {
+  const int r = c->r, ld = c->ld;
+  const char *e = getenv("CPARLS_SOLVE_DMMA");
+  const bool dmma = !(e && atoi(e) == 0) && r > 4 && ld <= 32 && ld % 8 == 0;
+  if (dmma) {
+    const size_t sm = sizeof(double) * solve_dmma_smem_d(ld);
+    switch (ld / 8) {
+      case 1: k_solve_dmma<1><<<(unsigned)grid, kRowThreads, sm, c->st>>>(M, n, r, ld, c->sd, B, c->gpart, &c->dv->touched, zero_m, fscale); break;
+      case 2: k_solve_dmma<2><<<(unsigned)grid, kRowThreads, sm, c->st>>>(M, n, r, ld, c->sd, B, c->gpart, &c->dv->touched, zero_m, fscale); break;
+      case 3: k_solve_dmma<3><<<(unsigned)grid, kRowThreads, sm, c->st>>>(M, n, r, ld, c->sd, B, c->gpart, &c->dv->touched, zero_m, fscale); break;
+      default: k_solve_dmma<4><<<(unsigned)grid, kRowThreads, sm, c->st>>>(M, n, r, ld, c->sd, B, c->gpart, &c->dv->touched, zero_m, fscale); break;
+    }
+  } else {
+    RSWITCH(r, k_solve_rows_t<RM><<<(unsigned)grid, kRowThreads, solve_smem(r, ld), c->st>>>(
+                   M, n, r, ld, c->sd, B, c->gpart, &c->dv->touched, zero_m, fscale));
+  }
+}
 size_t krp_smem(int r, int ld) { return sizeof(double) * (tile_d(ld) + kRowThreads + 64); }
 size_t prep_smem(int r) { return sizeof(double) * 4 * (size_t)r * r; }
 size_t warp_tiles_d(int ld) { return (size_t)(kRowThreads / 32) * kWarpRows * warp_tile_stride(ld); }
@@ -424,6 +444,8 @@ void set_attrs_rm() {
 
 void set_kernel_attrs(int r, int ld) {
   max_dyn_smem(k_bkt_accum<4>);
+  max_dyn_smem(k_solve_dmma<1>); max_dyn_smem(k_solve_dmma<2>); max_dyn_smem(k_solve_dmma<3>);
+  max_dyn_smem(k_solve_dmma<4>);
   max_dyn_smem(k_fit_tma<float, 1>); max_dyn_smem(k_fit_tma<float, 2>); max_dyn_smem(k_fit_tma<float, 3>);
   max_dyn_smem(k_fit_tma<double, 1>); max_dyn_smem(k_fit_tma<double, 2>); max_dyn_smem(k_fit_tma<double, 3>);
   set_attrs_rm<4>(); set_attrs_rm<8>(); set_attrs_rm<16>(); set_attrs_rm<28>(); set_attrs_rm<32>();
@@ -1213,8 +1235,7 @@ void solve_impl(cparls_ctx *c, int k, cparls_solve_info *info) {
     }
     CK(cudaMemsetAsync(&c->dv->touched, 0, sizeof(unsigned long long), c->st));
     const int64_t bgrid = row_grid(c, ceil_div(std::max<int64_t>(nown, 1), kRowThreads));
-    RSWITCH(r, k_solve_rows_t<RM><<<(unsigned)bgrid, kRowThreads, solve_smem(r, ld), c->st>>>(
-                   c->M + r0 * ld, nown, r, ld, c->sd, c->A[k] + r0 * ld, c->gpart, &c->dv->touched, 0, nullptr));
+    launch_solve_rows(c, c->M + r0 * ld, nown, c->A[k] + r0 * ld, bgrid, 0, nullptr);
     CK_LAUNCH();
     c->m_dirty = true;   // M holds this mode's rows (no zeroing pass)
     kt.stop();
@@ -1295,9 +1316,7 @@ void solve_impl(cparls_ctx *c, int k, cparls_solve_info *info) {
     const int64_t grid = row_grid(c, ceil_div(std::max<int64_t>(nown, 1), kRowThreads));
     CK(cudaMemsetAsync(&c->dv->touched, 0, sizeof(unsigned long long), c->st));
     KTimer kts(c, KT_SOLVE);
-    RSWITCH(r, k_solve_rows_t<RM><<<(unsigned)grid, kRowThreads, solve_smem(r, ld), c->st>>>(
-                   c->M + r0 * ld, nown, r, ld, c->sd, c->A[k] + r0 * ld, c->gpart, &c->dv->touched, 1,
-                   c->fx_on ? c->fx_scale : nullptr));
+    launch_solve_rows(c, c->M + r0 * ld, nown, c->A[k] + r0 * ld, grid, 1, c->fx_on ? c->fx_scale : nullptr);
     kts.stop();
     CK_LAUNCH();
     k_pairs_reduce<<<pairs_reduce_grid(r), 256, 0, c->st>>>(c->gpart, grid, r, c->sd->BtB);
@@ -1416,8 +1435,7 @@ void als_update_impl(cparls_ctx *c, int k) {
   const int64_t grid = row_grid(c, ceil_div(std::max<int64_t>(nk, 1), kRowThreads));
   CK(cudaMemsetAsync(&c->dv->touched, 0, sizeof(unsigned long long), c->st));
   KTimer kts(c, KT_SOLVE);
-  RSWITCH(r, k_solve_rows_t<RM><<<(unsigned)grid, kRowThreads, solve_smem(r, ld), c->st>>>(
-                 c->M, nk, r, ld, c->sd, c->A[k], c->gpart, &c->dv->touched, 1, nullptr));
+  launch_solve_rows(c, c->M, nk, c->A[k], grid, 1, nullptr);
   kts.stop();
   CK_LAUNCH();
   k_pairs_reduce<<<pairs_reduce_grid(r), 256, 0, c->st>>>(c->gpart, grid, r, c->sd->BtB);

@@ -343,6 +343,130 @@ __global__ void __launch_bounds__(kRowThreads, 2) k_lev_rows_w(double *__restric
   }
 }
 
+// ---------------------------------------------------------------- solve on FP64 tensor cores
+// B = M G^+ and the block partial of B^T B with DMMA (mma.sync m8n8k4 f64)
+// for ld = 8 NT <= 32 (r in 5..32).  k_solve_rows_t streams G^+ operands from
+// shared memory for every row and FMA (ncu: LSU/smem wavefronts ~70%, FP64
+// pipe ~23%); here a warp owns 32-row tiles: per 8-row slab the M fragments
+// are loaded once (fixed-point M converted on load), D = M G^+ takes
+// 2 NT^2 x 4 DMMAs with G^+ fragments read from shared memory, and the SYRK
+// B^T B accumulates the NT(NT+1)/2 upper 8x8 tiles in registers (one DMMA per
+// tile per 4 rows).  Fragment layout (m8n8k4, f64): A[g][t], B[t][g],
+// C[g][2t..2t+1] with g = lane/4, t = lane%4.  Per-warp partials are summed in
+// a fixed order: the result is deterministic.
+__device__ __forceinline__ void dmma_884(double (&c)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(c[0]), "+d"(c[1])
+               : "d"(a), "d"(b));
+}
+
+__host__ __device__ constexpr size_t solve_dmma_smem_d(int LD) {
+  return (size_t)LD * LD + LD + (size_t)(kRowThreads / 32) * kWarpRows * (LD + 2) + 64;
+}
+
+template <int NT>
+__global__ void __launch_bounds__(kRowThreads, 2) k_solve_dmma(double *__restrict__ M, int64_t n, int r, int ld,
+                                                               const SolveDev *__restrict__ sd,
+                                                               double *__restrict__ B, double *__restrict__ part,
+                                                               unsigned long long *__restrict__ touched, int zero_m,
+                                                               const double *__restrict__ fscale) {
+  constexpr int LD = NT * 8, KS = NT * 2, NP = NT * (NT + 1) / 2;
+  constexpr int S = LD + 2;   // even: 16-byte aligned tile rows
+  extern __shared__ __align__(16) double smem[];
+  double *Gs = smem;          // LD x LD, G^+ zero padded
+  double *fs = Gs + LD * LD;  // 2^-e_c (fixed-point RHS) or 1
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, gid = lane >> 2, tig = lane & 3;
+  double *tile = fs + LD + (size_t)w * kWarpRows * S;
+  const bool fixed = fscale != nullptr && fscale[2 * kMaxRank] != 0.0;
+  for (int i = threadIdx.x; i < LD * LD; i += blockDim.x) {
+    const int p = i / LD, c = i - p * LD;
+    Gs[i] = (p < r && c < r) ? sd->Ginv[p * r + c] : 0.0;
+  }
+  for (int i = threadIdx.x; i < LD; i += blockDim.x) fs[i] = (fixed && i < r) ? fscale[kMaxRank + i] : 1.0;
+  __syncthreads();
+  double sacc[NP][2];
+#pragma unroll
+  for (int q = 0; q < NP; ++q) sacc[q][0] = sacc[q][1] = 0.0;
+  unsigned long long ntouch = 0;
+  const int64_t ntiles = ceil_div(n, kWarpRows);
+  const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t t = (int64_t)blockIdx.x * (blockDim.x >> 5) + w; t < ntiles; t += nwarps) {
+    const int64_t base = t * kWarpRows;
+    const int rows = (int)min((int64_t)kWarpRows, n - base);
+    warp_stage(M + base * ld, rows, ld, tile, S, zero_m ? M + base * ld : nullptr);
+    __syncwarp();
+#pragma unroll
+    for (int m = 0; m < 4; ++m) {
+      const int row = m * 8 + gid;
+      double a[KS];
+      bool nzr = false;
+#pragma unroll
+      for (int ks = 0; ks < KS; ++ks) {
+        const int c = ks * 4 + tig;
+        double v = row < rows ? tile[row * S + c] : 0.0;
+        if (fixed) v = (double)__double_as_longlong(v) * fs[c];
+        a[ks] = v;
+        nzr |= (v != 0.0);
+      }
+      unsigned f = nzr;
+      f |= __shfl_xor_sync(0xffffffffu, f, 1);
+      f |= __shfl_xor_sync(0xffffffffu, f, 2);
+      if (tig == 0 && f) ++ntouch;
+      double d[NT][2];
+#pragma unroll
+      for (int nn = 0; nn < NT; ++nn) d[nn][0] = d[nn][1] = 0.0;
+#pragma unroll
+      for (int ks = 0; ks < KS; ++ks)
+#pragma unroll
+        for (int nn = 0; nn < NT; ++nn) dmma_884(d[nn], a[ks], Gs[(ks * 4 + tig) * LD + nn * 8 + gid]);
+      __syncwarp();   // every lane has read its M fragments of this slab
+#pragma unroll
+      for (int nn = 0; nn < NT; ++nn)
+        *reinterpret_cast<double2 *>(tile + row * S + nn * 8 + 2 * tig) = make_double2(d[nn][0], d[nn][1]);
+    }
+    __syncwarp();
+    warp_store(B + base * ld, rows, ld, tile, S);
+    // B^T B over this tile's rows (rows >= `rows` are zero)
+#pragma unroll
+    for (int ks = 0; ks < kWarpRows / 4; ++ks) {
+      const double *xr = tile + (ks * 4 + tig) * S + gid;
+      double v[NT];
+#pragma unroll
+      for (int tq = 0; tq < NT; ++tq) v[tq] = xr[tq * 8];
+      int pi = 0;
+#pragma unroll
+      for (int p = 0; p < NT; ++p)
+#pragma unroll
+        for (int q = p; q < NT; ++q) dmma_884(sacc[pi++], v[p], v[q]);
+    }
+    __syncwarp();
+  }
+  unsigned long long nt = warp_sum<unsigned long long>(ntouch);
+  if (lane == 0 && nt) atomicAdd(touched, nt);
+  __syncthreads();
+  // per-warp partials -> block partial (upper triangle), fixed summation order
+  double *red = smem;   // 8 x LD x LD (fits in the tiles' space)
+  {
+    int pi = 0;
+#pragma unroll
+    for (int p = 0; p < NT; ++p)
+#pragma unroll
+      for (int q = p; q < NT; ++q, ++pi) {
+        double *dst = red + (size_t)w * LD * LD + (p * 8 + gid) * LD + q * 8 + 2 * tig;
+        dst[0] = sacc[pi][0];
+        dst[1] = sacc[pi][1];
+      }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < r * r; i += blockDim.x) {
+    const int p = i / r, q = i - p * r;
+    if (p > q) continue;
+    double sum = 0.0;
+    for (int ww = 0; ww < (int)(blockDim.x >> 5); ++ww) sum += red[(size_t)ww * LD * LD + p * LD + q];
+    part[(int64_t)blockIdx.x * r * r + i] = sum;
+  }
+}
+
 // ---------------------------------------------------------------- KrpSamp + Gram
 // z_j = A_{m_1}(i_1,:) * ... * A_{m_d}(i_d,:) (eq:Zrow P:214, left to right),
 // Z (s_bar x ld, padding zero) and the block partial of sum_j w_j^2 z_j z_j^T.

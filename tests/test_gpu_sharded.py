@@ -93,7 +93,7 @@ def lockstep_sharded(T, rank, P, iters, s, seed):
                 As, ls = sh.get_factor(k)
                 nb = np.linalg.norm(Bg)
                 assert np.linalg.norm(Bs - Bg) <= 1e-11 * max(nb, 1e-300)
-                np.testing.assert_allclose(ls, lg, rtol=1e-12)
+                np.testing.assert_allclose(ls, lg, rtol=1e-11)   # B^T B summation grouping differs by shard
                 np.testing.assert_allclose(sh.get_ptilde(k), g.get_ptilde(k), rtol=1e-10, atol=1e-16)
         fg = g.fit()
         fs = on_shards(P, lambda p: shards[p].fit())
