@@ -113,10 +113,13 @@ KERNEL_NAMES = {"rhs": "k_rhs", "fit": "k_fit_sub", "solve_rows": "k_solve_dmma"
 
 def kernel_names(r):
     """Timer labels (cparls_stats.kernel_ms ids) -> kernel names; the solve
-    runs on FP64 tensor cores (k_solve_dmma) for r in 5..32."""
+    runs on FP64 tensor cores (k_solve_dmma) for r in 5..32, the leverage pass
+    only when CPARLS_LEV_DMMA=1 (k_lev_dmma)."""
     names = dict(KERNEL_NAMES)
     if not (4 < r <= 32) or os.environ.get("CPARLS_SOLVE_DMMA") == "0":
         names["solve_rows"] = "k_solve_rows_t"
+    if 4 < r <= 32 and os.environ.get("CPARLS_LEV_DMMA") == "1":
+        names["lev_rows"] = "k_lev_dmma"
     return names
 
 

@@ -446,6 +446,7 @@ void set_kernel_attrs(int r, int ld) {
   max_dyn_smem(k_bkt_accum<4>);
   max_dyn_smem(k_solve_dmma<1>); max_dyn_smem(k_solve_dmma<2>); max_dyn_smem(k_solve_dmma<3>);
   max_dyn_smem(k_solve_dmma<4>);
+  max_dyn_smem(k_lev_dmma<1>); max_dyn_smem(k_lev_dmma<2>); max_dyn_smem(k_lev_dmma<3>); max_dyn_smem(k_lev_dmma<4>);
   max_dyn_smem(k_fit_tma<float, 1>); max_dyn_smem(k_fit_tma<float, 2>); max_dyn_smem(k_fit_tma<float, 3>);
   max_dyn_smem(k_fit_tma<double, 1>); max_dyn_smem(k_fit_tma<double, 2>); max_dyn_smem(k_fit_tma<double, 3>);
   set_attrs_rm<4>(); set_attrs_rm<8>(); set_attrs_rm<16>(); set_attrs_rm<28>(); set_attrs_rm<32>();
@@ -470,10 +471,29 @@ void lev_rows_and_cdf(cparls_ctx *c, int k, const double *lam) {
     const unsigned g = (unsigned)row_grid(c, ceil_div(n, kWarpRows * (kRowThreads / 32)));
     CK(cudaMemsetAsync(c->tile_u64, 0, sizeof(uint64_t) * nt, c->st));
     KTimer kt(c, KT_LEV);
-    RSWITCH(c->r, k_lev_rows_w<RM><<<g, kRowThreads, lev_w_smem(c->r, c->ld), c->st>>>(
-                      c->A[k], n, c->r, c->ld, lam, c->md[k], c->pt[k], c->C[k],
-                      reinterpret_cast<unsigned long long *>(c->tile_u64), &c->md[k]->alpha,
-                      reinterpret_cast<unsigned long long *>(&c->md[k]->drawable)));
+    // opt-in (CPARLS_LEV_DMMA=1): the DMMA leverage pass measured 0.60 ms per C4
+    // launch against 0.51 for k_lev_rows_w (which skips W's zero lower triangle)
+    const char *e = getenv("CPARLS_LEV_DMMA");
+    const int ld = c->ld;
+    if ((e && atoi(e) == 1) && c->r > 4 && ld <= 32 && ld % 8 == 0) {   // FP64 tensor cores
+      const size_t sm = sizeof(double) * lev_dmma_smem_d(ld);
+      unsigned long long *ts = reinterpret_cast<unsigned long long *>(c->tile_u64);
+      unsigned long long *dr = reinterpret_cast<unsigned long long *>(&c->md[k]->drawable);
+#define LEVD(NT) k_lev_dmma<NT><<<g, kRowThreads, sm, c->st>>>(c->A[k], n, c->r, ld, lam, c->md[k], c->pt[k], \
+                                                              c->C[k], ts, &c->md[k]->alpha, dr)
+      switch (ld / 8) {
+        case 1: LEVD(1); break;
+        case 2: LEVD(2); break;
+        case 3: LEVD(3); break;
+        default: LEVD(4); break;
+      }
+#undef LEVD
+    } else {
+      RSWITCH(c->r, k_lev_rows_w<RM><<<g, kRowThreads, lev_w_smem(c->r, c->ld), c->st>>>(
+                        c->A[k], n, c->r, c->ld, lam, c->md[k], c->pt[k], c->C[k],
+                        reinterpret_cast<unsigned long long *>(c->tile_u64), &c->md[k]->alpha,
+                        reinterpret_cast<unsigned long long *>(&c->md[k]->drawable)));
+    }
     kt.stop();
   }
   CK_LAUNCH();

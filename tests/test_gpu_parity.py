@@ -567,3 +567,20 @@ def test_fit_bulk_copy_kernel_matches(name, monkeypatch):
     monkeypatch.setenv("CPARLS_FIT_TMA", "1")
     f1 = g.fit()
     assert f0 == f1
+
+
+def test_lev_dmma_option_matches(monkeypatch):
+    """The opt-in DMMA leverage pass (CPARLS_LEV_DMMA=1) gives the same
+    leverage scores as k_lev_rows_w to rounding (<= 1e-13 relative)."""
+    need_gpu()
+    T = synth.make("C2", device="cuda")
+    from paper_2006_16438_b200 import Cparls
+    out = {}
+    for flag in ("0", "1"):
+        monkeypatch.setenv("CPARLS_LEV_DMMA", flag)
+        g = Cparls(T.dims, T.coords, T.vals, 25, init_seed=4)
+        g.run(1, 1 << 12, 9, fit_every=0)
+        out[flag] = [g.get_ptilde(m) for m in range(4)] + [g.get_factor(m)[0] for m in range(4)]
+        g.close()
+    for a, b in zip(out["0"], out["1"]):
+        np.testing.assert_allclose(b, a, rtol=1e-13, atol=1e-300)
