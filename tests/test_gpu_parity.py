@@ -571,16 +571,22 @@ def test_fit_bulk_copy_kernel_matches(name, monkeypatch):
 
 def test_lev_dmma_option_matches(monkeypatch):
     """The opt-in DMMA leverage pass (CPARLS_LEV_DMMA=1) gives the same
-    leverage scores as k_lev_rows_w to rounding (<= 1e-13 relative)."""
+    leverage scores as k_lev_rows_w to rounding (<= 1e-13 relative), for the
+    initial factors and for set_factor inputs (ranks 25 and 12)."""
     need_gpu()
     T = synth.make("C2", device="cuda")
     from paper_2006_16438_b200 import Cparls
-    out = {}
-    for flag in ("0", "1"):
-        monkeypatch.setenv("CPARLS_LEV_DMMA", flag)
-        g = Cparls(T.dims, T.coords, T.vals, 25, init_seed=4)
-        g.run(1, 1 << 12, 9, fit_every=0)
-        out[flag] = [g.get_ptilde(m) for m in range(4)] + [g.get_factor(m)[0] for m in range(4)]
-        g.close()
-    for a, b in zip(out["0"], out["1"]):
-        np.testing.assert_allclose(b, a, rtol=1e-13, atol=1e-300)
+    rng = np.random.default_rng(3)
+    for r in (25, 12):
+        A = [rng.standard_normal((n, r)) for n in T.dims]
+        out = {}
+        for flag in ("0", "1"):
+            monkeypatch.setenv("CPARLS_LEV_DMMA", flag)
+            g = Cparls(T.dims, T.coords, T.vals, r, init_seed=4)
+            pts = [g.get_ptilde(m) for m in range(4)]
+            for m in range(4):
+                g.set_factor(m, A[m])
+            out[flag] = pts + [g.get_ptilde(m) for m in range(4)]
+            g.close()
+        for a, b in zip(out["0"], out["1"]):
+            np.testing.assert_allclose(b, a, rtol=1e-13, atol=1e-300)
