@@ -287,7 +287,7 @@ def run_reference(args):
     cb = oracle_sample(args.config, args.sample_frac, steps, args.tau)
     line = {"impl": "reference", "metric": METRIC, "value": cb["value"], "unit": "iterations/s",
             "n_gpus": args.gpus, "steps": steps, "warmup": args.warmup,
-            "ms_per_step": 1000.0 / cb["value"], "higher_is_better": True, "scaling": "weak",
+            "ms_per_step": 1000.0 / cb["value"], "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": args.config, "dims": list(cfg.dims), "rank": cfg.rank, "s": cfg.s,
                        "tau": "1/s" if args.tau < 0 else args.tau, "oracle_sample": cb["sample"]},
