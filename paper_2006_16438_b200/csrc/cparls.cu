@@ -10,6 +10,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <thread>
 #include <cub/device/device_radix_sort.cuh>
 #include <new>
 #include <numeric>
@@ -272,7 +273,19 @@ void rows_to_host(cparls_ctx *c, double *dst, const double *src, int64_t rows, i
     const int b = (int)(i & 1);
     CK(cudaEventSynchronize(c->stage_ev[b]));
     const int64_t r0 = i * per, nr = std::min(per, rows - r0);
-    std::memcpy(dst + r0 * r, c->stage[b], (size_t)nr * pitch_h);
+    // host copy out of the pinned buffer on a few threads (first-touch page
+    // faults of the destination dominate a single-threaded memcpy)
+    char *d = reinterpret_cast<char *>(dst + r0 * r);
+    const char *src_h = static_cast<const char *>(c->stage[b]);
+    const size_t bytes = (size_t)nr * pitch_h;
+    constexpr int kThreads = 8;
+    const size_t part = (bytes + kThreads - 1) / kThreads;
+    std::thread th[kThreads];
+    for (int t = 0; t < kThreads; ++t) {
+      const size_t o = std::min(bytes, (size_t)t * part), len = std::min(bytes, o + part) - o;
+      th[t] = std::thread([=] { if (len) std::memcpy(d + o, src_h + o, len); });
+    }
+    for (auto &x : th) x.join();
   };
   for (int64_t i = 0; i < nch; ++i) {
     const int b = (int)(i & 1);
