@@ -585,27 +585,43 @@ __global__ void __launch_bounds__(kRowThreads) k_krp_gram_t(const uint64_t *__re
     const int64_t base = t * kRowThreads;
     const int rows = (int)min((int64_t)kRowThreads, sbar - base);
     __syncthreads();
-    for (int jj = w; jj < rows; jj += kRowThreads / 32) {
-      const int64_t j = base + jj;
-      uint64_t key = skey[j];
-      double z0 = 1.0, z1 = 1.0;
+    // a warp forms 4 rows per step: their key decodes and factor-row loads
+    // are independent, so 4 gathers per mode are in flight at once
+    constexpr int QR = 4;
+    for (int jj0 = w * QR; jj0 < rows; jj0 += (kRowThreads / 32) * QR) {
+      uint64_t key[QR];
+      double z0[QR], z1[QR];
+#pragma unroll
+      for (int q = 0; q < QR; ++q) {
+        key[q] = jj0 + q < rows ? skey[base + jj0 + q] : 0ull;
+        z0[q] = z1[q] = 1.0;
+      }
       for (int m = 0; m < om.d; ++m) {
-        uint64_t i = key % (uint64_t)om.n[m];
-        key /= (uint64_t)om.n[m];
-        const double *row = om.A[m] + i * ld;
-        if (lane < r) {
-          double a = __ldg(row + lane);
-          z0 = (m == 0) ? a : z0 * a;
+        double a0[QR], a1[QR];
+#pragma unroll
+        for (int q = 0; q < QR; ++q) {
+          const uint64_t i = key[q] % (uint64_t)om.n[m];
+          key[q] /= (uint64_t)om.n[m];
+          const double *row = om.A[m] + i * ld;
+          a0[q] = lane < r ? __ldg(row + lane) : 0.0;
+          a1[q] = lane + 32 < r ? __ldg(row + lane + 32) : 0.0;
         }
-        if (lane + 32 < r) {
-          double a = __ldg(row + lane + 32);
-          z1 = (m == 0) ? a : z1 * a;
+#pragma unroll
+        for (int q = 0; q < QR; ++q) {
+          z0[q] = (m == 0) ? a0[q] : z0[q] * a0[q];
+          z1[q] = (m == 0) ? a1[q] : z1[q] * a1[q];
         }
       }
-      double *x = tile + jj * S;
-      if (lane < ld) x[lane] = lane < r ? z0 : 0.0;
-      if (lane + 32 < ld) x[lane + 32] = lane + 32 < r ? z1 : 0.0;
-      if (lane == 0) wt[jj] = sw2[j];
+#pragma unroll
+      for (int q = 0; q < QR; ++q) {
+        const int jj = jj0 + q;
+        if (jj < rows) {
+          double *x = tile + jj * S;
+          if (lane < ld) x[lane] = lane < r ? z0[q] : 0.0;
+          if (lane + 32 < ld) x[lane + 32] = lane + 32 < r ? z1[q] : 0.0;
+          if (lane == 0) wt[jj] = sw2[base + jj];
+        }
+      }
     }
     __syncthreads();
     store_rows(Z + base * ld, rows, ld, tile, S);
