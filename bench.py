@@ -32,7 +32,7 @@ METRIC = "CP-ARLS-LEV ALS iterations/sec (r=25, s=2^17) and % of HBM roofline"
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="C4")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
