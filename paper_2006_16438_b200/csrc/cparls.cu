@@ -161,6 +161,11 @@ struct cparls_ctx {
   // pinned double buffer for copies into pageable host memory (rows_to_host)
   void *stage[2] = {nullptr, nullptr};
   long long *hscr = nullptr;    // small pinned scratch: async scalar reads folded into later syncs
+  // side stream: the fixed-point scales (k_colabs_part, k_fixed_scales) run
+  // concurrently with the fiber lookup and window bounds of the same step
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  bool fx_pending = false;
   cudaEvent_t stage_ev[2] = {nullptr, nullptr};
   // frozen stratified fit sample (fitest.cuh, AMB-32)
   bool have_fs = false;
@@ -1163,6 +1168,16 @@ void lookup_impl(cparls_ctx *c, int k) {
   c->stats.bytes_lookup += (double)sbar * 16.0;
 }
 
+// per-column fixed-point scales 2^e_c of the sampled RHS (kernels.cuh, AMB-35)
+void launch_fixed_scales(cparls_ctx *c, int64_t sbar, cudaStream_t st) {
+  const int nbc = 148;
+  k_colabs_part<<<nbc, 256, 0, st>>>(c->Z, c->sw2, sbar, c->r, c->ld, c->gpart);
+  CK_LAUNCH();
+  k_fixed_scales<<<1, 64, 0, st>>>(c->gpart, nbc, c->r, &c->dv->maxabs, c->dupmax, c->fx_scale);
+  CK_LAUNCH();
+  LAUNCHED(c, 2);
+}
+
 void solve_impl(cparls_ctx *c, int k, cparls_solve_info *info) {
   if (!c->have_sample || c->smode != k) throw ApiError(CPARLS_ESTATE, "solve_mode without a current sample of this mode");
   const int r = c->r, ld = c->ld;
@@ -1185,6 +1200,15 @@ void solve_impl(cparls_ctx *c, int k, cparls_solve_info *info) {
     }
     c->stats.bytes_gram += (double)sbar * (om.d * r * 8.0 + 16.0);
     ph.end();
+  }
+  // fixed-point scales of the atomic RHS on the side stream, overlapping K7
+  c->fx_pending = false;
+  if (sbar > 0 && c->rhs_fixed && c->opts.rhs_path != 2 && c->opts.rhs_path != 3) {
+    CK(cudaEventRecord(c->ev_fork, c->st));
+    CK(cudaStreamWaitEvent(c->side, c->ev_fork, 0));
+    launch_fixed_scales(c, sbar, c->side);
+    CK(cudaEventRecord(c->ev_join, c->side));
+    c->fx_pending = true;
   }
   // K7: lookup of the sampled fibers
   {
@@ -1313,12 +1337,9 @@ void solve_impl(cparls_ctx *c, int k, cparls_solve_info *info) {
         LAUNCHED(c, 4);
       }
       if (c->fx_on) {   // per-column fixed-point scales from the sample (kernels.cuh)
-        const int nbc = 148;
-        k_colabs_part<<<nbc, 256, 0, c->st>>>(c->Z, c->sw2, sbar, r, ld, c->gpart);
-        CK_LAUNCH();
-        k_fixed_scales<<<1, 64, 0, c->st>>>(c->gpart, nbc, r, &c->dv->maxabs, c->dupmax, c->fx_scale);
-        CK_LAUNCH();
-        LAUNCHED(c, 2);
+        if (c->fx_pending) CK(cudaStreamWaitEvent(c->st, c->ev_join, 0));   // computed on the side stream
+        else launch_fixed_scales(c, sbar, c->st);
+        c->fx_pending = false;
       }
       CK(cudaMemsetAsync(&c->dv->counter, 0, sizeof(unsigned long long), c->st));
       const int grid = 148 * grid_mult;
@@ -1341,6 +1362,10 @@ void solve_impl(cparls_ctx *c, int k, cparls_solve_info *info) {
     ph.end();
   }
   // K9: solve + normalize + leverage refresh
+  if (c->fx_pending) {   // side-stream scales not consumed (no atomic RHS ran): join before gpart is reused
+    CK(cudaStreamWaitEvent(c->st, c->ev_join, 0));
+    c->fx_pending = false;
+  }
   {
     Phase ph(c, &c->stats.ms_solve);
     if (!use_bkt) {
@@ -1862,6 +1887,9 @@ cparls_status cparls_create(cparls_ctx **out, int32_t nmodes, const int64_t *dim
     }
     set_kernel_attrs(c->r, c->ld);
     CK(cudaHostAlloc(reinterpret_cast<void **>(&c->hscr), 64 * sizeof(long long), cudaHostAllocDefault));
+    CK(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));
+    CK(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
     c->dv = dalloc_t<DevScalars>(c, 1);
     CK(cudaMemsetAsync(c->dv, 0, sizeof(DevScalars), c->st));
     c->sd = dalloc_t<SolveDev>(c, 1);
@@ -2022,6 +2050,9 @@ cparls_status cparls_destroy(cparls_ctx *c) {
   for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
   for (void *p : c->allocs) cudaFree(p);
   if (c->hscr) cudaFreeHost(c->hscr);
+  if (c->ev_fork) cudaEventDestroy(c->ev_fork);
+  if (c->ev_join) cudaEventDestroy(c->ev_join);
+  if (c->side) cudaStreamDestroy(c->side);
   for (int b = 0; b < 2; ++b) {
     if (c->stage[b]) cudaFreeHost(c->stage[b]);
     if (c->stage_ev[b]) cudaEventDestroy(c->stage_ev[b]);
