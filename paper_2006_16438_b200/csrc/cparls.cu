@@ -874,6 +874,9 @@ int64_t run_didx(cparls_ctx *c, const OtherModes &om, double tau, int *which) {
   const int d = om.d;
   int64_t ncand[kMaxModes] = {0};
   // candidates per mode (ordered compaction), then stable sort by p~ descending
+  // every mode's candidates first (independent), then one read of all counts
+  // (a sync per mode before)
+  static_assert(kMaxModes <= 32, "candidate counts fit the pinned scratch");
   for (int j = 0; j < d; ++j) {
     const int64_t n = om.n[j];
     const int64_t nb = ceil_div(n, kScanTile);
@@ -884,7 +887,12 @@ int64_t run_didx(cparls_ctx *c, const OtherModes &om, double tau, int *which) {
     k_cand_scatter<<<(unsigned)nb, kScanThreads, 0, c->st>>>(om, j, tau, c->i64part, c->ckey[j], c->cidx[j]);
     CK_LAUNCH();
     LAUNCHED(c, 3);
-    const int64_t nc = read_dev(c, &c->dv->total);
+    CK(cudaMemcpyAsync(c->hscr + 40 + j, &c->dv->total, sizeof(long long), cudaMemcpyDeviceToHost, c->st));
+  }
+  sync(c);
+  for (int j = 0; j < d; ++j) {
+    const int64_t n = om.n[j];
+    const int64_t nc = c->hscr[40 + j];
     if (nc > 1) {
       int res = radix_sort_pairs(c->ckey[j], c->cidx[j], c->ckey_tmp, c->cidx_tmp, nc, 64, c->rhist, c->st,
                                  &c->stats.kernel_launches);
