@@ -129,6 +129,10 @@ struct cparls_ctx {
   unsigned long long *hkey = nullptr;
   uint32_t *hcnt = nullptr;
   double *hp = nullptr;
+  uint32_t *hfirst = nullptr;   // first draw index per hash slot (deterministic combine)
+  uint32_t *rslot = nullptr;    // per random draw: its slot
+  int64_t *rflag = nullptr, *rpos = nullptr;
+  bool sample_sort = getenv("CPARLS_SAMPLE_SORT") && atoi(getenv("CPARLS_SAMPLE_SORT")) == 1;
   uint64_t hsize = 0;
   // bookkeeping
   std::vector<void *> allocs;
@@ -816,7 +820,8 @@ void alloc_sample_buffers(cparls_ctx *c, int64_t s) {
   for (void *p : {(void *)c->skey, (void *)c->sw2, (void *)c->sp, (void *)c->scnt, (void *)c->sisdet, (void *)c->Z,
                   (void *)c->lo, (void *)c->len, (void *)c->off, (void *)c->rkey, (void *)c->rp, (void *)c->hkey,
                   (void *)c->hcnt, (void *)c->hp, (void *)c->skey2, (void *)c->sw2_2, (void *)c->sp2,
-                  (void *)c->scnt2, (void *)c->sisdet2, (void *)c->sperm, (void *)c->sperm2, (void *)c->shist})
+                  (void *)c->scnt2, (void *)c->sisdet2, (void *)c->sperm, (void *)c->sperm2, (void *)c->shist,
+                  (void *)c->hfirst, (void *)c->rslot, (void *)c->rflag, (void *)c->rpos})
     dfree(c, p);
   c->skey = dalloc_t<uint64_t>(c, cap);
   c->sw2 = dalloc_t<double>(c, cap);
@@ -843,6 +848,11 @@ void alloc_sample_buffers(cparls_ctx *c, int64_t s) {
   c->hkey = dalloc_t<unsigned long long>(c, (int64_t)hs);
   c->hcnt = dalloc_t<uint32_t>(c, (int64_t)hs);
   c->hp = dalloc_t<double>(c, (int64_t)hs);
+  c->hfirst = dalloc_t<uint32_t>(c, (int64_t)hs);
+  CK(cudaMemsetAsync(c->hfirst, 0xFF, sizeof(uint32_t) * hs, c->st));
+  c->rslot = dalloc_t<uint32_t>(c, cap);
+  c->rflag = dalloc_t<int64_t>(c, cap);
+  c->rpos = dalloc_t<int64_t>(c, cap);
   CK(cudaMemsetAsync(c->hkey, 0xFF, sizeof(unsigned long long) * hs, c->st));
   CK(cudaMemsetAsync(c->hcnt, 0, sizeof(uint32_t) * hs, c->st));
   int64_t part_need = ceil_div(cap, kScanTile) + 16;
@@ -1099,22 +1109,26 @@ void sample_impl(cparls_ctx *c, int k, int64_t s, uint64_t seed, uint64_t step, 
   // ---- CIDX (combine repeats)
   int64_t nuniq = 0;
   if (have > 0) {
-    CK(cudaMemsetAsync(&c->dv->counter, 0, sizeof(unsigned long long), c->st));
-    k_cidx_insert<<<(unsigned)ceil_div(have, 256), 256, 0, c->st>>>(c->rkey, c->rp, have, c->hkey, c->hcnt, c->hp,
-                                                                    c->hsize - 1);
+    // deterministic combine: unique rows in first-draw order (AMB-35)
+    const unsigned gb = (unsigned)ceil_div(have, 256);
+    k_cidx_insert_first<<<gb, 256, 0, c->st>>>(c->rkey, c->rp, have, c->hkey, c->hcnt, c->hp, c->hfirst,
+                                               c->hsize - 1);
     CK_LAUNCH();
-    k_cidx_emit<<<(unsigned)ceil_div((int64_t)c->hsize, 256), 256, 0, c->st>>>(
-        c->hkey, c->hcnt, c->hp, c->hsize, &c->dv->pdet, s_rnd, sdet, &c->dv->counter, c->skey, c->sw2, c->sp,
-        c->scnt, c->sisdet);
+    k_cidx_first_flags<<<gb, 256, 0, c->st>>>(c->rkey, have, c->hkey, c->hfirst, c->hsize - 1, c->rflag, c->rslot);
     CK_LAUNCH();
-    LAUNCHED(c, 2);
-    nuniq = (int64_t)read_dev(c, &c->dv->counter);
+    exclusive_scan_i64(c->rflag, c->rpos, have, c->i64part, &c->dv->total, c->st);
+    k_cidx_emit_first<<<gb, 256, 0, c->st>>>(c->rflag, c->rpos, c->rslot, have, c->hkey, c->hcnt, c->hp,
+                                             c->hfirst, &c->dv->pdet, s_rnd, sdet, c->skey, c->sw2, c->sp,
+                                             c->scnt, c->sisdet);
+    CK_LAUNCH();
+    LAUNCHED(c, 6);
+    nuniq = (int64_t)read_dev(c, &c->dv->total);
   }
-  // canonical order: the DIDX list and the CIDX hash emit in an order that
-  // depends on thread timing; sorting by the (unique) key makes Z, the sampled
-  // Gram and the solve bit-reproducible (AMB-35) and walks the factor rows and
-  // the fiber directory in key order
-  if (sdet + nuniq > 1) {
+  // The device order is already deterministic (DIDX list order, then the
+  // random rows in first-draw order), so Z, the sampled Gram and the solve are
+  // bit-reproducible (AMB-35).  CPARLS_SAMPLE_SORT=1 additionally sorts the
+  // sample by key (walks factor rows and the fiber directory in key order).
+  if (c->sample_sort && sdet + nuniq > 1) {
     const int64_t n = sdet + nuniq;
     int end_bit = 0;
     {

@@ -540,6 +540,67 @@ __global__ void k_cidx_emit(unsigned long long *__restrict__ hkey, uint32_t *__r
   hcnt[h] = 0;
 }
 
+// Deterministic combine (AMB-35): the unique random rows are emitted in the
+// order of their first draw (attempt order, itself deterministic) instead of
+// hash-slot order via an atomic counter.  insert also keeps the first draw
+// index per slot; flags marks each key's first draw (and its slot); an
+// exclusive scan of the flags gives the output positions.
+__global__ void k_cidx_insert_first(const uint64_t *__restrict__ rkey, const double *__restrict__ rp, int64_t n,
+                                    unsigned long long *__restrict__ hkey, uint32_t *__restrict__ hcnt,
+                                    double *__restrict__ hp, uint32_t *__restrict__ hfirst, uint64_t hmask) {
+  int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n) return;
+  uint64_t k = rkey[t];
+  uint64_t h = mix64(k) & hmask;
+  while (true) {
+    unsigned long long prev = atomicCAS(&hkey[h], kEmptyKey, (unsigned long long)k);
+    if (prev == kEmptyKey || prev == k) {
+      atomicAdd(&hcnt[h], 1u);
+      atomicMin(&hfirst[h], (uint32_t)t);
+      if (prev == kEmptyKey) hp[h] = rp[t];   // p depends only on the key
+      return;
+    }
+    h = (h + 1) & hmask;
+  }
+}
+
+__global__ void k_cidx_first_flags(const uint64_t *__restrict__ rkey, int64_t n,
+                                   const unsigned long long *__restrict__ hkey,
+                                   const uint32_t *__restrict__ hfirst, uint64_t hmask,
+                                   int64_t *__restrict__ flag, uint32_t *__restrict__ slot) {
+  int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n) return;
+  const uint64_t k = rkey[t];
+  uint64_t h = mix64(k) & hmask;
+  while (hkey[h] != k) h = (h + 1) & hmask;
+  slot[t] = (uint32_t)h;
+  flag[t] = hfirst[h] == (uint32_t)t ? 1 : 0;
+}
+
+// w^2 = c (1 - p_det) / (s_rnd p)  (P:537 with s -> s_rnd, AMB-3); resets the slot
+__global__ void k_cidx_emit_first(const int64_t *__restrict__ flag, const int64_t *__restrict__ pos,
+                                  const uint32_t *__restrict__ slot, int64_t n,
+                                  unsigned long long *__restrict__ hkey, uint32_t *__restrict__ hcnt,
+                                  const double *__restrict__ hp, uint32_t *__restrict__ hfirst,
+                                  const double *__restrict__ pdet_ptr, int64_t s_rnd, int64_t base,
+                                  uint64_t *__restrict__ skey, double *__restrict__ sw2, double *__restrict__ sp,
+                                  int32_t *__restrict__ scnt, uint8_t *__restrict__ sdet) {
+  int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n || !flag[t]) return;
+  const uint32_t h = slot[t];
+  const uint32_t c = hcnt[h];
+  const double p = hp[h];
+  const int64_t o = base + pos[t];
+  skey[o] = hkey[h];
+  scnt[o] = (int32_t)c;
+  sp[o] = p;
+  sw2[o] = ((double)c * (1.0 - *pdet_ptr)) / ((double)s_rnd * p);
+  sdet[o] = 0;
+  hkey[h] = kEmptyKey;   // reset for the next sample
+  hcnt[h] = 0;
+  hfirst[h] = 0xFFFFFFFFu;
+}
+
 // ======================================================================
 // K7 TnsrSamp lookup: equal_range of each sampled key in the
 // mode-k sorted keys, narrowed by the top-level directory.
