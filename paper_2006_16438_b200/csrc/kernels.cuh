@@ -216,15 +216,27 @@ __global__ void __launch_bounds__(kLevThreads) k_cdf_final(uint64_t *__restrict_
   if (i < n) C[i] = tile_off[blockIdx.x] + ex + q;
 }
 
-// exclusive scan of u64 tile sums (single block)
+// exclusive scan of u64 tile sums (single block): each thread scans
+// kScanItems consecutive entries serially, one block scan per 2048 (integer
+// adds: the result does not depend on the grouping)
 __global__ void k_scan_u64_single(uint64_t *part, int64_t nb) {
   unsigned long long carry = 0;
-  for (int64_t base = 0; base < nb; base += kScanThreads) {
-    int64_t idx = base + threadIdx.x;
-    unsigned long long v = idx < nb ? part[idx] : 0ull;
+  for (int64_t base = 0; base < nb; base += kScanTile) {
+    const int64_t b0 = base + (int64_t)threadIdx.x * kScanItems;
+    unsigned long long v[kScanItems];
+    unsigned long long sum = 0;
+#pragma unroll
+    for (int i = 0; i < kScanItems; ++i) {
+      v[i] = b0 + i < nb ? part[b0 + i] : 0ull;
+      sum += v[i];
+    }
     unsigned long long tot;
-    unsigned long long ex = block_excl_scan<unsigned long long>(v, &tot);
-    if (idx < nb) part[idx] = carry + ex;
+    unsigned long long ex = carry + block_excl_scan<unsigned long long>(sum, &tot);
+#pragma unroll
+    for (int i = 0; i < kScanItems; ++i) {
+      if (b0 + i < nb) part[b0 + i] = ex;
+      ex += v[i];
+    }
     carry += tot;
     __syncthreads();
   }
