@@ -16,8 +16,12 @@
  *    cparls_create / cparls_set_factor may be host or device pointers (detected
  *    with cudaPointerGetAttributes) and may be freed on return.  Output
  *    buffers are caller-owned HOST pointers unless stated otherwise.
- *  - Stream: all device work is issued on opts.stream (a cudaStream_t, e.g.
+ *  - Stream: all device work is ordered on opts.stream (a cudaStream_t, e.g.
  *    torch.cuda.current_stream().cuda_stream); NULL = legacy default stream.
+ *    Within a call, small independent kernels may run on a context-owned side
+ *    stream that forks from and joins back into opts.stream via events.
+ *  - Determinism: with the default fixed-point RHS (rhs_path 0/1) repeated
+ *    runs with the same inputs, seed and steps give bit-identical factors.
  *  - Modes are 0-based; "other modes" of mode k are m_1 < ... < m_d (d = D-1).
  *  - Row-major factors: A_k is n_k x r, element (i,c) at A[i*r + c].
  *  - Multi-GPU is SPMD (world_size > 1): every rank passes its own chunk of the
