@@ -170,6 +170,7 @@ struct cparls_ctx {
   cudaStream_t side = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   bool fx_pending = false;
+  int stats_pending_k = -1;     // a solve's m_k / touched rows copied to hscr[48..49], folded at the next sync
   cudaEvent_t stage_ev[2] = {nullptr, nullptr};
   // frozen stratified fit sample (fitest.cuh, AMB-32)
   bool have_fs = false;
@@ -246,7 +247,22 @@ bool is_device_ptr(const void *p) {
   return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
 }
 
-void sync(cparls_ctx *c) { CK(cudaStreamSynchronize(c->st)); }
+void fold_step_stats(cparls_ctx *c, int k, int64_t mk, unsigned long long touched) {
+  c->mk = mk;
+  c->stats.bytes_rhs += (double)mk * (4.0 + (c->vf32 ? 4.0 : 8.0)) + (double)touched * c->r * 8.0 * 2;
+  c->stats.last_matched_nnz = mk;
+  c->stats.sum_matched_nnz += mk;
+  c->stats.touched_rows[k] = (int64_t)touched;
+}
+
+void sync(cparls_ctx *c) {
+  CK(cudaStreamSynchronize(c->st));
+  if (c->stats_pending_k >= 0) {   // a solve without an info request left its counters here
+    const int k = c->stats_pending_k;
+    c->stats_pending_k = -1;
+    fold_step_stats(c, k, (int64_t)c->hscr[48], (unsigned long long)c->hscr[49]);
+  }
+}
 
 bool is_pinned_host(const void *p) {
   cudaPointerAttributes a;
@@ -1418,27 +1434,21 @@ void solve_impl(cparls_ctx *c, int k, cparls_solve_info *info) {
     c->stats.bytes_solve += (double)nk * r * 8.0 * 3;
     ph.end();
   }
-  // info (one sync)
-  struct {
-    int64_t mk;
-    unsigned long long touched;
-  } hv;
+  // step counters: into pinned scratch; with an info request read now (one
+  // sync), otherwise folded into the stats at the next sync (no sync here)
   if (c->world > 1) c->comm->allreduce_u64(reinterpret_cast<unsigned long long *>(&c->dv->mk), 1, c->st);
-  CK(cudaMemcpyAsync(&hv.mk, &c->dv->mk, sizeof(long long), cudaMemcpyDeviceToHost, c->st));
-  CK(cudaMemcpyAsync(&hv.touched, &c->dv->touched, sizeof(unsigned long long), cudaMemcpyDeviceToHost, c->st));
-  int ru = 0, fb = 0;
-  CK(cudaMemcpyAsync(&ru, &c->sd->rank_used, sizeof(int), cudaMemcpyDeviceToHost, c->st));
-  CK(cudaMemcpyAsync(&fb, &c->sd->chol_fallback, sizeof(int), cudaMemcpyDeviceToHost, c->st));
-  sync(c);
-  c->mk = hv.mk;
-  c->stats.bytes_rhs += (double)hv.mk * (4.0 + (c->vf32 ? 4.0 : 8.0)) + (double)hv.touched * r * 8.0 * 2;
-  c->stats.last_matched_nnz = hv.mk;
-  c->stats.sum_matched_nnz += hv.mk;
-  c->stats.touched_rows[k] = (int64_t)hv.touched;
+  if (c->stats_pending_k >= 0) sync(c);   // (cannot happen inside run: sampling syncs first)
+  CK(cudaMemcpyAsync(c->hscr + 48, &c->dv->mk, sizeof(long long), cudaMemcpyDeviceToHost, c->st));
+  CK(cudaMemcpyAsync(c->hscr + 49, &c->dv->touched, sizeof(unsigned long long), cudaMemcpyDeviceToHost, c->st));
+  c->stats_pending_k = k;
   c->stats.mode_steps++;
   if (info) {
-    info->matched_nnz = hv.mk;
-    info->touched_rows = (int64_t)hv.touched;
+    int ru = 0, fb = 0;
+    CK(cudaMemcpyAsync(&ru, &c->sd->rank_used, sizeof(int), cudaMemcpyDeviceToHost, c->st));
+    CK(cudaMemcpyAsync(&fb, &c->sd->chol_fallback, sizeof(int), cudaMemcpyDeviceToHost, c->st));
+    sync(c);   // folds the counters
+    info->matched_nnz = c->stats.last_matched_nnz;
+    info->touched_rows = c->stats.touched_rows[k];
     info->rank_used = ru;
     info->chol_fallback = fb;
   }
@@ -2502,6 +2512,7 @@ cparls_status cparls_owned_rows(const cparls_ctx *c, int32_t mode, int64_t *lo, 
 cparls_status cparls_get_stats(cparls_ctx *c, cparls_stats *s) {
   if (!c || !s) return CPARLS_EINVAL;
   return guarded(c, [&] {
+    sync(c);   // folds a pending step's counters
     ktimers_resolve(c);
     *s = c->stats;
   });
@@ -2510,6 +2521,7 @@ cparls_status cparls_get_stats(cparls_ctx *c, cparls_stats *s) {
 cparls_status cparls_reset_stats(cparls_ctx *c) {
   if (!c) return CPARLS_EINVAL;
   return guarded(c, [&] {
+    sync(c);   // a pending step's counters belong to the old stats
     ktimers_resolve(c);
     c->stats = cparls_stats{};
   });
