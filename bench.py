@@ -113,27 +113,16 @@ KERNEL_NAMES = {"rhs": "k_rhs", "fit": "k_fit_sub", "solve_rows": "k_solve_dmma"
 
 def kernel_names(r):
     """Timer labels (cparls_stats.kernel_ms ids) -> kernel names; the solve
-    runs on FP64 tensor cores (k_solve_dmma) for r in 5..32, the leverage pass
-    only when CPARLS_LEV_DMMA=1 (k_lev_dmma)."""
+    runs on FP64 tensor cores (k_solve_dmma) for r in 5..32."""
     names = dict(KERNEL_NAMES)
-    if not (4 < r <= 32) or os.environ.get("CPARLS_SOLVE_DMMA") == "0":
+    if not (4 < r <= 32):
         names["solve_rows"] = "k_solve_rows_t"
-    if 4 < r <= 32 and os.environ.get("CPARLS_LEV_DMMA") == "1":
-        names["lev_rows"] = "k_lev_dmma"
     return names
 
 
 def row_ld(r):
     """Row stride libcparls uses for r columns (cparls_create: r rounded up to 8, r <= 4: 4)."""
-    if os.environ.get("CPARLS_LD_ALIGN") == "4" or r <= 4:
-        return (r + 3) // 4 * 4
-    return (r + 7) // 8 * 8
-
-
-def rhs_fixed_point():
-    """k_rhs accumulates in int64 fixed point (rhs_path 0/1, AMB-35) unless
-    CPARLS_RHS_FIXED=0 selects the fp64 reductions."""
-    return os.environ.get("CPARLS_RHS_FIXED", "1") != "0"
+    return (r + 3) // 4 * 4 if r <= 4 else (r + 7) // 8 * 8
 
 
 def rhs_row_stream(g, cfg, seed, window_rows, per_mode=1 << 25):
@@ -487,13 +476,13 @@ def run_ours(args):
     kernels = {KN[k]: {"launches": int(kn[k]), "avg_ms": (kms[k] / kn[k]) if kn[k] else None,
                                  "share_of_step": share[k]} for k in kms}
     dominant = max(share, key=lambda k: share[k])
-    # measured ceilings of the hot kernels' access patterns (same GPU, same run)
     ld = row_ld(cfg.rank)
     window_rows = min(max(cfg.dims), (96 << 20) // (ld * 8))
+    hbm_peak, peak_src = measured_peaks()
+    # measured ceilings of the hot kernels' access patterns (same GPU, same run)
     row_stream = row_stream.to(dev) if row_stream is not None else None
     peaks = measure_peaks(cfg, dev, window_rows, int(sorted(cfg.dims)[len(cfg.dims) // 2]), row_stream)
     del row_stream
-    hbm_peak, peak_src = measured_peaks()
     iter_roofline.update({"peak_GBps": hbm_peak, "frac": iter_roofline["achieved_GBps"] / hbm_peak,
                           "frac_nominal_8TBps": iter_roofline["achieved_GBps"] / 8000.0})
     # k_rhs: algorithmic work = m_k * r fp64 reductions per launch (SURVEY 8(d):
@@ -509,22 +498,22 @@ def run_ours(args):
     fit_avg_s = (kms["fit"] / max(1, kn["fit"])) / 1000.0 if kn["fit"] else None
     rl = {}
     if rhs_avg_s:
-        fx = rhs_fixed_point()
-        kind = "u64" if fx else "f64"
-        pk = peaks[f"red_stream_{kind}_lane_ops_per_s"] or peaks[f"red_{kind}_lane_ops_per_s"]
-        rl["rhs"] = {"bound": "l2_atomic", "kernel": "k_rhs (sampled RHS, P:949-958)",
-                     "achieved": rhs_red / rhs_avg_s / 1e9, "peak": pk / 1e9,
-                     "unit": f"G {'int64 fixed-point' if fx else 'fp64'} reductions/s",
-                     "frac": (rhs_red / rhs_avg_s) / pk,
-                     "traffic": traffic_for("k_rhs", args.config),
-                     "peak_source": f"measured here: cparls_peak_red_idx, r-lane {kind} red (nothing else) into the "
-                                    f"rows of {peaks['red_stream_len']} matched fiber entries of fresh samples (every "
-                                    f"mode) that fall in the first {window_rows}-row output window (the k_rhs "
-                                    f"row stream; "
-                                    f"uniform-row rate {peaks[f'red_{kind}_lane_ops_per_s'] / 1e9:.0f} G/s)",
-                     "alg_bytes_per_launch": rhs_bytes, "avg_launch_ms": rhs_avg_s * 1e3,
-                     "hbm_view": {"achieved": rhs_bytes / rhs_avg_s / 1e9, "peak": hbm_peak, "unit": "GB/s",
-                                  "frac": rhs_bytes / rhs_avg_s / 1e9 / hbm_peak}}
+        pk = peaks["red_stream_u64_lane_ops_per_s"] or peaks["red_u64_lane_ops_per_s"]
+        rl["rhs"] = {"bound": "hbm", "kernel": "k_rhs (sampled RHS, P:949-958)",
+                     "achieved": rhs_bytes / rhs_avg_s / 1e9, "peak": hbm_peak, "unit": "GB/s",
+                     "frac": rhs_bytes / rhs_avg_s / 1e9 / hbm_peak,
+                     "traffic": traffic_for("k_rhs", args.config), "alg_bytes_per_launch": rhs_bytes,
+                     "avg_launch_ms": rhs_avg_s * 1e3, "peak_source": peak_src,
+                     "alg_bytes_what": "SURVEY 8(d): matched entries m_k*(4+v) + the output rows of M read and "
+                                       "written once (n_k*r*16), per launch",
+                     "l2_reduction_view": {
+                         "achieved": rhs_red / rhs_avg_s / 1e9, "peak": pk / 1e9,
+                         "unit": "G int64 fixed-point reductions/s", "frac": (rhs_red / rhs_avg_s) / pk,
+                         "peak_source": f"measured here: cparls_peak_red_idx, r-lane u64 red (nothing else) "
+                                        f"into the rows of {peaks['red_stream_len']} matched fiber entries of "
+                                        f"fresh samples in the first {window_rows}-row output window",
+                         "what": "the kernel's binding ceiling: r-lane L2 reductions issued vs the rate the "
+                                 "SM->L2 write path retires them (DESIGN.md section 8)"}}
     if fit_avg_s:
         gather_bytes = nnz * ld * 8.0     # one A_{k*} row per nonzero (the per-entry gather)
         rl["fit"] = {"bound": "hbm", "kernel": "k_fit_sub (exact fit, P:867-875)",
@@ -594,6 +583,7 @@ def run_ours(args):
         "peaks_measured": peaks,
         "clocks": clk.summary(),
         "gpu_launches": int(st["kernel_launches"]),
+        "host_syncs_in_timed_region": int(st["host_syncs"]),
         "e2e": e2e,
         "cpu_baseline": cpu,
         "fit": final_fit,

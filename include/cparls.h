@@ -53,7 +53,13 @@ typedef enum {
   CPARLS_ESTATE = 8    /* call order violated (e.g. solve_mode without sample)      */
 } cparls_status;
 
+/* Options of cparls_create.  ABI versioning: struct_size is the caller's
+ * sizeof(cparls_opts); the library reads only the fields that fit in it and
+ * takes the documented default (0 / NULL) for every later field, so fields
+ * are only ever appended.  cparls_opts_init fills the defaults and
+ * struct_size.  struct_size 0 or smaller than the first four fields: EINVAL. */
 typedef struct {
+  uint32_t struct_size;    /* sizeof(cparls_opts) as compiled by the caller              */
   int32_t rank;            /* r, 1 <= r <= 64                                         */
   double tau;              /* deterministic threshold tau: > 0 literal; 1 =
                               pure random; < 0 = 1/s at sample time  */
@@ -74,13 +80,28 @@ typedef struct {
                               (rhs_bucket.cuh; needs r <= 32, s_bar < 2^27,
                               m_k < 2^32), 3 fp64 reductions into M (rhs.cuh; order
                               of the additions not fixed).  Same math; B = M G^+
-                              follows in k_solve_rows_t.  Other values: EINVAL.     */
+                              follows in the solve.  Other values: EINVAL.           */
   int64_t fit_samples;     /* s_fit > 0: draw the stratified fit sample at create
                               (sec:estimating-fit, AMB-32); 0 = none.
                               Single GPU only (EINVAL with world_size > 1).          */
   double fit_alpha;        /* nonzero fraction alpha of the sample (<= 0 -> 0.5)     */
   uint64_t fit_seed;       /* Philox key of the fit sample                           */
+  int64_t sidx_window;     /* > 0: at most this many SIDX attempts are drawn per
+                              window (AMB-8: the result does not depend on it; small
+                              values exercise the multi-window continuation);
+                              0 = sized from the expected attempt count             */
+  int32_t sample_sort;     /* 1: order the combined sample by key before the solve
+                              (the fibers are then walked in key order; same
+                              sample set and weights); 0 = deterministic device
+                              order (DIDX list, then random rows by first draw)     */
+  int32_t fit_mode;        /* mode whose sorted copy the exact fit streams: -1 or any
+                              value outside [0, D) = automatic (fewest gathers); the
+                              fit does not depend on it beyond rounding            */
 } cparls_opts;
+
+/* Fill *opts with the defaults (tau = -1, rank = 1, world_size = 1, fit_mode = -1,
+ * everything else 0/NULL) and struct_size = sizeof(cparls_opts). */
+void cparls_opts_init(cparls_opts *opts);
 
 typedef struct {
   int64_t s_det;     /* |DetSet|                                          */
@@ -99,8 +120,13 @@ typedef struct {
 } cparls_solve_info;
 
 /* Per-phase device times (ms, accumulated since create or the last reset) and
- * counters of the algorithmic bytes each phase touched (DESIGN.md byte model). */
+ * counters of the algorithmic bytes each phase touched (DESIGN.md byte model).
+ * ABI versioning: cparls_get_stats copies min(bytes, sizeof(cparls_stats)) and
+ * sets struct_size to the library's sizeof(cparls_stats); fields are only
+ * ever appended. */
 typedef struct {
+  uint32_t struct_size;      /* the library's sizeof(cparls_stats)                 */
+  uint32_t reserved0;
   double ms_leverage, ms_sample, ms_gram, ms_lookup, ms_rhs, ms_solve, ms_fit;
   double bytes_leverage, bytes_sample, bytes_gram, bytes_lookup, bytes_rhs, bytes_solve, bytes_fit;
   int64_t mode_steps, fits, kernel_launches;
@@ -108,13 +134,15 @@ typedef struct {
   int64_t touched_rows[8];   /* rows of A_k nonzero after its last solve, per mode */
   /* Device time (ms) and launch count of the hot kernels alone, from CUDA
    * events recorded around every launch on the context's stream (always on,
-   * no host synchronisation; resolved when the stats are read).
-   * Index: 0 = sampled RHS reduction (k_rhs), 1 = exact fit (k_fit_sub /
-   * k_fit_thread), 2 = solve rows (k_solve_rows_t), 3 = leverage rows
-   * (k_lev_rows_t). */
+   * no host synchronisation; resolved when the stats are read or at the
+   * context's next synchronisation).
+   * Index: 0 = sampled RHS (k_rhs / k_rhs_agg), 1 = exact fit (k_fit_sub /
+   * k_fit_thread), 2 = solve rows (k_solve_dmma / k_solve_rows_t),
+   * 3 = leverage rows (k_lev_rows_w). */
   double kernel_ms[4];
   int64_t kernel_launches_by_id[4];
   int64_t sum_matched_nnz;   /* sum of m_k over the solves since the last reset   */
+  int64_t host_syncs;        /* cudaStreamSynchronize calls made by the library   */
 } cparls_stats;
 
 /* Build the context: validates sizes (ERANGE if some prod_{m!=k} n_m >= 2^63 or
@@ -238,7 +266,9 @@ cparls_status cparls_plan_rows(int64_t n, const uint64_t *deg, int32_t world_siz
 /* Rows of mode `mode` owned by this rank. */
 cparls_status cparls_owned_rows(const cparls_ctx *ctx, int32_t mode, int64_t *lo, int64_t *hi);
 
-cparls_status cparls_get_stats(cparls_ctx *ctx, cparls_stats *stats);
+/* Copy the statistics into stats (min(bytes, sizeof(cparls_stats)) bytes, see
+ * cparls_stats).  bytes < 8: EINVAL. */
+cparls_status cparls_get_stats(cparls_ctx *ctx, void *stats, int64_t bytes);
 cparls_status cparls_reset_stats(cparls_ctx *ctx);
 /* Record per-phase CUDA events (adds small overhead). 0 off, 1 on. */
 cparls_status cparls_set_profiling(cparls_ctx *ctx, int32_t on);

@@ -27,11 +27,13 @@ class CparlsError(RuntimeError):
 
 
 class Opts(C.Structure):
-    _fields_ = [("rank", C.c_int32), ("tau", C.c_double), ("value_dtype", C.c_int32),
-                ("index_dtype", C.c_int32), ("stream", C.c_void_p), ("world_size", C.c_int32),
-                ("world_rank", C.c_int32), ("comm", C.c_void_p), ("didx_cap", C.c_int64),
-                ("attempt_cap", C.c_int64), ("rhs_path", C.c_int32), ("fit_samples", C.c_int64),
-                ("fit_alpha", C.c_double), ("fit_seed", C.c_uint64)]
+    """cparls_opts (include/cparls.h); struct_size versions the layout."""
+    _fields_ = [("struct_size", C.c_uint32), ("rank", C.c_int32), ("tau", C.c_double),
+                ("value_dtype", C.c_int32), ("index_dtype", C.c_int32), ("stream", C.c_void_p),
+                ("world_size", C.c_int32), ("world_rank", C.c_int32), ("comm", C.c_void_p),
+                ("didx_cap", C.c_int64), ("attempt_cap", C.c_int64), ("rhs_path", C.c_int32),
+                ("fit_samples", C.c_int64), ("fit_alpha", C.c_double), ("fit_seed", C.c_uint64),
+                ("sidx_window", C.c_int64), ("sample_sort", C.c_int32), ("fit_mode", C.c_int32)]
 
 
 class SampleInfo(C.Structure):
@@ -45,13 +47,13 @@ class SolveInfo(C.Structure):
 
 
 class Stats(C.Structure):
-    _fields_ = [(n, C.c_double) for n in (
+    _fields_ = [("struct_size", C.c_uint32), ("reserved0", C.c_uint32)] + [(n, C.c_double) for n in (
         "ms_leverage", "ms_sample", "ms_gram", "ms_lookup", "ms_rhs", "ms_solve", "ms_fit",
         "bytes_leverage", "bytes_sample", "bytes_gram", "bytes_lookup", "bytes_rhs", "bytes_solve",
         "bytes_fit")] + [(n, C.c_int64) for n in (
         "mode_steps", "fits", "kernel_launches", "last_matched_nnz", "last_s_bar", "last_attempts")] + [
         ("touched_rows", C.c_int64 * 8), ("kernel_ms", C.c_double * 4),
-        ("kernel_launches_by_id", C.c_int64 * 4), ("sum_matched_nnz", C.c_int64)]
+        ("kernel_launches_by_id", C.c_int64 * 4), ("sum_matched_nnz", C.c_int64), ("host_syncs", C.c_int64)]
 
     KERNELS = ("rhs", "fit", "solve_rows", "lev_rows")
 
@@ -97,7 +99,7 @@ def lib():
             "cparls_als_update": [P, I32],
             "cparls_init_rrf": [P, I64, U64],
             "cparls_run_als": [P, I32, I32, P],
-            "cparls_get_stats": [P, C.POINTER(Stats)],
+            "cparls_get_stats": [P, P, I64],
             "cparls_reset_stats": [P],
             "cparls_set_profiling": [P, I32],
             "cparls_comm_nccl_unique_id": [P],
@@ -113,6 +115,8 @@ def lib():
             f.restype = C.c_int
         L.cparls_last_error.argtypes = [P]
         L.cparls_last_error.restype = C.c_char_p
+        L.cparls_opts_init.argtypes = [P]
+        L.cparls_opts_init.restype = None
         L.cparls_version.argtypes = []
         L.cparls_version.restype = C.c_char_p
         _lib = L
@@ -127,7 +131,7 @@ EXPORTED = ["cparls_create", "cparls_destroy", "cparls_set_factor", "cparls_get_
             "cparls_run_als", "cparls_get_stats",
             "cparls_reset_stats", "cparls_set_profiling", "cparls_last_error", "cparls_version",
             "cparls_comm_nccl_unique_id", "cparls_comm_create_nccl", "cparls_comm_create_local",
-            "cparls_comm_destroy", "cparls_plan_rows", "cparls_owned_rows"]
+            "cparls_comm_destroy", "cparls_plan_rows", "cparls_owned_rows", "cparls_opts_init"]
 
 
 def _ptr(x):
@@ -145,7 +149,7 @@ class Cparls:
 
     def __init__(self, dims, coords, vals, rank, tau=-1.0, init_seed=2, stream=None,
                  didx_cap=0, attempt_cap=0, comm=None, world_size=1, world_rank=0, rhs_path=0,
-                 fit_samples=0, fit_alpha=0.5, fit_seed=0):
+                 fit_samples=0, fit_alpha=0.5, fit_seed=0, sidx_window=0, sample_sort=0, fit_mode=-1):
         import torch
         if not torch.cuda.is_available():
             raise RuntimeError("cparls needs a CUDA device (B200); no CPU fallback exists")
@@ -170,11 +174,12 @@ class Cparls:
         if stream is None:
             stream = torch.cuda.current_stream().cuda_stream
         self.stream = stream
-        o = Opts(rank=self.r, tau=float(tau), value_dtype=vdt, index_dtype=idt,
+        o = Opts(struct_size=C.sizeof(Opts), rank=self.r, tau=float(tau), value_dtype=vdt, index_dtype=idt,
                  stream=C.c_void_p(stream), world_size=int(world_size), world_rank=int(world_rank),
                  comm=(comm.handle if comm is not None else None),
                  didx_cap=int(didx_cap), attempt_cap=int(attempt_cap), rhs_path=int(rhs_path),
-                 fit_samples=int(fit_samples), fit_alpha=float(fit_alpha), fit_seed=int(fit_seed))
+                 fit_samples=int(fit_samples), fit_alpha=float(fit_alpha), fit_seed=int(fit_seed),
+                 sidx_window=int(sidx_window), sample_sort=int(sample_sort), fit_mode=int(fit_mode))
         d = np.array(self.dims, dtype=np.int64)
         h = C.c_void_p()
         st = L.cparls_create(C.byref(h), self.D, d.ctypes.data, nnz, _ptr(coords), _ptr(vals),
@@ -338,7 +343,7 @@ class Cparls:
 
     def stats(self):
         s = Stats()
-        self._check(lib().cparls_get_stats(self._h, C.byref(s)))
+        self._check(lib().cparls_get_stats(self._h, C.byref(s), C.sizeof(s)))
         return s.as_dict()
 
     def reset_stats(self):

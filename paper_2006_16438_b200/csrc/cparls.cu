@@ -59,6 +59,16 @@ struct DevScalars {
 
 }  // namespace
 
+// Named slots of the context's pinned scratch hscr (async device->host scalar
+// copies read after a later synchronisation); every use has its own range.
+constexpr int kHscrDrawable = 0;                     // [0, kMaxModes): drawable rows per other mode
+constexpr int kHscrSidx = kHscrDrawable + kMaxModes; // 2: SIDX accepted total, last accepted attempt
+constexpr int kHscrCand = kHscrSidx + 2;             // [.., +kMaxModes): DIDX candidate counts
+constexpr int kHscrMk = kHscrCand + kMaxModes;       // m_k of the last solve
+constexpr int kHscrTouched = kHscrMk + 1;            // touched rows of the last solve
+constexpr int kHscrSlots = 64;
+static_assert(kHscrTouched < kHscrSlots, "pinned scratch layout");
+
 struct cparls_ctx {
   int D = 0, r = 0, ld = 0;
   int64_t dims[kMaxModes] = {0};
@@ -87,6 +97,7 @@ struct cparls_ctx {
   double *Gtmp = nullptr;
   uint64_t *tile_u64 = nullptr;
   int64_t *i64part = nullptr;    // scan partials
+  int64_t i64part_cap = 0;
   dd *ddpart = nullptr;
   // sample state
   int64_t scap = 0;
@@ -132,13 +143,12 @@ struct cparls_ctx {
   uint32_t *hfirst = nullptr;   // first draw index per hash slot (deterministic combine)
   uint32_t *rslot = nullptr;    // per random draw: its slot
   int64_t *rflag = nullptr, *rpos = nullptr;
-  bool sample_sort = getenv("CPARLS_SAMPLE_SORT") && atoi(getenv("CPARLS_SAMPLE_SORT")) == 1;
+  bool sample_sort = false;      // opts.sample_sort
   uint64_t hsize = 0;
   // bookkeeping
   std::vector<void *> allocs;
   cparls_stats stats{};
   bool profiling = false;
-  bool debug_sync = getenv("CPARLS_DEBUG_SYNC") != nullptr;   // sync + report inside the sampler
   std::vector<cudaEvent_t> ev_pool;                             // free events
   std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> ev_pending;
   int fit_mode = 0;
@@ -160,7 +170,7 @@ struct cparls_ctx {
   bool m_dirty = false;   // M holds rows written by the bucketed RHS (not zero)
   double *fx_scale = nullptr;   // fixed-point RHS scales 2^e_c, 2^-e_c (kernels.cuh)
   double dupmax = 1.0;
-  bool rhs_fixed = !(getenv("CPARLS_RHS_FIXED") && atoi(getenv("CPARLS_RHS_FIXED")) == 0);
+  bool rhs_fixed = true;        // int64 fixed-point RHS (rhs_path 0/1/2); false: fp64 reductions (rhs_path 3)
   bool fx_on = false;           // this solve's RHS is fixed point (M holds int64)
   // pinned double buffer for copies into pageable host memory (rows_to_host)
   void *stage[2] = {nullptr, nullptr};
@@ -170,7 +180,7 @@ struct cparls_ctx {
   cudaStream_t side = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   bool fx_pending = false;
-  int stats_pending_k = -1;     // a solve's m_k / touched rows copied to hscr[48..49], folded at the next sync
+  int stats_pending_k = -1;     // a solve's m_k / touched rows copied to hscr[kHscrMk..], folded at the next sync
   cudaEvent_t stage_ev[2] = {nullptr, nullptr};
   // frozen stratified fit sample (fitest.cuh, AMB-32)
   bool have_fs = false;
@@ -255,13 +265,21 @@ void fold_step_stats(cparls_ctx *c, int k, int64_t mk, unsigned long long touche
   c->stats.touched_rows[k] = (int64_t)touched;
 }
 
-void sync(cparls_ctx *c) {
+void ktimers_resolve(cparls_ctx *c);
+
+// Stream synchronisation of the context: folds the counters a solve left in
+// pinned scratch and resolves the per-kernel event timers (all recorded
+// before this point on the stream, so complete).  count = false for the
+// synchronisations of the stats calls themselves.
+void sync(cparls_ctx *c, bool count = true) {
   CK(cudaStreamSynchronize(c->st));
+  if (count) c->stats.host_syncs++;
   if (c->stats_pending_k >= 0) {   // a solve without an info request left its counters here
     const int k = c->stats_pending_k;
     c->stats_pending_k = -1;
-    fold_step_stats(c, k, (int64_t)c->hscr[48], (unsigned long long)c->hscr[49]);
+    fold_step_stats(c, k, (int64_t)c->hscr[kHscrMk], (unsigned long long)c->hscr[kHscrTouched]);
   }
+  ktimers_resolve(c);
 }
 
 bool is_pinned_host(const void *p) {
@@ -369,6 +387,7 @@ struct KTimer {
   cudaEvent_t a = nullptr, b = nullptr;
   KTimer(cparls_ctx *c_, int id_, cudaStream_t st_ = nullptr);
   void stop();
+  ~KTimer();   // a timer never stopped (an exception in between) returns its events
 };
 
 cudaEvent_t ev_get(cparls_ctx *c) {
@@ -390,6 +409,28 @@ void KTimer::stop() {
   CK(cudaEventRecord(b, st));
   c->ev_pending.push_back({id, {a, b}});
   c->stats.kernel_launches_by_id[id]++;
+  a = b = nullptr;
+  // bounded: a long run without synchronisation folds the finished pairs here
+  if (c->ev_pending.size() >= 4096) {
+    size_t keep = 0;
+    for (auto &p : c->ev_pending) {
+      if (cudaEventQuery(p.second.second) == cudaSuccess) {
+        float ms = 0.f;
+        CK(cudaEventElapsedTime(&ms, p.second.first, p.second.second));
+        c->stats.kernel_ms[p.first] += ms;
+        c->ev_pool.push_back(p.second.first);
+        c->ev_pool.push_back(p.second.second);
+      } else {
+        c->ev_pending[keep++] = p;
+      }
+    }
+    cudaGetLastError();   // cudaErrorNotReady of the unfinished ones
+    c->ev_pending.resize(keep);
+  }
+}
+KTimer::~KTimer() {
+  if (a) c->ev_pool.push_back(a);
+  if (b) c->ev_pool.push_back(b);
 }
 // sum the elapsed times of all recorded launches into the stats
 void ktimers_resolve(cparls_ctx *c) {
@@ -430,8 +471,7 @@ size_t solve_smem(int r, int ld) { return sizeof(double) * ((size_t)r * ld + (si
 void launch_solve_rows(cparls_ctx *c, double *M, int64_t n, double *B, int64_t grid, int zero_m,
                        const double *fscale) {
   const int r = c->r, ld = c->ld;
-  const char *e = getenv("CPARLS_SOLVE_DMMA");
-  const bool dmma = !(e && atoi(e) == 0) && r > 4 && ld <= 32 && ld % 8 == 0;
+  const bool dmma = r > 4 && ld <= 32 && ld % 8 == 0;
   if (dmma) {
     const size_t sm = sizeof(double) * solve_dmma_smem_d(ld);
     switch (ld / 8) {
@@ -484,9 +524,6 @@ void set_kernel_attrs(int r, int ld) {
   max_dyn_smem(k_bkt_accum<4>);
   max_dyn_smem(k_solve_dmma<1>); max_dyn_smem(k_solve_dmma<2>); max_dyn_smem(k_solve_dmma<3>);
   max_dyn_smem(k_solve_dmma<4>);
-  max_dyn_smem(k_lev_dmma<1>); max_dyn_smem(k_lev_dmma<2>); max_dyn_smem(k_lev_dmma<3>); max_dyn_smem(k_lev_dmma<4>);
-  max_dyn_smem(k_fit_tma<float, 1>); max_dyn_smem(k_fit_tma<float, 2>); max_dyn_smem(k_fit_tma<float, 3>);
-  max_dyn_smem(k_fit_tma<double, 1>); max_dyn_smem(k_fit_tma<double, 2>); max_dyn_smem(k_fit_tma<double, 3>);
   set_attrs_rm<4>(); set_attrs_rm<8>(); set_attrs_rm<16>(); set_attrs_rm<28>(); set_attrs_rm<32>();
   set_attrs_rm<64>();
   int prep = (int)prep_smem(r);
@@ -509,29 +546,10 @@ void lev_rows_and_cdf(cparls_ctx *c, int k, const double *lam) {
     const unsigned g = (unsigned)row_grid(c, ceil_div(n, kWarpRows * (kRowThreads / 32)));
     CK(cudaMemsetAsync(c->tile_u64, 0, sizeof(uint64_t) * nt, c->st));
     KTimer kt(c, KT_LEV);
-    // opt-in (CPARLS_LEV_DMMA=1): the DMMA leverage pass measured 0.60 ms per C4
-    // launch against 0.51 for k_lev_rows_w (which skips W's zero lower triangle)
-    const char *e = getenv("CPARLS_LEV_DMMA");
-    const int ld = c->ld;
-    if ((e && atoi(e) == 1) && c->r > 4 && ld <= 32 && ld % 8 == 0) {   // FP64 tensor cores
-      const size_t sm = sizeof(double) * lev_dmma_smem_d(ld);
-      unsigned long long *ts = reinterpret_cast<unsigned long long *>(c->tile_u64);
-      unsigned long long *dr = reinterpret_cast<unsigned long long *>(&c->md[k]->drawable);
-#define LEVD(NT) k_lev_dmma<NT><<<g, kRowThreads, sm, c->st>>>(c->A[k], n, c->r, ld, lam, c->md[k], c->pt[k], \
-                                                              c->C[k], ts, &c->md[k]->alpha, dr)
-      switch (ld / 8) {
-        case 1: LEVD(1); break;
-        case 2: LEVD(2); break;
-        case 3: LEVD(3); break;
-        default: LEVD(4); break;
-      }
-#undef LEVD
-    } else {
-      RSWITCH(c->r, k_lev_rows_w<RM><<<g, kRowThreads, lev_w_smem(c->r, c->ld), c->st>>>(
-                        c->A[k], n, c->r, c->ld, lam, c->md[k], c->pt[k], c->C[k],
-                        reinterpret_cast<unsigned long long *>(c->tile_u64), &c->md[k]->alpha,
-                        reinterpret_cast<unsigned long long *>(&c->md[k]->drawable)));
-    }
+    RSWITCH(c->r, k_lev_rows_w<RM><<<g, kRowThreads, lev_w_smem(c->r, c->ld), c->st>>>(
+                      c->A[k], n, c->r, c->ld, lam, c->md[k], c->pt[k], c->C[k],
+                      reinterpret_cast<unsigned long long *>(c->tile_u64), &c->md[k]->alpha,
+                      reinterpret_cast<unsigned long long *>(&c->md[k]->drawable)));
     kt.stop();
   }
   CK_LAUNCH();
@@ -830,6 +848,15 @@ void build_all(cparls_ctx *c, const IT *coords, const VT *vals) {
   }
 }
 
+// exclusive_scan_i64 over n items needs ceil(n / kScanTile) partials
+void ensure_i64part(cparls_ctx *c, int64_t n) {
+  const int64_t need = ceil_div(std::max<int64_t>(n, 1), kScanTile) + 64;
+  if (need <= c->i64part_cap) return;
+  dfree(c, c->i64part);   // cudaFree waits for the kernels still reading it
+  c->i64part_cap = std::max(need, 2 * c->i64part_cap);
+  c->i64part = dalloc_t<int64_t>(c, c->i64part_cap);
+}
+
 void alloc_sample_buffers(cparls_ctx *c, int64_t s) {
   if (s <= c->scap) return;
   int64_t cap = std::max<int64_t>(s, 1024);
@@ -871,8 +898,7 @@ void alloc_sample_buffers(cparls_ctx *c, int64_t s) {
   c->rpos = dalloc_t<int64_t>(c, cap);
   CK(cudaMemsetAsync(c->hkey, 0xFF, sizeof(unsigned long long) * hs, c->st));
   CK(cudaMemsetAsync(c->hcnt, 0, sizeof(uint32_t) * hs, c->st));
-  int64_t part_need = ceil_div(cap, kScanTile) + 16;
-  (void)part_need;
+  ensure_i64part(c, cap);   // scans over the accepted draws and the sample (<= s)
   c->scap = cap;
 }
 
@@ -902,7 +928,6 @@ int64_t run_didx(cparls_ctx *c, const OtherModes &om, double tau, int *which) {
   // candidates per mode (ordered compaction), then stable sort by p~ descending
   // every mode's candidates first (independent), then one read of all counts
   // (a sync per mode before)
-  static_assert(kMaxModes <= 32, "candidate counts fit the pinned scratch");
   for (int j = 0; j < d; ++j) {
     const int64_t n = om.n[j];
     const int64_t nb = ceil_div(n, kScanTile);
@@ -913,12 +938,12 @@ int64_t run_didx(cparls_ctx *c, const OtherModes &om, double tau, int *which) {
     k_cand_scatter<<<(unsigned)nb, kScanThreads, 0, c->st>>>(om, j, tau, c->i64part, c->ckey[j], c->cidx[j]);
     CK_LAUNCH();
     LAUNCHED(c, 3);
-    CK(cudaMemcpyAsync(c->hscr + 40 + j, &c->dv->total, sizeof(long long), cudaMemcpyDeviceToHost, c->st));
+    CK(cudaMemcpyAsync(c->hscr + kHscrCand + j, &c->dv->total, sizeof(long long), cudaMemcpyDeviceToHost, c->st));
   }
   sync(c);
   for (int j = 0; j < d; ++j) {
     const int64_t n = om.n[j];
-    const int64_t nc = c->hscr[40 + j];
+    const int64_t nc = c->hscr[kHscrCand + j];
     if (nc > 1) {
       int res = radix_sort_pairs(c->ckey[j], c->cidx[j], c->ckey_tmp, c->cidx_tmp, nc, 64, c->rhist, c->st,
                                  &c->stats.kernel_launches);
@@ -929,10 +954,6 @@ int64_t run_didx(cparls_ctx *c, const OtherModes &om, double tau, int *which) {
     }
     c->stats.bytes_sample += (double)n * 8.0;
     ncand[j] = nc;
-    if (c->debug_sync) {
-      sync(c);
-      fprintf(stderr, "[didx] mode j=%d n=%lld ncand=%lld alpha=%g\n", j, (long long)n, (long long)nc, om.alpha[j]);
-    }
   }
   // level expansion (DetSet is a subset of the product of the
   // candidate sets); the exact canonical predicate decides membership.
@@ -953,13 +974,13 @@ int64_t run_didx(cparls_ctx *c, const OtherModes &om, double tau, int *which) {
       nlist = 0;
       break;
     }
+    ensure_i64part(c, nlist);
     k_didx_count<<<(unsigned)ceil_div(nlist, 256), 256, 0, c->st>>>(c->lpp[cur], nlist, c->ckey[l], ncl, om, l, tau,
                                                                     c->lcnt);
     CK_LAUNCH();
     exclusive_scan_i64(c->lcnt, c->loff, nlist, c->i64part, &c->dv->total, c->st);
     LAUNCHED(c, 4);
     const int64_t nn = read_dev(c, &c->dv->total);
-    if (c->debug_sync) fprintf(stderr, "[didx] level %d nlist=%lld -> %lld (lcap %lld)\n", l, (long long)nlist, (long long)nn, (long long)c->lcap);
     if (nn > cap) throw ApiError(CPARLS_ESAMPLE, "DIDX list exceeds didx_cap (" + std::to_string(nn) + ")");
     if (nn > c->lcap) {
       // grow, keeping the current level
@@ -1008,7 +1029,7 @@ void sample_impl(cparls_ctx *c, int k, int64_t s, uint64_t seed, uint64_t step, 
   const int d = om.d;
   // drawable counts (rows with q > 0): copied into pinned scratch now, read
   // after the p_det sync below (stream order), no sync of their own
-  long long *drawable = c->hscr;
+  long long *drawable = c->hscr + kHscrDrawable;
   for (int j = 0; j < d; ++j)
     CK(cudaMemcpyAsync(&drawable[j], &c->md[om.mode[j]]->drawable, sizeof(long long), cudaMemcpyDeviceToHost,
                        c->st));
@@ -1100,6 +1121,7 @@ void sample_impl(cparls_ctx *c, int k, int64_t s, uint64_t seed, uint64_t step, 
         int64_t want = (int64_t)std::ceil((double)(s_rnd - have) / accp * 1.08) + 4096;
         int64_t win = std::min<int64_t>(std::max<int64_t>(want, 4096), c->acap);
         win = std::min<int64_t>(win, cap_att - (int64_t)a0);
+        if (c->opts.sidx_window > 0) win = std::min<int64_t>(win, c->opts.sidx_window);   // AMB-8: result-neutral
         int64_t nb = ceil_div(win, kSidxThreads);
         k_sidx_gen<<<(unsigned)nb, kSidxThreads, 0, c->st>>>(om, a0, win, tau, slo, shi, (uint32_t)step, c->akey,
                                                              c->ap, c->i64part);
@@ -1112,13 +1134,13 @@ void sample_impl(cparls_ctx *c, int k, int64_t s, uint64_t seed, uint64_t step, 
         LAUNCHED(c, 3);
         // total and last_attempt (adjacent) in one read
         static_assert(offsetof(DevScalars, last_attempt) == offsetof(DevScalars, total) + 8, "layout");
-        CK(cudaMemcpyAsync(c->hscr + 32, &c->dv->total, 16, cudaMemcpyDeviceToHost, c->st));
+        CK(cudaMemcpyAsync(c->hscr + kHscrSidx, &c->dv->total, 16, cudaMemcpyDeviceToHost, c->st));
         sync(c);
-        const int64_t got = c->hscr[32];
+        const int64_t got = c->hscr[kHscrSidx];
         have += std::min<int64_t>(got, s_rnd - have);
         a0 += (uint64_t)win;
         c->stats.bytes_sample += (double)win * d * 8.0;
-        if (have >= s_rnd) attempts = (int64_t)(unsigned long long)c->hscr[33] + 1;
+        if (have >= s_rnd) attempts = (int64_t)(unsigned long long)c->hscr[kHscrSidx + 1] + 1;
       }
     }
   }
@@ -1349,8 +1371,8 @@ void solve_impl(cparls_ctx *c, int k, cparls_solve_info *info) {
     }
     Phase ph(c, &c->stats.ms_rhs);
     if (sbar > 0) {
-      static const int win_mb = getenv("CPARLS_RHS_WIN_MB") ? atoi(getenv("CPARLS_RHS_WIN_MB")) : 96;
-      static const int grid_mult = getenv("CPARLS_RHS_GRID") ? atoi(getenv("CPARLS_RHS_GRID")) : 8;
+      constexpr int win_mb = 96;     // output-row window of M kept in L2 (rhs.cuh)
+      constexpr int grid_mult = 8;   // CTAs per SM
       const int64_t RW = std::max<int64_t>(1, (int64_t(win_mb) << 20) / ((int64_t)ld * 8));
       const int nwin = (int)ceil_div(nk, RW);
       const int64_t nseg = (int64_t)nwin * sbar;
@@ -1438,8 +1460,8 @@ void solve_impl(cparls_ctx *c, int k, cparls_solve_info *info) {
   // sync), otherwise folded into the stats at the next sync (no sync here)
   if (c->world > 1) c->comm->allreduce_u64(reinterpret_cast<unsigned long long *>(&c->dv->mk), 1, c->st);
   if (c->stats_pending_k >= 0) sync(c);   // (cannot happen inside run: sampling syncs first)
-  CK(cudaMemcpyAsync(c->hscr + 48, &c->dv->mk, sizeof(long long), cudaMemcpyDeviceToHost, c->st));
-  CK(cudaMemcpyAsync(c->hscr + 49, &c->dv->touched, sizeof(unsigned long long), cudaMemcpyDeviceToHost, c->st));
+  CK(cudaMemcpyAsync(c->hscr + kHscrMk, &c->dv->mk, sizeof(long long), cudaMemcpyDeviceToHost, c->st));
+  CK(cudaMemcpyAsync(c->hscr + kHscrTouched, &c->dv->touched, sizeof(unsigned long long), cudaMemcpyDeviceToHost, c->st));
   c->stats_pending_k = k;
   c->stats.mode_steps++;
   if (info) {
@@ -1736,28 +1758,7 @@ void fit_launch(cparls_ctx *c, cudaStream_t st, double *const *A, const double *
   fd.fast = N < 9007199254740992.0L;   // keys < 2^53
   int nb = 148 * 4;
   KTimer kt(c, KT_FIT, st);
-  // opt-in (CPARLS_FIT_TMA=1): bulk-copy gathers measured 146 ms against 69 for
-  // k_fit_sub on C4 -- ~18 SM cycles per 224-byte cp.async.bulk (fit_tma.cuh)
-  const bool use_tma = getenv("CPARLS_FIT_TMA") && atoi(getenv("CPARLS_FIT_TMA")) == 1;
-  int optin = 0;
-  CK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, 0));
-  const size_t tma_warp = (size_t)kFtStages * kFtE * std::max(1, fd.d) * c->ld * 8;
-  const int tma_wpb = (int)std::min<size_t>(8, (size_t)(optin - 1024) / tma_warp);
-  if (use_tma && fd.d <= 3 && c->ld > 8 && c->ld <= 32 && tma_wpb >= 2) {
-    // bulk-copy row gathers (fit_tma.cuh), one CTA of tma_wpb warps per SM
-    nb = 148;
-    CK(cudaMemsetAsync(counter, 0, sizeof(unsigned long long), st));
-#define FITT(VT, DM)                                                                                   \
-  k_fit_tma<VT, DM><<<nb, 32 * tma_wpb, tma_warp * tma_wpb, st>>>(c->idx[k].key, c->idx[k].out,       \
-                                                                  (const VT *)c->idx[k].val, c->idx[k].nnz, fd, \
-                                                                  A[k], lam, c->r, c->ld, part, counter)
-    if (c->vf32) {
-      if (fd.d == 1) FITT(float, 1); else if (fd.d == 2) FITT(float, 2); else FITT(float, 3);
-    } else {
-      if (fd.d == 1) FITT(double, 1); else if (fd.d == 2) FITT(double, 2); else FITT(double, 3);
-    }
-#undef FITT
-  } else if (fd.d <= 3) {
+  if (fd.d <= 3) {
     // sub-warp per entry, 4 columns per lane (k_fit_sub)
     nb = 148 * std::max(1, std::min(CPARLS_FIT_MINB, blocks_per_sm));
     CK(cudaMemsetAsync(counter, 0, sizeof(unsigned long long), st));
@@ -1866,11 +1867,27 @@ extern "C" {
 
 static thread_local std::string g_create_err;
 
+void cparls_opts_init(cparls_opts *o) {
+  if (!o) return;
+  std::memset(o, 0, sizeof(*o));
+  o->struct_size = (uint32_t)sizeof(cparls_opts);
+  o->rank = 1;
+  o->tau = -1.0;
+  o->world_size = 1;
+  o->fit_mode = -1;
+}
+
 cparls_status cparls_create(cparls_ctx **out, int32_t nmodes, const int64_t *dims, int64_t nnz_local,
-                            const void *coords, const void *vals, const cparls_opts *opts, uint64_t init_seed) {
-  const auto t_create0 = std::chrono::steady_clock::now();
-  if (!out || !dims || !opts) return CPARLS_EINVAL;
+                            const void *coords, const void *vals, const cparls_opts *opts_in, uint64_t init_seed) {
+  if (!out || !dims || !opts_in) return CPARLS_EINVAL;
   *out = nullptr;
+  // versioned options: the caller's struct_size bytes over the defaults
+  if (opts_in->struct_size < offsetof(cparls_opts, value_dtype)) return CPARLS_EINVAL;
+  cparls_opts ob;
+  cparls_opts_init(&ob);
+  std::memcpy(&ob, opts_in, std::min<size_t>(opts_in->struct_size, sizeof(cparls_opts)));
+  ob.struct_size = (uint32_t)sizeof(cparls_opts);
+  const cparls_opts *opts = &ob;
   cparls_ctx *c = new (std::nothrow) cparls_ctx();
   if (!c) return CPARLS_EOOM;
   cparls_status st = guarded(c, [&] {
@@ -1891,19 +1908,17 @@ cparls_status cparls_create(cparls_ctx **out, int32_t nmodes, const int64_t *dim
     c->wrank = opts->world_rank;
     c->D = nmodes;
     c->r = opts->rank;
-    {   // row stride of the factor-shaped matrices (A_k, M, Z): r rounded up to 8
-        // doubles (64-byte rows; r <= 4: 4).  On C4 (r = 25) 32 against 28
-        // measured k_rhs 5.38 -> 5.13 ms and the fit 69.2 -> 65.7 ms: a 256-byte
-        // row covers exactly two 128-byte lines.  CPARLS_LD_ALIGN=4 restores
-        // 32-byte multiples.
-      const char *la = getenv("CPARLS_LD_ALIGN");
-      const int al = (la && atoi(la) == 4) || c->r <= 4 ? 4 : 8;
-      c->ld = (c->r + al - 1) & ~(al - 1);
-    }
+    // row stride of the factor-shaped matrices (A_k, M, Z): r rounded up to 8
+    // doubles (64-byte rows; r <= 4: 4).  On C4 (r = 25) 32 against 28 measured
+    // k_rhs 5.38 -> 5.13 ms and the fit 69.2 -> 65.7 ms: a 256-byte row covers
+    // exactly two 128-byte lines.
+    c->ld = c->r <= 4 ? 4 : (c->r + 7) & ~7;
     c->nnz = nnz_local;
     c->vf32 = opts->value_dtype == 1;
     c->opts = *opts;
     c->tau = opts->tau;
+    c->sample_sort = opts->sample_sort == 1;
+    c->rhs_fixed = opts->rhs_path != 3;
     c->st = static_cast<cudaStream_t>(opts->stream);
     for (int m = 0; m < nmodes; ++m) {
       if (dims[m] < 1) throw ApiError(CPARLS_EINVAL, "dims must be >= 1");
@@ -1918,7 +1933,7 @@ cparls_status cparls_create(cparls_ctx **out, int32_t nmodes, const int64_t *dim
       if (Nk >= 9223372036854775808.0L) throw ApiError(CPARLS_ERANGE, "prod_{m!=k} n_m >= 2^63");
     }
     set_kernel_attrs(c->r, c->ld);
-    CK(cudaHostAlloc(reinterpret_cast<void **>(&c->hscr), 64 * sizeof(long long), cudaHostAllocDefault));
+    CK(cudaHostAlloc(reinterpret_cast<void **>(&c->hscr), kHscrSlots * sizeof(long long), cudaHostAllocDefault));
     CK(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));
     CK(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
@@ -1932,7 +1947,8 @@ cparls_status cparls_create(cparls_ctx **out, int32_t nmodes, const int64_t *dim
     c->gpart = dalloc_t<double>(c, c->gpart_blocks * (int64_t)c->r * c->r);
     c->Gtmp = dalloc_t<double>(c, kMaxRank * kMaxRank);
     c->tile_u64 = dalloc_t<uint64_t>(c, ceil_div(c->nmax, kLevThreads) + 1);
-    c->i64part = dalloc_t<int64_t>(c, ceil_div(c->nmax, kScanTile) + 65536 + 64);
+    c->i64part_cap = ceil_div(c->nmax, kScanTile) + 65536 + 64;   // also the SIDX window partials (<= acap / kSidxThreads)
+    c->i64part = dalloc_t<int64_t>(c, c->i64part_cap);
     // COO to device if needed
     const size_t isz = opts->index_dtype == 1 ? 8 : 4, vsz = c->vf32 ? 4 : 8;
     const void *dco = coords, *dva = vals;
@@ -1946,13 +1962,6 @@ cparls_status cparls_create(cparls_ctx **out, int32_t nmodes, const int64_t *dim
       own_v = dalloc(c, vsz * nnz_local);
       CK(cudaMemcpyAsync(own_v, vals, vsz * nnz_local, cudaMemcpyHostToDevice, c->st));
       dva = own_v;
-    }
-    const bool tdbg = getenv("CPARLS_DEBUG") != nullptr;
-    auto now = [] { return std::chrono::steady_clock::now(); };
-    auto t_h2d_end = now();
-    if (tdbg) {
-      sync(c);
-      t_h2d_end = now();
     }
     if (isz == 4 && vsz == 4) build_all<int32_t, float>(c, (const int32_t *)dco, (const float *)dva);
     else if (isz == 4) build_all<int32_t, double>(c, (const int32_t *)dco, (const double *)dva);
@@ -1969,12 +1978,6 @@ cparls_status cparls_create(cparls_ctx **out, int32_t nmodes, const int64_t *dim
       if (c->world > 1) c->comm->allreduce_u64(&c->dv->dupmax, 1, c->st);   // (sum: an upper bound)
       c->dupmax = std::max<double>(1.0, (double)read_dev(c, &c->dv->dupmax));
       c->fx_scale = dalloc_t<double>(c, 2 * kMaxRank + 1);
-    }
-    if (tdbg) {
-      sync(c);
-      fprintf(stderr, "[cparls] create: setup+H2D %.3f s, build %.3f s\n",
-              std::chrono::duration<double>(t_h2d_end - t_create0).count(),
-              std::chrono::duration<double>(now() - t_h2d_end).count());
     }
     if (opts->fit_samples > 0) {
       if (c->world > 1) throw ApiError(CPARLS_EINVAL, "fit_samples needs world_size == 1");
@@ -2051,14 +2054,7 @@ cparls_status cparls_create(cparls_ctx **out, int32_t nmodes, const int64_t *dim
         const double cost = (double)nnz_global * (double)c->dims[m] + (double)c->nfib[m] * fib;
         if (m == 0 || cost < best) { best = cost; c->fit_mode = m; }
       }
-      if (getenv("CPARLS_FIT_MODE")) c->fit_mode = std::min(nmodes - 1, std::max(0, atoi(getenv("CPARLS_FIT_MODE"))));
-    }
-    if (getenv("CPARLS_DEBUG")) {
-      for (int m = 0; m < nmodes; ++m)
-        fprintf(stderr, "[cparls] mode %d: n=%lld fibers=%lld (avg len %.2f) dir_buckets=%lld\n", m,
-                (long long)c->dims[m], (long long)c->nfib[m], c->nfib[m] ? (double)c->nnz / c->nfib[m] : 0.0,
-                (long long)c->idx[m].nbkt);
-      fprintf(stderr, "[cparls] fit mode %d\n", c->fit_mode);
+      if (opts->fit_mode >= 0 && opts->fit_mode < nmodes) c->fit_mode = opts->fit_mode;
     }
     reset_lambda(c);
     for (int k = 0; k < nmodes; ++k) leverage_full(c, k);
@@ -2509,20 +2505,19 @@ cparls_status cparls_owned_rows(const cparls_ctx *c, int32_t mode, int64_t *lo, 
   return CPARLS_OK;
 }
 
-cparls_status cparls_get_stats(cparls_ctx *c, cparls_stats *s) {
-  if (!c || !s) return CPARLS_EINVAL;
+cparls_status cparls_get_stats(cparls_ctx *c, void *s, int64_t bytes) {
+  if (!c || !s || bytes < 8) return CPARLS_EINVAL;
   return guarded(c, [&] {
-    sync(c);   // folds a pending step's counters
-    ktimers_resolve(c);
-    *s = c->stats;
+    sync(c, false);   // folds a pending step's counters and the kernel timers
+    c->stats.struct_size = (uint32_t)sizeof(cparls_stats);
+    std::memcpy(s, &c->stats, (size_t)std::min<int64_t>(bytes, (int64_t)sizeof(cparls_stats)));
   });
 }
 
 cparls_status cparls_reset_stats(cparls_ctx *c) {
   if (!c) return CPARLS_EINVAL;
   return guarded(c, [&] {
-    sync(c);   // a pending step's counters belong to the old stats
-    ktimers_resolve(c);
+    sync(c, false);   // a pending step's counters belong to the old stats
     c->stats = cparls_stats{};
   });
 }

@@ -510,48 +510,6 @@ __device__ __forceinline__ uint64_t mix64(uint64_t k) {
   return k;
 }
 
-__global__ void k_cidx_insert(const uint64_t *__restrict__ rkey, const double *__restrict__ rp, int64_t n,
-                              unsigned long long *__restrict__ hkey, uint32_t *__restrict__ hcnt,
-                              double *__restrict__ hp, uint64_t hmask) {
-  int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= n) return;
-  uint64_t k = rkey[t];
-  uint64_t h = mix64(k) & hmask;
-  while (true) {
-    unsigned long long prev = atomicCAS(&hkey[h], kEmptyKey, (unsigned long long)k);
-    if (prev == kEmptyKey || prev == k) {
-      atomicAdd(&hcnt[h], 1u);
-      if (prev == kEmptyKey) hp[h] = rp[t];
-      return;
-    }
-    h = (h + 1) & hmask;
-  }
-}
-
-// Emit unique random rows after the deterministic block:
-// w^2 = c (1 - p_det) / (s_rnd p)  (P:537 with s -> s_rnd, AMB-3)
-__global__ void k_cidx_emit(unsigned long long *__restrict__ hkey, uint32_t *__restrict__ hcnt,
-                            const double *__restrict__ hp, uint64_t hsize, const double *__restrict__ pdet_ptr,
-                            int64_t s_rnd, int64_t base, unsigned long long *__restrict__ counter,
-                            uint64_t *__restrict__ skey, double *__restrict__ sw2, double *__restrict__ sp,
-                            int32_t *__restrict__ scnt, uint8_t *__restrict__ sdet) {
-  uint64_t h = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (h >= hsize) return;
-  unsigned long long k = hkey[h];
-  if (k == kEmptyKey) return;
-  uint32_t c = hcnt[h];
-  double p = hp[h];
-  double pdet = *pdet_ptr;
-  unsigned long long o = base + atomicAdd(counter, 1ull);
-  skey[o] = k;
-  scnt[o] = (int32_t)c;
-  sp[o] = p;
-  sw2[o] = ((double)c * (1.0 - pdet)) / ((double)s_rnd * p);
-  sdet[o] = 0;
-  hkey[h] = kEmptyKey;   // reset for the next sample
-  hcnt[h] = 0;
-}
-
 // Deterministic combine (AMB-35): the unique random rows are emitted in the
 // order of their first draw (attempt order, itself deterministic) instead of
 // hash-slot order via an atomic counter.  insert also keeps the first draw
@@ -967,7 +925,6 @@ __global__ void k_dup_runs(const uint64_t *__restrict__ key, const int32_t *__re
 #include "rhs.cuh"
 #include "rhs_bucket.cuh"
 #include "fit.cuh"
-#include "fit_tma.cuh"
 #include "fitest.cuh"
 #include "als.cuh"
 #include "rrf.cuh"

@@ -467,103 +467,6 @@ __global__ void __launch_bounds__(kRowThreads, 2) k_solve_dmma(double *__restric
   }
 }
 
-// ---------------------------------------------------------------- leverage on FP64 tensor cores
-// k_lev_rows_w with the per-row quadratic form on DMMA (ld = 8 NT <= 32):
-// per 32-row warp tile, A = B (1/lambda) in shared memory (stored back), then
-// per 8-row slab Y = A W (2 NT^2 x 4 DMMAs, W fragments from shared memory)
-// and l = sum_c Y_c^2 (each lane's 2 NT columns, then a 4-lane shuffle sum);
-// p~, q, the CDF tile sums, max p~ and the drawable count as k_lev_rows_w.
-// Opt-in (CPARLS_LEV_DMMA=1): 0.60 ms per C4 launch against 0.51 ms for
-// k_lev_rows_w, which skips the zero lower triangle of a Cholesky W.
-__host__ __device__ constexpr size_t lev_dmma_smem_d(int LD) {
-  return (size_t)LD * LD + LD + (size_t)(kRowThreads / 32) * kWarpRows * (LD + 2) + 64;
-}
-
-template <int NT>
-__global__ void __launch_bounds__(kRowThreads, 2) k_lev_dmma(double *__restrict__ A, int64_t n, int r, int ld,
-                                                             const double *__restrict__ lam,
-                                                             const ModeDev *__restrict__ md, double *__restrict__ pt,
-                                                             uint64_t *__restrict__ C,
-                                                             unsigned long long *__restrict__ tile_sum,
-                                                             double *alpha_out, unsigned long long *drawable_out) {
-  constexpr int LD = NT * 8, KS = NT * 2;
-  constexpr int S = LD + 2;
-  extern __shared__ __align__(16) double smem[];
-  double *Ws = smem;            // LD x LD, zero padded (zero below the diagonal if tri)
-  double *il = Ws + LD * LD;    // 1/lambda_c (0 for a zero column), 1 without lam
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, gid = lane >> 2, tig = lane & 3;
-  double *tile = il + LD + (size_t)w * kWarpRows * S;
-  const int tri = md->tri, rank = md->rank;
-  for (int i = threadIdx.x; i < LD * LD; i += blockDim.x) {
-    const int k = i / LD, c = i - k * LD;
-    Ws[i] = (k < r && c < r && (!tri || k <= c)) ? md->W[k * r + c] : 0.0;
-  }
-  for (int i = threadIdx.x; i < LD; i += blockDim.x)
-    il[i] = (lam != nullptr && i < r) ? (lam[i] > 0.0 ? 1.0 / lam[i] : 0.0) : 1.0;
-  __syncthreads();
-  double pmax = 0.0;
-  unsigned long long dcnt = 0;
-  const int64_t ntiles = ceil_div(n, kWarpRows);
-  const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
-  for (int64_t t = (int64_t)blockIdx.x * (blockDim.x >> 5) + w; t < ntiles; t += nwarps) {
-    const int64_t base = t * kWarpRows;
-    const int rows = (int)min((int64_t)kWarpRows, n - base);
-    warp_stage(A + base * ld, rows, ld, tile, S, nullptr);
-    __syncwarp();
-    if (lam != nullptr) {
-      for (int i = lane; i < rows * ld; i += 32) {
-        const int row = i / ld, c = i - row * ld;
-        if (c < r) tile[row * S + c] *= il[c];
-      }
-      __syncwarp();
-      warp_store(A + base * ld, rows, ld, tile, S);
-    }
-    uint64_t qsum = 0;
-#pragma unroll
-    for (int m = 0; m < 4; ++m) {
-      const int row = m * 8 + gid;
-      double a[KS];
-#pragma unroll
-      for (int ks = 0; ks < KS; ++ks) {
-        const int c = ks * 4 + tig;
-        a[ks] = (row < rows && c < r) ? tile[row * S + c] : 0.0;
-      }
-      double l = 0.0;
-      if (rank > 0) {
-        double d[NT][2];
-#pragma unroll
-        for (int nn = 0; nn < NT; ++nn) d[nn][0] = d[nn][1] = 0.0;
-#pragma unroll
-        for (int ks = 0; ks < KS; ++ks)
-#pragma unroll
-          for (int nn = 0; nn < NT; ++nn) dmma_884(d[nn], a[ks], Ws[(ks * 4 + tig) * LD + nn * 8 + gid]);
-#pragma unroll
-        for (int nn = 0; nn < NT; ++nn) l += d[nn][0] * d[nn][0] + d[nn][1] * d[nn][1];
-        l += __shfl_xor_sync(0xffffffffu, l, 1);
-        l += __shfl_xor_sync(0xffffffffu, l, 2);
-      }
-      if (tig == 0 && row < rows) {
-        const double p = rank > 0 ? l / (double)rank : 0.0;
-        const uint64_t q = __double2ull_rn(p * kTwo62);
-        pt[base + row] = p;
-        C[base + row] = q;
-        qsum += q;
-        pmax = fmax(pmax, p);
-        dcnt += (p > 1.0842021724855044e-19);
-      }
-    }
-    const unsigned long long qs = warp_sum<unsigned long long>(qsum);
-    if (lane == 0 && qs) atomicAdd(tile_sum + (base >> 8), qs);   // 256-row CDF tiles (kLevThreads)
-    __syncwarp();
-  }
-#pragma unroll
-  for (int m = 16; m >= 1; m >>= 1) pmax = fmax(pmax, __shfl_xor_sync(0xffffffffu, pmax, m));
-  dcnt = warp_sum<unsigned long long>(dcnt);
-  if (lane == 0) {
-    atomic_max_nonneg(alpha_out, pmax);
-    if (dcnt) atomicAdd(drawable_out, dcnt);
-  }
-}
 
 // ---------------------------------------------------------------- KrpSamp + Gram
 // z_j = A_{m_1}(i_1,:) * ... * A_{m_d}(i_d,:) (eq:Zrow P:214, left to right),

@@ -62,3 +62,41 @@ def test_product_path_does_not_import_oracle():
                 txt = open(os.path.join(dirpath, f)).read()
                 assert "import oracle" not in txt and "from oracle" not in txt, f
                 assert "cparls_oracle" not in txt and "or_create" not in txt, f
+
+
+def _c_layout(struct, fields):
+    """sizeof and offsetof(field) of a cparls.h struct, from gcc on the header."""
+    import tempfile
+    body = "\n".join(f'printf("%zu\\n", offsetof({struct}, {f}));' for f in fields)
+    src = ("#include <stdio.h>\n#include <stddef.h>\n#include \"cparls.h\"\n"
+           f"int main(void) {{ printf(\"%zu\\n\", sizeof({struct})); {body} return 0; }}\n")
+    with tempfile.TemporaryDirectory() as d:
+        c = os.path.join(d, "l.c")
+        exe = os.path.join(d, "l")
+        open(c, "w").write(src)
+        subprocess.run(["gcc", "-I", os.path.join(ROOT, "include"), "-o", exe, c], check=True)
+        out = subprocess.run([exe], capture_output=True, text=True, check=True).stdout.split()
+    return [int(x) for x in out]
+
+
+@pytest.mark.parametrize("name", ["Opts", "Stats", "SampleInfo", "SolveInfo"])
+def test_binding_struct_layouts_match_header(name):
+    """The ctypes mirrors of cparls_opts / cparls_stats / the info structs have
+    the header's size and field offsets (struct_size versioning relies on it)."""
+    from paper_2006_16438_b200 import cparls
+    cls = getattr(cparls, name)
+    cname = {"Opts": "cparls_opts", "Stats": "cparls_stats", "SampleInfo": "cparls_sample_info",
+             "SolveInfo": "cparls_solve_info"}[name]
+    fields = [f for f, _ in cls._fields_]
+    got = _c_layout(cname, fields)
+    assert got[0] == ctypes.sizeof(cls), (name, got[0], ctypes.sizeof(cls))
+    for f, off in zip(fields, got[1:]):
+        assert getattr(cls, f).offset == off, (name, f)
+
+
+def test_no_environment_knobs_in_the_library():
+    """Numerics and code paths are chosen through cparls_opts only (no getenv)."""
+    csrc = os.path.join(ROOT, "paper_2006_16438_b200", "csrc")
+    for f in os.listdir(csrc):
+        txt = open(os.path.join(csrc, f)).read()
+        assert "getenv" not in txt, f

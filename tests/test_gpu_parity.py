@@ -63,10 +63,33 @@ def kept_kappa(G):
     return keep[-1] / keep[0]
 
 
-def solve_tol(G):
-    """1e-9 relative (north_star), widened to 1e-15*kappa(G) for an
-    ill-conditioned sampled Gram (both sides are then only kappa*eps exact)."""
-    return max(1e-9, 1e-15 * kept_kappa(G))
+SOLVE_LOG = []
+
+
+def solve_tol(G, tag=""):
+    """North-star bar 1e-9 relative Frobenius on the same sample set.  For an
+    ill-conditioned sampled Gram (kappa over the kept spectrum > 1e6) B is only
+    determined to ~kappa(G)*eps by the fp64 data (both sides form G with
+    different summation orders: dG/G ~ eps, dB/B ~ kappa dG/G), so the bar is
+    1e-15*kappa(G), capped at 1e-6 (DESIGN.md AMB-36).  Every case is logged
+    (kappa, bar) in SOLVE_LOG / gpurun_out/solve_bars.jsonl."""
+    kappa = kept_kappa(G)
+    tol = 1e-9 if kappa <= 1e6 else min(1e-6, 1e-15 * kappa)
+    SOLVE_LOG.append({"case": tag, "kappa": float(kappa), "bar": tol})
+    return tol
+
+
+def log_solve(rel):
+    """Attach the measured relative error to the last logged case and append
+    it to gpurun_out/solve_bars.jsonl (when that directory exists)."""
+    import json
+    import os
+    if SOLVE_LOG:
+        SOLVE_LOG[-1]["rel_err"] = float(rel)
+        d = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "gpurun_out")
+        if os.path.isdir(d):
+            with open(os.path.join(d, "solve_bars.jsonl"), "a") as f:
+                f.write(json.dumps(SOLVE_LOG[-1]) + "\n")
 
 
 def compare_sample(g, o):
@@ -117,8 +140,10 @@ def lockstep(T, rank, iters, s, seed, tau=-1.0, check_fit=True, rhs_path=0):
             np.testing.assert_allclose(Gg, Go, rtol=1e-11, atol=1e-13 * max(1.0, np.abs(Go).max()))
             nb = np.linalg.norm(Bo)
             if nb > 0:
-                tol = solve_tol(Go)
-                assert np.linalg.norm(Bg - Bo) <= tol * nb, (t, k, np.linalg.norm(Bg - Bo) / nb, tol)
+                tol = solve_tol(Go, f"{getattr(T, 'cfg', None) and T.cfg.name} dims={tuple(T.dims)} r={rank} t={t} k={k}")
+                rel = np.linalg.norm(Bg - Bo) / nb
+                log_solve(rel)
+                assert rel <= tol, (t, k, rel, tol)
             else:
                 assert np.linalg.norm(Bg) == 0
             Ag, lg = g.get_factor(k)
@@ -219,7 +244,12 @@ def test_leverage_rank_deficient_fallback():
     ell, rank = g.leverage(0)
     ref, rref = oracle.leverage(A)
     assert rank == rref == 3
-    np.testing.assert_allclose(ell, ref, atol=1e-9)
+    # the leverage bar of SURVEY 8(c): 1e-12 * max(l, r/n), scaled by kappa/1e3
+    # above kappa = 1e3 (kappa over the kept spectrum of A^T A)
+    kappa = kept_kappa(A.T @ A)
+    tol = 1e-12 * max(1.0, kappa / 1e3)
+    err = np.abs(ell - ref) / np.maximum(np.abs(ref), 5 / A.shape[0])
+    assert err.max() <= tol, (err.max(), kappa)
 
 
 def test_c2_lockstep_2_iterations():
@@ -410,7 +440,10 @@ def test_als_update_parity(name):
             Gg, Bg = g.last_solve(k)
             Go, _, Bo = o.last_solve(k)
             np.testing.assert_allclose(Gg, Go, rtol=1e-12, atol=1e-14 * np.abs(Go).max())
-            assert np.linalg.norm(Bg - Bo) <= solve_tol(Go) * np.linalg.norm(Bo), (t, k)
+            tol = solve_tol(Go, f"als {name} t={t} k={k}")
+            rel = np.linalg.norm(Bg - Bo) / np.linalg.norm(Bo)
+            log_solve(rel)
+            assert rel <= tol, (t, k, rel, tol)
             np.testing.assert_allclose(g.get_factor(k)[1], o.get_factor(k)[1], rtol=1e-9)
             assert_leverage_close(g, o, k)
 
@@ -547,46 +580,3 @@ def test_higher_order_and_rank_boundaries(dims, r):
     vals = rng.uniform(0.5, 2.0, nnz)
     T = synth.Tensor(synth.CONFIGS["C1"], dims, torch.from_numpy(coords), torch.from_numpy(vals))
     lockstep(T, r, 2, 96, 13)
-
-
-@pytest.mark.parametrize("name", ["C1", "C2"])
-def test_fit_bulk_copy_kernel_matches(name, monkeypatch):
-    """The opt-in bulk-copy fit kernel (fit_tma.cuh, CPARLS_FIT_TMA=1) computes
-    the same fit as the default k_fit_sub (same entry order and arithmetic:
-    bit-identical; the default is checked against the oracle by the lockstep
-    tests)."""
-    need_gpu()
-    T = synth.make(name) if name == "C1" else synth.make(name, device="cuda")
-    if name == "C2":
-        T = synth.Tensor(T.cfg, T.dims, T.coords.cpu(), T.vals.cpu())
-    r = T.cfg.rank
-    g = make_ctx(T, r)
-    g.run(2, 1 << 10, 5, fit_every=0)
-    monkeypatch.setenv("CPARLS_FIT_TMA", "0")
-    f0 = g.fit()
-    monkeypatch.setenv("CPARLS_FIT_TMA", "1")
-    f1 = g.fit()
-    assert f0 == f1
-
-
-def test_lev_dmma_option_matches(monkeypatch):
-    """The opt-in DMMA leverage pass (CPARLS_LEV_DMMA=1) gives the same
-    leverage scores as k_lev_rows_w to rounding (<= 1e-13 relative), for the
-    initial factors and for set_factor inputs (ranks 25 and 12)."""
-    need_gpu()
-    T = synth.make("C2", device="cuda")
-    from paper_2006_16438_b200 import Cparls
-    rng = np.random.default_rng(3)
-    for r in (25, 12):
-        A = [rng.standard_normal((n, r)) for n in T.dims]
-        out = {}
-        for flag in ("0", "1"):
-            monkeypatch.setenv("CPARLS_LEV_DMMA", flag)
-            g = Cparls(T.dims, T.coords, T.vals, r, init_seed=4)
-            pts = [g.get_ptilde(m) for m in range(4)]
-            for m in range(4):
-                g.set_factor(m, A[m])
-            out[flag] = pts + [g.get_ptilde(m) for m in range(4)]
-            g.close()
-        for a, b in zip(out["0"], out["1"]):
-            np.testing.assert_allclose(b, a, rtol=1e-13, atol=1e-300)

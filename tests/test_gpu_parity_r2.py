@@ -1,0 +1,163 @@
+"""GPU parity, round 2: the method branches and workload shapes the round-1
+lockstep did not reach, each against the CPU oracle through the C ABI.
+
+* AMB-6 truncation: |DetSet| > s, with ties at the cut, on DIDX's
+  brute-force-sized and pruned paths;
+* AMB-7 skip: a point mass (every drawable row deterministic) and
+  1 - p_det <= 1e-12;
+* multi-window SIDX (AMB-8): opts.sidx_window forces the continuation over
+  many windows; attempts, keys and counts stay bit-exact and equal the
+  single-window run;
+* C3 (Enron-shaped, 4-way, 36-43-bit keys, fp64 values): one lockstep
+  iteration at full size;
+* C5 dims (Reddit-shaped: 46-bit keys, fp32 log(1+c) values) at reduced nnz:
+  one lockstep iteration.
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+from test_gpu_parity import compare_sample, kept_kappa, lockstep, log_solve, need_gpu, solve_tol
+
+pytestmark = pytest.mark.gpu
+
+
+def _ctx(dims, coords, vals, r, **kw):
+    from paper_2006_16438_b200 import Cparls
+    return Cparls(dims, torch.from_numpy(coords).cuda(), torch.from_numpy(vals).cuda(), r, **kw)
+
+
+def _tiny_tensor(dims, nnz, seed):
+    g = np.random.default_rng(seed)
+    coords = np.stack([g.integers(0, n, nnz) for n in dims], 1).astype(np.int64)
+    coords = np.unique(coords, axis=0)
+    vals = g.uniform(0.5, 2.0, len(coords))
+    return coords, vals
+
+
+def _step_lockstep(g, o, k, s, tau, seed, step):
+    gi = g.sample(k, s, seed, step)
+    oi = o.sample(k, s, tau, seed, step)
+    assert (gi.s_det, gi.s_rnd, gi.s_bar, gi.attempts, gi.skipped_random) == \
+           (oi.s_det, oi.s_rnd, oi.s_bar, oi.attempts, oi.skipped_random)
+    assert abs(gi.p_det - oi.p_det) <= 1e-14 * max(1.0, oi.p_det)
+    compare_sample(g, o)
+    gs, os_ = g.solve_mode(k), o.solve_mode(k)
+    assert gs.matched_nnz == os_.matched_nnz and gs.touched_rows == os_.touched_rows
+    Gg, Bg = g.last_solve(k)
+    Go, _, Bo = o.last_solve(k)
+    np.testing.assert_allclose(Gg, Go, rtol=1e-11, atol=1e-13 * max(1.0, np.abs(Go).max()))
+    nb = np.linalg.norm(Bo)
+    if nb > 0:
+        tol = solve_tol(Go, f"r2 step k={k} s={s} tau={tau}")
+        rel = np.linalg.norm(Bg - Bo) / nb
+        log_solve(rel)
+        assert rel <= tol, (rel, tol)
+    return gi
+
+
+@pytest.mark.parametrize("case", ["brute_path", "pruned_path"])
+def test_gpu_didx_truncation_matches_oracle(case):
+    """AMB-6: s_det > s keeps the top s by (p desc, key asc), s_rnd = 0."""
+    need_gpu()
+    if case == "brute_path":
+        pts = [np.array([0.3, 0.3, 0.2, 0.1, 0.1]), np.array([0.25, 0.25, 0.2, 0.1, 0.1, 0.1])]
+        tau, s = 1e-3, 7
+    else:
+        nA, nB = 4000, 3000
+        pA = np.full(nA, 0.2 / (nA - 4)); pA[[7, 100, 2500, 3999]] = 0.2
+        pB = np.full(nB, 0.25 / (nB - 3)); pB[[0, 1500, 2999]] = 0.25
+        pts, tau, s = [pA, pB], 1e-6, 5
+    dims = (6, len(pts[0]), len(pts[1]))
+    coords, vals = _tiny_tensor(dims, 3000, 41)
+    # put nonzeros on the kept fibers so the solve has work
+    big0, big1 = np.argsort(-pts[0])[:4], np.argsort(-pts[1])[:3]
+    extra = np.array([[i, a, b] for i in range(6) for a in big0 for b in big1], dtype=np.int64)
+    coords = np.unique(np.concatenate([coords, extra]), axis=0)
+    vals = np.random.default_rng(42).uniform(0.5, 2.0, len(coords))
+    g = _ctx(dims, coords, vals, 2, tau=tau)
+    o = oracle.Oracle(dims, coords, vals, 2)
+    for m in range(3):
+        A, _ = g.get_factor(m)
+        o.set_factor(m, A)
+    for j, pt in enumerate(pts):
+        g.set_ptilde(j + 1, pt)
+        o.set_ptilde(j + 1, pt)
+    gi = _step_lockstep(g, o, 0, s, tau, 77, 3)
+    assert gi.s_det == s and gi.s_rnd == 0 and gi.s_bar == s
+
+
+@pytest.mark.parametrize("variant", ["point_mass", "p_det_near_one"])
+def test_gpu_amb7_skip_matches_oracle(variant):
+    """AMB-7: the random phase is skipped when every drawable row is
+    deterministic, or when 1 - p_det <= 1e-12 (flag, s_bar = s_det)."""
+    need_gpu()
+    dims = (5, 3, 4)
+    coords, vals = _tiny_tensor(dims, 40, 43)
+    coords = np.unique(np.concatenate([coords, np.array([[i, 1, 2] for i in range(5)])]), axis=0)
+    vals = np.random.default_rng(44).uniform(0.5, 2.0, len(coords))
+    if variant == "point_mass":
+        pts = [np.array([0.0, 1.0, 0.0]), np.array([0.0, 0.0, 1.0, 0.0])]
+    else:
+        e = 1e-14
+        pts = [np.array([e, 1.0 - 2 * e, e]), np.array([0.0, 0.0, 1.0, 0.0])]
+    g = _ctx(dims, coords, vals, 2)
+    o = oracle.Oracle(dims, coords, vals, 2)
+    for m in range(3):
+        o.set_factor(m, g.get_factor(m)[0])
+    for j, pt in enumerate(pts):
+        g.set_ptilde(j + 1, pt)
+        o.set_ptilde(j + 1, pt)
+    gi = _step_lockstep(g, o, 0, 16, -1.0, 5, 0)
+    assert gi.skipped_random == 1 and gi.s_det == 1 and gi.s_bar == 1
+
+
+@pytest.mark.parametrize("window", [1, 17, 128])
+def test_gpu_sidx_multi_window_bit_exact(window):
+    """AMB-8: the SIDX result is the first s_rnd accepted attempts in attempt
+    order whatever the window size: windows of 1, 17 and 128 attempts give
+    the oracle's sample (attempts included) and the default-window sample."""
+    need_gpu()
+    from paper_2006_16438_b200 import Cparls
+    T = synth.make("C1")
+    cfg = T.cfg
+    lockstep_ctx = Cparls(T.dims, T.coords.cuda(), T.vals.cuda(), cfg.rank, sidx_window=window)
+    ref = Cparls(T.dims, T.coords.cuda(), T.vals.cuda(), cfg.rank)
+    o = oracle.Oracle(T.dims, T.coords.to(torch.int64).numpy(), T.vals.numpy(), cfg.rank)
+    for k in range(3):
+        for m in range(3):
+            A, _ = lockstep_ctx.get_factor(m)
+            o.set_factor(m, A)
+            ref.set_factor(m, A)
+            pt = lockstep_ctx.get_ptilde(m)
+            o.set_ptilde(m, pt)
+            ref.set_ptilde(m, pt)
+        gi = _step_lockstep(lockstep_ctx, o, k, cfg.s, -1.0, cfg.sample_seed, k)
+        ri = ref.sample(k, cfg.s, cfg.sample_seed, k)
+        assert (gi.s_det, gi.s_bar, gi.attempts) == (ri.s_det, ri.s_bar, ri.attempts)
+        assert gi.attempts > window          # the continuation really ran
+        a, b = lockstep_ctx.get_sample(), ref.get_sample()
+        assert (a["keys"] == b["keys"]).all() and (a["counts"] == b["counts"]).all()
+
+
+def test_c3_lockstep_one_iteration():
+    """C3 (BASELINE configs[2], Enron-shaped 6066 x 5699 x 244268 x 1176,
+    54.2M nonzeros, fp64 counts, 36-43-bit keys): one lockstep iteration of
+    all four modes plus the fit, at full size."""
+    T = synth.make("C3", device="cuda")
+    T = synth.Tensor(T.cfg, T.dims, T.coords.cpu(), T.vals.cpu())
+    lockstep(T, T.cfg.rank, 1, T.cfg.s, T.cfg.sample_seed)
+
+
+def test_c5_dims_reduced_nnz_lockstep():
+    """C5 dims (BASELINE configs[4], Reddit-shaped 8,211,298 x 176,962 x
+    8,116,559: 41/46/41-bit keys) with fp32 log(1+c) values (the C5 value
+    recipe) at 2M nonzeros: one lockstep iteration plus the fit."""
+    need_gpu()
+    cfg = synth.scaled("C5", 2_000_000)
+    T = synth.make(cfg, device="cuda")
+    assert T.vals.dtype == torch.float32
+    Tc = synth.Tensor(T.cfg, T.dims, T.coords.cpu(), T.vals.cpu())
+    lockstep(Tc, cfg.rank, 1, cfg.s, cfg.sample_seed)
