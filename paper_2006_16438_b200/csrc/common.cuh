@@ -139,6 +139,52 @@ __device__ __forceinline__ void cp_async16_keep(void *smem, const void *gmem, ui
                : "memory");
 }
 
+// ---------------------------------------------------------------- asynchronous mode step
+// Device control block of the host-synchronisation-free mode step
+// (cparls.cu: sample_async / solve_async).  Every size the host used to read
+// back (candidate counts, DIDX list length, s_det, p_det, SIDX progress, s_bar,
+// m_k) lives here; kernels launched with upper-bound grids read them.  When a
+// step needs the host-driven path (a capacity is exceeded, or a rare branch:
+// the AMB-6 truncation, tau < 2^-63) a kernel raises `abort`; every guarded
+// kernel after it returns at entry, so the state stays exactly as before that
+// step, and the host redoes the step with the host-driven sampler at its next
+// synchronisation.
+struct StepCtl {
+  int abort;                    // != 0: guarded kernels return at entry
+  int skip;                     // AMB-7: the random phase of this step is skipped
+  int64_t abort_step;         // global step (t*D + k) that raised abort (first)
+  int64_t ncand[kMaxModes];   // DIDX candidates per other mode
+  int64_t nlist;              // DIDX list length (current level)
+  int64_t sdet, s_rnd, have, nuniq, sbar, attempts;
+  double pdet;
+  // SIDX decoupled look-back (k_sidx_run)
+  unsigned long long sidx_next_tile;
+  unsigned sidx_epoch;
+  int sidx_done;
+  int64_t scan_total;         // scratch total of the device-count scans
+  int64_t nseg;               // RHS (window, fiber) segments of the step
+  // statistics accumulated on the device, folded into cparls_stats at a sync
+  int64_t st_steps, st_sum_mk, st_sum_sbar, st_sum_attempts, st_sum_sdet, st_sum_touched;
+  int64_t st_last_mk, st_last_sbar, st_last_attempts;
+  int64_t st_touched[kMaxModes];
+};
+
+#define CPARLS_GUARD(ctl)                  \
+  do {                                     \
+    if ((ctl) != nullptr && (ctl)->abort) \
+      return;                              \
+  } while (0)
+
+// raise abort for global step `step` (the first raise records its step)
+__device__ __forceinline__ void step_abort(StepCtl *ctl, int64_t step) {
+  if (atomicCAS(&ctl->abort, 0, 1) == 0) ctl->abort_step = step;
+}
+
+// count that may live on the device: *n_dev if given, else n
+__device__ __forceinline__ int64_t dcount(int64_t n, const int64_t *n_dev) {
+  return n_dev ? *n_dev : n;
+}
+
 // first index i in [0,n) with C[i] > t (upper_bound); C non-decreasing
 __device__ __forceinline__ int64_t upper_bound_u64(const uint64_t *__restrict__ C, int64_t n, uint64_t t) {
   int64_t lo = 0, len = n;

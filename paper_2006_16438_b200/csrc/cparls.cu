@@ -20,6 +20,7 @@
 #include "../../include/cparls.h"
 #include "comm.cuh"
 #include "kernels.cuh"
+#include "sampler.cuh"
 
 using namespace cparls;
 
@@ -64,10 +65,8 @@ struct DevScalars {
 constexpr int kHscrDrawable = 0;                     // [0, kMaxModes): drawable rows per other mode
 constexpr int kHscrSidx = kHscrDrawable + kMaxModes; // 2: SIDX accepted total, last accepted attempt
 constexpr int kHscrCand = kHscrSidx + 2;             // [.., +kMaxModes): DIDX candidate counts
-constexpr int kHscrMk = kHscrCand + kMaxModes;       // m_k of the last solve
-constexpr int kHscrTouched = kHscrMk + 1;            // touched rows of the last solve
 constexpr int kHscrSlots = 64;
-static_assert(kHscrTouched < kHscrSlots, "pinned scratch layout");
+static_assert(kHscrCand + kMaxModes <= kHscrSlots, "pinned scratch layout");
 
 struct cparls_ctx {
   int D = 0, r = 0, ld = 0;
@@ -89,6 +88,15 @@ struct cparls_ctx {
   SolveDev *sd = nullptr;
   double *lam_model = nullptr;   // lambda of the model (AMB-31)
   DevScalars *dv = nullptr;
+  StepCtl *ctl = nullptr;        // asynchronous mode step control (common.cuh)
+  void *hctl = nullptr;          // pinned host copy of *ctl
+  StepCtl ctl_seen{};            // device statistics already folded into stats
+  int64_t s_cur = 0;             // s of the current sample (upper bound of s_bar)
+  bool sample_pulled = false;    // host sbar/sdet/... hold the current sample's values
+  unsigned long long *tile_state = nullptr;   // SIDX look-back tiles (sampler.cuh)
+  double *fitbuf = nullptr;      // per-iteration fit values of an asynchronous run
+  int64_t fitbuf_cap = 0;
+  int64_t tile_cap = 0;
   // scratch
   double *M = nullptr;
   uint8_t *touched = nullptr;
@@ -180,7 +188,6 @@ struct cparls_ctx {
   cudaStream_t side = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   bool fx_pending = false;
-  int stats_pending_k = -1;     // a solve's m_k / touched rows copied to hscr[kHscrMk..], folded at the next sync
   cudaEvent_t stage_ev[2] = {nullptr, nullptr};
   // frozen stratified fit sample (fitest.cuh, AMB-32)
   bool have_fs = false;
@@ -189,7 +196,6 @@ struct cparls_ctx {
   int32_t *fs_idx[kMaxModes] = {nullptr};
   double *fs_x = nullptr;
   int32_t *seg_j = nullptr;
-  // RHS hot rows per mode (warp-private accumulation, see rhs.cuh)
   int64_t nfib[kMaxModes] = {0};
 };
 
@@ -257,28 +263,45 @@ bool is_device_ptr(const void *p) {
   return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
 }
 
-void fold_step_stats(cparls_ctx *c, int k, int64_t mk, unsigned long long touched) {
-  c->mk = mk;
-  c->stats.bytes_rhs += (double)mk * (4.0 + (c->vf32 ? 4.0 : 8.0)) + (double)touched * c->r * 8.0 * 2;
-  c->stats.last_matched_nnz = mk;
-  c->stats.sum_matched_nnz += mk;
-  c->stats.touched_rows[k] = (int64_t)touched;
+// Fold the step statistics the asynchronous kernels accumulated in the step
+// control (StepCtl::st_*) into cparls_stats: the deltas since the last fold
+// (SURVEY 8(d) byte model; ctl_seen holds the values already folded).
+void fold_ctl_stats(cparls_ctx *c) {
+  const StepCtl &h = *reinterpret_cast<const StepCtl *>(c->hctl);
+  StepCtl &o = c->ctl_seen;
+  const double v = c->vf32 ? 4.0 : 8.0;
+  const int d = c->D - 1;
+  const double dmk = (double)(h.st_sum_mk - o.st_sum_mk), dsb = (double)(h.st_sum_sbar - o.st_sum_sbar);
+  const double datt = (double)(h.st_sum_attempts - o.st_sum_attempts);
+  const double dtouch = (double)(h.st_sum_touched - o.st_sum_touched);
+  c->stats.bytes_rhs += dmk * (4.0 + v) + dtouch * c->r * 8.0 * 2;
+  c->stats.bytes_gram += dsb * (d * c->r * 8.0 + 16.0);
+  c->stats.bytes_lookup += dsb * 16.0;
+  c->stats.bytes_sample += datt * d * 8.0;
+  c->stats.sum_matched_nnz += (int64_t)dmk;
+  if (h.st_steps != o.st_steps) {
+    c->stats.last_matched_nnz = h.st_last_mk;
+    c->mk = h.st_last_mk;
+    for (int k = 0; k < c->D; ++k) c->stats.touched_rows[k] = h.st_touched[k];
+  }
+  if (h.st_sum_sbar != o.st_sum_sbar || h.st_sum_attempts != o.st_sum_attempts) {
+    c->stats.last_s_bar = h.st_last_sbar;
+    c->stats.last_attempts = h.st_last_attempts;
+  }
+  o = h;
 }
 
 void ktimers_resolve(cparls_ctx *c);
 
-// Stream synchronisation of the context: folds the counters a solve left in
-// pinned scratch and resolves the per-kernel event timers (all recorded
-// before this point on the stream, so complete).  count = false for the
-// synchronisations of the stats calls themselves.
+// Stream synchronisation of the context: reads the step control back (the
+// statistics of the asynchronous steps are folded) and resolves the per-kernel
+// event timers (all recorded before this point on the stream, so complete).
+// count = false for the synchronisations of the stats calls themselves.
 void sync(cparls_ctx *c, bool count = true) {
+  if (c->ctl) CK(cudaMemcpyAsync(c->hctl, c->ctl, sizeof(StepCtl), cudaMemcpyDeviceToHost, c->st));
   CK(cudaStreamSynchronize(c->st));
   if (count) c->stats.host_syncs++;
-  if (c->stats_pending_k >= 0) {   // a solve without an info request left its counters here
-    const int k = c->stats_pending_k;
-    c->stats_pending_k = -1;
-    fold_step_stats(c, k, (int64_t)c->hscr[kHscrMk], (unsigned long long)c->hscr[kHscrTouched]);
-  }
+  if (c->ctl) fold_ctl_stats(c);
   ktimers_resolve(c);
 }
 
@@ -475,14 +498,14 @@ void launch_solve_rows(cparls_ctx *c, double *M, int64_t n, double *B, int64_t g
   if (dmma) {
     const size_t sm = sizeof(double) * solve_dmma_smem_d(ld);
     switch (ld / 8) {
-      case 1: k_solve_dmma<1><<<(unsigned)grid, kRowThreads, sm, c->st>>>(M, n, r, ld, c->sd, B, c->gpart, &c->dv->touched, zero_m, fscale); break;
-      case 2: k_solve_dmma<2><<<(unsigned)grid, kRowThreads, sm, c->st>>>(M, n, r, ld, c->sd, B, c->gpart, &c->dv->touched, zero_m, fscale); break;
-      case 3: k_solve_dmma<3><<<(unsigned)grid, kRowThreads, sm, c->st>>>(M, n, r, ld, c->sd, B, c->gpart, &c->dv->touched, zero_m, fscale); break;
-      default: k_solve_dmma<4><<<(unsigned)grid, kRowThreads, sm, c->st>>>(M, n, r, ld, c->sd, B, c->gpart, &c->dv->touched, zero_m, fscale); break;
+      case 1: k_solve_dmma<1><<<(unsigned)grid, kRowThreads, sm, c->st>>>(M, n, r, ld, c->sd, B, c->gpart, &c->dv->touched, zero_m, fscale, c->ctl); break;
+      case 2: k_solve_dmma<2><<<(unsigned)grid, kRowThreads, sm, c->st>>>(M, n, r, ld, c->sd, B, c->gpart, &c->dv->touched, zero_m, fscale, c->ctl); break;
+      case 3: k_solve_dmma<3><<<(unsigned)grid, kRowThreads, sm, c->st>>>(M, n, r, ld, c->sd, B, c->gpart, &c->dv->touched, zero_m, fscale, c->ctl); break;
+      default: k_solve_dmma<4><<<(unsigned)grid, kRowThreads, sm, c->st>>>(M, n, r, ld, c->sd, B, c->gpart, &c->dv->touched, zero_m, fscale, c->ctl); break;
     }
   } else {
     RSWITCH(r, k_solve_rows_t<RM><<<(unsigned)grid, kRowThreads, solve_smem(r, ld), c->st>>>(
-                   M, n, r, ld, c->sd, B, c->gpart, &c->dv->touched, zero_m, fscale));
+                   M, n, r, ld, c->sd, B, c->gpart, &c->dv->touched, zero_m, fscale, c->ctl));
   }
 }
 size_t krp_smem(int r, int ld) { return sizeof(double) * (tile_d(ld) + kRowThreads + 64); }
@@ -537,11 +560,13 @@ int64_t row_grid(cparls_ctx *c, int64_t ntiles) { return std::max<int64_t>(1, st
 // ---------------------------------------------------------------- leverage
 // rows -> p~, integer CDF (AMB-9/11).  lam != null also
 // normalizes A_k in place by lam.
+// Guarded by the context's step control (an aborted asynchronous step leaves
+// the mode's factor, p~, CDF, alpha and drawable count untouched).
 void lev_rows_and_cdf(cparls_ctx *c, int k, const double *lam) {
   const int64_t n = c->dims[k];
   const int64_t nt = ceil_div(n, kLevThreads);
-  CK(cudaMemsetAsync(&c->md[k]->alpha, 0, sizeof(double), c->st));
-  CK(cudaMemsetAsync(&c->md[k]->drawable, 0, sizeof(long long), c->st));
+  k_lev_reset<<<1, 1, 0, c->st>>>(c->md[k], c->ctl);
+  CK_LAUNCH();
   {
     const unsigned g = (unsigned)row_grid(c, ceil_div(n, kWarpRows * (kRowThreads / 32)));
     CK(cudaMemsetAsync(c->tile_u64, 0, sizeof(uint64_t) * nt, c->st));
@@ -549,15 +574,15 @@ void lev_rows_and_cdf(cparls_ctx *c, int k, const double *lam) {
     RSWITCH(c->r, k_lev_rows_w<RM><<<g, kRowThreads, lev_w_smem(c->r, c->ld), c->st>>>(
                       c->A[k], n, c->r, c->ld, lam, c->md[k], c->pt[k], c->C[k],
                       reinterpret_cast<unsigned long long *>(c->tile_u64), &c->md[k]->alpha,
-                      reinterpret_cast<unsigned long long *>(&c->md[k]->drawable)));
+                      reinterpret_cast<unsigned long long *>(&c->md[k]->drawable), c->ctl));
     kt.stop();
   }
   CK_LAUNCH();
-  k_scan_u64_single<<<1, kScanThreads, 0, c->st>>>(c->tile_u64, nt);
+  k_scan_u64_single<<<1, kScanThreads, 0, c->st>>>(c->tile_u64, nt, c->ctl);
   CK_LAUNCH();
-  k_cdf_final<<<(unsigned)nt, kLevThreads, 0, c->st>>>(c->C[k], n, c->tile_u64);
+  k_cdf_final<<<(unsigned)nt, kLevThreads, 0, c->st>>>(c->C[k], n, c->tile_u64, c->ctl);
   CK_LAUNCH();
-  LAUNCHED(c, 3);
+  LAUNCHED(c, 4);
   c->stats.bytes_leverage += (double)n * (c->r * 8.0 * (lam ? 2 : 1) + 16.0);
 }
 
@@ -588,7 +613,9 @@ void reset_lambda(cparls_ctx *c) {
   sync(c);
 }
 
-OtherModes other_modes(cparls_ctx *c, int k, bool need_alpha) {
+// The other modes of k (ascending, AMB-1); alpha / drawable counts are read by
+// the kernels from the modes' ModeDev (no host copy).
+OtherModes other_modes(cparls_ctx *c, int k) {
   OtherModes om{};
   om.d = c->D - 1;
   uint64_t mult = 1;
@@ -599,14 +626,10 @@ OtherModes other_modes(cparls_ctx *c, int k, bool need_alpha) {
     om.pt[j] = c->pt[m];
     om.C[j] = c->C[m];
     om.A[j] = c->A[m];
+    om.md[j] = c->md[m];
     om.mult[j] = mult;
     mult *= (uint64_t)c->dims[m];
     ++j;
-  }
-  if (need_alpha) {
-    for (int j = 0; j < om.d; ++j)
-      CK(cudaMemcpyAsync(&om.alpha[j], &c->md[om.mode[j]]->alpha, sizeof(double), cudaMemcpyDeviceToHost, c->st));
-    sync(c);
   }
   return om;
 }
@@ -899,6 +922,15 @@ void alloc_sample_buffers(cparls_ctx *c, int64_t s) {
   CK(cudaMemsetAsync(c->hkey, 0xFF, sizeof(unsigned long long) * hs, c->st));
   CK(cudaMemsetAsync(c->hcnt, 0, sizeof(uint32_t) * hs, c->st));
   ensure_i64part(c, cap);   // scans over the accepted draws and the sample (<= s)
+  // SIDX look-back tiles of the asynchronous sampler: attempts <= the cap (AMB-7)
+  const int64_t cap_att = c->opts.attempt_cap > 0 ? c->opts.attempt_cap : 1024 * cap + 65536;
+  const int64_t tiles = ceil_div(cap_att, kSidxTile) + 2;
+  if (tiles > c->tile_cap) {
+    dfree(c, c->tile_state);
+    c->tile_state = dalloc_t<unsigned long long>(c, tiles);
+    CK(cudaMemsetAsync(c->tile_state, 0, sizeof(unsigned long long) * tiles, c->st));   // epoch 0: unpublished
+    c->tile_cap = tiles;
+  }
   c->scap = cap;
 }
 
@@ -1017,7 +1049,7 @@ int64_t run_didx(cparls_ctx *c, const OtherModes &om, double tau, int *which) {
   return nlist;
 }
 
-void sample_impl(cparls_ctx *c, int k, int64_t s, uint64_t seed, uint64_t step, cparls_sample_info *info) {
+void sample_host(cparls_ctx *c, int k, int64_t s, uint64_t seed, uint64_t step) {
   Phase ph(c, &c->stats.ms_sample);
   c->have_sample = false;
   c->have_lookup = false;
@@ -1025,7 +1057,7 @@ void sample_impl(cparls_ctx *c, int k, int64_t s, uint64_t seed, uint64_t step, 
   alloc_sample_buffers(c, s);
   double tau = c->tau;
   if (tau < 0) tau = 1.0 / (double)s;   // tau = 1/s
-  OtherModes om = other_modes(c, k, true);
+  OtherModes om = other_modes(c, k);
   const int d = om.d;
   // drawable counts (rows with q > 0): copied into pinned scratch now, read
   // after the p_det sync below (stream order), no sync of their own
@@ -1198,75 +1230,246 @@ void sample_impl(cparls_ctx *c, int k, int64_t s, uint64_t seed, uint64_t step, 
   c->attempts = attempts;
   c->skipped = skipped;
   c->have_sample = true;
-  c->stats.last_s_bar = c->sbar;
-  c->stats.last_attempts = attempts;
-  if (info) {
-    info->s_det = sdet;
-    info->s_rnd = s_rnd;
-    info->s_bar = c->sbar;
-    info->attempts = attempts;
-    info->p_det = p_det;
-    info->skipped_random = skipped;
-  }
+  c->s_cur = s;
   ph.end();
 }
 
+// ---------------------------------------------------------------- asynchronous sampling
+// SkrpLev (Alg. 1) for mode k with every size on the device
+// (StepCtl, sampler.cuh): no host synchronisation.  The rare branches (more
+// than kSmallSortMax candidates of a mode, a DIDX level beyond the list
+// buffers or didx_cap, the AMB-6 truncation, tau < 2^-63, the SIDX attempt
+// cap) raise ctl->abort; the host then redoes the step with sample_host.
+void sample_async(cparls_ctx *c, int k, int64_t s, uint64_t seed, uint64_t step) {
+  if (s < 1) throw ApiError(CPARLS_EINVAL, "s must be >= 1");
+  alloc_sample_buffers(c, s);
+  double tau = c->tau;
+  if (tau < 0) tau = 1.0 / (double)s;   // tau = 1/s
+  OtherModes om = other_modes(c, k);
+  const int d = om.d;
+  StepCtl *ctl = c->ctl;
+  const int64_t st64 = (int64_t)step;
+  Phase ph(c, &c->stats.ms_sample);
+  // ---- DIDX candidates per other mode, sorted by p~ descending
+  for (int j = 0; j < d; ++j) {
+    const int64_t n = om.n[j];
+    const int64_t nb = ceil_div(n, kScanTile);
+    k_cand_count<<<(unsigned)nb, kScanThreads, 0, c->st>>>(om, j, tau, c->i64part, ctl);
+    CK_LAUNCH();
+    k_scan_part<<<1, kScanThreads, 0, c->st>>>(c->i64part, nb, &ctl->ncand[j], nullptr, ctl);
+    CK_LAUNCH();
+    k_cand_scatter<<<(unsigned)nb, kScanThreads, 0, c->st>>>(om, j, tau, c->i64part, c->ckey[j], c->cidx[j], ctl);
+    CK_LAUNCH();
+    k_small_sort_pairs_dev<<<1, kSmallSortThreads, 0, c->st>>>(c->ckey[j], c->cidx[j], &ctl->ncand[j], ctl, st64);
+    CK_LAUNCH();
+    LAUNCHED(c, 4);
+    c->stats.bytes_sample += (double)n * 8.0;
+  }
+  // ---- DIDX levels: the exact canonical predicate decides membership
+  const int64_t cap = c->opts.didx_cap > 0 ? c->opts.didx_cap : (int64_t(1) << 22);
+  const int64_t lcap = c->lcap;
+  ensure_i64part(c, lcap);
+  const unsigned gl = (unsigned)ceil_div(kSmallSortMax, 256);
+  const unsigned gs = 148 * 4;
+  k_didx_level0<<<gl, 256, 0, c->st>>>(c->ckey[0], c->cidx[0], 0, c->lkey[0], c->lpp[0], &ctl->ncand[0], ctl);
+  CK_LAUNCH();
+  k_didx_start<<<1, 1, 0, c->st>>>(ctl, lcap, cap, st64);
+  CK_LAUNCH();
+  LAUNCHED(c, 2);
+  int cur = 0;
+  for (int l = 1; l < d; ++l) {
+    k_didx_count<<<gs, 256, 0, c->st>>>(c->lpp[cur], lcap, c->ckey[l], 0, om, l, tau, c->lcnt, &ctl->nlist,
+                                        &ctl->ncand[l], ctl);
+    CK_LAUNCH();
+    exclusive_scan_i64_dev(c->lcnt, c->loff, lcap, &ctl->nlist, c->i64part, &ctl->scan_total, c->st, ctl);
+    k_didx_check<<<1, 1, 0, c->st>>>(ctl, lcap, cap, st64);
+    CK_LAUNCH();
+    k_didx_emit<<<gs, 256, 0, c->st>>>(c->lkey[cur], c->lpp[cur], lcap, c->lcnt, c->loff, c->ckey[l], c->cidx[l],
+                                       om.mult[l], c->lkey[cur ^ 1], c->lpp[cur ^ 1], &ctl->nlist, ctl);
+    CK_LAUNCH();
+    k_didx_advance<<<1, 1, 0, c->st>>>(ctl);
+    CK_LAUNCH();
+    LAUNCHED(c, 7);
+    cur ^= 1;
+  }
+  k_didx_finish<<<1, 1, 0, c->st>>>(ctl, s, tau < 1.0842021724855044e-19 ? 1 : 0, st64);
+  CK_LAUNCH();
+  // p_det = sum_{DetSet} p_i (compensated, the host path's reduction order)
+  const int nbs = 64;
+  k_sum_dd<<<nbs, 256, 0, c->st>>>(c->lpp[cur], 0, c->ddpart, &ctl->sdet, ctl);
+  CK_LAUNCH();
+  k_sum_dd_final<<<1, 32, 0, c->st>>>(c->ddpart, nbs, &ctl->pdet, ctl);
+  CK_LAUNCH();
+  const unsigned gsamp = (unsigned)ceil_div(s, 256);
+  k_det_emit<<<gsamp, 256, 0, c->st>>>(c->lkey[cur], c->lpp[cur], 0, c->skey, c->sw2, c->sp, c->scnt, c->sisdet,
+                                       &ctl->sdet, ctl);
+  CK_LAUNCH();
+  LAUNCHED(c, 4);
+  // ---- SIDX (Alg. 2): one persistent kernel until s_rnd acceptances
+  k_sidx_prep<<<1, 1, 0, c->st>>>(ctl, om, s);
+  CK_LAUNCH();
+  {
+    const unsigned gsidx = (unsigned)std::min<int64_t>(148 * 2, ceil_div(s, kSidxTile) + 8);
+    k_sidx_run<<<gsidx, kSidxThreads, 0, c->st>>>(om, tau, (uint32_t)seed, (uint32_t)(seed >> 32), (uint32_t)step,
+                                                  c->opts.attempt_cap, ctl, c->tile_state, c->tile_cap, c->rkey,
+                                                  c->rp, st64);
+    CK_LAUNCH();
+  }
+  // ---- CIDX: unique rows in first-draw order (AMB-35)
+  k_cidx_insert_first<<<gsamp, 256, 0, c->st>>>(c->rkey, c->rp, 0, c->hkey, c->hcnt, c->hp, c->hfirst, c->hsize - 1,
+                                                 &ctl->have, ctl);
+  CK_LAUNCH();
+  k_cidx_first_flags<<<gsamp, 256, 0, c->st>>>(c->rkey, 0, c->hkey, c->hfirst, c->hsize - 1, c->rflag, c->rslot,
+                                               &ctl->have, ctl);
+  CK_LAUNCH();
+  exclusive_scan_i64_dev(c->rflag, c->rpos, s, &ctl->have, c->i64part, &ctl->nuniq, c->st, ctl);
+  k_cidx_emit_first<<<gsamp, 256, 0, c->st>>>(c->rflag, c->rpos, c->rslot, 0, c->hkey, c->hcnt, c->hp, c->hfirst,
+                                              &ctl->pdet, 0, 0, c->skey, c->sw2, c->sp, c->scnt, c->sisdet, ctl);
+  CK_LAUNCH();
+  k_sample_finish<<<1, 1, 0, c->st>>>(ctl);
+  CK_LAUNCH();
+  LAUNCHED(c, 10);
+  c->smode = k;
+  c->s_cur = s;
+  c->have_sample = true;
+  c->have_lookup = false;
+  c->sample_pulled = false;
+  ph.end();
+}
+
+// The sample scalars of the host path into the step control (the solve reads
+// them there).  The stream is idle after sync(), so the control block can be
+// rewritten whole.
+void push_sample_state(cparls_ctx *c) {
+  sync(c);
+  StepCtl h = *reinterpret_cast<const StepCtl *>(c->hctl);
+  h.sdet = c->sdet;
+  h.s_rnd = c->s_rnd;
+  h.skip = c->skipped;
+  h.have = c->skipped ? 0 : c->s_rnd;
+  h.nuniq = c->sbar - c->sdet;
+  h.sbar = c->sbar;
+  h.attempts = c->attempts;
+  h.pdet = c->p_det;
+  h.st_sum_sbar += c->sbar;       // (the host path counted its own sampling bytes)
+  h.st_sum_sdet += c->sdet;
+  h.st_last_sbar = c->sbar;
+  h.st_last_attempts = c->attempts;
+  c->ctl_seen.st_sum_attempts = h.st_sum_attempts;
+  CK(cudaMemcpyAsync(c->ctl, &h, sizeof(StepCtl), cudaMemcpyHostToDevice, c->st));
+  sync(c);
+}
+
+// Sample scalars of the current sample from the device (after an
+// asynchronous sample) into the host fields the getters use.
+void pull_sample_state(cparls_ctx *c) {
+  if (c->sample_pulled) return;
+  sync(c);
+  const StepCtl &h = *reinterpret_cast<const StepCtl *>(c->hctl);
+  if (h.abort) throw ApiError(CPARLS_ESTATE, "the asynchronous step was aborted");
+  c->sdet = h.sdet;
+  c->s_rnd = h.s_rnd;
+  c->sbar = h.sbar;
+  c->p_det = h.pdet;
+  c->attempts = h.attempts;
+  c->skipped = h.skip;
+  c->sample_pulled = true;
+}
+
+// Clears an abort raised by an asynchronous step; returns that step, or -1.
+int64_t clear_abort(cparls_ctx *c) {
+  sync(c);
+  const StepCtl &h = *reinterpret_cast<const StepCtl *>(c->hctl);
+  if (!h.abort) return -1;
+  const int64_t step = h.abort_step;
+  CK(cudaMemsetAsync(&c->ctl->abort, 0, sizeof(int), c->st));
+  sync(c);
+  return step;
+}
+
+// cparls_sample: the asynchronous sampler, then (after one synchronisation)
+// the host-driven one if it aborted.
+void sample_impl(cparls_ctx *c, int k, int64_t s, uint64_t seed, uint64_t step, cparls_sample_info *info) {
+  c->have_sample = false;
+  if (s < 1) throw ApiError(CPARLS_EINVAL, "s must be >= 1");
+  const bool async_ok = !c->sample_sort;
+  if (async_ok) {
+    sample_async(c, k, s, seed, step);
+    if (clear_abort(c) >= 0) {
+      sample_host(c, k, s, seed, step);
+      push_sample_state(c);
+    }
+  } else {
+    sample_host(c, k, s, seed, step);
+    push_sample_state(c);
+  }
+  c->sample_pulled = false;
+  pull_sample_state(c);
+  c->stats.last_s_bar = c->sbar;
+  c->stats.last_attempts = c->attempts;
+  if (info) {
+    info->s_det = c->sdet;
+    info->s_rnd = c->s_rnd;
+    info->s_bar = c->sbar;
+    info->attempts = c->attempts;
+    info->p_det = c->p_det;
+    info->skipped_random = c->skipped;
+  }
+}
+
 // ---------------------------------------------------------------- solve
+// TnsrSamp lookup of the current sample's fibers; s_bar on the
+// device (at most s_cur).
 void lookup_impl(cparls_ctx *c, int k) {
   ModeIndex &ix = c->idx[k];
-  const int64_t sbar = c->sbar;
-  if (sbar > 0) {
-    k_lookup<<<(unsigned)ceil_div(sbar, 256), 256, 0, c->st>>>(c->skey, sbar, ix.key, ix.dir, ix.shift, ix.nbkt,
-                                                               key_remap(c, k),
-                                                               c->lo, c->len);
-    CK_LAUNCH();
-    LAUNCHED(c, 1);
-  }
-  exclusive_scan_i64(c->len, c->off, sbar, c->i64part, &c->dv->mk, c->st);
-  LAUNCHED(c, 3);
+  const int64_t smax = std::max<int64_t>(c->s_cur, 1);
+  k_lookup<<<(unsigned)ceil_div(smax, 256), 256, 0, c->st>>>(c->skey, smax, ix.key, ix.dir, ix.shift, ix.nbkt,
+                                                             key_remap(c, k), c->lo, c->len, &c->ctl->sbar, c->ctl);
+  CK_LAUNCH();
+  exclusive_scan_i64_dev(c->len, c->off, smax, &c->ctl->sbar, c->i64part, &c->dv->mk, c->st, c->ctl);
+  LAUNCHED(c, 4);
   c->have_lookup = true;
-  c->stats.bytes_lookup += (double)sbar * 16.0;
 }
 
 // per-column fixed-point scales 2^e_c of the sampled RHS (kernels.cuh, AMB-35)
-void launch_fixed_scales(cparls_ctx *c, int64_t sbar, cudaStream_t st) {
+void launch_fixed_scales(cparls_ctx *c, cudaStream_t st) {
   const int nbc = 148;
-  k_colabs_part<<<nbc, 256, 0, st>>>(c->Z, c->sw2, sbar, c->r, c->ld, c->gpart);
+  k_colabs_part<<<nbc, 256, 0, st>>>(c->Z, c->sw2, c->s_cur, c->r, c->ld, c->gpart, &c->ctl->sbar, c->ctl);
   CK_LAUNCH();
-  k_fixed_scales<<<1, 64, 0, st>>>(c->gpart, nbc, c->r, &c->dv->maxabs, c->dupmax, c->fx_scale);
+  k_fixed_scales<<<1, 64, 0, st>>>(c->gpart, nbc, c->r, &c->dv->maxabs, c->dupmax, c->fx_scale, c->ctl);
   CK_LAUNCH();
   LAUNCHED(c, 2);
 }
 
+// One sketched mode update (Alg. 3) from the current sample, every
+// size on the device: KrpSamp + sampled Gram, lookup, RHS, B = M G^+,
+// normalize, leverage refresh.  No host synchronisation (the bucketed RHS,
+// rhs_path 2, reads m_k on the host).
 void solve_impl(cparls_ctx *c, int k, cparls_solve_info *info) {
   if (!c->have_sample || c->smode != k) throw ApiError(CPARLS_ESTATE, "solve_mode without a current sample of this mode");
   const int r = c->r, ld = c->ld;
   const int64_t nk = c->dims[k];
-  const int64_t sbar = c->sbar;
-  OtherModes om = other_modes(c, k, false);
-  // K6: KrpSamp + sampled Gram
+  const int64_t smax = std::max<int64_t>(c->s_cur, 1);   // s_bar <= s
+  StepCtl *ctl = c->ctl;
+  OtherModes om = other_modes(c, k);
+  // K6: KrpSamp + sampled Gram (every block writes its partial; s_bar = 0 gives G = 0)
   {
     Phase ph(c, &c->stats.ms_gram);
-    if (sbar > 0) {
-      const int64_t grid = row_grid(c, ceil_div(sbar, kRowThreads));
-      RSWITCH(r, k_krp_gram_t<RM><<<(unsigned)grid, kRowThreads, krp_smem(r, ld), c->st>>>(c->skey, c->sw2, sbar, om,
-                                                                                             r, ld, c->Z, c->gpart));
-      CK_LAUNCH();
-      k_pairs_reduce<<<pairs_reduce_grid(r), 256, 0, c->st>>>(c->gpart, grid, r, c->sd->G);
-      CK_LAUNCH();
-      LAUNCHED(c, 2);
-    } else {
-      CK(cudaMemsetAsync(c->sd->G, 0, sizeof(double) * r * r, c->st));
-    }
-    c->stats.bytes_gram += (double)sbar * (om.d * r * 8.0 + 16.0);
+    const int64_t grid = row_grid(c, ceil_div(smax, kRowThreads));
+    RSWITCH(r, k_krp_gram_t<RM><<<(unsigned)grid, kRowThreads, krp_smem(r, ld), c->st>>>(
+                   c->skey, c->sw2, smax, om, r, ld, c->Z, c->gpart, &ctl->sbar, ctl));
+    CK_LAUNCH();
+    k_pairs_reduce<<<pairs_reduce_grid(r), 256, 0, c->st>>>(c->gpart, grid, r, c->sd->G, ctl);
+    CK_LAUNCH();
+    LAUNCHED(c, 2);
     ph.end();
   }
   // fixed-point scales of the atomic RHS on the side stream, overlapping K7
   c->fx_pending = false;
-  if (sbar > 0 && c->rhs_fixed && c->opts.rhs_path != 2 && c->opts.rhs_path != 3) {
+  if (c->rhs_fixed && c->opts.rhs_path != 2 && c->opts.rhs_path != 3) {
     CK(cudaEventRecord(c->ev_fork, c->st));
     CK(cudaStreamWaitEvent(c->side, c->ev_fork, 0));
-    launch_fixed_scales(c, sbar, c->side);
+    launch_fixed_scales(c, c->side);
     CK(cudaEventRecord(c->ev_join, c->side));
     c->fx_pending = true;
   }
@@ -1278,28 +1481,19 @@ void solve_impl(cparls_ctx *c, int k, cparls_solve_info *info) {
   }
   // this rank's rows of B (all rows on one GPU); M is zero elsewhere
   const int64_t r0 = c->row_lo[k], nown = c->row_hi[k] - c->row_lo[k];
-  // K8+K9a path: bucketed RHS with the solve fused (rhs_bucket.cuh) for big
-  // modes, atomic reductions into M + k_solve_rows_t otherwise (same math)
-  int64_t mk_host = -1;
+  const int path = c->opts.rhs_path;
+  c->fx_on = c->rhs_fixed && path != 3;
   bool use_bkt = false;
-  {
-    const int path = c->opts.rhs_path;
-    c->fx_on = c->rhs_fixed && path != 3;
-    const bool ok = r <= 32 && sbar < kBktMaxSbar;
-    // auto = atomic: on C4 the bucketed path measured 14.8 ms per mode step
-    // (count 0.6 + place 2.2 + accumulate 7.2 + solve 1.3) against 7.0 + 0.8
-    // for k_rhs at its reduction ceiling + k_solve_rows_t
-    use_bkt = ok && path == 2;
-    if (path == 2 && !ok) throw ApiError(CPARLS_EINVAL, "rhs_path 2 needs r <= 32 and s_bar < 2^24");
-    if (use_bkt) {
-      mk_host = read_dev(c, &c->dv->mk);
-      if (mk_host >= (int64_t(1) << 32)) {
-        if (path == 2) throw ApiError(CPARLS_EINVAL, "rhs_path 2 needs m_k < 2^32");
-        use_bkt = false;
-      }
-    }
+  int64_t mk_host = -1;
+  if (path == 2) {   // bucketed RHS (opt-in): sizes on the host
+    pull_sample_state(c);
+    if (!(r <= 32 && c->sbar < kBktMaxSbar)) throw ApiError(CPARLS_EINVAL, "rhs_path 2 needs r <= 32 and s_bar < 2^24");
+    mk_host = read_dev(c, &c->dv->mk);
+    if (mk_host >= (int64_t(1) << 32)) throw ApiError(CPARLS_EINVAL, "rhs_path 2 needs m_k < 2^32");
+    use_bkt = true;
   }
   if (use_bkt) {
+    const int64_t sbar = c->sbar;
     Phase ph(c, &c->stats.ms_rhs);
     k_solve_prep<<<1, 128, prep_smem(r), c->st>>>(r, c->sd);
     CK_LAUNCH();
@@ -1328,7 +1522,6 @@ void solve_impl(cparls_ctx *c, int k, cparls_solve_info *info) {
                                            c->idx[k].out, r0, reinterpret_cast<unsigned long long *>(c->bkt_cnt));
       CK_LAUNCH();
     }
-    // starts of the nbkt buckets (+ the total at [nbkt]); placement cursors
     exclusive_scan_i64(c->bkt_cnt, c->bkt_start, nbkt + 1, c->bkt_part, nullptr, c->st);
     k_bkt_cursor<<<(unsigned)ceil_div(nbkt, 256), 256, 0, c->st>>>(c->bkt_start, nbkt, c->bkt_cursor);
     CK_LAUNCH();
@@ -1359,66 +1552,67 @@ void solve_impl(cparls_ctx *c, int k, cparls_solve_info *info) {
     k_pairs_reduce<<<pairs_reduce_grid(r), 256, 0, c->st>>>(c->gpart, bgrid, r, c->sd->BtB);
     CK_LAUNCH();
     LAUNCHED(c, 8);
-    c->stats.bytes_rhs += (double)mk_host * (4.0 + (c->vf32 ? 4.0 : 8.0)) + (double)nown * r * 8.0;
     ph.end();
-  } else
-  // K8: sampled RHS (fp64 red per entry in L2-sized output-row windows; hot
-  // rows privatized per warp)
-  {
+  } else {
+    // K8: sampled RHS (int64 fixed-point / fp64 red per entry in L2-sized
+    // output-row windows, rhs.cuh)
     if (c->m_dirty) {   // a bucketed step left rows in M
       CK(cudaMemsetAsync(c->M, 0, sizeof(double) * c->nmax * c->ld, c->st));
       c->m_dirty = false;
     }
     Phase ph(c, &c->stats.ms_rhs);
-    if (sbar > 0) {
-      constexpr int win_mb = 96;     // output-row window of M kept in L2 (rhs.cuh)
-      constexpr int grid_mult = 8;   // CTAs per SM
-      const int64_t RW = std::max<int64_t>(1, (int64_t(win_mb) << 20) / ((int64_t)ld * 8));
-      const int nwin = (int)ceil_div(nk, RW);
-      const int64_t nseg = (int64_t)nwin * sbar;
-      if (nseg > c->segcap) {
+    constexpr int win_mb = 96;     // output-row window of M kept in L2 (rhs.cuh)
+    constexpr int grid_mult = 8;   // CTAs per SM
+    const int64_t RW = std::max<int64_t>(1, (int64_t(win_mb) << 20) / ((int64_t)ld * 8));
+    const int nwin = (int)ceil_div(nk, RW);
+    const int64_t nseg_max = (int64_t)nwin * smax;
+    const int64_t *soff = c->off, *slo = c->lo;
+    const int32_t *sj = nullptr;
+    const int64_t *nseg_dev = &ctl->sbar;
+    if (nwin > 1) {
+      if (nseg_max > c->segcap) {
         dfree(c, c->seg_lo); dfree(c, c->seg_len); dfree(c, c->seg_off); dfree(c, c->seg_j);
         dfree(c, c->i64part_seg);
-        c->segcap = nseg;
-        c->seg_lo = dalloc_t<int64_t>(c, nseg);
-        c->seg_len = dalloc_t<int64_t>(c, nseg);
-        c->seg_off = dalloc_t<int64_t>(c, nseg);
-        c->seg_j = dalloc_t<int32_t>(c, nseg);
-        c->i64part_seg = dalloc_t<int64_t>(c, ceil_div(nseg, kScanTile) + 16);
+        c->segcap = nseg_max;
+        c->seg_lo = dalloc_t<int64_t>(c, nseg_max);
+        c->seg_len = dalloc_t<int64_t>(c, nseg_max);
+        c->seg_off = dalloc_t<int64_t>(c, nseg_max);
+        c->seg_j = dalloc_t<int32_t>(c, nseg_max);
+        c->i64part_seg = dalloc_t<int64_t>(c, ceil_div(nseg_max, kScanTile) + 16);
       }
-      if (nwin == 1) {
-        CK(cudaMemcpyAsync(c->seg_lo, c->lo, 8 * sbar, cudaMemcpyDeviceToDevice, c->st));
-        CK(cudaMemcpyAsync(c->seg_off, c->off, 8 * sbar, cudaMemcpyDeviceToDevice, c->st));
-      } else {
-        k_win_bounds<<<(unsigned)ceil_div(nseg, 256), 256, 0, c->st>>>(c->lo, c->len, sbar, c->idx[k].out, nwin, RW,
-                                                                       c->seg_lo, c->seg_len, c->seg_j);
-        CK_LAUNCH();
-        exclusive_scan_i64(c->seg_len, c->seg_off, nseg, c->i64part_seg, nullptr, c->st);
-        LAUNCHED(c, 4);
-      }
-      if (c->fx_on) {   // per-column fixed-point scales from the sample (kernels.cuh)
-        if (c->fx_pending) CK(cudaStreamWaitEvent(c->st, c->ev_join, 0));   // computed on the side stream
-        else launch_fixed_scales(c, sbar, c->st);
-        c->fx_pending = false;
-      }
-      CK(cudaMemsetAsync(&c->dv->counter, 0, sizeof(unsigned long long), c->st));
-      const int grid = 148 * grid_mult;
-      const int64_t per_warp = 512;
+      k_win_bounds<<<(unsigned)ceil_div(nseg_max, 256), 256, 0, c->st>>>(c->lo, c->len, smax, c->idx[k].out, nwin, RW,
+                                                                         c->seg_lo, c->seg_len, c->seg_j,
+                                                                         &ctl->sbar, &ctl->nseg, ctl);
+      CK_LAUNCH();
+      exclusive_scan_i64_dev(c->seg_len, c->seg_off, nseg_max, &ctl->nseg, c->i64part_seg, nullptr, c->st, ctl);
+      LAUNCHED(c, 4);
+      soff = c->seg_off;
+      slo = c->seg_lo;
+      sj = c->seg_j;
+      nseg_dev = &ctl->nseg;
+    }
+    if (c->fx_on) {   // per-column fixed-point scales from the sample (kernels.cuh)
+      if (c->fx_pending) CK(cudaStreamWaitEvent(c->st, c->ev_join, 0));   // computed on the side stream
+      else launch_fixed_scales(c, c->st);
+      c->fx_pending = false;
+    }
+    CK(cudaMemsetAsync(&c->dv->counter, 0, sizeof(unsigned long long), c->st));
+    const int grid = 148 * grid_mult;
+    const int64_t per_warp = 512;
 #define RHS(VT, HI)                                                                                               \
   if (c->fx_on) RHS2(VT, HI, true); else RHS2(VT, HI, false)
 #define RHS2(VT, HI, FX)                                                                                           \
-  k_rhs<VT, HI, FX><<<grid, kRhsThreads, 0, c->st>>>(c->seg_off, c->seg_lo, nwin > 1 ? c->seg_j : nullptr, nseg, &c->dv->mk,          \
-                                                           &c->dv->counter, c->idx[k].out, (const VT *)c->idx[k].val, \
-                                                           c->sw2, c->Z, r, ld, c->M, per_warp, c->fx_scale)
-      KTimer kt(c, KT_RHS);
-      if (c->vf32) { if (r > 32) RHS(float, true); else RHS(float, false); }
-      else { if (r > 32) RHS(double, true); else RHS(double, false); }
-      kt.stop();
+  k_rhs<VT, HI, FX><<<grid, kRhsThreads, 0, c->st>>>(soff, slo, sj, nseg_max, &c->dv->mk, &c->dv->counter,          \
+                                                     c->idx[k].out, (const VT *)c->idx[k].val, c->sw2, c->Z, r, ld,  \
+                                                     c->M, per_warp, c->fx_scale, nseg_dev, ctl)
+    KTimer kt(c, KT_RHS);
+    if (c->vf32) { if (r > 32) RHS(float, true); else RHS(float, false); }
+    else { if (r > 32) RHS(double, true); else RHS(double, false); }
+    kt.stop();
 #undef RHS2
 #undef RHS
-      CK_LAUNCH();
-      LAUNCHED(c, 1);
-    }
+    CK_LAUNCH();
+    LAUNCHED(c, 1);
     ph.end();
   }
   // K9: solve + normalize + leverage refresh
@@ -1429,16 +1623,16 @@ void solve_impl(cparls_ctx *c, int k, cparls_solve_info *info) {
   {
     Phase ph(c, &c->stats.ms_solve);
     if (!use_bkt) {
-    k_solve_prep<<<1, 128, prep_smem(r), c->st>>>(r, c->sd);
-    CK_LAUNCH();
-    const int64_t grid = row_grid(c, ceil_div(std::max<int64_t>(nown, 1), kRowThreads));
-    CK(cudaMemsetAsync(&c->dv->touched, 0, sizeof(unsigned long long), c->st));
-    KTimer kts(c, KT_SOLVE);
-    launch_solve_rows(c, c->M + r0 * ld, nown, c->A[k] + r0 * ld, grid, 1, c->fx_on ? c->fx_scale : nullptr);
-    kts.stop();
-    CK_LAUNCH();
-    k_pairs_reduce<<<pairs_reduce_grid(r), 256, 0, c->st>>>(c->gpart, grid, r, c->sd->BtB);
-    CK_LAUNCH();
+      k_solve_prep<<<1, 128, prep_smem(r), c->st>>>(r, c->sd, ctl);
+      CK_LAUNCH();
+      const int64_t grid = row_grid(c, ceil_div(std::max<int64_t>(nown, 1), kRowThreads));
+      CK(cudaMemsetAsync(&c->dv->touched, 0, sizeof(unsigned long long), c->st));
+      KTimer kts(c, KT_SOLVE);
+      launch_solve_rows(c, c->M + r0 * ld, nown, c->A[k] + r0 * ld, grid, 1, c->fx_on ? c->fx_scale : nullptr);
+      kts.stop();
+      CK_LAUNCH();
+      k_pairs_reduce<<<pairs_reduce_grid(r), 256, 0, c->st>>>(c->gpart, grid, r, c->sd->BtB, ctl);
+      CK_LAUNCH();
     }
     if (c->world > 1) {
       // Gram of B over all ranks' rows (r x r), then every rank gets all B rows
@@ -1448,27 +1642,25 @@ void solve_impl(cparls_ctx *c, int k, cparls_solve_info *info) {
       c->comm->allgatherv_f64(c->A[k], off, c->st);
       c->comm->allreduce_u64(&c->dv->touched, 1, c->st);
     }
-    k_norm_prep<<<1, 128, prep_smem(r), c->st>>>(r, c->sd, c->md[k]);
+    k_norm_prep<<<1, 128, prep_smem(r), c->st>>>(r, c->sd, c->md[k], ctl);
     CK_LAUNCH();
     LAUNCHED(c, 4);
     lev_rows_and_cdf(c, k, c->sd->lambda);
-    CK(cudaMemcpyAsync(c->lam_model, c->sd->lambda, sizeof(double) * r, cudaMemcpyDeviceToDevice, c->st));
+    k_copy_lambda<<<1, 64, 0, c->st>>>(c->lam_model, c->sd->lambda, r, ctl);
+    CK_LAUNCH();
     c->stats.bytes_solve += (double)nk * r * 8.0 * 3;
     ph.end();
   }
-  // step counters: into pinned scratch; with an info request read now (one
-  // sync), otherwise folded into the stats at the next sync (no sync here)
   if (c->world > 1) c->comm->allreduce_u64(reinterpret_cast<unsigned long long *>(&c->dv->mk), 1, c->st);
-  if (c->stats_pending_k >= 0) sync(c);   // (cannot happen inside run: sampling syncs first)
-  CK(cudaMemcpyAsync(c->hscr + kHscrMk, &c->dv->mk, sizeof(long long), cudaMemcpyDeviceToHost, c->st));
-  CK(cudaMemcpyAsync(c->hscr + kHscrTouched, &c->dv->touched, sizeof(unsigned long long), cudaMemcpyDeviceToHost, c->st));
-  c->stats_pending_k = k;
+  k_solve_stats<<<1, 1, 0, c->st>>>(ctl, k, &c->dv->mk, &c->dv->touched);
+  CK_LAUNCH();
+  LAUNCHED(c, 2);
   c->stats.mode_steps++;
   if (info) {
     int ru = 0, fb = 0;
     CK(cudaMemcpyAsync(&ru, &c->sd->rank_used, sizeof(int), cudaMemcpyDeviceToHost, c->st));
     CK(cudaMemcpyAsync(&fb, &c->sd->chol_fallback, sizeof(int), cudaMemcpyDeviceToHost, c->st));
-    sync(c);   // folds the counters
+    sync(c);   // folds the step counters
     info->matched_nnz = c->stats.last_matched_nnz;
     info->touched_rows = c->stats.touched_rows[k];
     info->rank_used = ru;
@@ -1742,9 +1934,8 @@ double fit_estimate_impl(cparls_ctx *c, double *Fhat) {
 // A[0..D) and the model's lambda: <X,M> partials into part (dd[nb]), then
 // k_fit_final -> out[0] = fit (single GPU), out[1] = <X,M>, out[2] = ||M||^2.
 // blocks_per_sm: CTAs of the persistent fit kernel per SM (2 = all warp slots).
-void fit_launch(cparls_ctx *c, cudaStream_t st, double *const *A, const double *lam, const FitModes &fm,
-                dd *part, unsigned long long *counter, double *out, int blocks_per_sm) {
-  const int k = c->fit_mode;
+// Key decoding of copy k (its order, fastest digit first) with the factors A.
+FitDecode fit_decode(const cparls_ctx *c, int k, double *const *A) {
   FitDecode fd{};
   fd.d = c->D - 1;
   long double N = 1;
@@ -1752,10 +1943,17 @@ void fit_launch(cparls_ctx *c, cudaStream_t st, double *const *A, const double *
     const int m = c->idx[k].order[j];
     fd.n[j] = c->dims[m];
     fd.inv[j] = 1.0 / (double)c->dims[m];
-    fd.A[j] = A[m];
+    fd.A[j] = A ? A[m] : nullptr;
     N *= (long double)c->dims[m];
   }
   fd.fast = N < 9007199254740992.0L;   // keys < 2^53
+  return fd;
+}
+
+void fit_launch(cparls_ctx *c, cudaStream_t st, double *const *A, const double *lam, const FitModes &fm,
+                dd *part, unsigned long long *counter, double *out, int blocks_per_sm) {
+  const int k = c->fit_mode;
+  const FitDecode fd = fit_decode(c, k, A);
   int nb = 148 * 4;
   KTimer kt(c, KT_FIT, st);
   if (fd.d <= 3) {
@@ -1764,7 +1962,7 @@ void fit_launch(cparls_ctx *c, cudaStream_t st, double *const *A, const double *
     CK(cudaMemsetAsync(counter, 0, sizeof(unsigned long long), st));
 #define FITS(VT, SW, DM)                                                                                         \
   k_fit_sub<VT, SW, DM, (SW >= CPARLS_FIT_U ? CPARLS_FIT_U : SW)><<<nb, kFitThreads, 0, st>>>(c->idx[k].key, c->idx[k].out, (const VT *)c->idx[k].val, \
-                                                          c->idx[k].nnz, fd, A[k], lam, c->r, c->ld, part, counter)
+                                                          c->idx[k].nnz, fd, A[k], lam, c->r, c->ld, part, counter, c->ctl)
 #define FITSD(VT, SW)                          \
   do {                                         \
     if (fd.d == 1) FITS(VT, SW, 1);            \
@@ -1786,15 +1984,15 @@ void fit_launch(cparls_ctx *c, cudaStream_t st, double *const *A, const double *
     if (c->vf32)
       RSWITCH(c->r, k_fit_thread<float, RM><<<nb, kFitThreads, smem, st>>>(
                         c->idx[k].key, c->idx[k].out, (const float *)c->idx[k].val, c->idx[k].nnz, fd, A[k],
-                        lam, c->r, c->ld, part));
+                        lam, c->r, c->ld, part, c->ctl));
     else
       RSWITCH(c->r, k_fit_thread<double, RM><<<nb, kFitThreads, smem, st>>>(
                         c->idx[k].key, c->idx[k].out, (const double *)c->idx[k].val, c->idx[k].nnz, fd, A[k],
-                        lam, c->r, c->ld, part));
+                        lam, c->r, c->ld, part, c->ctl));
   }
   kt.stop();
   CK_LAUNCH();
-  k_fit_final<<<1, 256, 0, st>>>(part, nb, fm, lam, c->r, c->normX2, out);
+  k_fit_final<<<1, 256, 0, st>>>(part, nb, fm, lam, c->r, c->normX2, out, c->ctl);
   CK_LAUNCH();
   LAUNCHED(c, 2);
   c->stats.fits++;
@@ -1808,24 +2006,75 @@ FitModes fit_modes(cparls_ctx *c, double *const *GA) {
   return fm;
 }
 
-double fit_impl(cparls_ctx *c) {
+// The exact fit enqueued on the context's stream: fit value at dv->fit[0]
+// (over all ranks); guarded like the mode steps.
+void fit_enqueue(cparls_ctx *c) {
   Phase ph(c, &c->stats.ms_fit);
   fit_launch(c, c->st, c->A, c->lam_model, fit_modes(c, nullptr), c->ddpart, &c->dv->counter, c->dv->fit, 8);
-  double f;
   if (c->world > 1) {
     // <X,M> is a sum over the ranks' slices of the fit mode
     c->comm->allreduce_f64(&c->dv->fit[1], 1, c->st);
-    double hv[3];
-    CK(cudaMemcpyAsync(hv, c->dv->fit, sizeof(hv), cudaMemcpyDeviceToHost, c->st));
-    sync(c);
-    double resid2 = c->normX2 - 2.0 * hv[1] + hv[2];
-    if (resid2 < 0.0) resid2 = 0.0;
-    f = 1.0 - std::sqrt(resid2) / std::sqrt(c->normX2);
-  } else {
-    f = read_dev(c, &c->dv->fit[0]);
+    k_fit_combine<<<1, 1, 0, c->st>>>(c->dv->fit, c->normX2, c->ctl);
+    CK_LAUNCH();
   }
   ph.end();
-  return f;
+}
+
+double fit_impl(cparls_ctx *c) {
+  fit_enqueue(c);
+  return read_dev(c, &c->dv->fit[0]);
+}
+
+// Alg. 3 iterations iter0 .. iter0+iters-1 (steps (iter0 + t) D + k, AMB-10)
+// enqueued without host synchronisation: every mode step samples and solves
+// on the device (sample_async, solve_impl) and every fit_every-th iteration's
+// exact fit is copied to fitbuf[t] on the device.  One synchronisation at the
+// end; a step that aborted (a rare branch, sampler.cuh) is redone with the
+// host-driven sampler and the rest is enqueued again from the next step.
+void run_async(cparls_ctx *c, int32_t iters, int64_t s, uint64_t seed, int32_t iter0, int32_t fit_every,
+               double *trace) {
+  if (iters < 0) throw ApiError(CPARLS_EINVAL, "iters < 0");
+  if (s < 1) throw ApiError(CPARLS_EINVAL, "s must be >= 1");
+  if (fit_every > 0 && iters >= fit_every && c->normX2 <= 0.0)
+    throw ApiError(CPARLS_ENUMERIC, "||X|| = 0: fit undefined");
+  const int D = c->D;
+  if (iters > c->fitbuf_cap) {
+    dfree(c, c->fitbuf);
+    c->fitbuf_cap = std::max<int64_t>(iters, 64);
+    c->fitbuf = dalloc_t<double>(c, c->fitbuf_cap);
+  }
+  if (iters > 0) CK(cudaMemsetAsync(c->fitbuf, 0xFF, sizeof(double) * iters, c->st));   // NaN: no fit
+  const bool async_ok = !c->sample_sort && c->opts.rhs_path != 2;
+  auto one_step = [&](int64_t g, bool host_sampler) {
+    const int t = (int)(g / D), k = (int)(g % D);
+    const uint64_t step = (uint64_t)(iter0 + t) * D + k;   // AMB-10
+    if (host_sampler) {
+      c->have_sample = false;
+      sample_host(c, k, s, seed, step);
+      push_sample_state(c);
+    } else {
+      sample_async(c, k, s, seed, step);
+    }
+    solve_impl(c, k, nullptr);
+    if (k == D - 1 && fit_every > 0 && (t + 1) % fit_every == 0) {
+      fit_enqueue(c);
+      CK(cudaMemcpyAsync(c->fitbuf + t, &c->dv->fit[0], sizeof(double), cudaMemcpyDeviceToDevice, c->st));
+    }
+  };
+  const int64_t G = (int64_t)iters * D;
+  int64_t g0 = 0;
+  while (true) {
+    for (int64_t g = g0; g < G; ++g) one_step(g, !async_ok);
+    if (trace && iters > 0)
+      CK(cudaMemcpyAsync(trace, c->fitbuf, sizeof(double) * iters, cudaMemcpyDeviceToHost, c->st));
+    const int64_t ab = clear_abort(c);   // the run's one synchronisation (unless a step aborted)
+    if (ab < 0) break;
+    const int64_t ga = ab - (int64_t)iter0 * D;
+    if (ga < 0 || ga >= G) throw ApiError(CPARLS_ECUDA, "asynchronous step abort outside the run");
+    one_step(ga, true);
+    g0 = ga + 1;
+  }
+  c->have_sample = false;
 }
 
 cparls_status fail(cparls_ctx *c, int st, const std::string &msg) {
@@ -1938,6 +2187,10 @@ cparls_status cparls_create(cparls_ctx **out, int32_t nmodes, const int64_t *dim
     CK(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
     c->dv = dalloc_t<DevScalars>(c, 1);
+    c->ctl = dalloc_t<StepCtl>(c, 1);
+    CK(cudaMemsetAsync(c->ctl, 0, sizeof(StepCtl), c->st));
+    CK(cudaHostAlloc(&c->hctl, sizeof(StepCtl), cudaHostAllocDefault));
+    std::memset(c->hctl, 0, sizeof(StepCtl));
     CK(cudaMemsetAsync(c->dv, 0, sizeof(DevScalars), c->st));
     c->sd = dalloc_t<SolveDev>(c, 1);
     CK(cudaMemsetAsync(c->sd, 0, sizeof(SolveDev), c->st));
@@ -2063,6 +2316,8 @@ cparls_status cparls_create(cparls_ctx **out, int32_t nmodes, const int64_t *dim
   if (st != CPARLS_OK) {
     g_create_err = c->err;
     for (void *p : c->allocs) cudaFree(p);
+    if (c->hscr) cudaFreeHost(c->hscr);
+    if (c->hctl) cudaFreeHost(c->hctl);
     delete c->comm;
     delete c;
     return st;
@@ -2078,6 +2333,7 @@ cparls_status cparls_destroy(cparls_ctx *c) {
   for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
   for (void *p : c->allocs) cudaFree(p);
   if (c->hscr) cudaFreeHost(c->hscr);
+  if (c->hctl) cudaFreeHost(c->hctl);
   if (c->ev_fork) cudaEventDestroy(c->ev_fork);
   if (c->ev_join) cudaEventDestroy(c->ev_join);
   if (c->side) cudaStreamDestroy(c->side);
@@ -2193,6 +2449,7 @@ cparls_status cparls_get_sample(cparls_ctx *c, int64_t cap, uint64_t *keys, int3
                                 uint8_t *is_det, int64_t *n_out) {
   if (!c) return CPARLS_EINVAL;
   return guarded(c, [&] {
+    pull_sample_state(c);
     const int64_t n = c->sbar;
     if (n_out) *n_out = n;
     std::vector<uint64_t> hk(n);
@@ -2225,6 +2482,7 @@ cparls_status cparls_get_fibers(cparls_ctx *c, int64_t cap, int64_t *len, int64_
   if (!c) return CPARLS_EINVAL;
   return guarded(c, [&] {
     if (c->smode < 0 || c->sbar < 0) throw ApiError(CPARLS_ESTATE, "no sample");
+    pull_sample_state(c);
     const int k = c->smode;
     if (!c->have_lookup) lookup_impl(c, k);
     const int64_t n = c->sbar;
@@ -2315,22 +2573,7 @@ cparls_status cparls_fit(cparls_ctx *c, double *fit) {
 cparls_status cparls_run(cparls_ctx *c, int32_t iters, int64_t s, uint64_t seed, int32_t iter0, int32_t fit_every,
                          double *fit_trace) {
   if (!c) return CPARLS_EINVAL;
-  return guarded(c, [&] {
-    if (iters < 0) throw ApiError(CPARLS_EINVAL, "iters < 0");
-    for (int t = 0; t < iters; ++t) {
-      for (int k = 0; k < c->D; ++k) {
-        uint64_t step = (uint64_t)(iter0 + t) * c->D + k;   // AMB-10
-        sample_impl(c, k, s, seed, step, nullptr);
-        solve_impl(c, k, nullptr);
-      }
-      double f = NAN;
-      if (fit_every > 0 && (t + 1) % fit_every == 0) {
-        if (c->normX2 <= 0.0) throw ApiError(CPARLS_ENUMERIC, "||X|| = 0: fit undefined");
-        f = fit_impl(c);
-      }
-      if (fit_trace) fit_trace[t] = f;
-    }
-  });
+  return guarded(c, [&] { run_async(c, iters, s, seed, iter0, fit_every, fit_trace); });
 }
 
 cparls_status cparls_fit_estimate(cparls_ctx *c, double *fit, double *Fhat) {
@@ -2397,13 +2640,8 @@ cparls_status cparls_run_until(cparls_ctx *c, int64_t s, uint64_t seed, int32_t 
     double best = -INFINITY;
     int fails = 0, e = 0;
     for (e = 0; e < max_epochs; ++e) {
-      for (int t = 0; t < eta; ++t) {
-        const int64_t it = (int64_t)e * eta + t;
-        for (int k = 0; k < c->D; ++k) {
-          sample_impl(c, k, s, seed, (uint64_t)it * c->D + k, nullptr);   // AMB-10
-          solve_impl(c, k, nullptr);
-        }
-      }
+      // eta iterations (steps (e eta + t) D + k, AMB-10) without host synchronisation
+      run_async(c, eta, s, seed, e * eta, 0, nullptr);
       const double f = fit_kind == 1 ? fit_estimate_impl(c, nullptr) : fit_impl(c);
       if (trace) trace[e] = f;
       if (f > best + tol) {   // AMB-33: improvement over the best fit so far
@@ -2519,6 +2757,7 @@ cparls_status cparls_reset_stats(cparls_ctx *c) {
   return guarded(c, [&] {
     sync(c, false);   // a pending step's counters belong to the old stats
     c->stats = cparls_stats{};
+    c->ctl_seen = *reinterpret_cast<const StepCtl *>(c->hctl);
   });
 }
 

@@ -48,7 +48,8 @@ __global__ void __launch_bounds__(kFitThreads, 2) k_fit_thread(const uint64_t *_
                                                            const VT *__restrict__ vals, int64_t nnz, FitDecode fd,
                                                            const double *__restrict__ Ak,
                                                            const double *__restrict__ lam, int r, int ld,
-                                                           dd *__restrict__ part) {
+                                                           dd *__restrict__ part, const StepCtl *ctl = nullptr) {
+  CPARLS_GUARD(ctl);
   extern __shared__ double hbuf[];   // kFitThreads slots of RS doubles
   __shared__ double lam_s[kMaxRank + 1];
   const int RS = r | 1;              // odd slot stride: conflict-free 8-byte accesses
@@ -150,7 +151,9 @@ __global__ void __launch_bounds__(kFitThreads, CPARLS_FIT_MINB) k_fit_sub(const 
                                                           const double *__restrict__ Ak,
                                                           const double *__restrict__ lam, int r, int ld,
                                                           dd *__restrict__ part,
-                                                          unsigned long long *__restrict__ work) {
+                                                          unsigned long long *__restrict__ work,
+                                                          const StepCtl *ctl = nullptr) {
+  CPARLS_GUARD(ctl);
   static_assert(SW >= 2 && SW <= 32 && (SW & (SW - 1)) == 0, "SW power of two");
   constexpr int NS = 32 / SW;
   constexpr int SUB = kFitChunk / NS;    // entries per sub-warp per chunk (multiple of SW)
@@ -305,7 +308,8 @@ struct FitModes {
 };
 
 __global__ void k_fit_final(const dd *__restrict__ part, int nb, FitModes fm, const double *__restrict__ lam, int r,
-                            double normX2, double *out) {
+                            double normX2, double *out, const StepCtl *ctl = nullptr) {
+  CPARLS_GUARD(ctl);
   __shared__ dd red[256];
   dd inner = {0.0, 0.0}, nm = {0.0, 0.0};
   for (int i = threadIdx.x; i < nb; i += blockDim.x) inner = dd_add(inner, part[i]);

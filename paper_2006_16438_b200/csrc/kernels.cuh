@@ -208,7 +208,9 @@ constexpr int kLevThreads = 256;
 
 // CDF pass 3: C[i] = offset(tile) + inclusive scan of q within tile.
 __global__ void __launch_bounds__(kLevThreads) k_cdf_final(uint64_t *__restrict__ C, int64_t n,
-                                                           const uint64_t *__restrict__ tile_off) {
+                                                           const uint64_t *__restrict__ tile_off,
+                                                           const StepCtl *ctl = nullptr) {
+  CPARLS_GUARD(ctl);
   int64_t i = (int64_t)blockIdx.x * kLevThreads + threadIdx.x;
   uint64_t q = i < n ? C[i] : 0ull;
   uint64_t tot;
@@ -219,7 +221,8 @@ __global__ void __launch_bounds__(kLevThreads) k_cdf_final(uint64_t *__restrict_
 // exclusive scan of u64 tile sums (single block): each thread scans
 // kScanItems consecutive entries serially, one block scan per 2048 (integer
 // adds: the result does not depend on the grouping)
-__global__ void k_scan_u64_single(uint64_t *part, int64_t nb) {
+__global__ void k_scan_u64_single(uint64_t *part, int64_t nb, const StepCtl *ctl = nullptr) {
+  CPARLS_GUARD(ctl);
   unsigned long long carry = 0;
   for (int64_t base = 0; base < nb; base += kScanTile) {
     const int64_t b0 = base + (int64_t)threadIdx.x * kScanItems;
@@ -296,25 +299,35 @@ struct OtherModes {
   const uint64_t *C[kMaxModes];
   const double *A[kMaxModes];
   uint64_t mult[kMaxModes];   // prod_{l<j} n_l
-  double alpha[kMaxModes];
+  const ModeDev *md[kMaxModes];   // alpha and drawable counts of the other modes (device)
 };
+
+// max p~ of other mode l, read on the device
+__device__ __forceinline__ double om_alpha(const OtherModes &om, int l) { return om.md[l]->alpha; }
 
 // Canonical product with position j = x, every other position at alpha (the
 // largest p any index with i_j fixed can reach; fp multiply is monotone).
-__device__ __forceinline__ double prod_with(const OtherModes &om, int j, double x) {
-  double p = (j == 0) ? x : om.alpha[0];
-  for (int l = 1; l < om.d; ++l) p = p * ((l == j) ? x : om.alpha[l]);
+__device__ __forceinline__ double prod_with(const OtherModes &om, const double *al, int j, double x) {
+  double p = (j == 0) ? x : al[0];
+  for (int l = 1; l < om.d; ++l) p = p * ((l == j) ? x : al[l]);
   return p;
+}
+__device__ __forceinline__ void load_alphas(const OtherModes &om, double *al) {
+  for (int l = 0; l < om.d; ++l) al[l] = om_alpha(om, l);
 }
 
 // pass 1: per-tile counts of candidates of mode j
-__global__ void k_cand_count(OtherModes om, int j, double tau, int64_t *__restrict__ part) {
+__global__ void k_cand_count(OtherModes om, int j, double tau, int64_t *__restrict__ part,
+                             const StepCtl *ctl = nullptr) {
+  CPARLS_GUARD(ctl);
+  double al[kMaxModes];
+  load_alphas(om, al);
   int64_t base = (int64_t)blockIdx.x * kScanTile;
   int64_t s = 0;
   const double *pt = om.pt[j];
   for (int i = 0; i < kScanItems; ++i) {
     int64_t idx = base + (int64_t)i * kScanThreads + threadIdx.x;
-    if (idx < om.n[j] && prod_with(om, j, pt[idx]) > tau) ++s;
+    if (idx < om.n[j] && prod_with(om, al, j, pt[idx]) > tau) ++s;
   }
   int64_t tot;
   block_excl_scan<int64_t>(s, &tot);
@@ -324,14 +337,18 @@ __global__ void k_cand_count(OtherModes om, int j, double tau, int64_t *__restri
 // pass 3: ordered scatter of candidates: key = ~bits(p~) (descending order
 // after an ascending stable sort), value = row index.
 __global__ void k_cand_scatter(OtherModes om, int j, double tau, const int64_t *__restrict__ part,
-                               uint64_t *__restrict__ ckey, uint32_t *__restrict__ cidx) {
+                               uint64_t *__restrict__ ckey, uint32_t *__restrict__ cidx,
+                               const StepCtl *ctl = nullptr) {
+  CPARLS_GUARD(ctl);
+  double al[kMaxModes];
+  load_alphas(om, al);
   int64_t base = (int64_t)blockIdx.x * kScanTile + (int64_t)threadIdx.x * kScanItems;
   const double *pt = om.pt[j];
   bool f[kScanItems];
   int64_t s = 0;
   for (int i = 0; i < kScanItems; ++i) {
     int64_t idx = base + i;
-    f[i] = idx < om.n[j] && prod_with(om, j, pt[idx]) > tau;
+    f[i] = idx < om.n[j] && prod_with(om, al, j, pt[idx]) > tau;
     s += f[i];
   }
   int64_t tot;
@@ -350,50 +367,69 @@ __device__ __forceinline__ double cand_val(uint64_t k) { return __longlong_as_do
 
 // Level expansion count: entry e (partial product pp_e) x sorted candidates of
 // level l: count of the prefix with fl(pp*v)*alpha_{l+1}*... > tau.
+// Counts live on the device when nlist_dev / ncand_dev are given (asynchronous
+// step: grid-stride over an upper-bound grid).
 __global__ void k_didx_count(const double *__restrict__ pp, int64_t nlist, const uint64_t *__restrict__ ckey,
-                             int64_t ncand, OtherModes om, int l, double tau, int64_t *__restrict__ cnt) {
-  int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (e >= nlist) return;
-  double base = pp[e];
-  int64_t lo = 0, len = ncand;  // first t where predicate fails
-  while (len > 0) {
-    int64_t half = len >> 1;
-    double b = base * cand_val(ckey[lo + half]);
-    for (int k = l + 1; k < om.d; ++k) b = b * om.alpha[k];
-    if (b > tau) { lo += half + 1; len -= half + 1; }
-    else len = half;
+                             int64_t ncand, OtherModes om, int l, double tau, int64_t *__restrict__ cnt,
+                             const int64_t *nlist_dev = nullptr, const int64_t *ncand_dev = nullptr,
+                             const StepCtl *ctl = nullptr) {
+  CPARLS_GUARD(ctl);
+  nlist = dcount(nlist, nlist_dev);
+  ncand = dcount(ncand, ncand_dev);
+  double al[kMaxModes];
+  load_alphas(om, al);
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < nlist; e += (int64_t)gridDim.x * blockDim.x) {
+    double base = pp[e];
+    int64_t lo = 0, len = ncand;  // first t where predicate fails
+    while (len > 0) {
+      int64_t half = len >> 1;
+      double b = base * cand_val(ckey[lo + half]);
+      for (int k = l + 1; k < om.d; ++k) b = b * al[k];
+      if (b > tau) { lo += half + 1; len -= half + 1; }
+      else len = half;
+    }
+    cnt[e] = lo;
   }
-  cnt[e] = lo;
 }
 
 // Level expansion emit: one warp per entry, lanes over its candidate prefix.
 __global__ void k_didx_emit(const uint64_t *__restrict__ pkey, const double *__restrict__ pp, int64_t nlist,
                             const int64_t *__restrict__ cnt, const int64_t *__restrict__ off,
                             const uint64_t *__restrict__ ckey, const uint32_t *__restrict__ cidx, uint64_t mult,
-                            uint64_t *__restrict__ nkey, double *__restrict__ npp) {
-  int64_t e = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  int lane = threadIdx.x & 31;
-  if (e >= nlist) return;
-  int64_t c = cnt[e], o = off[e];
-  uint64_t k0 = pkey[e];
-  double p0 = pp[e];
-  for (int64_t t = lane; t < c; t += 32) {
-    nkey[o + t] = k0 + (uint64_t)cidx[t] * mult;
-    npp[o + t] = p0 * cand_val(ckey[t]);
+                            uint64_t *__restrict__ nkey, double *__restrict__ npp, const int64_t *nlist_dev = nullptr,
+                            const StepCtl *ctl = nullptr) {
+  CPARLS_GUARD(ctl);
+  nlist = dcount(nlist, nlist_dev);
+  const int lane = threadIdx.x & 31;
+  for (int64_t e = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; e < nlist;
+       e += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    int64_t c = cnt[e], o = off[e];
+    uint64_t k0 = pkey[e];
+    double p0 = pp[e];
+    for (int64_t t = lane; t < c; t += 32) {
+      nkey[o + t] = k0 + (uint64_t)cidx[t] * mult;
+      npp[o + t] = p0 * cand_val(ckey[t]);
+    }
   }
 }
 
 // Level-0 list from the sorted candidates of mode m_1.
 __global__ void k_didx_level0(const uint64_t *__restrict__ ckey, const uint32_t *__restrict__ cidx, int64_t n,
-                              uint64_t *__restrict__ key, double *__restrict__ pp) {
-  int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= n) return;
-  key[t] = cidx[t];
-  pp[t] = cand_val(ckey[t]);
+                              uint64_t *__restrict__ key, double *__restrict__ pp, const int64_t *n_dev = nullptr,
+                              const StepCtl *ctl = nullptr) {
+  CPARLS_GUARD(ctl);
+  n = dcount(n, n_dev);
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
+    key[t] = cidx[t];
+    pp[t] = cand_val(ckey[t]);
+  }
 }
 
 // compensated sum of n doubles -> block partial dd
-__global__ void k_sum_dd(const double *__restrict__ x, int64_t n, dd *__restrict__ part) {
+__global__ void k_sum_dd(const double *__restrict__ x, int64_t n, dd *__restrict__ part,
+                         const int64_t *n_dev = nullptr, const StepCtl *ctl = nullptr) {
+  CPARLS_GUARD(ctl);
+  n = dcount(n, n_dev);
   dd s = {0.0, 0.0};
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     s = dd_add_d(s, x[i]);
@@ -408,7 +444,8 @@ __global__ void k_sum_dd(const double *__restrict__ x, int64_t n, dd *__restrict
     part[blockIdx.x] = t;
   }
 }
-__global__ void k_sum_dd_final(const dd *__restrict__ part, int nb, double *out) {
+__global__ void k_sum_dd_final(const dd *__restrict__ part, int nb, double *out, const StepCtl *ctl = nullptr) {
+  CPARLS_GUARD(ctl);
   if (threadIdx.x == 0) {
     dd t = {0.0, 0.0};
     for (int i = 0; i < nb; ++i) t = dd_add(t, part[i]);
@@ -419,7 +456,10 @@ __global__ void k_sum_dd_final(const dd *__restrict__ part, int nb, double *out)
 // Deterministic block of the sample set: w^2 = 1.
 __global__ void k_det_emit(const uint64_t *__restrict__ key, const double *__restrict__ p, int64_t n,
                            uint64_t *__restrict__ skey, double *__restrict__ sw2, double *__restrict__ sp,
-                           int32_t *__restrict__ scnt, uint8_t *__restrict__ sdet) {
+                           int32_t *__restrict__ scnt, uint8_t *__restrict__ sdet, const int64_t *n_dev = nullptr,
+                           const StepCtl *ctl = nullptr) {
+  CPARLS_GUARD(ctl);
+  n = dcount(n, n_dev);
   int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= n) return;
   skey[t] = key[t]; sw2[t] = 1.0; sp[t] = p[t]; scnt[t] = 1; sdet[t] = 1;
@@ -517,7 +557,10 @@ __device__ __forceinline__ uint64_t mix64(uint64_t k) {
 // exclusive scan of the flags gives the output positions.
 __global__ void k_cidx_insert_first(const uint64_t *__restrict__ rkey, const double *__restrict__ rp, int64_t n,
                                     unsigned long long *__restrict__ hkey, uint32_t *__restrict__ hcnt,
-                                    double *__restrict__ hp, uint32_t *__restrict__ hfirst, uint64_t hmask) {
+                                    double *__restrict__ hp, uint32_t *__restrict__ hfirst, uint64_t hmask,
+                                    const int64_t *n_dev = nullptr, const StepCtl *ctl = nullptr) {
+  CPARLS_GUARD(ctl);
+  n = dcount(n, n_dev);
   int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= n) return;
   uint64_t k = rkey[t];
@@ -537,7 +580,10 @@ __global__ void k_cidx_insert_first(const uint64_t *__restrict__ rkey, const dou
 __global__ void k_cidx_first_flags(const uint64_t *__restrict__ rkey, int64_t n,
                                    const unsigned long long *__restrict__ hkey,
                                    const uint32_t *__restrict__ hfirst, uint64_t hmask,
-                                   int64_t *__restrict__ flag, uint32_t *__restrict__ slot) {
+                                   int64_t *__restrict__ flag, uint32_t *__restrict__ slot,
+                                   const int64_t *n_dev = nullptr, const StepCtl *ctl = nullptr) {
+  CPARLS_GUARD(ctl);
+  n = dcount(n, n_dev);
   int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= n) return;
   const uint64_t k = rkey[t];
@@ -554,7 +600,10 @@ __global__ void k_cidx_emit_first(const int64_t *__restrict__ flag, const int64_
                                   const double *__restrict__ hp, uint32_t *__restrict__ hfirst,
                                   const double *__restrict__ pdet_ptr, int64_t s_rnd, int64_t base,
                                   uint64_t *__restrict__ skey, double *__restrict__ sw2, double *__restrict__ sp,
-                                  int32_t *__restrict__ scnt, uint8_t *__restrict__ sdet) {
+                                  int32_t *__restrict__ scnt, uint8_t *__restrict__ sdet,
+                                  const StepCtl *ctl = nullptr) {
+  CPARLS_GUARD(ctl);
+  if (ctl) { n = ctl->have; s_rnd = ctl->s_rnd; base = ctl->sdet; }   // asynchronous step: device sizes
   int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= n || !flag[t]) return;
   const uint32_t h = slot[t];
@@ -587,7 +636,10 @@ struct KeyRemap {
 
 __global__ void k_lookup(const uint64_t *__restrict__ skey, int64_t sbar, const uint64_t *__restrict__ keys,
                          const int64_t *__restrict__ dir, int shift, int64_t nbkt, KeyRemap rm,
-                         int64_t *__restrict__ lo_out, int64_t *__restrict__ len_out) {
+                         int64_t *__restrict__ lo_out, int64_t *__restrict__ len_out,
+                         const int64_t *sbar_dev = nullptr, const StepCtl *ctl = nullptr) {
+  CPARLS_GUARD(ctl);
+  sbar = dcount(sbar, sbar_dev);
   int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= sbar) return;
   uint64_t k = skey[j];
@@ -629,7 +681,8 @@ __global__ void k_lookup(const uint64_t *__restrict__ skey, int64_t sbar, const 
 // ======================================================================
 // Single block: Cholesky of the sampled Gram with pivot test; fallback to the
 // eigen pseudo-inverse (AMB-12).  Ginv = G^{-1} (or G^+).
-__global__ void k_solve_prep(int r, SolveDev *sd) {
+__global__ void k_solve_prep(int r, SolveDev *sd, const StepCtl *ctl = nullptr) {
+  CPARLS_GUARD(ctl);
   extern __shared__ double sm[];
   double *G = sm, *L = sm + r * r, *Li = sm + 2 * r * r;
   __shared__ int ok;
@@ -679,7 +732,8 @@ __global__ void k_solve_prep(int r, SolveDev *sd) {
 
 // lambda_c = ||B(:,c)||, G_A = B^T B / (lambda lambda^T), then the
 // leverage preparation of the normalized factor.
-__global__ void k_norm_prep(int r, SolveDev *sd, ModeDev *md) {
+__global__ void k_norm_prep(int r, SolveDev *sd, ModeDev *md, const StepCtl *ctl = nullptr) {
+  CPARLS_GUARD(ctl);
   extern __shared__ double sm[];
   double *GA = sm + 3 * r * r;   // beyond lev_prep's scratch
   for (int c = threadIdx.x; c < r; c += blockDim.x) sd->lambda[c] = sqrt(fmax(sd->BtB[c * r + c], 0.0));
@@ -863,7 +917,10 @@ __global__ void k_sample_permute(const uint32_t *__restrict__ perm, int64_t n, c
 // 2^-60 U_c, and 64-bit integer reductions run ~15% faster than fp64 ones
 // (libcparls_peaks.so: 635 vs ~550 G lane-ops/s on this pattern).
 __global__ void k_colabs_part(const double *__restrict__ Z, const double *__restrict__ sw2, int64_t sbar, int r,
-                              int ld, double *__restrict__ part /* gridDim.x x r */) {
+                              int ld, double *__restrict__ part /* gridDim.x x r */,
+                              const int64_t *sbar_dev = nullptr, const StepCtl *ctl = nullptr) {
+  CPARLS_GUARD(ctl);
+  sbar = dcount(sbar, sbar_dev);
   const int c = threadIdx.x & 63;
   double s = 0.0;
   if (c < r)
@@ -882,7 +939,8 @@ __global__ void k_colabs_part(const double *__restrict__ Z, const double *__rest
 
 // scale[c] = 2^e_c, scale[kMaxRank + c] = 2^-e_c (exact powers of two)
 __global__ void k_fixed_scales(const double *__restrict__ part, int nb, int r, const double *maxabs, double dupmax,
-                               double *__restrict__ scale) {
+                               double *__restrict__ scale, const StepCtl *ctl = nullptr) {
+  CPARLS_GUARD(ctl);
   const int c = threadIdx.x;
   int e = 0;
   bool ok = true;

@@ -3,6 +3,8 @@
 // 256-thread blocks, 8 items per thread, warp-shuffle scans, __match_any_sync
 // stable ranking.
 #pragma once
+#include <algorithm>
+
 #include "common.cuh"
 
 namespace cparls {
@@ -47,7 +49,12 @@ __device__ __forceinline__ T block_excl_scan(T v, T *total) {
 }
 
 // ---- generic 3-phase exclusive scan of int64 counts ---------------------------
-__global__ void k_scan_partials(const int64_t *__restrict__ in, int64_t n, int64_t *__restrict__ part) {
+// n_dev: the count lives on the device (grid sized for an upper bound, blocks
+// past the count write zero partials); ctl: asynchronous-step guard.
+__global__ void k_scan_partials(const int64_t *__restrict__ in, int64_t n, int64_t *__restrict__ part,
+                                const int64_t *n_dev = nullptr, const StepCtl *ctl = nullptr) {
+  CPARLS_GUARD(ctl);
+  n = dcount(n, n_dev);
   int64_t base = (int64_t)blockIdx.x * kScanTile;
   int64_t s = 0;
 #pragma unroll
@@ -61,7 +68,10 @@ __global__ void k_scan_partials(const int64_t *__restrict__ in, int64_t n, int64
 }
 
 // single block: exclusive scan of part[0..nb) in place; total -> *total
-__global__ void k_scan_part(int64_t *part, int64_t nb, int64_t *total) {
+__global__ void k_scan_part(int64_t *part, int64_t nb, int64_t *total, const int64_t *n_dev = nullptr,
+                            const StepCtl *ctl = nullptr) {
+  CPARLS_GUARD(ctl);
+  if (n_dev) nb = ceil_div(*n_dev, kScanTile);
   int64_t carry = 0;
   for (int64_t base = 0; base < nb; base += kScanThreads) {
     int64_t idx = base + threadIdx.x;
@@ -76,7 +86,11 @@ __global__ void k_scan_part(int64_t *part, int64_t nb, int64_t *total) {
 }
 
 __global__ void k_scan_final(const int64_t *__restrict__ in, int64_t n, const int64_t *__restrict__ part,
-                             int64_t *__restrict__ out) {
+                             int64_t *__restrict__ out, const int64_t *n_dev = nullptr,
+                             const StepCtl *ctl = nullptr) {
+  CPARLS_GUARD(ctl);
+  n = dcount(n, n_dev);
+  if ((int64_t)blockIdx.x * kScanTile >= n) return;
   int64_t base = (int64_t)blockIdx.x * kScanTile + (int64_t)threadIdx.x * kScanItems;
   int64_t v[kScanItems];
   int64_t s = 0;
@@ -110,6 +124,20 @@ inline int exclusive_scan_i64(const int64_t *in, int64_t *out, int64_t n, int64_
   k_scan_part<<<1, kScanThreads, 0, st>>>(part, nb, total);
   CK_LAUNCH();
   k_scan_final<<<(unsigned)nb, kScanThreads, 0, st>>>(in, n, part, out);
+  CK_LAUNCH();
+  return 3;
+}
+
+// The same scan with the count on the device (n_dev, at most n_max) inside an
+// asynchronous step: grids sized for n_max, no host synchronisation.
+inline int exclusive_scan_i64_dev(const int64_t *in, int64_t *out, int64_t n_max, const int64_t *n_dev,
+                                  int64_t *part, int64_t *total, cudaStream_t st, const StepCtl *ctl) {
+  const int64_t nb = ceil_div(std::max<int64_t>(n_max, 1), kScanTile);
+  k_scan_partials<<<(unsigned)nb, kScanThreads, 0, st>>>(in, n_max, part, n_dev, ctl);
+  CK_LAUNCH();
+  k_scan_part<<<1, kScanThreads, 0, st>>>(part, nb, total, n_dev, ctl);
+  CK_LAUNCH();
+  k_scan_final<<<(unsigned)nb, kScanThreads, 0, st>>>(in, n_max, part, out, n_dev, ctl);
   CK_LAUNCH();
   return 3;
 }
@@ -224,6 +252,52 @@ constexpr int kSmallSortThreads = 1024;
 
 __global__ void __launch_bounds__(kSmallSortThreads) k_small_sort_pairs(uint64_t *__restrict__ keys,
                                                                         uint32_t *__restrict__ vals, int n) {
+  __shared__ uint64_t sk[kSmallSortMax];
+  __shared__ uint32_t sv[kSmallSortMax];
+  int np = 1;
+  while (np < n) np <<= 1;
+  for (int i = threadIdx.x; i < np; i += blockDim.x) {
+    sk[i] = i < n ? keys[i] : ~0ull;
+    sv[i] = i < n ? vals[i] : 0xFFFFFFFFu;
+  }
+  __syncthreads();
+  for (int size = 2; size <= np; size <<= 1) {
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      for (int t = threadIdx.x; t < (np >> 1); t += blockDim.x) {
+        const int lo = 2 * t - (t & (stride - 1));
+        const int hi = lo + stride;
+        const bool up = (lo & size) == 0;
+        const uint64_t a = sk[lo], b = sk[hi];
+        const uint32_t va = sv[lo], vb = sv[hi];
+        const bool gt = (a > b) || (a == b && va > vb);
+        if (gt == up) {
+          sk[lo] = b; sk[hi] = a;
+          sv[lo] = vb; sv[hi] = va;
+        }
+      }
+      __syncthreads();
+    }
+  }
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    keys[i] = sk[i];
+    vals[i] = sv[i];
+  }
+}
+
+// One-CTA sort with the count on the device: n > kSmallSortMax raises abort
+// (the step then goes to the host-driven path, which has the multi-CTA sort).
+__global__ void __launch_bounds__(kSmallSortThreads) k_small_sort_pairs_dev(uint64_t *__restrict__ keys,
+                                                                            uint32_t *__restrict__ vals,
+                                                                            const int64_t *n_dev, StepCtl *ctl,
+                                                                            int64_t step) {
+  CPARLS_GUARD(ctl);
+  const int64_t n64 = *n_dev;
+  if (n64 > kSmallSortMax) {
+    if (threadIdx.x == 0) step_abort(ctl, step);
+    return;
+  }
+  const int n = (int)n64;
+  if (n <= 1) return;
   __shared__ uint64_t sk[kSmallSortMax];
   __shared__ uint32_t sv[kSmallSortMax];
   int np = 1;

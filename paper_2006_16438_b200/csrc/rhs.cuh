@@ -144,7 +144,10 @@ __global__ void __launch_bounds__(kRhsThreads) k_rhs(const int64_t *__restrict__
                                                     const int32_t *__restrict__ outidx, const VT *__restrict__ vals,
                                                     const double *__restrict__ sw2, const double *__restrict__ Z,
                                                     int r, int ld, double *__restrict__ M, int64_t per_warp,
-                                                    const double *__restrict__ fscale) {
+                                                    const double *__restrict__ fscale,
+                                                    const int64_t *nseg_dev = nullptr, const StepCtl *ctl = nullptr) {
+  CPARLS_GUARD(ctl);
+  nseg = dcount(nseg, nseg_dev);
   __shared__ __align__(16) RhsEnt ents[kRhsThreads];
   RhsEnt *we = ents + (threadIdx.x & ~31);
   const int lane = threadIdx.x & 31;
@@ -165,8 +168,12 @@ __global__ void __launch_bounds__(kRhsThreads) k_rhs(const int64_t *__restrict__
 __global__ void k_win_bounds(const int64_t *__restrict__ lo, const int64_t *__restrict__ len, int64_t sbar,
                              const int32_t *__restrict__ outidx, int nwin, int64_t RW,
                              int64_t *__restrict__ seg_lo, int64_t *__restrict__ seg_len,
-                             int32_t *__restrict__ seg_j) {
+                             int32_t *__restrict__ seg_j, const int64_t *sbar_dev = nullptr,
+                             int64_t *nseg_out = nullptr, const StepCtl *ctl = nullptr) {
+  CPARLS_GUARD(ctl);
+  sbar = dcount(sbar, sbar_dev);
   const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (g == 0 && nseg_out) *nseg_out = (int64_t)nwin * sbar;
   if (g >= (int64_t)nwin * sbar) return;
   const int w = (int)(g / sbar);
   const int64_t j = g - (int64_t)w * sbar;

@@ -110,7 +110,9 @@ __global__ void __launch_bounds__(kRowThreads) k_solve_rows_t(double *__restrict
                                                              const SolveDev *__restrict__ sd, double *__restrict__ B,
                                                              double *__restrict__ part,
                                                              unsigned long long *__restrict__ touched,
-                                                             int zero_m, const double *__restrict__ fscale) {
+                                                             int zero_m, const double *__restrict__ fscale,
+                                                             const StepCtl *ctl = nullptr) {
+  CPARLS_GUARD(ctl);
   extern __shared__ __align__(16) double smem[];
   const int S = ld + 2;              // even: 16-byte aligned rows, conflict-free 16-byte row accesses
   double *Gi = smem;                 // G^+ with row stride ld (zero padded): 16-byte operand loads
@@ -258,7 +260,9 @@ __global__ void __launch_bounds__(kRowThreads, 2) k_lev_rows_w(double *__restric
                                                               uint64_t *__restrict__ C,
                                                               unsigned long long *__restrict__ tile_sum,
                                                               double *alpha_out,
-                                                              unsigned long long *drawable_out) {
+                                                              unsigned long long *drawable_out,
+                                                              const StepCtl *ctl = nullptr) {
+  CPARLS_GUARD(ctl);
   extern __shared__ __align__(16) double smem[];
   const int S = warp_tile_stride(ld);
   double *W = smem;                  // RMAX x RMAX, zero padded (and zero below the diagonal if tri)
@@ -369,7 +373,9 @@ __global__ void __launch_bounds__(kRowThreads, 2) k_solve_dmma(double *__restric
                                                                const SolveDev *__restrict__ sd,
                                                                double *__restrict__ B, double *__restrict__ part,
                                                                unsigned long long *__restrict__ touched, int zero_m,
-                                                               const double *__restrict__ fscale) {
+                                                               const double *__restrict__ fscale,
+                                                               const StepCtl *ctl = nullptr) {
+  CPARLS_GUARD(ctl);
   constexpr int LD = NT * 8, KS = NT * 2, NP = NT * (NT + 1) / 2;
   constexpr int S = LD + 2;   // even: 16-byte aligned tile rows
   extern __shared__ __align__(16) double smem[];
@@ -475,7 +481,11 @@ template <int RMAX>
 __global__ void __launch_bounds__(kRowThreads) k_krp_gram_t(const uint64_t *__restrict__ skey,
                                                            const double *__restrict__ sw2, int64_t sbar,
                                                            OtherModes om, int r, int ld, double *__restrict__ Z,
-                                                           double *__restrict__ part) {
+                                                           double *__restrict__ part,
+                                                           const int64_t *sbar_dev = nullptr,
+                                                           const StepCtl *ctl = nullptr) {
+  CPARLS_GUARD(ctl);
+  sbar = dcount(sbar, sbar_dev);
   extern __shared__ double smem[];
   const int S = ld + 1;
   double *tile = smem;

@@ -144,7 +144,9 @@ struct Syrk {
 
 // Sum nb block partials (full r*r layout, upper triangle valid) into a full
 // symmetric r x r matrix.  One warp per upper entry, double-double sums.
-__global__ void k_pairs_reduce(const double *__restrict__ part, int64_t nb, int r, double *__restrict__ G) {
+__global__ void k_pairs_reduce(const double *__restrict__ part, int64_t nb, int r, double *__restrict__ G,
+                               const StepCtl *ctl = nullptr) {
+  CPARLS_GUARD(ctl);
   const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (w >= (int64_t)r * r) return;

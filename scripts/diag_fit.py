@@ -32,18 +32,19 @@ def main():
     res = {}
     for fm in [int(x) for x in (sys.argv[1:] or ["-1"])]:
         g = Cparls(cfg.dims, T.coords, T.vals, cfg.rank, tau=-1.0, init_seed=cfg.init_seed, fit_mode=fm)
-        r = {"after_create": fit_ms(g)}
+        r = {"lib": os.environ.get("CPARLS_LIB", "default")}
+        r["after_create"] = fit_ms(g)
         g.run(3, cfg.s, 3, iter0=0, fit_every=0)
         r["after_3_iters"] = fit_ms(g)
-        g.run(5, cfg.s, 3, iter0=3, fit_every=0)
-        r["after_8_iters"] = fit_ms(g)
-        g.reset_stats()
-        t0 = time.perf_counter()
-        g.run(5, cfg.s, 3, iter0=8, fit_every=1)
-        torch.cuda.synchronize()
-        st = g.stats()
-        r["inside_run_fit_every_1"] = st["kernel_ms"]["fit"] / max(1, st["kernel_launches_by_id"]["fit"])
-        r["rhs_avg"] = st["kernel_ms"]["rhs"] / max(1, st["kernel_launches_by_id"]["rhs"])
+        if os.environ.get("DIAG_FIT_LONG"):
+            g.run(5, cfg.s, 3, iter0=3, fit_every=0)
+            r["after_8_iters"] = fit_ms(g)
+            g.reset_stats()
+            g.run(5, cfg.s, 3, iter0=8, fit_every=1)
+            torch.cuda.synchronize()
+            st = g.stats()
+            r["inside_run_fit_every_1"] = st["kernel_ms"]["fit"] / max(1, st["kernel_launches_by_id"]["fit"])
+            r["rhs_avg"] = st["kernel_ms"]["rhs"] / max(1, st["kernel_launches_by_id"]["rhs"])
         res[fm] = r
         g.close()
         torch.cuda.empty_cache()

@@ -140,6 +140,53 @@ __global__ void k_smem_rmw4(int srows, int r, int ld, int64_t per_warp, unsigned
   if (lane == 0 && t[0] == 12345) out[0] = t[1];
 }
 
+__device__ __forceinline__ unsigned smid() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%smid;" : "=r"(r));
+  return r;
+}
+// the k_rhs pattern restricted to CTAs on SMs < nsm (the others exit): does the
+// SM->L2 write path saturate with part of the chip?  Work counter = fixed total.
+__global__ void k_red_u64_sm(unsigned long long *M, int64_t rows, int r, int ld, int64_t total, unsigned nsm,
+                             unsigned long long *work, uint32_t salt) {
+  if (smid() >= nsm) return;
+  const int lane = threadIdx.x & 31;
+  while (true) {
+    unsigned long long t0 = 0;
+    if (lane == 0) t0 = atomicAdd(work, 64ull);
+    t0 = __shfl_sync(0xffffffffu, t0, 0);
+    if ((int64_t)t0 >= total) break;
+    for (int i = 0; i < 64; ++i) {
+      const int64_t row = rnd_row((uint32_t)t0, i, salt, rows);
+      if (lane < r) atomicAdd(M + row * ld + lane, 3ull);
+    }
+  }
+}
+// random 256-B row gathers (the fit's pattern) restricted to SMs < nsm
+__global__ void k_gather_sm(const double *__restrict__ Z, int64_t rows, int ld, int64_t total, unsigned nsm,
+                            unsigned long long *work, double *out, uint32_t salt) {
+  if (smid() >= nsm) return;
+  const int lane = threadIdx.x & 31;
+  const int sub = lane >> 3, sl = lane & 7;
+  double acc = 0.0;
+  while (true) {
+    unsigned long long t0 = 0;
+    if (lane == 0) t0 = atomicAdd(work, 256ull);
+    t0 = __shfl_sync(0xffffffffu, t0, 0);
+    if ((int64_t)t0 >= total) break;
+    for (int i = 0; i < 256; i += 16) {
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int64_t row = rnd_row((uint32_t)t0, i + 4 * u + sub, salt, rows);
+        const double2 *p = reinterpret_cast<const double2 *>(Z + row * ld + 4 * sl);
+        const double2 a = __ldg(p), b = __ldg(p + 1);
+        acc += a.x + a.y + b.x + b.y;
+      }
+    }
+  }
+  if (acc == 1234.5) out[0] = acc;
+}
+
 template <typename L>
 float time_it(L launch, int reps) {
   cudaEvent_t a, b;
@@ -190,6 +237,24 @@ int main() {
     const double bytes = (double)warps * pwg * ld * 8;
     printf("gather 256-B rows from %8lld rows (%6.1f MB): %7.1f GB/s  %6.2f G rows/s\n", (long long)rows,
            rows * ld * 8 / 1e6, bytes / ms / 1e6, warps * pwg / ms / 1e6);
+  }
+  {
+    unsigned long long *work;
+    cudaMalloc(&work, 8);
+    const int64_t total = 1 << 26;
+    for (unsigned nsm : {37u, 74u, 111u, 148u}) {
+      float ms = time_it([&](uint32_t s) {
+        cudaMemset(work, 0, 8);
+        k_red_u64_sm<<<blocks, threads>>>((unsigned long long *)M, 393216, r, ld, total, nsm, work, s);
+      }, 3);
+      printf("red.u64 x25 on %3u SMs: %6.2f G rows/s\n", nsm, total / ms / 1e6);
+      ms = time_it([&](uint32_t s) {
+        cudaMemset(work, 0, 8);
+        k_gather_sm<<<blocks, threads>>>((const double *)M, 1805187, ld, total, nsm, work, scr, s);
+      }, 3);
+      printf("gather 256-B rows (1.8M rows) on %3u SMs: %6.2f G rows/s  %7.1f GB/s\n", nsm, total / ms / 1e6,
+             total * 256.0 / ms / 1e6);
+    }
   }
   {
     int srows = 800;

@@ -67,16 +67,12 @@ SOLVE_LOG = []
 
 
 def solve_tol(G, tag=""):
-    """North-star bar 1e-9 relative Frobenius on the same sample set.  For an
-    ill-conditioned sampled Gram (kappa over the kept spectrum > 1e6) B is only
-    determined to ~kappa(G)*eps by the fp64 data (both sides form G with
-    different summation orders: dG/G ~ eps, dB/B ~ kappa dG/G), so the bar is
-    1e-15*kappa(G), capped at 1e-6 (DESIGN.md AMB-36).  Every case is logged
-    (kappa, bar) in SOLVE_LOG / gpurun_out/solve_bars.jsonl."""
-    kappa = kept_kappa(G)
-    tol = 1e-9 if kappa <= 1e6 else min(1e-6, 1e-15 * kappa)
-    SOLVE_LOG.append({"case": tag, "kappa": float(kappa), "bar": tol})
-    return tol
+    """North-star bar: 1e-9 relative Frobenius on the same sample set.  kappa
+    of the sampled Gram (over the kept spectrum, AMB-11) is logged with every
+    case in SOLVE_LOG / gpurun_out/solve_bars.jsonl (round 2: 226 cases, max
+    kappa 4.9e4, max relative error 8.4e-13)."""
+    SOLVE_LOG.append({"case": tag, "kappa": float(kept_kappa(G)), "bar": 1e-9})
+    return 1e-9
 
 
 def log_solve(rel):

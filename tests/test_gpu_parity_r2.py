@@ -161,3 +161,72 @@ def test_c5_dims_reduced_nnz_lockstep():
     assert T.vals.dtype == torch.float32
     Tc = synth.Tensor(T.cfg, T.dims, T.coords.cpu(), T.vals.cpu())
     lockstep(Tc, cfg.rank, 1, cfg.s, cfg.sample_seed)
+
+
+# ---------------------------------------------------------------- sync-free mode step
+def _factors(g):
+    return [g.get_factor(m) for m in range(g.D)]
+
+
+@pytest.mark.parametrize("name", ["C1", "C2"])
+def test_run_is_sync_free_and_equals_stepwise(name):
+    """cparls_run enqueues every mode step without host synchronisation (one
+    synchronisation per call, counted by cparls_stats.host_syncs) and gives
+    the bit-identical factors and fit trace of the same steps taken one
+    cparls_sample + cparls_solve_mode at a time (the fixed-point RHS makes a
+    step's result independent of how it was scheduled)."""
+    need_gpu()
+    from paper_2006_16438_b200 import Cparls
+    T = synth.make(name) if name == "C1" else synth.make(name, device="cuda")
+    cfg = T.cfg
+    a = Cparls(T.dims, T.coords.cuda(), T.vals.cuda(), cfg.rank)
+    b = Cparls(T.dims, T.coords.cuda(), T.vals.cuda(), cfg.rank)
+    iters = 3
+    a.reset_stats()
+    ta = a.run(iters, cfg.s, cfg.sample_seed, iter0=0, fit_every=1)
+    st = a.stats()
+    assert st["host_syncs"] <= 1, st["host_syncs"]
+    tb = []
+    D = len(T.dims)
+    for t in range(iters):
+        for k in range(D):
+            b.sample(k, cfg.s, cfg.sample_seed, t * D + k)
+            b.solve_mode(k)
+        tb.append(b.fit())
+    assert np.array_equal(np.asarray(ta), np.asarray(tb)), (ta, tb)
+    for (Aa, la), (Ab, lb) in zip(_factors(a), _factors(b)):
+        assert np.array_equal(Aa.view(np.uint64), Ab.view(np.uint64)) and np.array_equal(la, lb)
+    for m in range(D):
+        assert np.array_equal(a.get_ptilde(m), b.get_ptilde(m))
+
+
+def test_run_recovers_aborted_steps_with_the_host_sampler():
+    """tau = 1e-6 < 1/s makes |DetSet| > s in every step (AMB-6 truncation, a
+    host-path branch): every asynchronous step aborts and is redone by the
+    host sampler; the run still equals the oracle's steps (lockstep on the
+    first iteration) and the step-by-step GPU sequence."""
+    need_gpu()
+    from paper_2006_16438_b200 import Cparls
+    T = synth.make("C1")
+    cfg = T.cfg
+    a = Cparls(T.dims, T.coords.cuda(), T.vals.cuda(), cfg.rank, tau=1e-6)
+    b = Cparls(T.dims, T.coords.cuda(), T.vals.cuda(), cfg.rank, tau=1e-6)
+    ta = a.run(2, cfg.s, 9, iter0=0, fit_every=1)
+    tb = []
+    for t in range(2):
+        for k in range(3):
+            info = b.sample(k, cfg.s, 9, t * 3 + k)
+            assert info.s_det == cfg.s and info.s_rnd == 0
+            b.solve_mode(k)
+        tb.append(b.fit())
+    assert np.array_equal(np.asarray(ta), np.asarray(tb)), (ta, tb)
+    for (Aa, _), (Ab, _) in zip(_factors(a), _factors(b)):
+        assert np.array_equal(Aa.view(np.uint64), Ab.view(np.uint64))
+    # the truncated steps against the oracle
+    o = oracle.Oracle(T.dims, T.coords.to(torch.int64).numpy(), T.vals.numpy(), cfg.rank)
+    g = Cparls(T.dims, T.coords.cuda(), T.vals.cuda(), cfg.rank, tau=1e-6)
+    for k in range(3):
+        for m in range(3):
+            o.set_factor(m, g.get_factor(m)[0])
+            o.set_ptilde(m, g.get_ptilde(m))
+        _step_lockstep(g, o, k, cfg.s, 1e-6, 9, k)
