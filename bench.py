@@ -309,13 +309,10 @@ def run_ours(args):
     cfg = synth.CONFIGS[args.config]
     D = len(cfg.dims)
     t0 = time.perf_counter()
-    T = synth.make(cfg, device=dev, index_dtype=torch.int32)
+    # this rank's chunk of the COO only (cells rk, rk + ws, ... of the tensor);
+    # cparls_create routes the nonzeros to the owners of their rows
+    T = synth.make(cfg, device=dev, index_dtype=torch.int32, part=rk, parts=ws)
     coords, vals = T.coords, T.vals
-    if ws > 1:   # this rank's chunk of the COO; cparls_create routes rows to owners
-        coords = coords[rk::ws].contiguous()
-        vals = vals[rk::ws].contiguous()
-        del T
-        T = None
     torch.cuda.synchronize()
     t_gen = time.perf_counter() - t0
     nnz = cfg.nnz

@@ -143,6 +143,7 @@ typedef struct {
   int64_t kernel_launches_by_id[4];
   int64_t sum_matched_nnz;   /* sum of m_k over the solves since the last reset   */
   int64_t host_syncs;        /* cudaStreamSynchronize calls made by the library   */
+  double bytes_comm;         /* bytes this rank contributed to collectives (world_size > 1) */
 } cparls_stats;
 
 /* Build the context: validates sizes (ERANGE if some prod_{m!=k} n_m >= 2^63 or
@@ -261,8 +262,20 @@ cparls_status cparls_comm_create_nccl(int32_t world_size, int32_t rank, const ui
 cparls_status cparls_comm_create_local(int32_t world_size, cparls_comm **out);
 cparls_status cparls_comm_destroy(cparls_comm *comm);
 /* Host-only: row blocks of a mode from its global per-row nonzero counts deg[n]
- * (bound[p]..bound[p+1]-1 owned by rank p; bound has world_size+1 entries). */
-cparls_status cparls_plan_rows(int64_t n, const uint64_t *deg, int32_t world_size, int64_t *bound);
+ * (bound[p]..bound[p+1]-1 owned by rank p; bound has world_size+1 entries).
+ * A heavy row (deg > total/world_size: a Zipf head row) has its nonzeros
+ * spread over all ranks (by a hash of the other coordinates) and weighs
+ * ceil(deg/world_size); its partial RHS rows are summed over the ranks every
+ * mode step and the rank whose block contains it solves it.  heavy (n bytes,
+ * may be NULL) receives 1 for the heavy rows. */
+cparls_status cparls_plan_rows(int64_t n, const uint64_t *deg, int32_t world_size, int64_t *bound,
+                               uint8_t *heavy);
+/* Host-only: the rank cparls_create routes each nonzero to in the sharded
+ * build of mode `mode` (coords: nnz x nmodes int64; bound/heavy from
+ * cparls_plan_rows, heavy may be NULL): the owner of its row, or for a heavy
+ * row a hash of its other coordinates.  rank_out: nnz int32. */
+cparls_status cparls_route_nonzeros(int32_t nmodes, int32_t mode, int64_t nnz, const int64_t *coords,
+                                    int32_t world_size, const int64_t *bound, const uint8_t *heavy, int32_t *rank_out);
 /* Rows of mode `mode` owned by this rank. */
 cparls_status cparls_owned_rows(const cparls_ctx *ctx, int32_t mode, int64_t *lo, int64_t *hi);
 

@@ -53,7 +53,8 @@ class Stats(C.Structure):
         "bytes_fit")] + [(n, C.c_int64) for n in (
         "mode_steps", "fits", "kernel_launches", "last_matched_nnz", "last_s_bar", "last_attempts")] + [
         ("touched_rows", C.c_int64 * 8), ("kernel_ms", C.c_double * 4),
-        ("kernel_launches_by_id", C.c_int64 * 4), ("sum_matched_nnz", C.c_int64), ("host_syncs", C.c_int64)]
+        ("kernel_launches_by_id", C.c_int64 * 4), ("sum_matched_nnz", C.c_int64), ("host_syncs", C.c_int64),
+        ("bytes_comm", C.c_double)]
 
     KERNELS = ("rhs", "fit", "solve_rows", "lev_rows")
 
@@ -106,7 +107,8 @@ def lib():
             "cparls_comm_create_nccl": [I32, I32, P, C.POINTER(P)],
             "cparls_comm_create_local": [I32, C.POINTER(P)],
             "cparls_comm_destroy": [P],
-            "cparls_plan_rows": [I64, P, I32, P],
+            "cparls_plan_rows": [I64, P, I32, P, P],
+            "cparls_route_nonzeros": [I32, I32, I64, P, I32, P, P, P],
             "cparls_owned_rows": [P, I32, P, P],
         }
         for name, args in sig.items():
@@ -131,7 +133,8 @@ EXPORTED = ["cparls_create", "cparls_destroy", "cparls_set_factor", "cparls_get_
             "cparls_run_als", "cparls_get_stats",
             "cparls_reset_stats", "cparls_set_profiling", "cparls_last_error", "cparls_version",
             "cparls_comm_nccl_unique_id", "cparls_comm_create_nccl", "cparls_comm_create_local",
-            "cparls_comm_destroy", "cparls_plan_rows", "cparls_owned_rows", "cparls_opts_init"]
+            "cparls_comm_destroy", "cparls_plan_rows", "cparls_owned_rows", "cparls_opts_init",
+            "cparls_route_nonzeros"]
 
 
 def _ptr(x):
@@ -393,15 +396,32 @@ class Comm:
             self.handle = None
 
 
-def plan_rows(deg, world_size):
+def plan_rows(deg, world_size, with_heavy=False):
     """Row blocks (world_size + 1 bounds) balanced by the per-row counts deg
-    (host-only library call; cparls_plan_rows)."""
+    (host-only library call; cparls_plan_rows); with_heavy also returns the
+    heavy-row flags (rows whose nonzeros are spread over all ranks)."""
     deg = np.ascontiguousarray(deg, dtype=np.uint64)
     bound = np.zeros(int(world_size) + 1, dtype=np.int64)
-    st = lib().cparls_plan_rows(len(deg), deg.ctypes.data, int(world_size), bound.ctypes.data)
+    heavy = np.zeros(len(deg), dtype=np.uint8)
+    st = lib().cparls_plan_rows(len(deg), deg.ctypes.data, int(world_size), bound.ctypes.data, heavy.ctypes.data)
     if st != OK:
         raise CparlsError(st, "plan_rows")
-    return bound
+    return (bound, heavy.astype(bool)) if with_heavy else bound
+
+
+def route_nonzeros(coords, mode, world_size, bound, heavy=None):
+    """Rank of each nonzero in the sharded build of `mode` (host-only library
+    call; cparls_route_nonzeros): the row owner, or a hash for heavy rows."""
+    coords = np.ascontiguousarray(coords, dtype=np.int64)
+    bound = np.ascontiguousarray(bound, dtype=np.int64)
+    hv = None if heavy is None else np.ascontiguousarray(heavy, dtype=np.uint8)
+    out = np.zeros(coords.shape[0], dtype=np.int32)
+    st = lib().cparls_route_nonzeros(coords.shape[1], int(mode), coords.shape[0], coords.ctypes.data,
+                                     int(world_size), bound.ctypes.data, None if hv is None else hv.ctypes.data,
+                                     out.ctypes.data)
+    if st != OK:
+        raise CparlsError(st, "route_nonzeros")
+    return out
 
 
 def version():

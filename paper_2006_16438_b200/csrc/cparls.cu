@@ -166,6 +166,15 @@ struct cparls_ctx {
   int world = 1, wrank = 0;
   int64_t row_lo[kMaxModes] = {0}, row_hi[kMaxModes] = {0};
   std::vector<int64_t> bounds[kMaxModes];   // row blocks of every rank per mode
+  std::vector<int64_t> heavy[kMaxModes];    // heavy rows (nonzeros spread over the ranks), ascending
+  int64_t *heavy_dev[kMaxModes] = {nullptr};
+  uint8_t *heavy_own[kMaxModes] = {nullptr};   // this rank owns heavy row h
+  int64_t heavy_buf_n = 0;
+  double *heavy_buf = nullptr;              // |heavy| x ld exchange buffer
+  bool fac_dirty[kMaxModes] = {false};      // only the owned rows of A_k are current (world > 1)
+  double *Zg = nullptr;                     // sampled other-mode rows from their owners (s x d x ld)
+  int64_t *drow_lo = nullptr, *drow_hi = nullptr;   // owned row ranges of every mode (device)
+  int64_t zg_cap = 0;
   // RHS output-row windows (see rhs.cuh)
   int64_t segcap = 0;
   int64_t *seg_lo = nullptr, *seg_len = nullptr, *seg_off = nullptr, *i64part_seg = nullptr;
@@ -586,6 +595,53 @@ void lev_rows_and_cdf(cparls_ctx *c, int k, const double *lam) {
   c->stats.bytes_leverage += (double)n * (c->r * 8.0 * (lam ? 2 : 1) + 16.0);
 }
 
+// Sharded leverage refresh: normalize and score the owned rows
+// of A_k only, allgather p~_k (8 bytes per row instead of the factor rows),
+// then every rank forms q and the integer CDF of all rows from the identical
+// p~ bits (the same kernels as the set_ptilde path).
+void lev_rows_sharded(cparls_ctx *c, int k, const double *lam) {
+  const int64_t n = c->dims[k];
+  const int64_t r0 = c->row_lo[k], nown = c->row_hi[k] - c->row_lo[k];
+  const int64_t nt = ceil_div(n, kLevThreads);
+  if (nown > 0) {
+    const unsigned g = (unsigned)row_grid(c, ceil_div(nown, kWarpRows * (kRowThreads / 32)));
+    KTimer kt(c, KT_LEV);
+    RSWITCH(c->r, k_lev_rows_w<RM><<<g, kRowThreads, lev_w_smem(c->r, c->ld), c->st>>>(
+                      c->A[k] + r0 * c->ld, nown, c->r, c->ld, lam, c->md[k], c->pt[k] + r0, c->C[k] + r0,
+                      reinterpret_cast<unsigned long long *>(c->tile_u64), &c->md[k]->alpha,
+                      reinterpret_cast<unsigned long long *>(&c->md[k]->drawable), c->ctl));
+    kt.stop();
+    CK_LAUNCH();
+  }
+  std::vector<int64_t> off(c->world + 1);
+  for (int q = 0; q <= c->world; ++q) off[q] = q < c->world ? row_start(c, k, q) : n;
+  c->comm->allgatherv_f64(c->pt[k], off, c->st);
+  c->stats.bytes_comm += 8.0 * n;
+  k_lev_reset<<<1, 1, 0, c->st>>>(c->md[k], c->ctl);
+  k_q_from_pt<<<(unsigned)nt, kLevThreads, 0, c->st>>>(c->pt[k], n, c->C[k], c->tile_u64, &c->md[k]->alpha,
+                                                       reinterpret_cast<unsigned long long *>(&c->md[k]->drawable),
+                                                       c->ctl);
+  CK_LAUNCH();
+  k_scan_u64_single<<<1, kScanThreads, 0, c->st>>>(c->tile_u64, nt, c->ctl);
+  CK_LAUNCH();
+  k_cdf_final<<<(unsigned)nt, kLevThreads, 0, c->st>>>(c->C[k], n, c->tile_u64, c->ctl);
+  CK_LAUNCH();
+  LAUNCHED(c, 5);
+  c->stats.bytes_leverage += (double)nown * (c->r * 8.0 * 2 + 16.0) + (double)n * 16.0;
+  c->fac_dirty[k] = true;   // only the owned rows of A_k are current here
+}
+
+// Every rank gets every row of A_m (collective, SPMD): the per-epoch dense
+// allgather for the exact fit, and the factor getters of a sharded run.
+void gather_factor(cparls_ctx *c, int m) {
+  if (c->world <= 1 || !c->fac_dirty[m]) return;
+  std::vector<int64_t> off(c->world + 1);
+  for (int q = 0; q <= c->world; ++q) off[q] = (q < c->world ? row_start(c, m, q) : c->dims[m]) * c->ld;
+  c->comm->allgatherv_f64(c->A[m], off, c->st);
+  c->stats.bytes_comm += 8.0 * c->dims[m] * c->ld;
+  c->fac_dirty[m] = false;
+}
+
 void gram_of_rows(cparls_ctx *c, const double *A, int64_t n, double *G_out) {
   const int64_t grid = row_grid(c, ceil_div(n, kRowThreads));
   RSWITCH(c->r, k_gram_rows_t<RM><<<(unsigned)grid, kRowThreads, gram_smem(c->r, c->ld), c->st>>>(A, n, c->r, c->ld,
@@ -597,6 +653,7 @@ void gram_of_rows(cparls_ctx *c, const double *A, int64_t n, double *G_out) {
 }
 
 void leverage_full(cparls_ctx *c, int k) {
+  gather_factor(c, k);
   Phase ph(c, &c->stats.ms_leverage);
   gram_of_rows(c, c->A[k], c->dims[k], c->Gtmp);
   k_lev_prep<<<1, 128, prep_smem(c->r), c->st>>>(c->r, c->Gtmp, c->md[k]);
@@ -742,17 +799,32 @@ void build_index_mode(cparls_ctx *c, int k, const IT *coords, const VT *vals, in
   sync(c);
 }
 
-// Row partition of mode k into world contiguous blocks balanced by nonzeros:
-// bound[p] = first row whose exclusive prefix of deg reaches p*total/world.
-void plan_rows(int64_t n, const unsigned long long *deg, int world, int64_t *bound) {
+// Row partition of mode k into world contiguous blocks balanced by nonzeros
+// (SURVEY 8(e)).  A heavy row -- more nonzeros than a rank's share total/world
+// (a Zipf head row) -- has its nonzeros spread over all ranks (heavy_rank) and
+// weighs ceil(deg/world) in the plan; it is owned (solved) by the rank whose
+// block contains it, after its partial RHS rows are summed over the ranks.
+// bound[p] = first row whose exclusive prefix of the weights reaches
+// p*W/world.  heavy (n flags, may be null) receives the heavy rows.
+void plan_rows(int64_t n, const unsigned long long *deg, int world, int64_t *bound, uint8_t *heavy) {
   unsigned long long total = 0;
   for (int64_t i = 0; i < n; ++i) total += deg[i];
+  const unsigned long long share = total / (unsigned long long)world;
+  auto is_heavy = [&](int64_t i) { return world > 1 && deg[i] > share; };
+  auto weight = [&](int64_t i) {
+    return is_heavy(i) ? (deg[i] + (unsigned long long)world - 1) / (unsigned long long)world : deg[i];
+  };
+  unsigned long long W = 0;
+  for (int64_t i = 0; i < n; ++i) {
+    W += weight(i);
+    if (heavy) heavy[i] = is_heavy(i) ? 1 : 0;
+  }
   bound[0] = 0;
   unsigned long long run = 0;
   int64_t i = 0;
   for (int p = 1; p < world; ++p) {
-    const unsigned long long t = (unsigned long long)(((unsigned __int128)total * p) / world);
-    while (i < n && run < t) run += deg[i++];
+    const unsigned long long t = (unsigned long long)(((unsigned __int128)W * p) / world);
+    while (i < n && run < t) run += weight(i++);
     bound[p] = i;
   }
   bound[world] = n;
@@ -777,10 +849,27 @@ void route_and_build(cparls_ctx *c, int k, const IT *coords, const VT *vals) {
   sync(c);
   dfree(c, deg);
   std::vector<int64_t> bound(P + 1);
-  plan_rows(n, hdeg.data(), P, bound.data());
+  std::vector<uint8_t> hv(n);
+  plan_rows(n, hdeg.data(), P, bound.data(), hv.data());
   c->row_lo[k] = bound[c->wrank];
   c->row_hi[k] = bound[c->wrank + 1];
   c->bounds[k] = bound;
+  // heavy rows of mode k: nonzeros spread over the ranks; partial RHS rows summed
+  c->heavy[k].clear();
+  for (int64_t i = 0; i < n; ++i)
+    if (hv[i]) c->heavy[k].push_back(i);
+  uint8_t *dheavy = dalloc_t<uint8_t>(c, n);
+  CK(cudaMemcpyAsync(dheavy, hv.data(), n, cudaMemcpyHostToDevice, c->st));
+  if (!c->heavy[k].empty()) {
+    const int64_t nh = (int64_t)c->heavy[k].size();
+    c->heavy_dev[k] = dalloc_t<int64_t>(c, nh);
+    CK(cudaMemcpyAsync(c->heavy_dev[k], c->heavy[k].data(), sizeof(int64_t) * nh, cudaMemcpyHostToDevice, c->st));
+    std::vector<uint8_t> own(nh);
+    for (int64_t h = 0; h < nh; ++h) own[h] = c->heavy[k][h] >= c->row_lo[k] && c->heavy[k][h] < c->row_hi[k];
+    c->heavy_own[k] = dalloc_t<uint8_t>(c, nh);
+    CK(cudaMemcpyAsync(c->heavy_own[k], own.data(), nh, cudaMemcpyHostToDevice, c->st));
+    c->heavy_buf_n = std::max(c->heavy_buf_n, nh);
+  }
   // destination rank per local nonzero, stable order by destination
   int64_t *dbound = dalloc_t<int64_t>(c, P + 1);
   CK(cudaMemcpyAsync(dbound, bound.data(), sizeof(int64_t) * (P + 1), cudaMemcpyHostToDevice, c->st));
@@ -789,7 +878,8 @@ void route_and_build(cparls_ctx *c, int k, const IT *coords, const VT *vals) {
   unsigned long long *dcnt = dalloc_t<unsigned long long>(c, P);
   CK(cudaMemsetAsync(dcnt, 0, sizeof(unsigned long long) * P, c->st));
   if (nnz > 0) {
-    k_dest_rank<IT><<<(unsigned)ceil_div(nnz, 256), 256, 0, c->st>>>(coords, nnz, D, k, dbound, P, dk0, ix0, dcnt);
+    k_dest_rank<IT><<<(unsigned)ceil_div(nnz, 256), 256, 0, c->st>>>(coords, nnz, D, k, dbound, P, dk0, ix0, dcnt,
+                                                                     dheavy);
     CK_LAUNCH();
   }
   std::vector<unsigned long long> hcnt(P);
@@ -811,6 +901,7 @@ void route_and_build(cparls_ctx *c, int k, const IT *coords, const VT *vals) {
   }
   sync(c);
   dfree(c, tmp); dfree(c, dk0); dfree(c, dk1); dfree(c, ix0); dfree(c, ix1); dfree(c, dcnt); dfree(c, dbound);
+  dfree(c, dheavy);
   // exchange counts, then coordinates and values
   std::vector<int64_t> mine(P);
   for (int q = 0; q < P; ++q) mine[q] = (int64_t)hcnt[q];
@@ -1433,7 +1524,7 @@ void lookup_impl(cparls_ctx *c, int k) {
 
 // per-column fixed-point scales 2^e_c of the sampled RHS (kernels.cuh, AMB-35)
 void launch_fixed_scales(cparls_ctx *c, cudaStream_t st) {
-  const int nbc = 148;
+  const int nbc = 296;   // (gpart holds gpart_blocks x r x r >= nbc x r doubles)
   k_colabs_part<<<nbc, 256, 0, st>>>(c->Z, c->sw2, c->s_cur, c->r, c->ld, c->gpart, &c->ctl->sbar, c->ctl);
   CK_LAUNCH();
   k_fixed_scales<<<1, 64, 0, st>>>(c->gpart, nbc, c->r, &c->dv->maxabs, c->dupmax, c->fx_scale, c->ctl);
@@ -1452,12 +1543,36 @@ void solve_impl(cparls_ctx *c, int k, cparls_solve_info *info) {
   const int64_t smax = std::max<int64_t>(c->s_cur, 1);   // s_bar <= s
   StepCtl *ctl = c->ctl;
   OtherModes om = other_modes(c, k);
+  // sharded run: the sampled rows of the other modes from their
+  // owners (only the owned rows of a factor are current on a rank)
+  // per step the cheaper of: the sampled rows (s x d rows from their owners) or
+  // the other modes' dense factors (only those not yet gathered)
+  const double *zg = nullptr;
+  int64_t dense_rows = 0;
+  for (int j = 0; j < om.d; ++j)
+    if (c->fac_dirty[om.mode[j]]) dense_rows += om.n[j];
+  if (c->world > 1 && dense_rows <= smax * (int64_t)om.d) {
+    for (int j = 0; j < om.d; ++j) gather_factor(c, om.mode[j]);
+  } else if (c->world > 1) {
+    const int64_t need = smax * (int64_t)om.d * ld;
+    if (need > c->zg_cap) {
+      dfree(c, c->Zg);
+      c->zg_cap = need;
+      c->Zg = dalloc_t<double>(c, need);
+    }
+    k_owned_rows<<<(unsigned)std::min<int64_t>(ceil_div(smax * 32, 256), 148 * 16), 256, 0, c->st>>>(
+        c->skey, smax, &ctl->sbar, om, c->drow_lo, c->drow_hi, ld, c->Zg, ctl);
+    CK_LAUNCH();
+    c->comm->allreduce_f64(c->Zg, (size_t)need, c->st);
+    c->stats.bytes_comm += 8.0 * need;
+    zg = c->Zg;
+  }
   // K6: KrpSamp + sampled Gram (every block writes its partial; s_bar = 0 gives G = 0)
   {
     Phase ph(c, &c->stats.ms_gram);
     const int64_t grid = row_grid(c, ceil_div(smax, kRowThreads));
     RSWITCH(r, k_krp_gram_t<RM><<<(unsigned)grid, kRowThreads, krp_smem(r, ld), c->st>>>(
-                   c->skey, c->sw2, smax, om, r, ld, c->Z, c->gpart, &ctl->sbar, ctl));
+                   c->skey, c->sw2, smax, om, r, ld, c->Z, c->gpart, &ctl->sbar, ctl, zg));
     CK_LAUNCH();
     k_pairs_reduce<<<pairs_reduce_grid(r), 256, 0, c->st>>>(c->gpart, grid, r, c->sd->G, ctl);
     CK_LAUNCH();
@@ -1620,6 +1735,22 @@ void solve_impl(cparls_ctx *c, int k, cparls_solve_info *info) {
     CK(cudaStreamWaitEvent(c->st, c->ev_join, 0));
     c->fx_pending = false;
   }
+  // sharded: the heavy rows' partial RHS rows summed over the ranks (plan_rows)
+  if (c->world > 1 && !c->heavy[k].empty()) {
+    const int64_t nh = (int64_t)c->heavy[k].size(), blk = nh * ld;
+    if (!c->heavy_buf) c->heavy_buf = dalloc_t<double>(c, c->heavy_buf_n * ld * c->world);
+    k_heavy_gather<<<(unsigned)ceil_div(blk, 256), 256, 0, c->st>>>(c->M, c->heavy_dev[k], nh, ld,
+                                                                    c->heavy_buf + blk * c->wrank, ctl);
+    CK_LAUNCH();
+    std::vector<int64_t> off(c->world + 1);
+    for (int q = 0; q <= c->world; ++q) off[q] = blk * q;
+    c->comm->allgatherv_f64(c->heavy_buf, off, c->st);
+    k_heavy_sum<<<(unsigned)ceil_div(blk, 256), 256, 0, c->st>>>(c->M, c->heavy_dev[k], c->heavy_own[k], nh, ld,
+                                                                 c->heavy_buf, c->world,
+                                                                 c->fx_on ? c->fx_scale : nullptr, ctl);
+    CK_LAUNCH();
+    c->stats.bytes_comm += 8.0 * blk * c->world;
+  }
   {
     Phase ph(c, &c->stats.ms_solve);
     if (!use_bkt) {
@@ -1635,17 +1766,15 @@ void solve_impl(cparls_ctx *c, int k, cparls_solve_info *info) {
       CK_LAUNCH();
     }
     if (c->world > 1) {
-      // Gram of B over all ranks' rows (r x r), then every rank gets all B rows
+      // Gram of B over all ranks' owned rows (r x r): lambda and the leverage W
       c->comm->allreduce_f64(c->sd->BtB, (size_t)r * r, c->st);
-      std::vector<int64_t> off(c->world + 1);
-      for (int q = 0; q <= c->world; ++q) off[q] = q < c->world ? row_start(c, k, q) * ld : nk * ld;
-      c->comm->allgatherv_f64(c->A[k], off, c->st);
       c->comm->allreduce_u64(&c->dv->touched, 1, c->st);
     }
     k_norm_prep<<<1, 128, prep_smem(r), c->st>>>(r, c->sd, c->md[k], ctl);
     CK_LAUNCH();
     LAUNCHED(c, 4);
-    lev_rows_and_cdf(c, k, c->sd->lambda);
+    if (c->world > 1) lev_rows_sharded(c, k, c->sd->lambda);
+    else lev_rows_and_cdf(c, k, c->sd->lambda);
     k_copy_lambda<<<1, 64, 0, c->st>>>(c->lam_model, c->sd->lambda, r, ctl);
     CK_LAUNCH();
     c->stats.bytes_solve += (double)nk * r * 8.0 * 3;
@@ -2010,6 +2139,7 @@ FitModes fit_modes(cparls_ctx *c, double *const *GA) {
 // (over all ranks); guarded like the mode steps.
 void fit_enqueue(cparls_ctx *c) {
   Phase ph(c, &c->stats.ms_fit);
+  for (int m = 0; m < c->D; ++m) gather_factor(c, m);   // dense factors once per fit (per epoch)
   fit_launch(c, c->st, c->A, c->lam_model, fit_modes(c, nullptr), c->ddpart, &c->dv->counter, c->dv->fit, 8);
   if (c->world > 1) {
     // <X,M> is a sum over the ranks' slices of the fit mode
@@ -2220,6 +2350,10 @@ cparls_status cparls_create(cparls_ctx **out, int32_t nmodes, const int64_t *dim
     else if (isz == 4) build_all<int32_t, double>(c, (const int32_t *)dco, (const double *)dva);
     else if (vsz == 4) build_all<int64_t, float>(c, (const int64_t *)dco, (const float *)dva);
     else build_all<int64_t, double>(c, (const int64_t *)dco, (const double *)dva);
+    c->drow_lo = dalloc_t<int64_t>(c, kMaxModes);
+    c->drow_hi = dalloc_t<int64_t>(c, kMaxModes);
+    CK(cudaMemcpyAsync(c->drow_lo, c->row_lo, sizeof(int64_t) * kMaxModes, cudaMemcpyHostToDevice, c->st));
+    CK(cudaMemcpyAsync(c->drow_hi, c->row_hi, sizeof(int64_t) * kMaxModes, cudaMemcpyHostToDevice, c->st));
     sync(c);
     {   // duplicate coordinates bound the fixed-point RHS scale (kernels.cuh)
       CK(cudaMemsetAsync(&c->dv->dupmax, 0, sizeof(unsigned long long), c->st));
@@ -2354,6 +2488,7 @@ cparls_status cparls_set_factor(cparls_ctx *c, int32_t mode, const double *A) {
     CK(cudaMemcpy2DAsync(c->A[mode], sizeof(double) * c->ld, A, sizeof(double) * c->r, sizeof(double) * c->r, n,
                          is_device_ptr(A) ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, c->st));
     c->have_sample = false;
+    c->fac_dirty[mode] = false;   // every row given
     reset_lambda(c);
     leverage_full(c, mode);
     sync(c);
@@ -2364,6 +2499,7 @@ cparls_status cparls_get_factor(cparls_ctx *c, int32_t mode, double *A, double *
   if (!c) return CPARLS_EINVAL;
   return guarded(c, [&] {
     check_mode(c, mode);
+    gather_factor(c, mode);   // sharded: collective when only the owned rows are current
     if (A) rows_to_host(c, A, c->A[mode], c->dims[mode], c->r, c->ld);
     if (lambda) CK(cudaMemcpyAsync(lambda, c->lam_model, sizeof(double) * c->r, cudaMemcpyDefault, c->st));
     sync(c);
@@ -2549,6 +2685,7 @@ cparls_status cparls_get_last_solve(cparls_ctx *c, double *G, double *B) {
     if (B) {
       int k = c->smode_last_solved;
       if (k < 0) throw ApiError(CPARLS_ESTATE, "no solve yet");
+      gather_factor(c, k);
       std::vector<double> lam(r);
       CK(cudaMemcpy2DAsync(B, sizeof(double) * r, c->A[k], sizeof(double) * c->ld, sizeof(double) * r, c->dims[k],
                            cudaMemcpyDeviceToHost, c->st));
@@ -2730,9 +2867,19 @@ cparls_status cparls_comm_destroy(cparls_comm *cc) {
   return CPARLS_OK;
 }
 
-cparls_status cparls_plan_rows(int64_t n, const uint64_t *deg, int32_t world_size, int64_t *bound) {
+cparls_status cparls_plan_rows(int64_t n, const uint64_t *deg, int32_t world_size, int64_t *bound, uint8_t *heavy) {
   if (n < 0 || world_size < 1 || !bound || (n > 0 && !deg)) return CPARLS_EINVAL;
-  plan_rows(n, reinterpret_cast<const unsigned long long *>(deg), world_size, bound);
+  plan_rows(n, reinterpret_cast<const unsigned long long *>(deg), world_size, bound, heavy);
+  return CPARLS_OK;
+}
+
+cparls_status cparls_route_nonzeros(int32_t nmodes, int32_t mode, int64_t nnz, const int64_t *coords,
+                                    int32_t world_size, const int64_t *bound, const uint8_t *heavy, int32_t *rank_out) {
+  if (nmodes < 2 || nmodes > kMaxModes || mode < 0 || mode >= nmodes || nnz < 0 || world_size < 1 || !bound ||
+      (nnz > 0 && (!coords || !rank_out)))
+    return CPARLS_EINVAL;
+  for (int64_t e = 0; e < nnz; ++e)
+    rank_out[e] = route_rank<int64_t>(coords + e * nmodes, nmodes, mode, bound, world_size, heavy);
   return CPARLS_OK;
 }
 

@@ -114,6 +114,11 @@ __device__ void block_jacobi(int r, double *a, double *V) {
 // Returns 1 on success.  L lower (row stride r).
 // Whole block participates.
 __device__ int block_cholesky(int r, const double *G, double *L, int *ok_flag) {
+  // right-looking: L's lower triangle starts as G's and every column's
+  // trailing update runs in parallel (O(r) barriers, O(1) work per thread per
+  // step).  Entry (i, l) receives the subtractions L(i,q) L(l,q) for q = 0, 1,
+  // ... in the same order and form as the column-by-column (left-looking)
+  // formula, so the factor is bit-identical to it.
   __shared__ double maxdiag;
   if (threadIdx.x == 0) {
     double m = 0.0;
@@ -121,38 +126,47 @@ __device__ int block_cholesky(int r, const double *G, double *L, int *ok_flag) {
     maxdiag = m;
     *ok_flag = m > 0.0;
   }
-  for (int i = threadIdx.x; i < r * r; i += blockDim.x) L[i] = 0.0;
+  for (int i = threadIdx.x; i < r * r; i += blockDim.x) L[i] = (i % r <= i / r) ? G[i] : 0.0;
   __syncthreads();
   for (int j = 0; j < r; ++j) {
     if (threadIdx.x == 0 && *ok_flag) {
-      double dj = G[j * r + j];
-      for (int q = 0; q < j; ++q) dj -= L[j * r + q] * L[j * r + q];
+      const double dj = L[j * r + j];
       if (!(dj > kCholSafe * maxdiag)) *ok_flag = 0;
       else L[j * r + j] = sqrt(dj);
     }
     __syncthreads();
     if (!*ok_flag) return 0;
-    for (int i = j + 1 + threadIdx.x; i < r; i += blockDim.x) {
-      double v = G[i * r + j];
-      for (int q = 0; q < j; ++q) v -= L[i * r + q] * L[j * r + q];
-      L[i * r + j] = v / L[j * r + j];
+    const double ljj = L[j * r + j];
+    for (int i = j + 1 + threadIdx.x; i < r; i += blockDim.x) L[i * r + j] = L[i * r + j] / ljj;
+    __syncthreads();
+    const int t = r - j - 1;   // trailing block rows/cols j+1 .. r-1 (lower triangle)
+    for (int idx = threadIdx.x; idx < t * t; idx += blockDim.x) {
+      const int i = j + 1 + idx / t, l = j + 1 + idx % t;
+      if (l <= i) L[i * r + l] -= L[i * r + j] * L[l * r + j];
     }
     __syncthreads();
   }
   return 1;
 }
 
-// Lower-triangular inverse: Linv (row stride r), column c by thread c.
+// Lower-triangular inverse Linv = L^{-1} (row stride r) by row-oriented
+// forward substitution with all r right-hand sides in parallel (O(r)
+// barriers).  Entry (l, c) receives its subtractions in the order q = 0, 1, ...
+// (the q < c ones are exact zeros), so Linv is bit-identical to the
+// column-by-column formula.
 __device__ void block_tri_inverse(int r, const double *L, double *Linv) {
-  for (int c = threadIdx.x; c < r; c += blockDim.x) {
-    for (int i = 0; i < r; ++i) {
-      if (i < c) { Linv[i * r + c] = 0.0; continue; }
-      double v = (i == c) ? 1.0 : 0.0;
-      for (int q = c; q < i; ++q) v -= L[i * r + q] * Linv[q * r + c];
-      Linv[i * r + c] = v / L[i * r + i];
-    }
-  }
+  for (int i = threadIdx.x; i < r * r; i += blockDim.x) Linv[i] = (i / r == i % r) ? 1.0 : 0.0;
   __syncthreads();
+  for (int i = 0; i < r; ++i) {
+    for (int c = threadIdx.x; c <= i; c += blockDim.x) Linv[i * r + c] = Linv[i * r + c] / L[i * r + i];
+    __syncthreads();
+    const int t = r - i - 1;
+    for (int idx = threadIdx.x; idx < t * (i + 1); idx += blockDim.x) {
+      const int l = i + 1 + idx / (i + 1), c = idx % (i + 1);
+      Linv[l * r + c] -= L[l * r + i] * Linv[i * r + c];
+    }
+    __syncthreads();
+  }
 }
 
 // Leverage preparation from Gram G (r x r, global): W with l_i = ||a_i W||^2.
@@ -247,7 +261,9 @@ __global__ void k_scan_u64_single(uint64_t *part, int64_t nb, const StepCtl *ctl
 
 // Recompute q from given p~ (set_ptilde path), same rounding as k_lev_rows.
 __global__ void k_q_from_pt(const double *__restrict__ pt, int64_t n, uint64_t *__restrict__ C,
-                            uint64_t *__restrict__ tile_sum, double *alpha_out, unsigned long long *drawable_out) {
+                            uint64_t *__restrict__ tile_sum, double *alpha_out, unsigned long long *drawable_out,
+                            const StepCtl *ctl = nullptr) {
+  CPARLS_GUARD(ctl);
   int64_t i = (int64_t)blockIdx.x * kLevThreads + threadIdx.x;
   double p = i < n ? pt[i] : 0.0;
   uint64_t q = __double2ull_rn(p * kTwo62);
@@ -856,22 +872,45 @@ __global__ void k_coord_degree(const IT *__restrict__ coords, int64_t nnz, int D
     atomicAdd(deg + (int64_t)coords[e * D + k], 1ull);
 }
 
+// Destination rank of a nonzero in the sharded build of mode k:
+// the owner of its mode-k row, or -- for a heavy row -- a rank chosen by a hash
+// of its other coordinates (the row's nonzeros spread evenly over the ranks).
+__host__ __device__ __forceinline__ uint64_t heavy_hash(uint64_t k) {
+  k ^= k >> 33; k *= 0xff51afd7ed558ccdull; k ^= k >> 33; k *= 0xc4ceb9fe1a85ec53ull; k ^= k >> 33;
+  return k;
+}
+// rank of one nonzero (its D coordinates c): the owner of row c[k] (last p
+// with bound[p] <= c[k]), or for a heavy row the hash of its other coordinates
+template <typename IT>
+__host__ __device__ __forceinline__ int route_rank(const IT *c, int D, int k, const int64_t *bound, int P,
+                                                   const uint8_t *heavy) {
+  const int64_t row = (int64_t)c[k];
+  if (heavy && heavy[row]) {
+    uint64_t key = 0;
+    for (int m = 0; m < D; ++m)
+      if (m != k) key = key * 0x9E3779B97F4A7C15ull + (uint64_t)c[m];
+    return (int)(((unsigned __int128)heavy_hash(key) * (unsigned)P) >> 64);
+  }
+  int lo = 0, len = P;
+  while (len > 0) {
+    const int half = len >> 1;
+    if (bound[lo + half + 1] <= row) { lo += half + 1; len -= half + 1; }
+    else len = half;
+  }
+  return lo;
+}
+
 template <typename IT>
 __global__ void k_dest_rank(const IT *__restrict__ coords, int64_t nnz, int D, int k,
                             const int64_t *__restrict__ bound, int P, uint32_t *__restrict__ dest,
-                            uint32_t *__restrict__ idx, unsigned long long *__restrict__ cnt) {
+                            uint32_t *__restrict__ idx, unsigned long long *__restrict__ cnt,
+                            const uint8_t *__restrict__ heavy) {
   __shared__ unsigned long long h[256];
   for (int i = threadIdx.x; i < P; i += blockDim.x) h[i] = 0;
   __syncthreads();
   const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (e < nnz) {
-    const int64_t row = (int64_t)coords[e * D + k];
-    int lo = 0, len = P;   // last p with bound[p] <= row
-    while (len > 0) {
-      int half = len >> 1;
-      if (bound[lo + half + 1] <= row) { lo += half + 1; len -= half + 1; }
-      else len = half;
-    }
+    const int lo = route_rank<IT>(coords + e * D, D, k, bound, P, heavy);
     dest[e] = (uint32_t)lo;
     idx[e] = (uint32_t)e;
     atomicAdd(&h[lo], 1ull);
@@ -923,10 +962,18 @@ __global__ void k_colabs_part(const double *__restrict__ Z, const double *__rest
   sbar = dcount(sbar, sbar_dev);
   const int c = threadIdx.x & 63;
   double s = 0.0;
-  if (c < r)
-    for (int64_t j = (int64_t)blockIdx.x * (blockDim.x >> 6) + (threadIdx.x >> 6); j < sbar;
-         j += (int64_t)gridDim.x * (blockDim.x >> 6))
-      s += sw2[j] * fabs(Z[j * ld + c]);
+  if (c < r) {
+    // 4 rows per thread per step in flight (the loop is load-latency bound)
+    const int64_t stride = (int64_t)gridDim.x * (blockDim.x >> 6);
+    int64_t j = (int64_t)blockIdx.x * (blockDim.x >> 6) + (threadIdx.x >> 6);
+    for (; j + 3 * stride < sbar; j += 4 * stride) {
+      const double a0 = sw2[j] * fabs(Z[j * ld + c]), a1 = sw2[j + stride] * fabs(Z[(j + stride) * ld + c]);
+      const double a2 = sw2[j + 2 * stride] * fabs(Z[(j + 2 * stride) * ld + c]);
+      const double a3 = sw2[j + 3 * stride] * fabs(Z[(j + 3 * stride) * ld + c]);
+      s += a0 + a1 + a2 + a3;
+    }
+    for (; j < sbar; j += stride) s += sw2[j] * fabs(Z[j * ld + c]);
+  }
   __shared__ double red[256];
   red[threadIdx.x] = s;
   __syncthreads();

@@ -483,7 +483,8 @@ __global__ void __launch_bounds__(kRowThreads) k_krp_gram_t(const uint64_t *__re
                                                            OtherModes om, int r, int ld, double *__restrict__ Z,
                                                            double *__restrict__ part,
                                                            const int64_t *sbar_dev = nullptr,
-                                                           const StepCtl *ctl = nullptr) {
+                                                           const StepCtl *ctl = nullptr,
+                                                           const double *__restrict__ zg = nullptr) {
   CPARLS_GUARD(ctl);
   sbar = dcount(sbar, sbar_dev);
   extern __shared__ double smem[];
@@ -515,7 +516,9 @@ __global__ void __launch_bounds__(kRowThreads) k_krp_gram_t(const uint64_t *__re
         for (int q = 0; q < QR; ++q) {
           const uint64_t i = key[q] % (uint64_t)om.n[m];
           key[q] /= (uint64_t)om.n[m];
-          const double *row = om.A[m] + i * ld;
+          // sharded run: the rows come from their owners (zg, sample-major, d rows per sample)
+          const int64_t jz = jj0 + q < rows ? base + jj0 + q : 0;
+          const double *row = zg ? zg + (jz * (int64_t)om.d + m) * ld : om.A[m] + i * ld;
           a0[q] = lane < r ? __ldg(row + lane) : 0.0;
           a1[q] = lane + 32 < r ? __ldg(row + lane + 32) : 0.0;
         }

@@ -111,34 +111,61 @@ __global__ void __launch_bounds__(kSidxThreads) k_sidx_run(OtherModes om, double
       }
       break;
     }
+    // the thread's kSidxItems attempts advance together (one Philox call and
+    // one binary-search level of every attempt per step: kSidxItems
+    // independent L2 loads in flight per thread)
     uint64_t key[kSidxItems];
     double pv[kSidxItems];
+    uint64_t a_[kSidxItems];
+#pragma unroll
+    for (int it = 0; it < kSidxItems; ++it) {
+      a_[it] = (uint64_t)a0 + (uint64_t)threadIdx.x * kSidxItems + it;
+      key[it] = 0;
+      pv[it] = 1.0;
+    }
+    for (int lane = 0; lane < (om.d + 1) / 2; ++lane) {
+      uint32_t wd[kSidxItems][4];
+#pragma unroll
+      for (int it = 0; it < kSidxItems; ++it) {
+        const u32x4 x = philox4x32_10({(uint32_t)a_[it], (uint32_t)(a_[it] >> 32), step32, (uint32_t)lane}, seed_lo,
+                                      seed_hi);
+        wd[it][0] = x.x; wd[it][1] = x.y; wd[it][2] = x.z; wd[it][3] = x.w;
+      }
+      for (int jj = 0; jj < 2 && 2 * lane + jj < om.d; ++jj) {
+        const int j = 2 * lane + jj;
+        const uint64_t *C = om.C[j];
+        const int64_t n = om.n[j];
+        const uint64_t W = __ldg(C + n - 1);
+        uint64_t t[kSidxItems];
+        int64_t lo[kSidxItems];
+#pragma unroll
+        for (int it = 0; it < kSidxItems; ++it) {
+          const uint64_t R = ((uint64_t)wd[it][2 * jj + 1] << 32) | wd[it][2 * jj];
+          t[it] = __umul64hi(R, W);                                        // AMB-9
+          lo[it] = 0;
+        }
+        // upper_bound (first C[i] > t) of all items in lockstep by
+        // binary lifting: lo = #{i : C[i] <= t} (C is non-decreasing)
+        int64_t step = 1;
+        while (step * 2 <= n) step *= 2;
+        for (; step > 0; step >>= 1) {
+#pragma unroll
+          for (int it = 0; it < kSidxItems; ++it)
+            if (lo[it] + step <= n && __ldg(C + lo[it] + step - 1) <= t[it]) lo[it] += step;
+        }
+#pragma unroll
+        for (int it = 0; it < kSidxItems; ++it) {
+          const double v = __ldg(om.pt[j] + lo[it]);
+          pv[it] = (j == 0) ? v : pv[it] * v;                              // AMB-5
+          key[it] += (uint64_t)lo[it] * om.mult[j];
+        }
+      }
+    }
     unsigned accm = 0;
     int cnt = 0;
 #pragma unroll
     for (int it = 0; it < kSidxItems; ++it) {
-      const uint64_t a = (uint64_t)a0 + (uint64_t)threadIdx.x * kSidxItems + it;
-      uint32_t words[2 * kMaxModes];
-      for (int lane = 0; lane < (om.d + 1) / 2; ++lane) {
-        u32x4 x = philox4x32_10({(uint32_t)a, (uint32_t)(a >> 32), step32, (uint32_t)lane}, seed_lo, seed_hi);
-        words[4 * lane + 0] = x.x; words[4 * lane + 1] = x.y;
-        words[4 * lane + 2] = x.z; words[4 * lane + 3] = x.w;
-      }
-      uint64_t k = 0;
-      double p = 1.0;
-      for (int j = 0; j < om.d; ++j) {
-        const uint32_t lo = words[4 * (j / 2) + 2 * (j % 2)], hi = words[4 * (j / 2) + 2 * (j % 2) + 1];
-        const uint64_t R = ((uint64_t)hi << 32) | lo;
-        const uint64_t *C = om.C[j];
-        const uint64_t W = __ldg(C + om.n[j] - 1);
-        const int64_t i = upper_bound_u64(C, om.n[j], __umul64hi(R, W));   // AMB-9
-        const double v = __ldg(om.pt[j] + i);
-        p = (j == 0) ? v : p * v;                                           // AMB-5
-        k += (uint64_t)i * om.mult[j];
-      }
-      key[it] = k;
-      pv[it] = p;
-      const bool acc = p <= tau && (int64_t)a < cap_att;
+      const bool acc = pv[it] <= tau && (int64_t)a_[it] < cap_att;
       accm |= (unsigned)acc << it;
       cnt += acc;
     }
@@ -183,7 +210,7 @@ __global__ void __launch_bounds__(kSidxThreads) k_sidx_run(OtherModes om, double
         if (pos < need) {
           rkey[pos] = key[it];
           rp[pos] = pv[it];
-          if (pos == need - 1) ctl->attempts = a0 + (int64_t)threadIdx.x * kSidxItems + it + 1;
+          if (pos == need - 1) ctl->attempts = (int64_t)a_[it] + 1;
         }
         ++pos;
       }
@@ -235,6 +262,61 @@ __global__ void k_fit_combine(double *fit, double normX2, const StepCtl *ctl) {
   double resid2 = normX2 - 2.0 * fit[1] + fit[2];
   if (resid2 < 0.0) resid2 = 0.0;
   fit[0] = 1.0 - sqrt(resid2) / sqrt(normX2);
+}
+
+// ---------------------------------------------------------------- sharded mode step
+// The sampled rows of the other modes from their owners: rank p writes
+// A_m(i_m,:) into zg[(j d + slot) ld ..] when it owns row i_m of mode m
+// ([row_lo[m], row_hi[m])), zeros otherwise; an allreduce (one nonzero
+// contribution per element: exact) gives every rank every sampled row.
+__global__ void k_owned_rows(const uint64_t *__restrict__ skey, int64_t smax, const int64_t *sbar_dev,
+                             OtherModes om, const int64_t *row_lo, const int64_t *row_hi, int ld,
+                             double *__restrict__ zg, const StepCtl *ctl) {
+  CPARLS_GUARD(ctl);
+  const int64_t sbar = dcount(smax, sbar_dev);
+  const int lane = threadIdx.x & 31;
+  for (int64_t j = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; j < smax;
+       j += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    uint64_t key = j < sbar ? skey[j] : 0ull;
+    for (int m = 0; m < om.d; ++m) {
+      const uint64_t i = key % (uint64_t)om.n[m];
+      key /= (uint64_t)om.n[m];
+      const int mode = om.mode[m];
+      const bool own = j < sbar && (int64_t)i >= row_lo[mode] && (int64_t)i < row_hi[mode];
+      double *dst = zg + (j * (int64_t)om.d + m) * ld;
+      for (int cc = lane; cc < ld; cc += 32) dst[cc] = own ? om.A[m][i * ld + cc] : 0.0;
+    }
+  }
+}
+
+// Heavy rows (cparls.cu plan_rows): every rank holds a partial RHS row for
+// each.  Rank p copies its partials into block p of buf (P blocks of nh x ld);
+// after an allgather every rank sums the P blocks in rank order -- int64 when
+// the step's RHS is fixed point (exact), fp64 otherwise (fscale flag) -- the
+// owner keeps the sum and the others zero their copies (M is zero outside the
+// owned rows for the next RHS).
+__global__ void k_heavy_gather(const double *__restrict__ M, const int64_t *__restrict__ rows, int64_t nh, int ld,
+                               double *__restrict__ blk, const StepCtl *ctl) {
+  CPARLS_GUARD(ctl);
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < nh * ld; t += (int64_t)gridDim.x * blockDim.x)
+    blk[t] = M[rows[t / ld] * ld + t % ld];
+}
+__global__ void k_heavy_sum(double *__restrict__ M, const int64_t *__restrict__ rows,
+                            const uint8_t *__restrict__ own, int64_t nh, int ld, const double *__restrict__ buf,
+                            int P, const double *__restrict__ fscale, const StepCtl *ctl) {
+  CPARLS_GUARD(ctl);
+  const bool fixed = fscale && fscale[2 * kMaxRank] != 0.0;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < nh * ld; t += (int64_t)gridDim.x * blockDim.x) {
+    double v = 0.0;
+    if (fixed) {
+      long long q = 0;
+      for (int p = 0; p < P; ++p) q += __double_as_longlong(buf[(int64_t)p * nh * ld + t]);
+      v = __longlong_as_double(q);
+    } else {
+      for (int p = 0; p < P; ++p) v += buf[(int64_t)p * nh * ld + t];
+    }
+    M[rows[t / ld] * ld + t % ld] = own[t / ld] ? v : 0.0;
+  }
 }
 
 }  // namespace cparls

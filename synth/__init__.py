@@ -249,8 +249,12 @@ def _first_unique_positions(parts, total, target, device):
     return torch.cat(out)
 
 
-def generate_coords(cfg: Config, device="cpu", chunk: int = 1 << 27, out_dtype=torch.int64) -> torch.Tensor:
-    """nnz x D int64 coordinates (0-based), distinct, in first-draw order."""
+def generate_coords(cfg: Config, device="cpu", chunk: int = 1 << 27, out_dtype=torch.int64, part: int = 0,
+                    parts: int = 1) -> torch.Tensor:
+    """nnz x D int64 coordinates (0-based), distinct, in first-draw order.
+    parts > 1: only the cells at first-draw positions part, part + parts, ...
+    (a rank's chunk of the same tensor; the draws and the dedup are the same
+    on every rank, only the materialized coordinates are 1/parts)."""
     dims = cfg.dims
     D = len(dims)
     lo_bits = packed_key_layout(dims)
@@ -265,29 +269,32 @@ def generate_coords(cfg: Config, device="cpu", chunk: int = 1 << 27, out_dtype=t
         cdfs.append(torch.from_numpy(c).to(device))
     target = cfg.nnz
     total = int(target * 1.05) + 64
-    parts = []
+    keys = []
     drawn = 0
     while True:
         while drawn < total:
             cnt = min(chunk, total - drawn)
             cs = _draw_coords(drawn, cnt, cdfs, perms, cfg.coord_seed, device)
-            parts.append(_pack(cs, dims, lo_bits))
+            keys.append(_pack(cs, dims, lo_bits))
             del cs
             drawn += cnt
-        pos = _first_unique_positions(parts, drawn, target, device)
+        pos = _first_unique_positions(keys, drawn, target, device)
         if pos is not None:
             break
         total = int(total * 1.25) + 1024
+    if parts > 1:   # this rank's chunk: every parts-th cell in first-draw order
+        pos = pos[part::parts].contiguous()
+    target = pos.numel()
     # gather the selected keys chunk by chunk (positions ascending)
     sel = torch.empty(target, dtype=torch.int64, device=device)
     base = 0
-    for k in parts:
+    for k in keys:
         n = k.numel()
         lo_i = torch.searchsorted(pos, torch.tensor([base, base + n], device=device))
         a_, b_ = int(lo_i[0]), int(lo_i[1])
         sel[a_:b_] = k[pos[a_:b_] - base]
         base += n
-    del parts, pos
+    del keys, pos
     out = torch.empty((target, D), dtype=out_dtype, device=device)
     for c0 in range(0, target, chunk):
         cs = _unpack(sel[c0:c0 + chunk], dims, lo_bits)
@@ -368,7 +375,11 @@ class Tensor:
     vals: torch.Tensor
 
 
-def make(name_or_cfg, device="cpu", index_dtype=torch.int32, dense_planted=False) -> Tensor:
+def make(name_or_cfg, device="cpu", index_dtype=torch.int32, dense_planted=False, part: int = 0,
+         parts: int = 1) -> Tensor:
+    """The config's tensor; parts > 1 gives rank `part`'s chunk of it (cells
+    part, part + parts, ... in first-draw order) without materializing the
+    rest (multi-GPU bench: every rank builds only its share)."""
     cfg = CONFIGS[name_or_cfg] if isinstance(name_or_cfg, str) else name_or_cfg
     if dense_planted:
         # fully populated C1 variant for the recovery invariant (AMB-24)
@@ -376,7 +387,7 @@ def make(name_or_cfg, device="cpu", index_dtype=torch.int32, dense_planted=False
         coords = torch.stack([g.reshape(-1) for g in grids], dim=1).to(torch.int64)
         cfg = dataclasses.replace(cfg, nnz=coords.shape[0])
     else:
-        coords = generate_coords(cfg, device=device, out_dtype=index_dtype)
+        coords = generate_coords(cfg, device=device, out_dtype=index_dtype, part=part, parts=parts)
     vals = generate_values(cfg, coords)
     if coords.dtype != index_dtype:
         out = torch.empty(coords.shape, dtype=index_dtype, device=coords.device)

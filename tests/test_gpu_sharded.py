@@ -88,12 +88,16 @@ def lockstep_sharded(T, rank, P, iters, s, seed):
                 assert inf.matched_nnz == gs.matched_nnz and inf.touched_rows == gs.touched_rows
             _, Bg = g.last_solve(k)
             Ag, lg = g.get_factor(k)
-            for sh in shards:
-                _, Bs = sh.last_solve(k)
-                As, ls = sh.get_factor(k)
+            # factor getters of a sharded run are collective (only owned rows are current)
+            lasts = on_shards(P, lambda p: shards[p].last_solve(k))
+            facs = on_shards(P, lambda p: shards[p].get_factor(k))
+            for p, sh in enumerate(shards):
+                Bs = lasts[p][1]
+                As, ls = facs[p]
                 nb = np.linalg.norm(Bg)
                 assert np.linalg.norm(Bs - Bg) <= 1e-11 * max(nb, 1e-300)
                 np.testing.assert_allclose(ls, lg, rtol=1e-11)   # B^T B summation grouping differs by shard
+                # p~ of all rows from the owners' rows (allgather of p~ only)
                 np.testing.assert_allclose(sh.get_ptilde(k), g.get_ptilde(k), rtol=1e-10, atol=1e-16)
         fg = g.fit()
         fs = on_shards(P, lambda p: shards[p].fit())
@@ -110,22 +114,43 @@ def test_sharded_c1_lockstep(P):
     lockstep_sharded(T, 3, P, 3, 256, 3)
 
 
-def test_sharded_c2_lockstep_P4():
+@pytest.mark.parametrize("P", [4, 8])
+def test_sharded_c2_lockstep(P):
+    """C2 (Uber-shaped) at P = 4 and 8: mode 1 has 24 rows, so at P = 8 its Zipf
+    head rows hold more than a rank's share and are split over the ranks."""
     T = synth.make("C2", device="cuda")
     T = synth.Tensor(T.cfg, T.dims, T.coords.cpu(), T.vals.cpu())
-    lockstep_sharded(T, 25, 4, 1, 1 << 17, 3)
+    if P == 8:
+        from paper_2006_16438_b200 import plan_rows
+        deg = np.bincount(T.coords[:, 1].numpy(), minlength=T.dims[1]).astype(np.uint64)
+        _, heavy = plan_rows(deg, P, with_heavy=True)
+        assert heavy.any()
+    lockstep_sharded(T, 25, P, 1, 1 << 17, 3)
 
 
-def test_sharded_free_run_matches_single():
+@pytest.mark.parametrize("s", [256, 1 << 14])
+def test_sharded_communication_volume(s):
+    """Per mode step a rank exchanges the cheaper of the sampled other-mode
+    rows (s x (D-1) rows of ld doubles, from their owners) and those modes'
+    dense factors, plus p~_k (n_k doubles) and r x r Grams -- never more
+    (SURVEY 8(e)); both branches give the single-context samples."""
     need_gpu()
-    from paper_2006_16438_b200 import Cparls
-    T = synth.make("C1", dense_planted=True)
-    g = Cparls(T.dims, T.coords.cuda(), T.vals.cuda(), 3)
-    tg = g.run(4, 256, 3, fit_every=1)
-    comm, shards = make_shards(T, 2, 3)
-    ts = on_shards(2, lambda p: shards[p].run(4, 256, 3, fit_every=1))
-    for tr in ts:
-        np.testing.assert_allclose(tr, tg, atol=1e-8)
+    T = synth.make("C2", device="cuda")
+    T = synth.Tensor(T.cfg, T.dims, T.coords.cpu(), T.vals.cpu())
+    P, r = 4, 25
+    comm, shards = make_shards(T, P, r)
+    for sh in shards:
+        sh.reset_stats()
+    on_shards(P, lambda p: shards[p].run(1, s, 3, fit_every=0))
+    D = len(T.dims)
+    ld = 32
+    bound = 0.0
+    for k in range(D):
+        others = sum(n for m, n in enumerate(T.dims) if m != k)
+        bound += 8.0 * (min(s * (D - 1), others) * ld + T.dims[k] + 64 * ld * P + 2 * r * r)
+    for sh in shards:
+        b = sh.stats()["bytes_comm"]
+        assert 0 < b <= bound, (b, bound)
     for sh in shards:
         sh.close()
     comm.close()
