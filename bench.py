@@ -573,8 +573,8 @@ def run_ours(args):
                    "s": cfg.s, "tau": "1/s" if args.tau < 0 else args.tau, "fit_every": ETA,
                    "values": cfg.value_dtype, "l2": "inputs larger than L2 (per-mode sorted copies "
                    f"{nnz * (16 if cfg.value_dtype == 'f32' else 20) * D / 1e9:.1f} GB >> 126 MB)",
-                   "parallelism": f"row-sharded x{ws} (NCCL allreduce r x r + allgather of B rows per mode step)"
-                   if ws > 1 else "single GPU"},
+                   "parallelism": f"row-sharded x{ws} (per mode step: sampled rows from their owners, p~ allgather, "
+                                  f"r x r Gram allreduce; dense factors once per fit)" if ws > 1 else "single GPU"},
         "roofline": roofline,
         "kernels": kernels,
         "peaks_measured": peaks,

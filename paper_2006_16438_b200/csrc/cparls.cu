@@ -1400,7 +1400,7 @@ void sample_async(cparls_ctx *c, int k, int64_t s, uint64_t seed, uint64_t step)
   k_sidx_prep<<<1, 1, 0, c->st>>>(ctl, om, s);
   CK_LAUNCH();
   {
-    const unsigned gsidx = (unsigned)std::min<int64_t>(148 * 2, ceil_div(s, kSidxTile) + 8);
+    const unsigned gsidx = (unsigned)std::min<int64_t>(148 * 4, ceil_div(s, kSidxTile) + 8);
     k_sidx_run<<<gsidx, kSidxThreads, 0, c->st>>>(om, tau, (uint32_t)seed, (uint32_t)(seed >> 32), (uint32_t)step,
                                                   c->opts.attempt_cap, ctl, c->tile_state, c->tile_cap, c->rkey,
                                                   c->rp, st64);

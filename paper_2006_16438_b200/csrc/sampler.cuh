@@ -43,7 +43,7 @@ __global__ void k_didx_finish(StepCtl *ctl, int64_t s, int tiny_tau, int64_t ste
 }
 
 // ---------------------------------------------------------------- SIDX
-constexpr int kSidxItems = 8;
+constexpr int kSidxItems = 4;
 constexpr int kSidxTile = kSidxThreads * kSidxItems;   // attempts per tile
 
 // SIDX setup (Alg. 2 line 1; AMB-7): s_rnd = s - s_det; the random phase is
@@ -83,7 +83,7 @@ __device__ __forceinline__ unsigned long long tile_word(unsigned epoch, unsigned
 // always held by running CTAs), so the accepted attempts land at their
 // attempt-order positions (AMB-8) and the first s_rnd are kept.  The attempt
 // cap (AMB-7) sends the step to the host path (which reports ESAMPLE).
-__global__ void __launch_bounds__(kSidxThreads) k_sidx_run(OtherModes om, double tau, uint32_t seed_lo,
+__global__ void __launch_bounds__(kSidxThreads, 2) k_sidx_run(OtherModes om, double tau, uint32_t seed_lo,
                                                            uint32_t seed_hi, uint32_t step32, int64_t attempt_cap,
                                                            StepCtl *ctl, unsigned long long *tile_state,
                                                            int64_t tile_cap, uint64_t *__restrict__ rkey,
