@@ -249,6 +249,44 @@ __device__ __forceinline__ void warp_store(double *__restrict__ dst, int rows, i
   }
 }
 
+// p~_i = ||a_i W||^2 / rank of one normalized row x (16-byte aligned, r columns)
+// with W (RMAX x RMAX, zero padded; zero below the diagonal if tri): s_c =
+// sum_{k < r} a_k W_kc, l = sum_c s_c^2.  One definition for the leverage pass
+// and the fused solve + leverage pass, so both give the same bits.
+template <int RMAX>
+__device__ __forceinline__ double lev_of_row(const double *x, int r, const double *W, int tri, int rank) {
+  double a[RMAX];
+#pragma unroll
+  for (int c = 0; c < RMAX; c += 2) {
+    const double2 v = *reinterpret_cast<const double2 *>(x + c);
+    a[c] = (c < r) ? v.x : 0.0;
+    if (c + 1 < RMAX) a[c + 1] = (c + 1 < r) ? v.y : 0.0;
+  }
+  double l = 0.0;
+  if (rank > 0) {
+    // s_c = sum_{k < r} a_k W_kc over the zero-padded W (an upper
+    // triangular W's zeros below the diagonal leave the sums unchanged)
+    for (int c = 0; c < r; c += 4) {
+      double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+#pragma unroll
+      for (int k = 0; k < RMAX; ++k)
+        if (k < r && (!tri || k <= c + 3)) {
+          const double2 w01 = *reinterpret_cast<const double2 *>(W + k * RMAX + c);
+          const double2 w23 = *reinterpret_cast<const double2 *>(W + k * RMAX + c + 2);
+          s0 += a[k] * w01.x;
+          s1 += a[k] * w01.y;
+          s2 += a[k] * w23.x;
+          s3 += a[k] * w23.y;
+        }
+      l += s0 * s0;
+      if (c + 1 < r) l += s1 * s1;
+      if (c + 2 < r) l += s2 * s2;
+      if (c + 3 < r) l += s3 * s3;
+    }
+  }
+  return rank > 0 ? l / (double)rank : 0.0;
+}
+
 // l_i = ||a_i W||^2, p~_i = l_i / rank, q_i = rint(p~_i 2^62) into C, q summed
 // into the 256-row tile sums of the CDF scan (integer adds: order-free, exact);
 // lam != nullptr normalizes A in place first (a_ic = b_ic * (1/lambda_c),
@@ -297,37 +335,7 @@ __global__ void __launch_bounds__(kRowThreads, 2) k_lev_rows_w(double *__restric
     }
     uint64_t q = 0;
     if (lane < rows) {
-      const double *x = tile + lane * S;
-      double a[RMAX];
-#pragma unroll
-      for (int c = 0; c < RMAX; c += 2) {
-        const double2 v = *reinterpret_cast<const double2 *>(x + c);
-        a[c] = (c < r) ? v.x : 0.0;
-        if (c + 1 < RMAX) a[c + 1] = (c + 1 < r) ? v.y : 0.0;
-      }
-      double l = 0.0;
-      if (rank > 0) {
-        // s_c = sum_{k < r} a_k W_kc over the zero-padded W (an upper
-        // triangular W's zeros below the diagonal leave the sums unchanged)
-        for (int c = 0; c < r; c += 4) {
-          double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
-#pragma unroll
-          for (int k = 0; k < RMAX; ++k)
-            if (k < r && (!tri || k <= c + 3)) {
-              const double2 w01 = *reinterpret_cast<const double2 *>(W + k * RMAX + c);
-              const double2 w23 = *reinterpret_cast<const double2 *>(W + k * RMAX + c + 2);
-              s0 += a[k] * w01.x;
-              s1 += a[k] * w01.y;
-              s2 += a[k] * w23.x;
-              s3 += a[k] * w23.y;
-            }
-          l += s0 * s0;
-          if (c + 1 < r) l += s1 * s1;
-          if (c + 2 < r) l += s2 * s2;
-          if (c + 3 < r) l += s3 * s3;
-        }
-      }
-      const double p = rank > 0 ? l / (double)rank : 0.0;
+      const double p = lev_of_row<RMAX>(tile + lane * S, r, W, tri, rank);
       q = __double2ull_rn(p * kTwo62);
       pt[base + lane] = p;
       C[base + lane] = q;
