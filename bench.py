@@ -333,6 +333,8 @@ def run_ours(args):
                fit_samples=fit_samples, fit_seed=FIT_SEED)
     torch.cuda.synchronize()
     t_build = time.perf_counter() - t0
+    create_phases = dict(zip(["setup_and_input_ms", "sorted_copies_ms", "dups_fibers_fit_sample_ms",
+                              "factors_leverage_ms"], g.stats()["create_ms"]))
     del coords, vals, T
     torch.cuda.empty_cache()
 
@@ -552,11 +554,14 @@ def run_ours(args):
             tt = torch.tensor([ems], dtype=torch.float64)
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
             ems = float(tt[0])
+        create2 = dict(zip(["setup_and_input_ms", "sorted_copies_ms", "dups_fibers_fit_sample_ms",
+                            "factors_leverage_ms"], g2.stats()["create_ms"]))
         g2.close()
         h2d = hc.numel() * hc.element_size() + hv.numel() * hv.element_size()
         e2e = {"value": K / (ems / 1000.0), "unit": "iterations/s", "h2d_bytes_per_step": h2d // K,
                "d2h_bytes_per_step": d2h // K,
                "wall_s": {"create_from_host": w1 - w0, "run": w2 - w1, "factors_to_host": w3 - w2},
+               "create_phases": create2,
                "includes": "cparls_create from pinned host COO (H2D + per-mode index build) + K iterations + "
                            "fits every 5 + factors back to host"}
 
@@ -586,7 +591,7 @@ def run_ours(args):
         "fit": final_fit,
         "estimated_fit_variant": est,
         "cp_als_baseline": als,
-        "setup": {"generate_s": t_gen, "create_s": t_build, "rrf_init_ms": rrf_ms},
+        "setup": {"generate_s": t_gen, "create_s": t_build, "create_phases": create_phases, "rrf_init_ms": rrf_ms},
         "iteration_roofline": iter_roofline,
         "per_iteration": per_iteration,
         "fit_every_1": fe1,

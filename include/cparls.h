@@ -72,15 +72,13 @@ typedef struct {
   cparls_comm *comm;       /* required when world_size > 1 (cparls_comm_create_*)      */
   int64_t didx_cap;        /* max DIDX list length per level (0 -> default 1<<22)     */
   int64_t attempt_cap;     /* max SIDX attempts (0 -> 1024*s_rnd + 65536, AMB-7)      */
-  int32_t rhs_path;        /* sampled RHS kernels: 0 auto (= 1, the faster on B200),
-                              1 fixed-point int64 reductions into M (rhs.cuh, AMB-35:
-                              deterministic, per-column scale 2^e_c from a bound on
-                              |M|), 2 bucketed: entries placed into 32-row buckets,
-                              accumulated in shared memory without atomics
-                              (rhs_bucket.cuh; needs r <= 32, s_bar < 2^27,
-                              m_k < 2^32), 3 fp64 reductions into M (rhs.cuh; order
-                              of the additions not fixed).  Same math; B = M G^+
-                              follows in the solve.  Other values: EINVAL.           */
+  int32_t rhs_path;        /* sampled RHS kernels: 0 auto (= 1), 1 fixed-point int64
+                              reductions into M (rhs.cuh, AMB-35: deterministic,
+                              per-column scale 2^e_c from a bound on |M|), 3 fp64
+                              reductions into M (order of the additions not fixed).
+                              Same math; B = M G^+ follows.  2 (round 1's bucketed
+                              transposition, measured slower) and other values:
+                              EINVAL.                                               */
   int64_t fit_samples;     /* s_fit > 0: draw the stratified fit sample at create
                               (sec:estimating-fit, AMB-32); 0 = none.
                               Single GPU only (EINVAL with world_size > 1).          */
@@ -144,6 +142,9 @@ typedef struct {
   int64_t sum_matched_nnz;   /* sum of m_k over the solves since the last reset   */
   int64_t host_syncs;        /* cudaStreamSynchronize calls made by the library   */
   double bytes_comm;         /* bytes this rank contributed to collectives (world_size > 1) */
+  double create_ms[4];       /* cparls_create wall time: [0] setup + input copy to the
+                                device, [1] per-mode sorted copies, [2] duplicates,
+                                fiber counts, fit sample, [3] factors + leverage       */
 } cparls_stats;
 
 /* Build the context: validates sizes (ERANGE if some prod_{m!=k} n_m >= 2^63 or

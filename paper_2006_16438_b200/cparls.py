@@ -54,13 +54,14 @@ class Stats(C.Structure):
         "mode_steps", "fits", "kernel_launches", "last_matched_nnz", "last_s_bar", "last_attempts")] + [
         ("touched_rows", C.c_int64 * 8), ("kernel_ms", C.c_double * 4),
         ("kernel_launches_by_id", C.c_int64 * 4), ("sum_matched_nnz", C.c_int64), ("host_syncs", C.c_int64),
-        ("bytes_comm", C.c_double)]
+        ("bytes_comm", C.c_double), ("create_ms", C.c_double * 4)]
 
     KERNELS = ("rhs", "fit", "solve_rows", "lev_rows")
 
     def as_dict(self):
         d = {n: getattr(self, n) for n, _ in self._fields_}
         d["touched_rows"] = list(self.touched_rows)
+        d["create_ms"] = list(self.create_ms)
         d["kernel_ms"] = {k: self.kernel_ms[i] for i, k in enumerate(self.KERNELS)}
         d["kernel_launches_by_id"] = {k: self.kernel_launches_by_id[i] for i, k in enumerate(self.KERNELS)}
         return d

@@ -178,13 +178,6 @@ struct cparls_ctx {
   // RHS output-row windows (see rhs.cuh)
   int64_t segcap = 0;
   int64_t *seg_lo = nullptr, *seg_len = nullptr, *seg_off = nullptr, *i64part_seg = nullptr;
-  // bucketed RHS (rhs_bucket.cuh)
-  int64_t *bkt_cnt = nullptr, *bkt_start = nullptr, *bkt_part = nullptr;
-  unsigned long long *bkt_cursor = nullptr;
-  int64_t bkt_cap = 0, rec_cap = 0;
-  uint32_t *rec = nullptr;
-  double *recc = nullptr;
-  bool m_dirty = false;   // M holds rows written by the bucketed RHS (not zero)
   double *fx_scale = nullptr;   // fixed-point RHS scales 2^e_c, 2^-e_c (kernels.cuh)
   double dupmax = 1.0;
   bool rhs_fixed = true;        // int64 fixed-point RHS (rhs_path 0/1/2); false: fp64 reductions (rhs_path 3)
@@ -553,7 +546,6 @@ void set_attrs_rm() {
 }
 
 void set_kernel_attrs(int r, int ld) {
-  max_dyn_smem(k_bkt_accum<4>);
   max_dyn_smem(k_solve_dmma<1>); max_dyn_smem(k_solve_dmma<2>); max_dyn_smem(k_solve_dmma<3>);
   max_dyn_smem(k_solve_dmma<4>);
   set_attrs_rm<4>(); set_attrs_rm<8>(); set_attrs_rm<16>(); set_attrs_rm<28>(); set_attrs_rm<32>();
@@ -1534,8 +1526,7 @@ void launch_fixed_scales(cparls_ctx *c, cudaStream_t st) {
 
 // One sketched mode update (Alg. 3) from the current sample, every
 // size on the device: KrpSamp + sampled Gram, lookup, RHS, B = M G^+,
-// normalize, leverage refresh.  No host synchronisation (the bucketed RHS,
-// rhs_path 2, reads m_k on the host).
+// normalize, leverage refresh.  No host synchronisation.
 void solve_impl(cparls_ctx *c, int k, cparls_solve_info *info) {
   if (!c->have_sample || c->smode != k) throw ApiError(CPARLS_ESTATE, "solve_mode without a current sample of this mode");
   const int r = c->r, ld = c->ld;
@@ -1581,7 +1572,7 @@ void solve_impl(cparls_ctx *c, int k, cparls_solve_info *info) {
   }
   // fixed-point scales of the atomic RHS on the side stream, overlapping K7
   c->fx_pending = false;
-  if (c->rhs_fixed && c->opts.rhs_path != 2 && c->opts.rhs_path != 3) {
+  if (c->rhs_fixed) {
     CK(cudaEventRecord(c->ev_fork, c->st));
     CK(cudaStreamWaitEvent(c->side, c->ev_fork, 0));
     launch_fixed_scales(c, c->side);
@@ -1598,83 +1589,9 @@ void solve_impl(cparls_ctx *c, int k, cparls_solve_info *info) {
   const int64_t r0 = c->row_lo[k], nown = c->row_hi[k] - c->row_lo[k];
   const int path = c->opts.rhs_path;
   c->fx_on = c->rhs_fixed && path != 3;
-  bool use_bkt = false;
-  int64_t mk_host = -1;
-  if (path == 2) {   // bucketed RHS (opt-in): sizes on the host
-    pull_sample_state(c);
-    if (!(r <= 32 && c->sbar < kBktMaxSbar)) throw ApiError(CPARLS_EINVAL, "rhs_path 2 needs r <= 32 and s_bar < 2^24");
-    mk_host = read_dev(c, &c->dv->mk);
-    if (mk_host >= (int64_t(1) << 32)) throw ApiError(CPARLS_EINVAL, "rhs_path 2 needs m_k < 2^32");
-    use_bkt = true;
-  }
-  if (use_bkt) {
-    const int64_t sbar = c->sbar;
-    Phase ph(c, &c->stats.ms_rhs);
-    k_solve_prep<<<1, 128, prep_smem(r), c->st>>>(r, c->sd);
-    CK_LAUNCH();
-    const int64_t nbkt = std::max<int64_t>(1, ceil_div(nown, kBktRows));
-    if (nbkt + 1 > c->bkt_cap) {
-      dfree(c, c->bkt_cnt); dfree(c, c->bkt_start); dfree(c, c->bkt_cursor); dfree(c, c->bkt_part);
-      c->bkt_cap = nbkt + 1;
-      c->bkt_cnt = dalloc_t<int64_t>(c, c->bkt_cap);
-      c->bkt_start = dalloc_t<int64_t>(c, c->bkt_cap);
-      c->bkt_cursor = dalloc_t<unsigned long long>(c, c->bkt_cap);
-      c->bkt_part = dalloc_t<int64_t>(c, ceil_div(c->bkt_cap, kScanTile) + 16);
-    }
-    if (mk_host > c->rec_cap) {
-      dfree(c, c->rec); dfree(c, c->recc);
-      c->rec_cap = std::max<int64_t>(mk_host, 1) + (mk_host >> 3);
-      c->rec = dalloc_t<uint32_t>(c, c->rec_cap);
-      c->recc = dalloc_t<double>(c, c->rec_cap);
-    }
-    KTimer kt(c, KT_RHS);
-    CK(cudaMemsetAsync(c->bkt_cnt, 0, sizeof(int64_t) * (nbkt + 1), c->st));
-    const int grid = 148 * 8;
-    const int64_t per_warp = 512;
-    if (mk_host > 0) {
-      CK(cudaMemsetAsync(&c->dv->counter, 0, sizeof(unsigned long long), c->st));
-      k_bkt_count<<<grid, 256, 0, c->st>>>(c->off, c->lo, sbar, &c->dv->mk, &c->dv->counter, per_warp,
-                                           c->idx[k].out, r0, reinterpret_cast<unsigned long long *>(c->bkt_cnt));
-      CK_LAUNCH();
-    }
-    exclusive_scan_i64(c->bkt_cnt, c->bkt_start, nbkt + 1, c->bkt_part, nullptr, c->st);
-    k_bkt_cursor<<<(unsigned)ceil_div(nbkt, 256), 256, 0, c->st>>>(c->bkt_start, nbkt, c->bkt_cursor);
-    CK_LAUNCH();
-    if (mk_host > 0) {
-      CK(cudaMemsetAsync(&c->dv->counter, 0, sizeof(unsigned long long), c->st));
-      if (c->vf32)
-        k_bkt_place<float><<<grid, 256, 0, c->st>>>(c->off, c->lo, sbar, &c->dv->mk, &c->dv->counter, per_warp,
-                                                    c->idx[k].out, (const float *)c->idx[k].val, c->sw2, r0,
-                                                    c->bkt_cursor, c->rec, c->recc);
-      else
-        k_bkt_place<double><<<grid, 256, 0, c->st>>>(c->off, c->lo, sbar, &c->dv->mk, &c->dv->counter, per_warp,
-                                                     c->idx[k].out, (const double *)c->idx[k].val, c->sw2, r0,
-                                                     c->bkt_cursor, c->rec, c->recc);
-      CK_LAUNCH();
-    }
-    {
-      const int64_t agrid = std::max<int64_t>(1, std::min<int64_t>(ceil_div(nbkt, kBktThreads / 32), 148 * 3));
-      k_bkt_accum<4><<<(unsigned)agrid, kBktThreads, bkt_accum_smem(ld), c->st>>>(c->bkt_start, nbkt, c->rec, c->recc,
-                                                                                  c->Z, nown, ld, c->M + r0 * ld);
-      CK_LAUNCH();
-    }
-    CK(cudaMemsetAsync(&c->dv->touched, 0, sizeof(unsigned long long), c->st));
-    const int64_t bgrid = row_grid(c, ceil_div(std::max<int64_t>(nown, 1), kRowThreads));
-    launch_solve_rows(c, c->M + r0 * ld, nown, c->A[k] + r0 * ld, bgrid, 0, nullptr);
-    CK_LAUNCH();
-    c->m_dirty = true;   // M holds this mode's rows (no zeroing pass)
-    kt.stop();
-    k_pairs_reduce<<<pairs_reduce_grid(r), 256, 0, c->st>>>(c->gpart, bgrid, r, c->sd->BtB);
-    CK_LAUNCH();
-    LAUNCHED(c, 8);
-    ph.end();
-  } else {
+  {
     // K8: sampled RHS (int64 fixed-point / fp64 red per entry in L2-sized
     // output-row windows, rhs.cuh)
-    if (c->m_dirty) {   // a bucketed step left rows in M
-      CK(cudaMemsetAsync(c->M, 0, sizeof(double) * c->nmax * c->ld, c->st));
-      c->m_dirty = false;
-    }
     Phase ph(c, &c->stats.ms_rhs);
     constexpr int win_mb = 96;     // output-row window of M kept in L2 (rhs.cuh)
     constexpr int grid_mult = 8;   // CTAs per SM
@@ -1753,7 +1670,7 @@ void solve_impl(cparls_ctx *c, int k, cparls_solve_info *info) {
   }
   {
     Phase ph(c, &c->stats.ms_solve);
-    if (!use_bkt) {
+    {
       k_solve_prep<<<1, 128, prep_smem(r), c->st>>>(r, c->sd, ctl);
       CK_LAUNCH();
       const int64_t grid = row_grid(c, ceil_div(std::max<int64_t>(nown, 1), kRowThreads));
@@ -1812,10 +1729,6 @@ void als_update_impl(cparls_ctx *c, int k) {
     if (m != k && c->idx[m].order[c->D - 2] == k) cm = m;
   if (cm < 0) throw ApiError(CPARLS_ESTATE, "no copy with slowest key mode k");
   Phase ph(c, &c->stats.ms_rhs);
-  if (c->m_dirty) {
-    CK(cudaMemsetAsync(c->M, 0, sizeof(double) * c->nmax * c->ld, c->st));
-    c->m_dirty = false;
-  }
   FitDecode fd{};
   fd.d = c->D - 1;
   long double N = 1;
@@ -1890,10 +1803,6 @@ void init_rrf_impl(cparls_ctx *c, int64_t s_init, uint64_t seed) {
   if (c->world > 1) throw ApiError(CPARLS_EINVAL, "RRF initialization: single GPU only");
   if (s_init < 1) throw ApiError(CPARLS_EINVAL, "s_init >= 1");
   const int r = c->r, ld = c->ld;
-  if (c->m_dirty) {
-    CK(cudaMemsetAsync(c->M, 0, sizeof(double) * c->nmax * ld, c->st));
-    c->m_dirty = false;
-  }
   for (int k = 0; k < c->D; ++k) {
     const ModeIndex &ix = c->idx[k];
     const int64_t nnz = ix.nnz, nk = c->dims[k];
@@ -2174,7 +2083,7 @@ void run_async(cparls_ctx *c, int32_t iters, int64_t s, uint64_t seed, int32_t i
     c->fitbuf = dalloc_t<double>(c, c->fitbuf_cap);
   }
   if (iters > 0) CK(cudaMemsetAsync(c->fitbuf, 0xFF, sizeof(double) * iters, c->st));   // NaN: no fit
-  const bool async_ok = !c->sample_sort && c->opts.rhs_path != 2;
+  const bool async_ok = !c->sample_sort;
   auto one_step = [&](int64_t g, bool host_sampler) {
     const int t = (int)(g / D), k = (int)(g % D);
     const uint64_t step = (uint64_t)(iter0 + t) * D + k;   // AMB-10
@@ -2267,12 +2176,16 @@ cparls_status cparls_create(cparls_ctx **out, int32_t nmodes, const int64_t *dim
   std::memcpy(&ob, opts_in, std::min<size_t>(opts_in->struct_size, sizeof(cparls_opts)));
   ob.struct_size = (uint32_t)sizeof(cparls_opts);
   const cparls_opts *opts = &ob;
+  const auto t0 = std::chrono::steady_clock::now();
+  auto since = [&t0] { return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count(); };
+  double t_h2d = 0, t_build = 0, t_aux = 0;
   cparls_ctx *c = new (std::nothrow) cparls_ctx();
   if (!c) return CPARLS_EOOM;
   cparls_status st = guarded(c, [&] {
     if (nmodes < 2 || nmodes > kMaxModes) throw ApiError(CPARLS_EINVAL, "nmodes must be in [2, 8]");
     if (opts->rank < 1 || opts->rank > kMaxRank) throw ApiError(CPARLS_EINVAL, "rank must be in [1, 64]");
-    if (opts->rhs_path < 0 || opts->rhs_path > 3) throw ApiError(CPARLS_EINVAL, "rhs_path must be in [0, 3]");
+    if (opts->rhs_path < 0 || opts->rhs_path > 3 || opts->rhs_path == 2)
+      throw ApiError(CPARLS_EINVAL, "rhs_path must be 0, 1 or 3");
     if (nnz_local < 0) throw ApiError(CPARLS_EINVAL, "nnz < 0");
     if (nnz_local >= (int64_t(1) << 32)) throw ApiError(CPARLS_ERANGE, "nnz_local must be < 2^32 per GPU");
     if (nnz_local > 0 && (!coords || !vals)) throw ApiError(CPARLS_EINVAL, "null coords/vals");
@@ -2346,10 +2259,14 @@ cparls_status cparls_create(cparls_ctx **out, int32_t nmodes, const int64_t *dim
       CK(cudaMemcpyAsync(own_v, vals, vsz * nnz_local, cudaMemcpyHostToDevice, c->st));
       dva = own_v;
     }
+    sync(c);
+    t_h2d = since();
     if (isz == 4 && vsz == 4) build_all<int32_t, float>(c, (const int32_t *)dco, (const float *)dva);
     else if (isz == 4) build_all<int32_t, double>(c, (const int32_t *)dco, (const double *)dva);
     else if (vsz == 4) build_all<int64_t, float>(c, (const int64_t *)dco, (const float *)dva);
     else build_all<int64_t, double>(c, (const int64_t *)dco, (const double *)dva);
+    sync(c);
+    t_build = since();
     c->drow_lo = dalloc_t<int64_t>(c, kMaxModes);
     c->drow_hi = dalloc_t<int64_t>(c, kMaxModes);
     CK(cudaMemcpyAsync(c->drow_lo, c->row_lo, sizeof(int64_t) * kMaxModes, cudaMemcpyHostToDevice, c->st));
@@ -2443,9 +2360,15 @@ cparls_status cparls_create(cparls_ctx **out, int32_t nmodes, const int64_t *dim
       }
       if (opts->fit_mode >= 0 && opts->fit_mode < nmodes) c->fit_mode = opts->fit_mode;
     }
+    sync(c);
+    t_aux = since();
     reset_lambda(c);
     for (int k = 0; k < nmodes; ++k) leverage_full(c, k);
     sync(c);
+    c->stats.create_ms[0] = t_h2d;
+    c->stats.create_ms[1] = t_build - t_h2d;
+    c->stats.create_ms[2] = t_aux - t_build;
+    c->stats.create_ms[3] = since() - t_aux;
   });
   if (st != CPARLS_OK) {
     g_create_err = c->err;
@@ -2903,7 +2826,10 @@ cparls_status cparls_reset_stats(cparls_ctx *c) {
   if (!c) return CPARLS_EINVAL;
   return guarded(c, [&] {
     sync(c, false);   // a pending step's counters belong to the old stats
+    double cm[4];
+    std::memcpy(cm, c->stats.create_ms, sizeof(cm));
     c->stats = cparls_stats{};
+    std::memcpy(c->stats.create_ms, cm, sizeof(cm));   // create timings survive a reset
     c->ctl_seen = *reinterpret_cast<const StepCtl *>(c->hctl);
   });
 }

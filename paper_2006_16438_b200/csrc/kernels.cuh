@@ -1028,7 +1028,6 @@ __global__ void k_dup_runs(const uint64_t *__restrict__ key, const int32_t *__re
 
 #include "rows.cuh"
 #include "rhs.cuh"
-#include "rhs_bucket.cuh"
 #include "fit.cuh"
 #include "fitest.cuh"
 #include "als.cuh"

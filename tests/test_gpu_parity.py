@@ -159,31 +159,36 @@ def test_c1_lockstep_20_iterations():
     lockstep(T, cfg.rank, cfg.iters, cfg.s, cfg.sample_seed)
 
 
-@pytest.mark.parametrize("rhs_path", [1, 2, 3])
+@pytest.mark.parametrize("rhs_path", [1, 3])
 def test_c1_lockstep_rhs_paths(rhs_path):
-    """Every RHS + solve implementation (fixed-point int64 reductions into M,
-    the bucketed RHS with the fused solve, fp64 reductions into M) against the
-    oracle."""
+    """Both RHS implementations (fixed-point int64 reductions into M, fp64
+    reductions into M) against the oracle."""
     T = synth.make("C1")
     cfg = T.cfg
     lockstep(T, cfg.rank, 6, cfg.s, cfg.sample_seed, rhs_path=rhs_path)
 
 
-def test_c2_lockstep_bucket_path():
+def test_c2_lockstep_fp64_rhs_path():
     T = synth.make("C2", device="cuda")
     T = synth.Tensor(T.cfg, T.dims, T.coords.cpu(), T.vals.cpu())
-    lockstep(T, 25, 1, 1 << 17, 3, rhs_path=2)
+    lockstep(T, 25, 1, 1 << 17, 3, rhs_path=3)
 
 
 def test_rhs_paths_agree_f32_values():
-    """fp32-valued tensor (the C4/C5 storage): atomic and bucketed paths give
-    the same B to rounding (<= 1e-12 relative), over a few free-running steps."""
+    """fp32-valued tensor (the C4/C5 storage): the fixed-point and the fp64
+    reduction paths give the same B to the quantisation bound (<= 1e-11
+    relative), over a few free-running steps; the removed rhs_path 2 is
+    rejected."""
     need_gpu()
     cfg = synth.scaled("C2", 300_000)
     T = synth.make(cfg, device="cuda")
-    from paper_2006_16438_b200 import Cparls
+    from paper_2006_16438_b200 import Cparls, CparlsError
+    from paper_2006_16438_b200 import cparls as cp
+    with pytest.raises(CparlsError) as e:
+        Cparls(T.dims, T.coords, T.vals.float(), 25, rhs_path=2)
+    assert e.value.status == cp.EINVAL
     a = Cparls(T.dims, T.coords, T.vals.float(), 25, rhs_path=1)
-    b = Cparls(T.dims, T.coords, T.vals.float(), 25, rhs_path=2)
+    b = Cparls(T.dims, T.coords, T.vals.float(), 25, rhs_path=3)
     for t in range(2):
         for k in range(len(T.dims)):
             ia, ib = a.sample(k, 4096, 5, 4 * t + k), b.sample(k, 4096, 5, 4 * t + k)
@@ -192,7 +197,7 @@ def test_rhs_paths_agree_f32_values():
             assert (sa.matched_nnz, sa.touched_rows) == (sb.matched_nnz, sb.touched_rows)
             _, Ba = a.last_solve(k)
             _, Bb = b.last_solve(k)
-            assert np.linalg.norm(Ba - Bb) <= 1e-12 * np.linalg.norm(Ba), (t, k)
+            assert np.linalg.norm(Ba - Bb) <= 1e-11 * np.linalg.norm(Ba), (t, k)
             # continue both from identical factors so the comparison stays per-step
             A, _ = a.get_factor(k)
             b.set_factor(k, A)
