@@ -1593,7 +1593,10 @@ void solve_impl(cparls_ctx *c, int k, cparls_solve_info *info) {
     // K8: sampled RHS (int64 fixed-point / fp64 red per entry in L2-sized
     // output-row windows, rhs.cuh)
     Phase ph(c, &c->stats.ms_rhs);
-    constexpr int win_mb = 96;     // output-row window of M kept in L2 (rhs.cuh)
+#ifndef CPARLS_RHS_WIN_MB
+#define CPARLS_RHS_WIN_MB 96
+#endif
+    constexpr int win_mb = CPARLS_RHS_WIN_MB;   // output-row window of M kept in L2 (rhs.cuh)
     constexpr int grid_mult = 8;   // CTAs per SM
     const int64_t RW = std::max<int64_t>(1, (int64_t(win_mb) << 20) / ((int64_t)ld * 8));
     const int nwin = (int)ceil_div(nk, RW);

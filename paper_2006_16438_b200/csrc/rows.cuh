@@ -291,8 +291,14 @@ __device__ __forceinline__ double lev_of_row(const double *x, int r, const doubl
 // into the 256-row tile sums of the CDF scan (integer adds: order-free, exact);
 // lam != nullptr normalizes A in place first (a_ic = b_ic * (1/lambda_c),
 // within 1 ulp of the division, which cost ~10 FP64 instructions per element).
+#ifndef CPARLS_LEV_MINB
+#define CPARLS_LEV_MINB 2   // resident CTAs per SM the leverage pass is compiled for
+#endif
+#ifndef CPARLS_SOLVE_MINB
+#define CPARLS_SOLVE_MINB 2   // resident CTAs per SM the DMMA solve pass is compiled for
+#endif
 template <int RMAX>
-__global__ void __launch_bounds__(kRowThreads, 2) k_lev_rows_w(double *__restrict__ A, int64_t n, int r, int ld,
+__global__ void __launch_bounds__(kRowThreads, CPARLS_LEV_MINB) k_lev_rows_w(double *__restrict__ A, int64_t n, int r, int ld,
                                                               const double *__restrict__ lam,
                                                               const ModeDev *__restrict__ md, double *__restrict__ pt,
                                                               uint64_t *__restrict__ C,
@@ -377,7 +383,7 @@ __host__ __device__ constexpr size_t solve_dmma_smem_d(int LD) {
 }
 
 template <int NT>
-__global__ void __launch_bounds__(kRowThreads, 2) k_solve_dmma(double *__restrict__ M, int64_t n, int r, int ld,
+__global__ void __launch_bounds__(kRowThreads, CPARLS_SOLVE_MINB) k_solve_dmma(double *__restrict__ M, int64_t n, int r, int ld,
                                                                const SolveDev *__restrict__ sd,
                                                                double *__restrict__ B, double *__restrict__ part,
                                                                unsigned long long *__restrict__ touched, int zero_m,
