@@ -95,10 +95,17 @@ typedef struct {
   int32_t fit_mode;        /* mode whose sorted copy the exact fit streams: -1 or any
                               value outside [0, D) = automatic (fewest gathers); the
                               fit does not depend on it beyond rounding            */
+  int32_t rhs_hot_rows;    /* fixed-point RHS: rows of a mode whose entries are summed
+                              per CTA in shared memory before reaching M (the rows of
+                              largest degree; rhs.cuh).  -1 = automatic (as many as
+                              fit in shared memory, used for a mode when they hold
+                              at least 70% of its nonzeros); 0 = none; > 0 = at most
+                              this many, always used.  M is bit-identical either way
+                              (int64 sums).  Ignored for r > 32 and rhs_path 3.     */
 } cparls_opts;
 
 /* Fill *opts with the defaults (tau = -1, rank = 1, world_size = 1, fit_mode = -1,
- * everything else 0/NULL) and struct_size = sizeof(cparls_opts). */
+ * rhs_hot_rows = -1, everything else 0/NULL) and struct_size = sizeof(cparls_opts). */
 void cparls_opts_init(cparls_opts *opts);
 
 typedef struct {
@@ -145,6 +152,9 @@ typedef struct {
   double create_ms[4];       /* cparls_create wall time: [0] setup + input copy to the
                                 device, [1] per-mode sorted copies, [2] duplicates,
                                 fiber counts, fit sample, [3] factors + leverage       */
+  int32_t rhs_hot_rows[8];   /* per mode: rows summed in shared memory by the RHS
+                                (cparls_opts.rhs_hot_rows; 0 = none)                */
+  double rhs_hot_share[8];   /* per mode: fraction of this rank's nonzeros in them  */
 } cparls_stats;
 
 /* Build the context: validates sizes (ERANGE if some prod_{m!=k} n_m >= 2^63 or

@@ -33,7 +33,8 @@ class Opts(C.Structure):
                 ("world_size", C.c_int32), ("world_rank", C.c_int32), ("comm", C.c_void_p),
                 ("didx_cap", C.c_int64), ("attempt_cap", C.c_int64), ("rhs_path", C.c_int32),
                 ("fit_samples", C.c_int64), ("fit_alpha", C.c_double), ("fit_seed", C.c_uint64),
-                ("sidx_window", C.c_int64), ("sample_sort", C.c_int32), ("fit_mode", C.c_int32)]
+                ("sidx_window", C.c_int64), ("sample_sort", C.c_int32), ("fit_mode", C.c_int32),
+                ("rhs_hot_rows", C.c_int32)]
 
 
 class SampleInfo(C.Structure):
@@ -54,7 +55,8 @@ class Stats(C.Structure):
         "mode_steps", "fits", "kernel_launches", "last_matched_nnz", "last_s_bar", "last_attempts")] + [
         ("touched_rows", C.c_int64 * 8), ("kernel_ms", C.c_double * 4),
         ("kernel_launches_by_id", C.c_int64 * 4), ("sum_matched_nnz", C.c_int64), ("host_syncs", C.c_int64),
-        ("bytes_comm", C.c_double), ("create_ms", C.c_double * 4)]
+        ("bytes_comm", C.c_double), ("create_ms", C.c_double * 4), ("rhs_hot_rows", C.c_int32 * 8),
+        ("rhs_hot_share", C.c_double * 8)]
 
     KERNELS = ("rhs", "fit", "solve_rows", "lev_rows")
 
@@ -62,6 +64,8 @@ class Stats(C.Structure):
         d = {n: getattr(self, n) for n, _ in self._fields_}
         d["touched_rows"] = list(self.touched_rows)
         d["create_ms"] = list(self.create_ms)
+        d["rhs_hot_rows"] = list(self.rhs_hot_rows)
+        d["rhs_hot_share"] = list(self.rhs_hot_share)
         d["kernel_ms"] = {k: self.kernel_ms[i] for i, k in enumerate(self.KERNELS)}
         d["kernel_launches_by_id"] = {k: self.kernel_launches_by_id[i] for i, k in enumerate(self.KERNELS)}
         return d
@@ -153,7 +157,8 @@ class Cparls:
 
     def __init__(self, dims, coords, vals, rank, tau=-1.0, init_seed=2, stream=None,
                  didx_cap=0, attempt_cap=0, comm=None, world_size=1, world_rank=0, rhs_path=0,
-                 fit_samples=0, fit_alpha=0.5, fit_seed=0, sidx_window=0, sample_sort=0, fit_mode=-1):
+                 fit_samples=0, fit_alpha=0.5, fit_seed=0, sidx_window=0, sample_sort=0, fit_mode=-1,
+                 rhs_hot_rows=-1):
         import torch
         if not torch.cuda.is_available():
             raise RuntimeError("cparls needs a CUDA device (B200); no CPU fallback exists")
@@ -183,7 +188,8 @@ class Cparls:
                  comm=(comm.handle if comm is not None else None),
                  didx_cap=int(didx_cap), attempt_cap=int(attempt_cap), rhs_path=int(rhs_path),
                  fit_samples=int(fit_samples), fit_alpha=float(fit_alpha), fit_seed=int(fit_seed),
-                 sidx_window=int(sidx_window), sample_sort=int(sample_sort), fit_mode=int(fit_mode))
+                 sidx_window=int(sidx_window), sample_sort=int(sample_sort), fit_mode=int(fit_mode),
+                 rhs_hot_rows=int(rhs_hot_rows))
         d = np.array(self.dims, dtype=np.int64)
         h = C.c_void_p()
         st = L.cparls_create(C.byref(h), self.D, d.ctypes.data, nnz, _ptr(coords), _ptr(vals),

@@ -14,6 +14,45 @@ constexpr int kMaxRank = 64;
 constexpr unsigned long long kEmptyKey = 0xFFFFFFFFFFFFFFFFull;
 constexpr double kTwo62 = 4611686018427387904.0;  // 2^62
 
+// Division by an invariant divisor 1 <= d < 2^63 for any 64-bit dividend
+// (Granlund & Montgomery 1994, the round-up method): with l = ceil(log2 d),
+// m = floor(2^64 (2^l - d) / d) + 1, t = mulhi(m, x):
+// x / d = (t + ((x - t) >> min(l, 1))) >> max(l - 1, 0).  Replaces the ~70-
+// instruction 64-bit division when decoding sample keys into indices.
+struct FastDiv {
+  uint64_t m = 1;
+  uint64_t d = 1;
+  uint32_t s1 = 0, s2 = 0;
+};
+
+inline FastDiv make_fastdiv(uint64_t d) {
+  FastDiv f;
+  int l = 0;
+  while (l < 63 && (uint64_t(1) << l) < d) ++l;
+  const unsigned __int128 num = ((unsigned __int128)((uint64_t(1) << l) - d)) << 64;
+  f.m = (uint64_t)(num / d) + 1;
+  f.d = d;
+  f.s1 = l < 1 ? l : 1;
+  f.s2 = l > 1 ? l - 1 : 0;
+  return f;
+}
+
+__host__ __device__ __forceinline__ uint64_t fastdiv(uint64_t x, const FastDiv &f) {
+#ifdef __CUDA_ARCH__
+  const uint64_t t = __umul64hi(f.m, x);
+#else
+  const uint64_t t = (uint64_t)(((unsigned __int128)f.m * x) >> 64);
+#endif
+  return (t + ((x - t) >> f.s1)) >> f.s2;
+}
+
+// x / d with the remainder
+__host__ __device__ __forceinline__ uint64_t fastdivmod(uint64_t x, const FastDiv &f, uint64_t &rem) {
+  const uint64_t q = fastdiv(x, f);
+  rem = x - q * f.d;
+  return q;
+}
+
 struct CudaError : std::runtime_error {
   cudaError_t code;
   CudaError(cudaError_t c, const std::string &m) : std::runtime_error(m), code(c) {}

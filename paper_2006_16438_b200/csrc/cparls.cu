@@ -38,6 +38,13 @@ struct ModeIndex {
   // the slowest is mode (k+1) mod D, the rest by ascending n_m.  Sample keys
   // stay canonical (AMB-1) and are re-encoded by the lookup.
   int order[kMaxModes] = {};
+  // hot rows of the fixed-point RHS (rhs.cuh k_rhs_hot): hot_n > 0 enables;
+  // hot_slot (n_k entries, -1 = cold) and hot_rows (hot_n) are null when every
+  // row is hot (slot = row)
+  int32_t *hot_slot = nullptr;
+  int32_t *hot_rows = nullptr;
+  int hot_n = 0;
+  double hot_share = 0.0;    // fraction of this copy's nonzeros in the hot rows
 };
 
 // other modes of k, ascending n_m (ties: lower mode first)
@@ -56,6 +63,7 @@ struct DevScalars {
   double normX2;
   double maxabs;                    // max |x| over the nonzeros (fixed-point RHS bound)
   unsigned long long dupmax;        // longest run of duplicate coordinates in a copy
+  unsigned int done_count;          // k_gram_scales: blocks finished (the last resets it)
 };
 
 }  // namespace
@@ -102,6 +110,7 @@ struct cparls_ctx {
   uint8_t *touched = nullptr;
   double *gpart = nullptr;
   int64_t gpart_blocks = 0;
+  int nsm = 148;                 // SMs of the device (k_rhs_hot: one CTA each)
   double *Gtmp = nullptr;
   uint64_t *tile_u64 = nullptr;
   int64_t *i64part = nullptr;    // scan partials
@@ -185,11 +194,11 @@ struct cparls_ctx {
   // pinned double buffer for copies into pageable host memory (rows_to_host)
   void *stage[2] = {nullptr, nullptr};
   long long *hscr = nullptr;    // small pinned scratch: async scalar reads folded into later syncs
-  // side stream: the fixed-point scales (k_colabs_part, k_fixed_scales) run
-  // concurrently with the fiber lookup and window bounds of the same step
-  cudaStream_t side = nullptr;
+  double *cpart = nullptr;       // K6 block partials of sum_j w_j^2 |z_j| per column (fixed-point scales)
+  // auxiliary stream: G^+ (k_solve_prep) runs concurrently with the lookup and
+  // the RHS of the same step (it needs only the sampled Gram)
+  cudaStream_t aux = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
-  bool fx_pending = false;
   cudaEvent_t stage_ev[2] = {nullptr, nullptr};
   // frozen stratified fit sample (fitest.cuh, AMB-32)
   bool have_fs = false;
@@ -540,7 +549,6 @@ void set_attrs_rm() {
   max_dyn_smem(k_gram_rows_t<RM>);
   max_dyn_smem(k_solve_rows_t<RM>);
   max_dyn_smem(k_lev_rows_w<RM>);
-  max_dyn_smem(k_krp_gram_t<RM>);
   max_dyn_smem(k_fit_thread<float, RM>);
   max_dyn_smem(k_fit_thread<double, RM>);
 }
@@ -548,6 +556,7 @@ void set_attrs_rm() {
 void set_kernel_attrs(int r, int ld) {
   max_dyn_smem(k_solve_dmma<1>); max_dyn_smem(k_solve_dmma<2>); max_dyn_smem(k_solve_dmma<3>);
   max_dyn_smem(k_solve_dmma<4>);
+  max_dyn_smem(k_rhs_hot<float>); max_dyn_smem(k_rhs_hot<double>);
   set_attrs_rm<4>(); set_attrs_rm<8>(); set_attrs_rm<16>(); set_attrs_rm<28>(); set_attrs_rm<32>();
   set_attrs_rm<64>();
   int prep = (int)prep_smem(r);
@@ -648,7 +657,7 @@ void leverage_full(cparls_ctx *c, int k) {
   gather_factor(c, k);
   Phase ph(c, &c->stats.ms_leverage);
   gram_of_rows(c, c->A[k], c->dims[k], c->Gtmp);
-  k_lev_prep<<<1, 128, prep_smem(c->r), c->st>>>(c->r, c->Gtmp, c->md[k]);
+  k_lev_prep<<<1, kPrepThreads, prep_smem(c->r), c->st>>>(c->r, c->Gtmp, c->md[k], c->A[k], c->dims[k], c->ld);
   CK_LAUNCH();
   LAUNCHED(c, 1);
   c->stats.bytes_leverage += (double)c->dims[k] * c->r * 8.0;
@@ -672,6 +681,7 @@ OtherModes other_modes(cparls_ctx *c, int k) {
     if (m == k) continue;
     om.mode[j] = m;
     om.n[j] = c->dims[m];
+    om.div[j] = make_fastdiv((uint64_t)c->dims[m]);
     om.pt[j] = c->pt[m];
     om.C[j] = c->C[m];
     om.A[j] = c->A[m];
@@ -703,6 +713,7 @@ KeyRemap key_remap(const cparls_ctx *c, int k) {
   for (int j = 0, m = 0; m < c->D; ++m) {
     if (m == k) continue;
     rm.n[j] = c->dims[m];
+    rm.div[j] = make_fastdiv((uint64_t)c->dims[m]);
     uint64_t mult = 1;
     for (int q = 0; q < rm.d && order[q] != m; ++q) mult *= (uint64_t)c->dims[order[q]];
     rm.cmult[j] = mult;
@@ -713,6 +724,65 @@ KeyRemap key_remap(const cparls_ctx *c, int k) {
 }
 
 // ---------------------------------------------------------------- index build (K0)
+// Hot rows of mode k for the fixed-point RHS (rhs.cuh k_rhs_hot): the rows of
+// largest degree in this rank's copy (ties: lower row), as many as the
+// shared-memory accumulators hold.
+constexpr size_t kHotSmemBytes = 200 * 1024;
+
+int hot_capacity(int r) { return r > 32 ? 0 : (int)(kHotSmemBytes / (8 * (size_t)r)); }
+
+void build_hot_rows(cparls_ctx *c, int k) {
+  ModeIndex &ix = c->idx[k];
+  const int64_t nk = c->dims[k];
+  const int req = c->opts.rhs_hot_rows;
+  int64_t H = std::min<int64_t>(hot_capacity(c->r), nk);
+  if (req > 0) H = std::min<int64_t>(H, req);
+  if (req == 0 || H <= 0 || ix.nnz == 0 || c->opts.rhs_path == 3) return;
+  uint32_t *deg = dalloc_t<uint32_t>(c, nk);
+  CK(cudaMemsetAsync(deg, 0, sizeof(uint32_t) * nk, c->st));
+  k_row_degree<<<(unsigned)std::min<int64_t>(4096, ceil_div(ix.nnz, 256)), 256, 0, c->st>>>(ix.out, ix.nnz, deg);
+  CK_LAUNCH();
+  if (H == nk) {   // every row hot: slot = row
+    ix.hot_n = (int)H;
+    ix.hot_share = 1.0;
+    sync(c);
+    dfree(c, deg);
+    return;
+  }
+  // rows by degree, descending (stable: ties keep the lower row first)
+  uint32_t *deg1 = dalloc_t<uint32_t>(c, nk);
+  int32_t *rows0 = dalloc_t<int32_t>(c, nk), *rows1 = dalloc_t<int32_t>(c, nk);
+  k_iota_u32<<<(unsigned)ceil_div(nk, 256), 256, 0, c->st>>>(reinterpret_cast<uint32_t *>(rows0), nk);
+  CK_LAUNCH();
+  cub::DoubleBuffer<uint32_t> kb(deg, deg1);
+  cub::DoubleBuffer<int32_t> vb(rows0, rows1);
+  size_t tb = 0;
+  CK(cub::DeviceRadixSort::SortPairsDescending(nullptr, tb, kb, vb, nk, 0, 32, c->st));
+  void *tmp = dalloc(c, tb);
+  CK(cub::DeviceRadixSort::SortPairsDescending(tmp, tb, kb, vb, nk, 0, 32, c->st));
+  std::vector<uint32_t> top(H);
+  CK(cudaMemcpyAsync(top.data(), kb.Current(), sizeof(uint32_t) * H, cudaMemcpyDeviceToHost, c->st));
+  sync(c);
+  double hot = 0.0;
+  for (uint32_t d : top) hot += d;
+  ix.hot_share = hot / (double)ix.nnz;
+  if (req > 0 || ix.hot_share >= 0.7) {
+    ix.hot_n = (int)H;
+    ix.hot_rows = dalloc_t<int32_t>(c, H);
+    CK(cudaMemcpyAsync(ix.hot_rows, vb.Current(), sizeof(int32_t) * H, cudaMemcpyDeviceToDevice, c->st));
+    ix.hot_slot = dalloc_t<int32_t>(c, nk);
+    CK(cudaMemsetAsync(ix.hot_slot, 0xff, sizeof(int32_t) * nk, c->st));
+    k_hot_slots<<<(unsigned)ceil_div(H, 256), 256, 0, c->st>>>(ix.hot_rows, (int)H, ix.hot_slot);
+    CK_LAUNCH();
+    sync(c);
+  }
+  dfree(c, tmp);
+  dfree(c, deg);
+  dfree(c, deg1);
+  dfree(c, rows0);
+  dfree(c, rows1);
+}
+
 template <typename IT, typename VT>
 void build_index_mode(cparls_ctx *c, int k, const IT *coords, const VT *vals, int64_t nnz) {
   ModeIndex &ix = c->idx[k];
@@ -789,6 +859,7 @@ void build_index_mode(cparls_ctx *c, int k, const IT *coords, const VT *vals, in
     CK(cudaMemsetAsync(ix.dir, 0, sizeof(int64_t) * (ix.nbkt + 1), c->st));
   }
   sync(c);
+  build_hot_rows(c, k);
 }
 
 // Row partition of mode k into world contiguous blocks balanced by nonzeros
@@ -1515,15 +1586,6 @@ void lookup_impl(cparls_ctx *c, int k) {
 }
 
 // per-column fixed-point scales 2^e_c of the sampled RHS (kernels.cuh, AMB-35)
-void launch_fixed_scales(cparls_ctx *c, cudaStream_t st) {
-  const int nbc = 296;   // (gpart holds gpart_blocks x r x r >= nbc x r doubles)
-  k_colabs_part<<<nbc, 256, 0, st>>>(c->Z, c->sw2, c->s_cur, c->r, c->ld, c->gpart, &c->ctl->sbar, c->ctl);
-  CK_LAUNCH();
-  k_fixed_scales<<<1, 64, 0, st>>>(c->gpart, nbc, c->r, &c->dv->maxabs, c->dupmax, c->fx_scale, c->ctl);
-  CK_LAUNCH();
-  LAUNCHED(c, 2);
-}
-
 // One sketched mode update (Alg. 3) from the current sample, every
 // size on the device: KrpSamp + sampled Gram, lookup, RHS, B = M G^+,
 // normalize, leverage refresh.  No host synchronisation.
@@ -1561,24 +1623,41 @@ void solve_impl(cparls_ctx *c, int k, cparls_solve_info *info) {
   // K6: KrpSamp + sampled Gram (every block writes its partial; s_bar = 0 gives G = 0)
   {
     Phase ph(c, &c->stats.ms_gram);
+    // Z rows (+ column-sum partials of the fixed-point scales), then the Gram pass over Z
+    const int64_t kgrid = std::min<int64_t>(kKrpBlocks, std::max<int64_t>(1, ceil_div(smax, 4 * (kKrpThreads / 32))));
+    double *cp = c->rhs_fixed ? c->cpart : nullptr;
+#define KRP(DM, QR, HI)                                                                                            \
+  k_krp_rows<DM, QR, HI><<<(unsigned)kgrid, kKrpThreads, 0, c->st>>>(c->skey, c->sw2, smax, om, r, ld, c->Z, cp,    \
+                                                                      &ctl->sbar, ctl, zg)
+    if (r > 32) KRP(kMaxModes - 1, 1, true);
+    else if (om.d <= 2) KRP(2, 4, false);
+    else if (om.d == 3) KRP(3, 4, false);
+    else KRP(kMaxModes - 1, 1, false);
+#undef KRP
+    CK_LAUNCH();
     const int64_t grid = row_grid(c, ceil_div(smax, kRowThreads));
-    RSWITCH(r, k_krp_gram_t<RM><<<(unsigned)grid, kRowThreads, krp_smem(r, ld), c->st>>>(
-                   c->skey, c->sw2, smax, om, r, ld, c->Z, c->gpart, &ctl->sbar, ctl, zg));
+    RSWITCH(r, k_gram_rows_t<RM><<<(unsigned)grid, kRowThreads, krp_smem(r, ld), c->st>>>(
+                   c->Z, smax, r, ld, c->gpart, c->sw2, &ctl->sbar, ctl));
     CK_LAUNCH();
-    k_pairs_reduce<<<pairs_reduce_grid(r), 256, 0, c->st>>>(c->gpart, grid, r, c->sd->G, ctl);
+    if (c->rhs_fixed)   // the Gram and the fixed-point scales of the atomic RHS
+      k_gram_scales<<<gram_scales_grid(r), 256, 0, c->st>>>(c->gpart, c->cpart, grid, kgrid, r, c->sd->G,
+                                                             c->cpart + (int64_t)kKrpBlocks * r,
+                                                             &c->dv->maxabs, c->dupmax, c->fx_scale,
+                                                             &c->dv->done_count, ctl);
+    else
+      k_pairs_reduce<<<pairs_reduce_grid(r), 256, 0, c->st>>>(c->gpart, grid, r, c->sd->G, ctl);
     CK_LAUNCH();
-    LAUNCHED(c, 2);
+    LAUNCHED(c, 3);
     ph.end();
   }
-  // fixed-point scales of the atomic RHS on the side stream, overlapping K7
-  c->fx_pending = false;
-  if (c->rhs_fixed) {
-    CK(cudaEventRecord(c->ev_fork, c->st));
-    CK(cudaStreamWaitEvent(c->side, c->ev_fork, 0));
-    launch_fixed_scales(c, c->side);
-    CK(cudaEventRecord(c->ev_join, c->side));
-    c->fx_pending = true;
-  }
+  // G^+ of the sampled Gram (K9's r x r part) on the auxiliary stream,
+  // overlapping the lookup and the RHS; joined before B = M G^+
+  CK(cudaEventRecord(c->ev_fork, c->st));
+  CK(cudaStreamWaitEvent(c->aux, c->ev_fork, 0));
+  k_solve_prep<<<1, kPrepThreads, prep_smem(r), c->aux>>>(r, c->sd, ctl);
+  CK_LAUNCH();
+  LAUNCHED(c, 1);
+  CK(cudaEventRecord(c->ev_join, c->aux));
   // K7: lookup of the sampled fibers
   {
     Phase ph(c, &c->stats.ms_lookup);
@@ -1626,11 +1705,6 @@ void solve_impl(cparls_ctx *c, int k, cparls_solve_info *info) {
       sj = c->seg_j;
       nseg_dev = &ctl->nseg;
     }
-    if (c->fx_on) {   // per-column fixed-point scales from the sample (kernels.cuh)
-      if (c->fx_pending) CK(cudaStreamWaitEvent(c->st, c->ev_join, 0));   // computed on the side stream
-      else launch_fixed_scales(c, c->st);
-      c->fx_pending = false;
-    }
     CK(cudaMemsetAsync(&c->dv->counter, 0, sizeof(unsigned long long), c->st));
     const int grid = 148 * grid_mult;
     const int64_t per_warp = 512;
@@ -1641,7 +1715,17 @@ void solve_impl(cparls_ctx *c, int k, cparls_solve_info *info) {
                                                      c->idx[k].out, (const VT *)c->idx[k].val, c->sw2, c->Z, r, ld,  \
                                                      c->M, per_warp, c->fx_scale, nseg_dev, ctl)
     KTimer kt(c, KT_RHS);
-    if (c->vf32) { if (r > 32) RHS(float, true); else RHS(float, false); }
+    const ModeIndex &ix = c->idx[k];
+    if (c->fx_on && ix.hot_n > 0 && r <= 32) {   // hot rows summed per CTA in shared memory
+      const size_t hsm = 8 * (size_t)ix.hot_n * r;
+#define RHS_HOT(VT)                                                                                               \
+  k_rhs_hot<VT><<<c->nsm, kRhsHotThreads, hsm, c->st>>>(soff, slo, sj, nseg_max, &c->dv->mk, &c->dv->counter,      \
+                                                     ix.out, (const VT *)ix.val, c->sw2, c->Z, r, ld, c->M,       \
+                                                     per_warp, c->fx_scale, ix.hot_slot, ix.hot_rows, ix.hot_n,  \
+                                                     nseg_dev, ctl)
+      if (c->vf32) RHS_HOT(float); else RHS_HOT(double);
+#undef RHS_HOT
+    } else if (c->vf32) { if (r > 32) RHS(float, true); else RHS(float, false); }
     else { if (r > 32) RHS(double, true); else RHS(double, false); }
     kt.stop();
 #undef RHS2
@@ -1651,10 +1735,6 @@ void solve_impl(cparls_ctx *c, int k, cparls_solve_info *info) {
     ph.end();
   }
   // K9: solve + normalize + leverage refresh
-  if (c->fx_pending) {   // side-stream scales not consumed (no atomic RHS ran): join before gpart is reused
-    CK(cudaStreamWaitEvent(c->st, c->ev_join, 0));
-    c->fx_pending = false;
-  }
   // sharded: the heavy rows' partial RHS rows summed over the ranks (plan_rows)
   if (c->world > 1 && !c->heavy[k].empty()) {
     const int64_t nh = (int64_t)c->heavy[k].size(), blk = nh * ld;
@@ -1674,8 +1754,7 @@ void solve_impl(cparls_ctx *c, int k, cparls_solve_info *info) {
   {
     Phase ph(c, &c->stats.ms_solve);
     {
-      k_solve_prep<<<1, 128, prep_smem(r), c->st>>>(r, c->sd, ctl);
-      CK_LAUNCH();
+      CK(cudaStreamWaitEvent(c->st, c->ev_join, 0));   // G^+ from the auxiliary stream
       const int64_t grid = row_grid(c, ceil_div(std::max<int64_t>(nown, 1), kRowThreads));
       CK(cudaMemsetAsync(&c->dv->touched, 0, sizeof(unsigned long long), c->st));
       KTimer kts(c, KT_SOLVE);
@@ -1690,9 +1769,11 @@ void solve_impl(cparls_ctx *c, int k, cparls_solve_info *info) {
       c->comm->allreduce_f64(c->sd->BtB, (size_t)r * r, c->st);
       c->comm->allreduce_u64(&c->dv->touched, 1, c->st);
     }
-    k_norm_prep<<<1, 128, prep_smem(r), c->st>>>(r, c->sd, c->md[k], ctl);
+    // (single GPU: the short-mode test reads every row of B)
+    k_norm_prep<<<1, kPrepThreads, prep_smem(r), c->st>>>(r, c->sd, c->md[k], ctl, c->A[k],
+                                                          c->world == 1 ? c->dims[k] : 0, ld);
     CK_LAUNCH();
-    LAUNCHED(c, 4);
+    LAUNCHED(c, 3);
     if (c->world > 1) lev_rows_sharded(c, k, c->sd->lambda);
     else lev_rows_and_cdf(c, k, c->sd->lambda);
     k_copy_lambda<<<1, 64, 0, c->st>>>(c->lam_model, c->sd->lambda, r, ctl);
@@ -1779,7 +1860,7 @@ void als_update_impl(cparls_ctx *c, int k) {
   CK_LAUNCH();
   ph.end();
   Phase ph2(c, &c->stats.ms_solve);
-  k_solve_prep<<<1, 128, prep_smem(r), c->st>>>(r, c->sd);
+  k_solve_prep<<<1, kPrepThreads, prep_smem(r), c->st>>>(r, c->sd);
   CK_LAUNCH();
   const int64_t grid = row_grid(c, ceil_div(std::max<int64_t>(nk, 1), kRowThreads));
   CK(cudaMemsetAsync(&c->dv->touched, 0, sizeof(unsigned long long), c->st));
@@ -1789,7 +1870,7 @@ void als_update_impl(cparls_ctx *c, int k) {
   CK_LAUNCH();
   k_pairs_reduce<<<pairs_reduce_grid(r), 256, 0, c->st>>>(c->gpart, grid, r, c->sd->BtB);
   CK_LAUNCH();
-  k_norm_prep<<<1, 128, prep_smem(r), c->st>>>(r, c->sd, c->md[k]);
+  k_norm_prep<<<1, kPrepThreads, prep_smem(r), c->st>>>(r, c->sd, c->md[k], nullptr, c->A[k], nk, ld);
   CK_LAUNCH();
   LAUNCHED(c, 8);
   lev_rows_and_cdf(c, k, c->sd->lambda);
@@ -2166,6 +2247,7 @@ void cparls_opts_init(cparls_opts *o) {
   o->tau = -1.0;
   o->world_size = 1;
   o->fit_mode = -1;
+  o->rhs_hot_rows = -1;
 }
 
 cparls_status cparls_create(cparls_ctx **out, int32_t nmodes, const int64_t *dims, int64_t nnz_local,
@@ -2228,10 +2310,10 @@ cparls_status cparls_create(cparls_ctx **out, int32_t nmodes, const int64_t *dim
       if (Nk >= 9223372036854775808.0L) throw ApiError(CPARLS_ERANGE, "prod_{m!=k} n_m >= 2^63");
     }
     set_kernel_attrs(c->r, c->ld);
-    CK(cudaHostAlloc(reinterpret_cast<void **>(&c->hscr), kHscrSlots * sizeof(long long), cudaHostAllocDefault));
-    CK(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithFlags(&c->aux, cudaStreamNonBlocking));
     CK(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
+    CK(cudaHostAlloc(reinterpret_cast<void **>(&c->hscr), kHscrSlots * sizeof(long long), cudaHostAllocDefault));
     c->dv = dalloc_t<DevScalars>(c, 1);
     c->ctl = dalloc_t<StepCtl>(c, 1);
     CK(cudaMemsetAsync(c->ctl, 0, sizeof(StepCtl), c->st));
@@ -2243,7 +2325,13 @@ cparls_status cparls_create(cparls_ctx **out, int32_t nmodes, const int64_t *dim
     c->lam_model = dalloc_t<double>(c, kMaxRank);
     c->ddpart = dalloc_t<dd>(c, 4096);
     c->gpart_blocks = 148 * 2;
+    {
+      int dev = 0;
+      CK(cudaGetDevice(&dev));
+      CK(cudaDeviceGetAttribute(&c->nsm, cudaDevAttrMultiProcessorCount, dev));
+    }
     c->gpart = dalloc_t<double>(c, c->gpart_blocks * (int64_t)c->r * c->r);
+    c->cpart = dalloc_t<double>(c, (kKrpBlocks + 1) * (int64_t)c->r);   // + the column sums
     c->Gtmp = dalloc_t<double>(c, kMaxRank * kMaxRank);
     c->tile_u64 = dalloc_t<uint64_t>(c, ceil_div(c->nmax, kLevThreads) + 1);
     c->i64part_cap = ceil_div(c->nmax, kScanTile) + 65536 + 64;   // also the SIDX window partials (<= acap / kSidxThreads)
@@ -2372,10 +2460,17 @@ cparls_status cparls_create(cparls_ctx **out, int32_t nmodes, const int64_t *dim
     c->stats.create_ms[1] = t_build - t_h2d;
     c->stats.create_ms[2] = t_aux - t_build;
     c->stats.create_ms[3] = since() - t_aux;
+    for (int k = 0; k < c->D && k < 8; ++k) {
+      c->stats.rhs_hot_rows[k] = c->idx[k].hot_n;
+      c->stats.rhs_hot_share[k] = c->idx[k].hot_share;
+    }
   });
   if (st != CPARLS_OK) {
     g_create_err = c->err;
     for (void *p : c->allocs) cudaFree(p);
+  if (c->ev_fork) cudaEventDestroy(c->ev_fork);
+  if (c->ev_join) cudaEventDestroy(c->ev_join);
+  if (c->aux) cudaStreamDestroy(c->aux);
     if (c->hscr) cudaFreeHost(c->hscr);
     if (c->hctl) cudaFreeHost(c->hctl);
     delete c->comm;
@@ -2392,11 +2487,11 @@ cparls_status cparls_destroy(cparls_ctx *c) {
   for (auto &p : c->ev_pending) { cudaEventDestroy(p.second.first); cudaEventDestroy(p.second.second); }
   for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
   for (void *p : c->allocs) cudaFree(p);
-  if (c->hscr) cudaFreeHost(c->hscr);
-  if (c->hctl) cudaFreeHost(c->hctl);
   if (c->ev_fork) cudaEventDestroy(c->ev_fork);
   if (c->ev_join) cudaEventDestroy(c->ev_join);
-  if (c->side) cudaStreamDestroy(c->side);
+  if (c->aux) cudaStreamDestroy(c->aux);
+  if (c->hscr) cudaFreeHost(c->hscr);
+  if (c->hctl) cudaFreeHost(c->hctl);
   for (int b = 0; b < 2; ++b) {
     if (c->stage[b]) cudaFreeHost(c->stage[b]);
     if (c->stage_ev[b]) cudaEventDestroy(c->stage_ev[b]);
@@ -2829,10 +2924,12 @@ cparls_status cparls_reset_stats(cparls_ctx *c) {
   if (!c) return CPARLS_EINVAL;
   return guarded(c, [&] {
     sync(c, false);   // a pending step's counters belong to the old stats
-    double cm[4];
-    std::memcpy(cm, c->stats.create_ms, sizeof(cm));
+    const cparls_stats keep = c->stats;
     c->stats = cparls_stats{};
-    std::memcpy(c->stats.create_ms, cm, sizeof(cm));   // create timings survive a reset
+    // create-time facts survive a reset
+    std::memcpy(c->stats.create_ms, keep.create_ms, sizeof(keep.create_ms));
+    std::memcpy(c->stats.rhs_hot_rows, keep.rhs_hot_rows, sizeof(keep.rhs_hot_rows));
+    std::memcpy(c->stats.rhs_hot_share, keep.rhs_hot_share, sizeof(keep.rhs_hot_share));
     c->ctl_seen = *reinterpret_cast<const StepCtl *>(c->hctl);
   });
 }

@@ -11,7 +11,8 @@ struct ModeDev {
   double alpha;            // max p~
   long long drawable;      // #{i : p~_i > 2^-63}  (rows whose integer weight q_i > 0)
   int rank;                // kept rank (AMB-11)
-  int tri;                 // 1: W upper triangular (Cholesky); 0: full (eigen)
+  int tri;                 // 1: W upper triangular (Cholesky); 0: full (eigen);
+                           // 2: l_i = 1 (nk < r rows, full row rank; W unused)
   double W[kMaxRank * kMaxRank];   // l_i = || a_i W ||^2
   double GA[kMaxRank * kMaxRank];  // Gram of the (normalized) factor
 };
@@ -38,9 +39,10 @@ __host__ __device__ constexpr int npairs(int r) { return r * (r + 1) / 2; }
 // rotations per round, A <- J^T A J, V <- V J), whole block.  a, V: shared
 // r x r (row stride r).  Eigenvalues end on diag(a), vectors in V's columns.
 // Convergence test as the oracle's: off^2 <= 1e-34 diag^2.
+constexpr int kPrepThreads = 256;     // block of the single-block r x r kernels (k_*_prep)
 constexpr double kCholSafe = 1e-6;   // Cholesky fast path only if every pivot > kCholSafe * max_diag
 
-__device__ void block_jacobi(int r, double *a, double *V) {
+__device__ int block_jacobi(int r, double *a, double *V) {   // returns the sweeps taken
   __shared__ double cs[kMaxRank / 2 + 1], sn[kMaxRank / 2 + 1];
   __shared__ int pp[kMaxRank / 2 + 1], qq[kMaxRank / 2 + 1];
   __shared__ int done;
@@ -48,14 +50,33 @@ __device__ void block_jacobi(int r, double *a, double *V) {
   const int H = R / 2;
   for (int i = threadIdx.x; i < r * r; i += blockDim.x) V[i] = (i / r == i % r) ? 1.0 : 0.0;
   __syncthreads();
-  for (int sweep = 0; sweep < 60; ++sweep) {
+  __shared__ double red_off[32], red_diag[32];
+  double prev_off = 0.0;
+  int sweep = 0;
+  for (; sweep < 60; ++sweep) {
+    // off / diag: squared off-diagonal (upper) and diagonal sums, block-wide
+    double off = 0.0, diag = 0.0;
+    for (int i = threadIdx.x; i < r * r; i += blockDim.x) {
+      const int p = i / r, q = i % r;
+      const double x = a[i];
+      if (p == q) diag += x * x;
+      else if (q > p) off += x * x;
+    }
+#pragma unroll
+    for (int m = 16; m >= 1; m >>= 1) {
+      off += __shfl_xor_sync(0xffffffffu, off, m);
+      diag += __shfl_xor_sync(0xffffffffu, diag, m);
+    }
+    if ((threadIdx.x & 31) == 0) { red_off[threadIdx.x >> 5] = off; red_diag[threadIdx.x >> 5] = diag; }
+    __syncthreads();
     if (threadIdx.x == 0) {
-      double off = 0.0, diag = 0.0;
-      for (int i = 0; i < r; ++i) {
-        diag += a[i * r + i] * a[i * r + i];
-        for (int j = i + 1; j < r; ++j) off += a[i * r + j] * a[i * r + j];
-      }
-      done = (off <= 1e-34 * diag || off == 0.0);
+      off = 0.0; diag = 0.0;
+      for (int w = 0; w < (int)(blockDim.x + 31) / 32; ++w) { off += red_off[w]; diag += red_diag[w]; }
+      // converged, or stagnating at the rounding floor (a rank-deficient G's
+      // null-space block keeps off ~ (eps |G|)^2 from reaching 1e-34 |G|^2;
+      // quadratic convergence otherwise cuts off far below a quarter per sweep)
+      done = (off <= 1e-34 * diag || off == 0.0 || (sweep > 0 && off <= 1e-26 * diag && off > 0.25 * prev_off));
+      prev_off = off;
     }
     __syncthreads();
     if (done) break;
@@ -67,44 +88,65 @@ __device__ void block_jacobi(int r, double *a, double *V) {
         int p = min(x, y), q = max(x, y);
         double c = 1.0, sv = 0.0;
         if (q < r) {
-          double apq = a[p * r + q];
+          const double apq = a[p * r + q];
           if (apq != 0.0) {
-            double theta = (a[q * r + q] - a[p * r + p]) / (2.0 * apq);
-            double tt = (theta >= 0 ? 1.0 : -1.0) / (fabs(theta) + sqrt(theta * theta + 1.0));
-            c = 1.0 / sqrt(tt * tt + 1.0);
+            // t = tan of the angle zeroing a_pq: sgn(theta) / (|theta| + sqrt(theta^2 + 1))
+            // with theta = d / (2 a_pq), d = a_qq - a_pp, as 2 a_pq sgn(d) / (|d| +
+            // sqrt(d^2 + 4 a_pq^2)): one division and one square root
+            const double d = a[q * r + q] - a[p * r + p], two = 2.0 * apq;
+            const double tt = (d >= 0.0 ? two : -two) / (fabs(d) + sqrt(fma(d, d, two * two)));
+            c = rsqrt(fma(tt, tt, 1.0));
             sv = tt * c;
           }
         }
         pp[i] = p; qq[i] = q; cs[i] = c; sn[i] = sv;
       }
       __syncthreads();
-      for (int idx = threadIdx.x; idx < H * r; idx += blockDim.x) {   // rows: J^T A
-        int i = idx / r, k = idx % r;
-        int p = pp[i], q = qq[i];
-        if (q < r && sn[i] != 0.0) {
-          double c = cs[i], sv = sn[i];
-          double apk = a[p * r + k], aqk = a[q * r + k];
-          a[p * r + k] = c * apk - sv * aqk;
-          a[q * r + k] = sv * apk + c * aqk;
-        }
-      }
-      __syncthreads();
-      for (int idx = threadIdx.x; idx < H * r; idx += blockDim.x) {   // columns: A J, V J
-        int i = idx / r, k = idx % r;
-        int p = pp[i], q = qq[i];
-        if (q < r && sn[i] != 0.0) {
-          double c = cs[i], sv = sn[i];
-          double akp = a[k * r + p], akq = a[k * r + q];
-          a[k * r + p] = c * akp - sv * akq;
-          a[k * r + q] = sv * akp + c * akq;
-          double vkp = V[k * r + p], vkq = V[k * r + q];
-          V[k * r + p] = c * vkp - sv * vkq;
-          V[k * r + q] = sv * vkp + c * vkq;
+      // A <- J^T A J as independent 2x2 blocks (rows {p_i, q_i} x columns
+      // {p_j, q_j}: row rotation i, then column rotation j, the same
+      // operations as a row pass followed by a column pass) and V <- V J:
+      // one pass, one barrier per round
+      const int nblk = H * H;
+      for (int idx = threadIdx.x; idx < nblk + H * r; idx += blockDim.x) {
+        if (idx < nblk) {
+          const int i = idx / H, j = idx - i * H;
+          const int pi = pp[i], qi = qq[i], pj = pp[j], qj = qq[j];
+          const bool vi = qi < r, vj = qj < r;   // q = r: the dummy of an odd r
+          const bool ri = vi && sn[i] != 0.0, rj = vj && sn[j] != 0.0;
+          if (!ri && !rj) continue;
+          double x00 = a[pi * r + pj], x01 = vj ? a[pi * r + qj] : 0.0;
+          double x10 = vi ? a[qi * r + pj] : 0.0, x11 = vi && vj ? a[qi * r + qj] : 0.0;
+          if (ri) {
+            const double c = cs[i], sv = sn[i];
+            const double y00 = c * x00 - sv * x10, y10 = sv * x00 + c * x10;
+            const double y01 = c * x01 - sv * x11, y11 = sv * x01 + c * x11;
+            x00 = y00; x10 = y10; x01 = y01; x11 = y11;
+          }
+          if (rj) {
+            const double c = cs[j], sv = sn[j];
+            const double y00 = c * x00 - sv * x01, y01 = sv * x00 + c * x01;
+            const double y10 = c * x10 - sv * x11, y11 = sv * x10 + c * x11;
+            x00 = y00; x01 = y01; x10 = y10; x11 = y11;
+          }
+          a[pi * r + pj] = x00;
+          if (vj) a[pi * r + qj] = x01;
+          if (vi) a[qi * r + pj] = x10;
+          if (vi && vj) a[qi * r + qj] = x11;
+        } else {
+          const int t2 = idx - nblk, j = t2 / r, k = t2 - j * r;
+          const int p = pp[j], q = qq[j];
+          if (q < r && sn[j] != 0.0) {
+            const double c = cs[j], sv = sn[j];
+            const double vkp = V[k * r + p], vkq = V[k * r + q];
+            V[k * r + p] = c * vkp - sv * vkq;
+            V[k * r + q] = sv * vkp + c * vkq;
+          }
         }
       }
       __syncthreads();
     }
   }
+  return sweep;
 }
 
 // Cholesky G = L L^T in shared memory.  Fast path of G^+ only: accepted when
@@ -169,17 +211,125 @@ __device__ void block_tri_inverse(int r, const double *L, double *Linv) {
   }
 }
 
+// Block Cholesky + lower-triangular inverse for r <= 32 with kPrepThreads =
+// 256 threads as 32 columns x 8 row groups (thread (c, g) owns column c of
+// rows g, g+8, g+16, g+24): no index division, every thread takes the pivot's
+// square root itself (no serial section), each step's loads are issued before
+// its stores, two barriers per step.  The same operations in the same order
+// as block_cholesky + block_tri_inverse (entry (i,l) receives L(i,j) L(l,j)
+// for j = 0, 1, ...; Linv(l,c) its subtractions q = 0, 1, ...), so the
+// results are bit-identical.  G: r x r (row stride r); L, Linv: shared.
+// Returns 1 on success; 0 when a pivot fails kCholSafe (eigen path).
+__device__ int block_chol_inv32(int r, const double *G, double *L, double *Linv) {
+  const int c = threadIdx.x & 31, g = threadIdx.x >> 5;
+  double maxd = 0.0;
+  for (int j = 0; j < r; ++j) maxd = fmax(maxd, G[j * r + j]);
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const int i = g + 8 * k;
+    if (i < r && c < r) {
+      L[i * r + c] = c <= i ? G[i * r + c] : 0.0;
+      Linv[i * r + c] = i == c ? 1.0 : 0.0;
+    }
+  }
+  __syncthreads();
+  if (!(maxd > 0.0)) return 0;
+  for (int j = 0; j < r; ++j) {
+    __syncthreads();   // the previous step's trailing update is visible
+    const double dj = L[j * r + j];
+    if (!(dj > kCholSafe * maxd)) return 0;   // block-uniform
+    const double ljj = sqrt(dj);
+    if (g == 0 && c > j && c < r) L[c * r + j] = L[c * r + j] / ljj;
+    __syncthreads();
+    if (g == 0 && c == j) L[j * r + j] = ljj;   // nobody reads L(j,j) in this phase
+    if (c > j && c < r) {   // column c of the trailing rows i >= c
+      const double lcj = L[c * r + j];
+      double lij[4], cur[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int i = g + 8 * k;
+        const bool on = i >= c && i < r;
+        lij[k] = on ? L[i * r + j] : 0.0;
+        cur[k] = on ? L[i * r + c] : 0.0;
+      }
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int i = g + 8 * k;
+        if (i >= c && i < r) L[i * r + c] = cur[k] - lij[k] * lcj;
+      }
+    }
+  }
+  __syncthreads();
+  // L^{-1} by rows: row i divided by L(i,i), then subtracted from the rows below
+  for (int i = 0; i < r; ++i) {
+    const double lii = L[i * r + i];
+    if (g == 0 && c <= i) Linv[i * r + c] = Linv[i * r + c] / lii;
+    __syncthreads();
+    if (c <= i) {
+      const double xic = Linv[i * r + c];
+      double lli[4], cur[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int l = g + 8 * k;
+        const bool on = l > i && l < r;
+        lli[k] = on ? L[l * r + i] : 0.0;
+        cur[k] = on ? Linv[l * r + c] : 0.0;
+      }
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int l = g + 8 * k;
+        if (l > i && l < r) Linv[l * r + c] = cur[k] - lli[k] * xic;
+      }
+    }
+    __syncthreads();
+  }
+  return 1;
+}
+
+// Cholesky + inverse of the factor, whole block: Li = L^{-1} (row stride r)
+// in shared memory; the warp version for r <= 32.  Returns 1 on success.
+__device__ int block_chol_inv(int r, const double *G, double *L, double *Li, int *ok_flag) {
+  if (r <= 32 && blockDim.x == kPrepThreads) return block_chol_inv32(r, G, L, Li);
+  if (!block_cholesky(r, G, L, ok_flag)) return 0;
+  block_tri_inverse(r, L, Li);
+  return 1;
+}
+
 // Leverage preparation from Gram G (r x r, global): W with l_i = ||a_i W||^2.
 // Cholesky: W = L^{-T} (upper triangular).  Fallback: W = V_kept diag(mu^{-1/2}).
-__device__ void lev_prep_body(int r, const double *Gg, ModeDev *md) {
+// nk < r (fewer rows than columns, e.g. C2's 24-row mode at r = 25): when the
+// rows a_i = A(i,:) / lam (lam null: 1) are linearly independent -- the nk x nk
+// Gram A A^T passes the Cholesky test -- the hat matrix A (A^T A)^+ A^T is the
+// identity, so l_i = 1 and rank = nk exactly (AMB-11, the eigen cutoff keeps the
+// nk nonzero eigenvalues A^T A shares with A A^T); tri = 2 tells the leverage
+// pass.  Saves the r x r Jacobi of the rank-deficient Gram.
+__device__ bool short_full_row_rank(int r, const double *A, const double *lam, int64_t nk, int ld, double *H,
+                                    double *scratch, int *ok) {
+  if (!A || nk <= 0 || nk >= r || nk > 32) return false;
+  const int n = (int)nk;
+  for (int i = threadIdx.x; i < n * n; i += blockDim.x) {
+    const int p = i / n, q = i % n;
+    double h = 0.0;
+    for (int c = 0; c < r; ++c) {
+      const double ap = lam ? A[p * (int64_t)ld + c] / lam[c] : A[p * (int64_t)ld + c];
+      const double aq = lam ? A[q * (int64_t)ld + c] / lam[c] : A[q * (int64_t)ld + c];
+      h += ap * aq;
+    }
+    H[i] = h;
+  }
+  __syncthreads();
+  return block_cholesky(n, H, scratch, ok) != 0;
+}
+
+__device__ void lev_prep_body(int r, const double *Gg, ModeDev *md, const double *A = nullptr,
+                              const double *lam = nullptr, int64_t nk = 0, int ld = 0) {
   extern __shared__ double sm[];
   double *G = sm, *L = sm + r * r, *Li = sm + 2 * r * r;
   __shared__ int ok;
   for (int i = threadIdx.x; i < r * r; i += blockDim.x) { G[i] = Gg[i]; md->GA[i] = Gg[i]; }
   __syncthreads();
-  int good = block_cholesky(r, G, L, &ok);
+  int good = block_chol_inv(r, G, L, Li, &ok);
   if (good) {
-    block_tri_inverse(r, L, Li);
     // W = Li^T : W[p][c] = Li[c][p]
     for (int i = threadIdx.x; i < r * r; i += blockDim.x) {
       int p = i / r, c = i % r;
@@ -188,8 +338,13 @@ __device__ void lev_prep_body(int r, const double *Gg, ModeDev *md) {
     if (threadIdx.x == 0) { md->tri = 1; md->rank = r; }
     return;
   }
+  if (short_full_row_rank(r, A, lam, nk, ld, L, Li, &ok)) {
+    if (threadIdx.x == 0) { md->tri = 2; md->rank = (int)nk; }
+    return;
+  }
   // eigen fallback (AMB-11): W = V_kept diag(mu^{-1/2})
   double *a = L, *V = Li;
+  __syncthreads();
   for (int i = threadIdx.x; i < r * r; i += blockDim.x) a[i] = G[i];
   __syncthreads();
   block_jacobi(r, a, V);
@@ -213,7 +368,10 @@ __device__ void lev_prep_body(int r, const double *Gg, ModeDev *md) {
   if (threadIdx.x == 0) { md->tri = 0; md->rank = rank_s; }
 }
 
-__global__ void k_lev_prep(int r, const double *G, ModeDev *md) { lev_prep_body(r, G, md); }
+__global__ void k_lev_prep(int r, const double *G, ModeDev *md, const double *A = nullptr, int64_t nk = 0,
+                           int ld = 0) {
+  lev_prep_body(r, G, md, A, nullptr, nk, ld);
+}
 
 // ======================================================================
 // K1/K2: leverage rows -> p~ -> integer weights q (CDF pass 1)
@@ -316,6 +474,7 @@ struct OtherModes {
   const double *A[kMaxModes];
   uint64_t mult[kMaxModes];   // prod_{l<j} n_l
   const ModeDev *md[kMaxModes];   // alpha and drawable counts of the other modes (device)
+  FastDiv div[kMaxModes];     // division by n[j] (key decoding)
 };
 
 // max p~ of other mode l, read on the device
@@ -648,6 +807,7 @@ struct KeyRemap {
   int identity;
   int64_t n[kMaxModes];       // canonical order dims
   uint64_t cmult[kMaxModes];  // multiplier of canonical digit j in the copy's key
+  FastDiv div[kMaxModes];     // division by n[j]
 };
 
 __global__ void k_lookup(const uint64_t *__restrict__ skey, int64_t sbar, const uint64_t *__restrict__ keys,
@@ -662,8 +822,9 @@ __global__ void k_lookup(const uint64_t *__restrict__ skey, int64_t sbar, const 
   if (!rm.identity) {
     uint64_t t = k, kk = 0;
     for (int m = 0; m < rm.d; ++m) {
-      const uint64_t q = t / (uint64_t)rm.n[m];
-      kk += (t - q * (uint64_t)rm.n[m]) * rm.cmult[m];
+      uint64_t rem;
+      const uint64_t q = fastdivmod(t, rm.div[m], rem);
+      kk += rem * rm.cmult[m];
       t = q;
     }
     k = kk;
@@ -704,9 +865,9 @@ __global__ void k_solve_prep(int r, SolveDev *sd, const StepCtl *ctl = nullptr) 
   __shared__ int ok;
   for (int i = threadIdx.x; i < r * r; i += blockDim.x) G[i] = sd->G[i];
   __syncthreads();
-  int good = block_cholesky(r, G, L, &ok);
+  int good = block_chol_inv(r, G, L, Li, &ok);
   if (good) {
-    block_tri_inverse(r, L, Li);
+    __syncthreads();
     // Ginv = Li^T Li
     for (int i = threadIdx.x; i < r * r; i += blockDim.x) {
       int p = i / r, q = i % r;
@@ -748,7 +909,8 @@ __global__ void k_solve_prep(int r, SolveDev *sd, const StepCtl *ctl = nullptr) 
 
 // lambda_c = ||B(:,c)||, G_A = B^T B / (lambda lambda^T), then the
 // leverage preparation of the normalized factor.
-__global__ void k_norm_prep(int r, SolveDev *sd, ModeDev *md, const StepCtl *ctl = nullptr) {
+__global__ void k_norm_prep(int r, SolveDev *sd, ModeDev *md, const StepCtl *ctl = nullptr,
+                            const double *B = nullptr, int64_t nk = 0, int ld = 0) {
   CPARLS_GUARD(ctl);
   extern __shared__ double sm[];
   double *GA = sm + 3 * r * r;   // beyond lev_prep's scratch
@@ -760,7 +922,7 @@ __global__ void k_norm_prep(int r, SolveDev *sd, ModeDev *md, const StepCtl *ctl
     GA[i] = (lp > 0.0 && lq > 0.0) ? (sd->BtB[i] / lp) / lq : 0.0;
   }
   __syncthreads();
-  lev_prep_body(r, GA, md);
+  lev_prep_body(r, GA, md, B, sd->lambda, nk, ld);
 }
 
 // ======================================================================
@@ -955,63 +1117,79 @@ __global__ void k_sample_permute(const uint32_t *__restrict__ perm, int64_t n, c
 // integer sums (order-free, so the RHS is bit-reproducible) at a resolution of
 // 2^-60 U_c, and 64-bit integer reductions run ~15% faster than fp64 ones
 // (libcparls_peaks.so: 635 vs ~550 G lane-ops/s on this pattern).
-__global__ void k_colabs_part(const double *__restrict__ Z, const double *__restrict__ sw2, int64_t sbar, int r,
-                              int ld, double *__restrict__ part /* gridDim.x x r */,
-                              const int64_t *sbar_dev = nullptr, const StepCtl *ctl = nullptr) {
-  CPARLS_GUARD(ctl);
-  sbar = dcount(sbar, sbar_dev);
-  const int c = threadIdx.x & 63;
-  double s = 0.0;
-  if (c < r) {
-    // 4 rows per thread per step in flight (the loop is load-latency bound)
-    const int64_t stride = (int64_t)gridDim.x * (blockDim.x >> 6);
-    int64_t j = (int64_t)blockIdx.x * (blockDim.x >> 6) + (threadIdx.x >> 6);
-    for (; j + 3 * stride < sbar; j += 4 * stride) {
-      const double a0 = sw2[j] * fabs(Z[j * ld + c]), a1 = sw2[j + stride] * fabs(Z[(j + stride) * ld + c]);
-      const double a2 = sw2[j + 2 * stride] * fabs(Z[(j + 2 * stride) * ld + c]);
-      const double a3 = sw2[j + 3 * stride] * fabs(Z[(j + 3 * stride) * ld + c]);
-      s += a0 + a1 + a2 + a3;
-    }
-    for (; j < sbar; j += stride) s += sw2[j] * fabs(Z[j * ld + c]);
-  }
-  __shared__ double red[256];
-  red[threadIdx.x] = s;
-  __syncthreads();
-  if (threadIdx.x < 64) {
-    double t = 0.0;
-    for (int g = 0; g < (int)(blockDim.x >> 6); ++g) t += red[g * 64 + threadIdx.x];
-    if (threadIdx.x < r) part[(int64_t)blockIdx.x * r + threadIdx.x] = t;
-  }
-}
+// The column sums sum_j w_j^2 |z_jc| come per block from k_krp_rows (k_gram_scales).
 
-// scale[c] = 2^e_c, scale[kMaxRank + c] = 2^-e_c (exact powers of two)
-__global__ void k_fixed_scales(const double *__restrict__ part, int nb, int r, const double *maxabs, double dupmax,
-                               double *__restrict__ scale, const StepCtl *ctl = nullptr) {
+// K6 epilogue, one launch: the sampled Gram from k_gram_rows_t's block
+// partials (warp per upper entry, double-double, as k_pairs_reduce) and the
+// per-column fixed-point scales from k_krp_rows' column-sum partials (warp per
+// column; the last block to finish derives the scales from all columns).
+// scale[c] = 2^e_c, scale[kMaxRank + c] = 2^-e_c (exact powers of two),
+// scale[2 kMaxRank] = 1 for fixed point, 0 when this step falls back to fp64
+// reductions (k_rhs and k_solve_rows_t read the flag).
+__global__ void k_gram_scales(const double *__restrict__ part, const double *__restrict__ cpart, int64_t nb,
+                              int64_t nbc, int r,
+                              double *__restrict__ G, double *__restrict__ colsum, const double *maxabs,
+                              double dupmax, double *__restrict__ scale, unsigned int *done_count,
+                              const StepCtl *ctl = nullptr) {
   CPARLS_GUARD(ctl);
+  const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  const int64_t rr = (int64_t)r * r;
+  if (w < rr) {
+    const int p = (int)(w / r), q = (int)(w % r);
+    if (p <= q) {
+      dd sum = {0.0, 0.0};
+      for (int64_t b = lane; b < nb; b += 32) sum = dd_add_d(sum, part[b * rr + w]);
+      sum = warp_sum_dd(sum);
+      if (lane == 0) {
+        const double v = sum.hi + sum.lo;
+        G[p * r + q] = v;
+        G[q * r + p] = v;
+      }
+    }
+  } else if (w < rr + r) {
+    const int c = (int)(w - rr);
+    double u = 0.0;
+    for (int64_t b = lane; b < nbc; b += 32) u += cpart[b * r + c];
+    u = warp_sum<double>(u);
+    if (lane == 0) colsum[c] = u;
+  }
+  // last block: the scales from every column's sum
+  __shared__ int last;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = atomicAdd(done_count, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  __shared__ int ok_all;
+  if (threadIdx.x == 0) ok_all = 1;
+  __syncthreads();
   const int c = threadIdx.x;
   int e = 0;
-  bool ok = true;
   if (c < r) {
-    double u = 0.0;
-    for (int b = 0; b < nb; ++b) u += part[(int64_t)b * r + c];
-    u *= *maxabs * dupmax;
-    if (!(u < INFINITY)) ok = false;   // inf / NaN bound
+    const double u = __ldcg(colsum + c) * *maxabs * dupmax;
+    if (!(u < INFINITY)) atomicAnd(&ok_all, 0);   // inf / NaN bound
     else if (u > 0.0) {
       int ex;
       frexp(u, &ex);              // u < 2^ex
       e = 60 - ex;
-      if (e < -960 || e > 960) ok = false;   // 2^e_c or the terms' quanta out of range
+      if (e < -960 || e > 960) atomicAnd(&ok_all, 0);   // 2^e_c or the terms' quanta out of range
     }
   }
-  ok = __syncthreads_and(ok);
+  __syncthreads();
+  const bool ok = ok_all != 0;
   if (c < r) {
     scale[c] = ok ? ldexp(1.0, e) : 1.0;
     scale[kMaxRank + c] = ok ? ldexp(1.0, -e) : 1.0;
   }
-  // scale[2 kMaxRank]: 1 = fixed point, 0 = this step falls back to fp64
-  // reductions (k_rhs and k_solve_rows_t read the flag)
-  if (c == 0) scale[2 * kMaxRank] = ok ? 1.0 : 0.0;
+  if (c == 0) {
+    scale[2 * kMaxRank] = ok ? 1.0 : 0.0;
+    *done_count = 0u;   // ready for the next launch (stream-ordered)
+  }
 }
+
+inline unsigned gram_scales_grid(int r) { return (unsigned)ceil_div(((int64_t)r * r + r) * 32, 256); }
 
 // longest run of equal (key, out) in a sorted copy (duplicate coordinates)
 __global__ void k_dup_runs(const uint64_t *__restrict__ key, const int32_t *__restrict__ out, int64_t nnz,

@@ -80,12 +80,21 @@ __device__ __forceinline__ void store_rows_v(double *__restrict__ dst, int rows,
 }
 
 // ---------------------------------------------------------------- factor Gram
+// Block partials of sum_i w_i a_i a_i^T over the rows of A (w = null: unit
+// weights): the factor Gram, and the sampled Gram Z^T diag(w^2) Z (P:683,
+// P:900-901) with n = s_bar read on the device.
 template <int RMAX>
 __global__ void __launch_bounds__(kRowThreads) k_gram_rows_t(const double *__restrict__ A, int64_t n, int r, int ld,
-                                                            double *__restrict__ part) {
+                                                            double *__restrict__ part,
+                                                            const double *__restrict__ w = nullptr,
+                                                            const int64_t *n_dev = nullptr,
+                                                            const StepCtl *ctl = nullptr) {
+  CPARLS_GUARD(ctl);
+  n = dcount(n, n_dev);
   extern __shared__ double smem[];
   const int S = ld + 1;
   double *tile = smem;
+  double *wt = smem + kRowThreads * S;
   Syrk<RMAX> sy;
   sy.init(r);
   const int64_t ntiles = ceil_div(n, kRowThreads);
@@ -94,8 +103,9 @@ __global__ void __launch_bounds__(kRowThreads) k_gram_rows_t(const double *__res
     const int rows = (int)min((int64_t)kRowThreads, n - base);
     __syncthreads();
     stage_rows(A + base * ld, rows, ld, tile, S);
+    if (w && (int)threadIdx.x < rows) wt[threadIdx.x] = w[base + threadIdx.x];
     __syncthreads();
-    sy.accumulate(tile, rows, S, nullptr);
+    sy.accumulate(tile, rows, S, w ? wt : nullptr);
   }
   __syncthreads();
   sy.finish(r, smem, part + (int64_t)blockIdx.x * r * r);
@@ -255,6 +265,7 @@ __device__ __forceinline__ void warp_store(double *__restrict__ dst, int rows, i
 // and the fused solve + leverage pass, so both give the same bits.
 template <int RMAX>
 __device__ __forceinline__ double lev_of_row(const double *x, int r, const double *W, int tri, int rank) {
+  if (tri == 2) return 1.0 / (double)rank;   // full row rank, nk < r: the hat matrix is I
   double a[RMAX];
 #pragma unroll
   for (int c = 0; c < RMAX; c += 2) {
@@ -316,7 +327,7 @@ __global__ void __launch_bounds__(kRowThreads, CPARLS_LEV_MINB) k_lev_rows_w(dou
   const int tri = md->tri, rank = md->rank;
   for (int i = threadIdx.x; i < RMAX * RMAX; i += blockDim.x) {
     const int k = i / RMAX, c = i - k * RMAX;
-    W[i] = (k < r && c < r && (!tri || k <= c)) ? md->W[k * r + c] : 0.0;
+    W[i] = (k < r && c < r && tri < 2 && (!tri || k <= c)) ? md->W[k * r + c] : 0.0;
   }
   // 1 / lambda_c (0 for a zero column): one multiply per element instead of a division
   for (int i = threadIdx.x; i < RMAX; i += blockDim.x)
@@ -488,77 +499,83 @@ __global__ void __launch_bounds__(kRowThreads, CPARLS_SOLVE_MINB) k_solve_dmma(d
 }
 
 
-// ---------------------------------------------------------------- KrpSamp + Gram
-// z_j = A_{m_1}(i_1,:) * ... * A_{m_d}(i_d,:) (eq:Zrow P:214, left to right),
-// Z (s_bar x ld, padding zero) and the block partial of sum_j w_j^2 z_j z_j^T.
-template <int RMAX>
-__global__ void __launch_bounds__(kRowThreads) k_krp_gram_t(const uint64_t *__restrict__ skey,
-                                                           const double *__restrict__ sw2, int64_t sbar,
-                                                           OtherModes om, int r, int ld, double *__restrict__ Z,
-                                                           double *__restrict__ part,
-                                                           const int64_t *sbar_dev = nullptr,
-                                                           const StepCtl *ctl = nullptr,
-                                                           const double *__restrict__ zg = nullptr) {
+// ---------------------------------------------------------------- KrpSamp
+// z_j = A_{m_1}(i_1,:) * ... * A_{m_d}(i_d,:) (eq:Zrow P:214, left to right)
+// into Z (s_bar x ld, padding zero), and the block partial of the column sums
+// sum_j w_j^2 |z_j| (fixed-point RHS scales, k_gram_scales).  A warp forms QR
+// rows at once: all QR x d index decodes first, then all QR x d row loads in
+// flight together, then the products (DM >= d modes, unrolled).  Low register
+// use, so 64 warps per SM hide the gather latency; the sampled Gram
+// sum_j w_j^2 z_j z_j^T is a separate streaming pass over Z (k_gram_rows_t).
+constexpr int kKrpThreads = 256;
+constexpr int kKrpBlocks = 148 * 4;   // upper bound of k_krp_rows' grid (cpart partials)
+
+template <int DM, int QR, bool HI>
+__global__ void __launch_bounds__(kKrpThreads, DM * QR > 8 ? 3 : 4) k_krp_rows(const uint64_t *__restrict__ skey,
+                                                         const double *__restrict__ sw2, int64_t sbar,
+                                                         OtherModes om, int r, int ld, double *__restrict__ Z,
+                                                         double *__restrict__ cpart, const int64_t *sbar_dev,
+                                                         const StepCtl *ctl, const double *__restrict__ zg) {
   CPARLS_GUARD(ctl);
   sbar = dcount(sbar, sbar_dev);
-  extern __shared__ double smem[];
-  const int S = ld + 1;
-  double *tile = smem;
-  double *wt = smem + kRowThreads * S;
+  __shared__ double cabs_red[kKrpThreads / 32][64];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  Syrk<RMAX> sy;
-  sy.init(r);
-  const int64_t ntiles = ceil_div(sbar, kRowThreads);
-  for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
-    const int64_t base = t * kRowThreads;
-    const int rows = (int)min((int64_t)kRowThreads, sbar - base);
-    __syncthreads();
-    // a warp forms 4 rows per step: their key decodes and factor-row loads
-    // are independent, so 4 gathers per mode are in flight at once
-    constexpr int QR = 4;
-    for (int jj0 = w * QR; jj0 < rows; jj0 += (kRowThreads / 32) * QR) {
-      uint64_t key[QR];
-      double z0[QR], z1[QR];
+  const int64_t nw = (int64_t)gridDim.x * (kKrpThreads / 32);
+  double ca0 = 0.0, ca1 = 0.0;   // this lane's column sums of w^2 |z|
+  const int d = om.d;
+  for (int64_t j0 = ((int64_t)blockIdx.x * (kKrpThreads / 32) + w) * QR; j0 < sbar; j0 += nw * QR) {
+    const double *rowp[QR][DM];
 #pragma unroll
-      for (int q = 0; q < QR; ++q) {
-        key[q] = jj0 + q < rows ? skey[base + jj0 + q] : 0ull;
-        z0[q] = z1[q] = 1.0;
-      }
-      for (int m = 0; m < om.d; ++m) {
-        double a0[QR], a1[QR];
+    for (int q = 0; q < QR; ++q) {
+      const int64_t j = min(j0 + q, sbar - 1);
+      uint64_t key = skey[j];
 #pragma unroll
-        for (int q = 0; q < QR; ++q) {
-          const uint64_t i = key[q] % (uint64_t)om.n[m];
-          key[q] /= (uint64_t)om.n[m];
+      for (int m = 0; m < DM; ++m) {
+        if (m < d) {
+          uint64_t i;
+          key = fastdivmod(key, om.div[m], i);
           // sharded run: the rows come from their owners (zg, sample-major, d rows per sample)
-          const int64_t jz = jj0 + q < rows ? base + jj0 + q : 0;
-          const double *row = zg ? zg + (jz * (int64_t)om.d + m) * ld : om.A[m] + i * ld;
-          a0[q] = lane < r ? __ldg(row + lane) : 0.0;
-          a1[q] = lane + 32 < r ? __ldg(row + lane + 32) : 0.0;
-        }
-#pragma unroll
-        for (int q = 0; q < QR; ++q) {
-          z0[q] = (m == 0) ? a0[q] : z0[q] * a0[q];
-          z1[q] = (m == 0) ? a1[q] : z1[q] * a1[q];
-        }
-      }
-#pragma unroll
-      for (int q = 0; q < QR; ++q) {
-        const int jj = jj0 + q;
-        if (jj < rows) {
-          double *x = tile + jj * S;
-          if (lane < ld) x[lane] = lane < r ? z0[q] : 0.0;
-          if (lane + 32 < ld) x[lane + 32] = lane + 32 < r ? z1[q] : 0.0;
-          if (lane == 0) wt[jj] = sw2[base + jj];
+          rowp[q][m] = zg ? zg + (j * (int64_t)d + m) * ld : om.A[m] + i * ld;
         }
       }
     }
-    __syncthreads();
-    store_rows(Z + base * ld, rows, ld, tile, S);
-    sy.accumulate(tile, rows, S, wt);
+    double a0[QR][DM], a1[QR][HI ? DM : 1];
+#pragma unroll
+    for (int q = 0; q < QR; ++q)
+#pragma unroll
+      for (int m = 0; m < DM; ++m) {
+        a0[q][m] = m < d && lane < r ? __ldg(rowp[q][m] + lane) : 1.0;
+        if (HI) a1[q][HI ? m : 0] = m < d && lane + 32 < r ? __ldg(rowp[q][m] + lane + 32) : 1.0;
+      }
+#pragma unroll
+    for (int q = 0; q < QR; ++q) {
+      const int64_t j = j0 + q;
+      if (j >= sbar) break;
+      double z0 = a0[q][0], z1 = HI ? a1[q][0] : 0.0;
+#pragma unroll
+      for (int m = 1; m < DM; ++m)
+        if (m < d) { z0 *= a0[q][m]; if (HI) z1 *= a1[q][HI ? m : 0]; }
+      z0 = lane < r ? z0 : 0.0;
+      z1 = lane + 32 < r ? z1 : 0.0;
+      if (lane < ld) Z[j * ld + lane] = z0;
+      if (lane + 32 < ld) Z[j * ld + lane + 32] = z1;
+      if (cpart) {
+        const double wq = __ldg(sw2 + j);
+        ca0 += wq * fabs(z0);
+        ca1 += wq * fabs(z1);
+      }
+    }
   }
-  __syncthreads();
-  sy.finish(r, smem, part + (int64_t)blockIdx.x * r * r);
+  if (cpart) {   // block partial of sum_j w_j^2 |z_j| per column, warps in order
+    cabs_red[w][lane] = ca0;
+    cabs_red[w][lane + 32] = ca1;
+    __syncthreads();
+    if (threadIdx.x < r) {
+      double t = 0.0;
+      for (int g = 0; g < kKrpThreads / 32; ++g) t += cabs_red[g][threadIdx.x];
+      cpart[(int64_t)blockIdx.x * r + threadIdx.x] = t;
+    }
+  }
 }
 
 }  // namespace cparls

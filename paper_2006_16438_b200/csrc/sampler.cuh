@@ -279,8 +279,8 @@ __global__ void k_owned_rows(const uint64_t *__restrict__ skey, int64_t smax, co
        j += ((int64_t)gridDim.x * blockDim.x) >> 5) {
     uint64_t key = j < sbar ? skey[j] : 0ull;
     for (int m = 0; m < om.d; ++m) {
-      const uint64_t i = key % (uint64_t)om.n[m];
-      key /= (uint64_t)om.n[m];
+      uint64_t i;
+      key = fastdivmod(key, om.div[m], i);
       const int mode = om.mode[m];
       const bool own = j < sbar && (int64_t)i >= row_lo[mode] && (int64_t)i < row_hi[mode];
       double *dst = zg + (j * (int64_t)om.d + m) * ld;

@@ -230,3 +230,80 @@ def test_run_recovers_aborted_steps_with_the_host_sampler():
             o.set_factor(m, g.get_factor(m)[0])
             o.set_ptilde(m, g.get_ptilde(m))
         _step_lockstep(g, o, k, cfg.s, 1e-6, 9, k)
+
+
+# ---------------------------------------------------------------- hot-row RHS
+@pytest.mark.parametrize("name,hot", [("C1", -1), ("C1", 7), ("C2", -1), ("C2", 100), ("C3", -1)])
+def test_hot_row_rhs_is_bit_identical(name, hot):
+    """The fixed-point RHS with the hot rows summed per CTA in shared memory
+    (rhs.cuh k_rhs_hot; two 32-bit words with exact carries) gives the same
+    int64 sums as the plain L2 reductions, so the run's factors, p~ and fit
+    trace are bit-identical with and without it.  hot = -1: automatic (every
+    row hot on C1 and C2's small modes: slot = row); 7 / 100: a capped hot set
+    (hot_slot table, hot and cold entries mixed in every warp)."""
+    need_gpu()
+    from paper_2006_16438_b200 import Cparls
+    T = synth.make(name) if name == "C1" else synth.make(name, device="cuda")
+    cfg = T.cfg
+    a = Cparls(T.dims, T.coords.cuda(), T.vals.cuda(), cfg.rank, rhs_hot_rows=hot)
+    b = Cparls(T.dims, T.coords.cuda(), T.vals.cuda(), cfg.rank, rhs_hot_rows=0)
+    sa, sb = a.stats(), b.stats()
+    D = len(T.dims)
+    assert all(n == 0 for n in sb["rhs_hot_rows"])
+    used = [n for n in sa["rhs_hot_rows"][:D]]
+    assert any(n > 0 for n in used), sa["rhs_hot_rows"]
+    if hot > 0:
+        assert all(n == min(hot, T.dims[m]) for m, n in enumerate(used)), used
+    for m, n in enumerate(used):
+        if n == T.dims[m]:
+            assert sa["rhs_hot_share"][m] == 1.0
+        elif n > 0:
+            assert 0.0 < sa["rhs_hot_share"][m] < 1.0
+    del T
+    torch.cuda.empty_cache()
+    ta = a.run(2, cfg.s, cfg.sample_seed, iter0=0, fit_every=1)
+    tb = b.run(2, cfg.s, cfg.sample_seed, iter0=0, fit_every=1)
+    assert np.array_equal(np.asarray(ta), np.asarray(tb)), (ta, tb)
+    for (Aa, la), (Ab, lb) in zip(_factors(a), _factors(b)):
+        assert np.array_equal(Aa.view(np.uint64), Ab.view(np.uint64)) and np.array_equal(la, lb)
+    for m in range(D):
+        assert np.array_equal(a.get_ptilde(m), b.get_ptilde(m))
+
+
+# ---------------------------------------------------------------- short modes (n_k < r)
+@pytest.mark.parametrize("dup", [False, True])
+def test_leverage_short_mode(dup):
+    """A mode with fewer rows than r (C2's 24-row mode at r = 25).  Linearly
+    independent rows: the hat matrix is the identity, l_i = 1 and the kept
+    rank is n_k (kernels.cuh short_full_row_rank, AMB-11: the eigen cutoff of
+    A^T A keeps exactly the n_k eigenvalues it shares with A A^T).  Two equal
+    rows: the eigen path.  Both against the oracle's eigen pseudo-inverse."""
+    need_gpu()
+    from paper_2006_16438_b200 import Cparls
+    dims = (7, 30, 40)
+    r = 9
+    coords, vals = _tiny_tensor(dims, 3000, 5)
+    g = _ctx(dims, coords, vals, r)
+    rng = np.random.default_rng(11)
+    A = rng.uniform(0.1, 1.0, (dims[0], r))
+    if dup:
+        A[3] = A[1]
+    g.set_factor(0, A)
+    ell, rank = g.leverage(0)
+    ref, rref = oracle.leverage(A)
+    assert rank == rref == (dims[0] - 1 if dup else dims[0])
+    if not dup:
+        assert np.all(ell == 1.0)
+    kappa = kept_kappa(A.T @ A)
+    tol = 1e-12 * max(1.0, kappa / 1e3)
+    err = np.abs(ell - ref) / np.maximum(np.abs(ref), r / A.shape[0])
+    assert err.max() <= tol, (err.max(), kappa)
+    # p~ = l / rank feeds the sampler: one lockstep step of the short mode's
+    # neighbour (it samples mode 0's rows) against the oracle
+    pt = g.get_ptilde(0)
+    assert np.abs(pt - ref / rref).max() <= tol * max(1.0, (ref / rref).max())
+    o = oracle.Oracle(dims, coords, vals, r)
+    for m in range(3):
+        o.set_factor(m, g.get_factor(m)[0])
+        o.set_ptilde(m, g.get_ptilde(m))
+    _step_lockstep(g, o, 1, 256, -1.0, 3, 0)
