@@ -193,6 +193,7 @@ struct StepCtl {
   int skip;                     // AMB-7: the random phase of this step is skipped
   int64_t abort_step;         // global step (t*D + k) that raised abort (first)
   int64_t ncand[kMaxModes];   // DIDX candidates per other mode
+  unsigned long long cand_acc[kMaxModes];   // k_cand_append counters (k_cand_sort moves them to ncand, resets)
   int64_t nlist;              // DIDX list length (current level)
   int64_t sdet, s_rnd, have, nuniq, sbar, attempts;
   double pdet;

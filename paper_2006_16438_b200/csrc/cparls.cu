@@ -195,6 +195,7 @@ struct cparls_ctx {
   void *stage[2] = {nullptr, nullptr};
   long long *hscr = nullptr;    // small pinned scratch: async scalar reads folded into later syncs
   double *cpart = nullptr;       // K6 block partials of sum_j w_j^2 |z_j| per column (fixed-point scales)
+  ScanState scan;                // single-pass scans of the asynchronous step (prims.cuh)
   // auxiliary stream: G^+ (k_solve_prep) runs concurrently with the lookup and
   // the RHS of the same step (it needs only the sampled Gram)
   cudaStream_t aux = nullptr;
@@ -1025,6 +1026,25 @@ void build_all(cparls_ctx *c, const IT *coords, const VT *vals) {
   }
 }
 
+// the single-pass scan's tile states for n items (new memory is zeroed: epoch 0
+// never matches a call's epoch >= 1)
+void ensure_scan(cparls_ctx *c, int64_t n) {
+  const int64_t need = ceil_div(std::max<int64_t>(n, 1), kScanTile) + 1;
+  if (!c->scan.ticket) {
+    c->scan.ticket = dalloc_t<unsigned long long>(c, 1);
+    CK(cudaMemsetAsync(c->scan.ticket, 0, sizeof(unsigned long long), c->st));
+  }
+  if (need <= c->scan.cap) return;
+  dfree(c, c->scan.flag);   // cudaFree waits for the kernels still using them
+  dfree(c, c->scan.agg);
+  dfree(c, c->scan.inc);
+  c->scan.cap = std::max(need, 2 * c->scan.cap);
+  c->scan.flag = dalloc_t<unsigned long long>(c, c->scan.cap);
+  c->scan.agg = dalloc_t<int64_t>(c, c->scan.cap);
+  c->scan.inc = dalloc_t<int64_t>(c, c->scan.cap);
+  CK(cudaMemsetAsync(c->scan.flag, 0, sizeof(unsigned long long) * c->scan.cap, c->st));
+}
+
 // exclusive_scan_i64 over n items needs ceil(n / kScanTile) partials
 void ensure_i64part(cparls_ctx *c, int64_t n) {
   const int64_t need = ceil_div(std::max<int64_t>(n, 1), kScanTile) + 64;
@@ -1404,20 +1424,21 @@ void sample_async(cparls_ctx *c, int k, int64_t s, uint64_t seed, uint64_t step)
   StepCtl *ctl = c->ctl;
   const int64_t st64 = (int64_t)step;
   Phase ph(c, &c->stats.ms_sample);
-  // ---- DIDX candidates per other mode, sorted by p~ descending
-  for (int j = 0; j < d; ++j) {
-    const int64_t n = om.n[j];
-    const int64_t nb = ceil_div(n, kScanTile);
-    k_cand_count<<<(unsigned)nb, kScanThreads, 0, c->st>>>(om, j, tau, c->i64part, ctl);
+  // ---- DIDX candidates of every other mode, sorted by p~ descending
+  {
+    CandBufs cb{};
+    int64_t total = 0;
+    for (int j = 0; j < d; ++j) {
+      cb.key[j] = c->ckey[j];
+      cb.idx[j] = c->cidx[j];
+      total += om.n[j];
+      c->stats.bytes_sample += (double)om.n[j] * 8.0;
+    }
+    k_cand_append<<<(unsigned)std::min<int64_t>(148 * 8, ceil_div(total, 256)), 256, 0, c->st>>>(om, tau, cb, ctl);
     CK_LAUNCH();
-    k_scan_part<<<1, kScanThreads, 0, c->st>>>(c->i64part, nb, &ctl->ncand[j], nullptr, ctl);
+    k_cand_sort<<<(unsigned)d, kSmallSortThreads, 0, c->st>>>(cb, ctl, st64);
     CK_LAUNCH();
-    k_cand_scatter<<<(unsigned)nb, kScanThreads, 0, c->st>>>(om, j, tau, c->i64part, c->ckey[j], c->cidx[j], ctl);
-    CK_LAUNCH();
-    k_small_sort_pairs_dev<<<1, kSmallSortThreads, 0, c->st>>>(c->ckey[j], c->cidx[j], &ctl->ncand[j], ctl, st64);
-    CK_LAUNCH();
-    LAUNCHED(c, 4);
-    c->stats.bytes_sample += (double)n * 8.0;
+    LAUNCHED(c, 2);
   }
   // ---- DIDX levels: the exact canonical predicate decides membership
   const int64_t cap = c->opts.didx_cap > 0 ? c->opts.didx_cap : (int64_t(1) << 22);
@@ -1435,7 +1456,8 @@ void sample_async(cparls_ctx *c, int k, int64_t s, uint64_t seed, uint64_t step)
     k_didx_count<<<gs, 256, 0, c->st>>>(c->lpp[cur], lcap, c->ckey[l], 0, om, l, tau, c->lcnt, &ctl->nlist,
                                         &ctl->ncand[l], ctl);
     CK_LAUNCH();
-    exclusive_scan_i64_dev(c->lcnt, c->loff, lcap, &ctl->nlist, c->i64part, &ctl->scan_total, c->st, ctl);
+    ensure_scan(c, lcap);
+    exclusive_scan_i64_1p(c->lcnt, c->loff, lcap, &ctl->nlist, &ctl->scan_total, c->scan, c->st, ctl);
     k_didx_check<<<1, 1, 0, c->st>>>(ctl, lcap, cap, st64);
     CK_LAUNCH();
     k_didx_emit<<<gs, 256, 0, c->st>>>(c->lkey[cur], c->lpp[cur], lcap, c->lcnt, c->loff, c->ckey[l], c->cidx[l],
@@ -1443,7 +1465,7 @@ void sample_async(cparls_ctx *c, int k, int64_t s, uint64_t seed, uint64_t step)
     CK_LAUNCH();
     k_didx_advance<<<1, 1, 0, c->st>>>(ctl);
     CK_LAUNCH();
-    LAUNCHED(c, 7);
+    LAUNCHED(c, 5);
     cur ^= 1;
   }
   k_didx_finish<<<1, 1, 0, c->st>>>(ctl, s, tau < 1.0842021724855044e-19 ? 1 : 0, st64);
@@ -1476,13 +1498,14 @@ void sample_async(cparls_ctx *c, int k, int64_t s, uint64_t seed, uint64_t step)
   k_cidx_first_flags<<<gsamp, 256, 0, c->st>>>(c->rkey, 0, c->hkey, c->hfirst, c->hsize - 1, c->rflag, c->rslot,
                                                &ctl->have, ctl);
   CK_LAUNCH();
-  exclusive_scan_i64_dev(c->rflag, c->rpos, s, &ctl->have, c->i64part, &ctl->nuniq, c->st, ctl);
+  ensure_scan(c, s);
+  exclusive_scan_i64_1p(c->rflag, c->rpos, s, &ctl->have, &ctl->nuniq, c->scan, c->st, ctl);
   k_cidx_emit_first<<<gsamp, 256, 0, c->st>>>(c->rflag, c->rpos, c->rslot, 0, c->hkey, c->hcnt, c->hp, c->hfirst,
                                               &ctl->pdet, 0, 0, c->skey, c->sw2, c->sp, c->scnt, c->sisdet, ctl);
   CK_LAUNCH();
   k_sample_finish<<<1, 1, 0, c->st>>>(ctl);
   CK_LAUNCH();
-  LAUNCHED(c, 10);
+  LAUNCHED(c, 8);
   c->smode = k;
   c->s_cur = s;
   c->have_sample = true;
@@ -1580,8 +1603,9 @@ void lookup_impl(cparls_ctx *c, int k) {
   k_lookup<<<(unsigned)ceil_div(smax, 256), 256, 0, c->st>>>(c->skey, smax, ix.key, ix.dir, ix.shift, ix.nbkt,
                                                              key_remap(c, k), c->lo, c->len, &c->ctl->sbar, c->ctl);
   CK_LAUNCH();
-  exclusive_scan_i64_dev(c->len, c->off, smax, &c->ctl->sbar, c->i64part, &c->dv->mk, c->st, c->ctl);
-  LAUNCHED(c, 4);
+  ensure_scan(c, smax);
+  exclusive_scan_i64_1p(c->len, c->off, smax, &c->ctl->sbar, &c->dv->mk, c->scan, c->st, c->ctl);
+  LAUNCHED(c, 2);
   c->have_lookup = true;
 }
 
@@ -1698,8 +1722,9 @@ void solve_impl(cparls_ctx *c, int k, cparls_solve_info *info) {
                                                                          c->seg_lo, c->seg_len, c->seg_j,
                                                                          &ctl->sbar, &ctl->nseg, ctl);
       CK_LAUNCH();
-      exclusive_scan_i64_dev(c->seg_len, c->seg_off, nseg_max, &ctl->nseg, c->i64part_seg, nullptr, c->st, ctl);
-      LAUNCHED(c, 4);
+      ensure_scan(c, nseg_max);
+      exclusive_scan_i64_1p(c->seg_len, c->seg_off, nseg_max, &ctl->nseg, nullptr, c->scan, c->st, ctl);
+      LAUNCHED(c, 2);
       soff = c->seg_off;
       slo = c->seg_lo;
       sj = c->seg_j;

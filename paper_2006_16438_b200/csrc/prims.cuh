@@ -142,6 +142,115 @@ inline int exclusive_scan_i64_dev(const int64_t *in, int64_t *out, int64_t n_max
   return 3;
 }
 
+// ---- single-pass exclusive scan (decoupled look-back) ---------------------------
+// One launch instead of partials + part + final.  Tiles (kScanTile entries) are
+// taken in block start order from a monotonic ticket (a block waits only on
+// tiles of blocks that started before it); each publishes its aggregate, finds
+// its exclusive prefix by looking back over 32 predecessors at a time and
+// publishes its inclusive prefix.  Tile flags carry the call's epoch, so stale
+// flags of earlier calls read as "not yet published" and nothing is cleared
+// between calls; the value words are written before the flag (release) and
+// read after it (acquire).
+struct ScanState {
+  unsigned long long *flag = nullptr;   // (epoch << 2) | 1 aggregate, | 2 inclusive prefix
+  int64_t *agg = nullptr;
+  int64_t *inc = nullptr;
+  unsigned long long *ticket = nullptr;
+  int64_t cap = 0;                      // tiles
+  unsigned long long epoch = 0;         // host: calls so far
+  unsigned long long base = 0;          // host: tickets handed out so far
+};
+
+__device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long long *p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_u64(unsigned long long *p, unsigned long long v) {
+  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+__global__ void __launch_bounds__(kScanThreads) k_scan_1pass(const int64_t *in, int64_t *out, int64_t n_max,
+                                                             const int64_t *n_dev, int64_t *total,
+                                                             unsigned long long *flag, int64_t *agg,
+                                                             int64_t *inc, unsigned long long *ticket,
+                                                             unsigned long long epoch, unsigned long long base,
+                                                             const StepCtl *ctl) {
+  __shared__ int64_t s_tile, s_prefix;
+  if (threadIdx.x == 0) s_tile = (int64_t)(atomicAdd(ticket, 1ull) - base);
+  __syncthreads();
+  CPARLS_GUARD(ctl);   // after the ticket: the host counts one per block
+  const int64_t t = s_tile;
+  const int64_t n = n_dev ? min(*n_dev, n_max) : n_max;
+  const int64_t nt = ceil_div(n, kScanTile);
+  if (n <= 0) {
+    if (t == 0 && threadIdx.x == 0 && total) *total = 0;
+    return;
+  }
+  if (t >= nt) return;
+  const int64_t b0 = t * kScanTile + (int64_t)threadIdx.x * kScanItems;
+  int64_t v[kScanItems];
+  int64_t sum = 0;
+#pragma unroll
+  for (int i = 0; i < kScanItems; ++i) {
+    v[i] = b0 + i < n ? in[b0 + i] : 0;
+    sum += v[i];
+  }
+  int64_t tot;
+  const int64_t excl = block_excl_scan<int64_t>(sum, &tot);
+  if (threadIdx.x < 32) {
+    const int lane = threadIdx.x;
+    int64_t prefix = 0;
+    if (t == 0) {
+      if (lane == 0) { inc[0] = tot; st_release_u64(flag, (epoch << 2) | 2ull); }
+    } else {
+      if (lane == 0) { agg[t] = tot; st_release_u64(flag + t, (epoch << 2) | 1ull); }
+      int64_t j = t - 1;   // window [j - 31, j], lane l reads tile j - l
+      while (true) {
+        const int64_t jt = j - lane;
+        unsigned f = 2u;
+        int64_t val = 0;   // past tile 0: an empty inclusive prefix
+        if (jt >= 0) {
+          const unsigned long long w = ld_acquire_u64(flag + jt);
+          f = (w >> 2) == epoch ? (unsigned)(w & 3ull) : 0u;
+          if (f == 2u) val = *(volatile int64_t *)(inc + jt);
+          else if (f == 1u) val = *(volatile int64_t *)(agg + jt);
+        }
+        const unsigned incl = __ballot_sync(0xffffffffu, f == 2u);
+        const int stop = incl ? __ffs(incl) - 1 : 31;   // nearest inclusive predecessor
+        const unsigned unpub = __ballot_sync(0xffffffffu, f == 0u) & (0xffffffffu >> (31 - stop));
+        if (unpub) continue;
+        prefix += warp_sum<int64_t>(lane <= stop ? val : 0);
+        if (incl) break;
+        j -= 32;
+      }
+      if (lane == 0) { inc[t] = prefix + tot; st_release_u64(flag + t, (epoch << 2) | 2ull); }
+    }
+    if (lane == 0) s_prefix = prefix;
+  }
+  __syncthreads();
+  int64_t ex = s_prefix + excl;
+#pragma unroll
+  for (int i = 0; i < kScanItems; ++i) {
+    if (b0 + i < n) out[b0 + i] = ex;
+    ex += v[i];
+  }
+  if (t == nt - 1 && threadIdx.x == kScanThreads - 1 && total) *total = ex;
+}
+
+// The single-pass scan of n_dev (at most n_max) values; ss must hold
+// ceil(n_max / kScanTile) tiles.  in and out may alias.
+inline int exclusive_scan_i64_1p(const int64_t *in, int64_t *out, int64_t n_max, const int64_t *n_dev,
+                                 int64_t *total, ScanState &ss, cudaStream_t st, const StepCtl *ctl) {
+  const int64_t nb = std::max<int64_t>(1, ceil_div(n_max, kScanTile));
+  ++ss.epoch;
+  k_scan_1pass<<<(unsigned)nb, kScanThreads, 0, st>>>(in, out, n_max, n_dev, total, ss.flag, ss.agg, ss.inc,
+                                                       ss.ticket, ss.epoch, ss.base, ctl);
+  CK_LAUNCH();
+  ss.base += (unsigned long long)nb;
+  return 1;
+}
+
 // ---- stable LSD radix sort of (u64 key, u32 value) pairs ------------------------
 constexpr int kRadixBits = 8;
 constexpr int kRadixBins = 1 << kRadixBits;

@@ -10,6 +10,86 @@
 
 namespace cparls {
 
+// ---- DIDX candidates of every other mode in two launches:
+// k_cand_append marks the rows with prod_with(p~_i) > tau of all d modes in
+// one grid and appends them with a counter per mode (any order); k_cand_sort
+// (one CTA per mode) sorts each list by the composite (~bits(p~), row) --
+// p~ descending, ties by row -- which fixes the order whatever the append
+// order was.  A list longer than kSmallSortMax raises abort (host path).
+struct CandBufs {
+  uint64_t *key[kMaxModes];
+  uint32_t *idx[kMaxModes];
+};
+
+__global__ void k_cand_append(OtherModes om, double tau, CandBufs cb, StepCtl *ctl) {
+  CPARLS_GUARD(ctl);
+  double al[kMaxModes];
+  load_alphas(om, al);
+  int64_t total = 0;
+  for (int j = 0; j < om.d; ++j) total += om.n[j];
+  for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < total;
+       g += (int64_t)gridDim.x * blockDim.x) {
+    int j = 0;
+    int64_t idx = g;
+    while (idx >= om.n[j]) { idx -= om.n[j]; ++j; }
+    const double p = om.pt[j][idx];
+    if (prod_with(om, al, j, p) > tau) {
+      const unsigned long long pos = atomicAdd(&ctl->cand_acc[j], 1ull);
+      cb.key[j][pos] = ~(uint64_t)__double_as_longlong(p);
+      cb.idx[j][pos] = (uint32_t)idx;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kSmallSortThreads) k_cand_sort(CandBufs cb, StepCtl *ctl, int64_t step) {
+  CPARLS_GUARD(ctl);
+  const int j = blockIdx.x;
+  const int64_t n64 = (int64_t)*(volatile unsigned long long *)&ctl->cand_acc[j];
+  __syncthreads();   // every thread has read the count
+  if (threadIdx.x == 0) {
+    ctl->cand_acc[j] = 0ull;   // ready for the next step (stream-ordered)
+    ctl->ncand[j] = n64;
+  }
+  if (n64 > kSmallSortMax) {
+    if (threadIdx.x == 0) step_abort(ctl, step);
+    return;
+  }
+  const int n = (int)n64;
+  if (n <= 1) return;
+  __shared__ uint64_t sk[kSmallSortMax];
+  __shared__ uint32_t sv[kSmallSortMax];
+  uint64_t *keys = cb.key[j];
+  uint32_t *vals = cb.idx[j];
+  int np = 1;
+  while (np < n) np <<= 1;
+  for (int i = threadIdx.x; i < np; i += blockDim.x) {
+    sk[i] = i < n ? keys[i] : ~0ull;
+    sv[i] = i < n ? vals[i] : 0xFFFFFFFFu;
+  }
+  __syncthreads();
+  for (int size = 2; size <= np; size <<= 1) {
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      for (int t = threadIdx.x; t < (np >> 1); t += blockDim.x) {
+        const int lo = 2 * t - (t & (stride - 1));
+        const int hi = lo + stride;
+        const bool up = (lo & size) == 0;
+        const uint64_t a = sk[lo], b = sk[hi];
+        const uint32_t va = sv[lo], vb = sv[hi];
+        const bool gt = (a > b) || (a == b && va > vb);
+        if (gt == up) {
+          sk[lo] = b; sk[hi] = a;
+          sv[lo] = vb; sv[hi] = va;
+        }
+      }
+      __syncthreads();
+    }
+  }
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    keys[i] = sk[i];
+    vals[i] = sv[i];
+  }
+}
+
 // ---------------------------------------------------------------- DIDX control
 // Level 0 holds the candidates of mode m_1: nlist = ncand[0]; the DIDX list
 // capacity (lcap) and the didx_cap limit are checked here and at every level.
