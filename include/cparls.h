@@ -155,6 +155,8 @@ typedef struct {
   int32_t rhs_hot_rows[8];   /* per mode: rows summed in shared memory by the RHS
                                 (cparls_opts.rhs_hot_rows; 0 = none)                */
   double rhs_hot_share[8];   /* per mode: fraction of this rank's nonzeros in them  */
+  double build_ms[4];        /* create_ms[1] split: [0] cudaMalloc/cudaFree, [1] radix
+                                sorts, [2] key/payload kernels + directory, [3] hot rows */
 } cparls_stats;
 
 /* Build the context: validates sizes (ERANGE if some prod_{m!=k} n_m >= 2^63 or

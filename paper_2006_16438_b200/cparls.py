@@ -56,7 +56,7 @@ class Stats(C.Structure):
         ("touched_rows", C.c_int64 * 8), ("kernel_ms", C.c_double * 4),
         ("kernel_launches_by_id", C.c_int64 * 4), ("sum_matched_nnz", C.c_int64), ("host_syncs", C.c_int64),
         ("bytes_comm", C.c_double), ("create_ms", C.c_double * 4), ("rhs_hot_rows", C.c_int32 * 8),
-        ("rhs_hot_share", C.c_double * 8)]
+        ("rhs_hot_share", C.c_double * 8), ("build_ms", C.c_double * 4)]
 
     KERNELS = ("rhs", "fit", "solve_rows", "lev_rows")
 
@@ -66,6 +66,7 @@ class Stats(C.Structure):
         d["create_ms"] = list(self.create_ms)
         d["rhs_hot_rows"] = list(self.rhs_hot_rows)
         d["rhs_hot_share"] = list(self.rhs_hot_share)
+        d["build_ms"] = list(self.build_ms)
         d["kernel_ms"] = {k: self.kernel_ms[i] for i, k in enumerate(self.KERNELS)}
         d["kernel_launches_by_id"] = {k: self.kernel_launches_by_id[i] for i, k in enumerate(self.KERNELS)}
         return d

@@ -193,6 +193,7 @@ struct cparls_ctx {
   bool fx_on = false;           // this solve's RHS is fixed point (M holds int64)
   // pinned double buffer for copies into pageable host memory (rows_to_host)
   void *stage[2] = {nullptr, nullptr};
+  double *stage_dev[2] = {nullptr, nullptr};   // packed (ld -> r) rows on the device
   long long *hscr = nullptr;    // small pinned scratch: async scalar reads folded into later syncs
   double *cpart = nullptr;       // K6 block partials of sum_j w_j^2 |z_j| per column (fixed-point scales)
   ScanState scan;                // single-pass scans of the asynchronous step (prims.cuh)
@@ -209,6 +210,7 @@ struct cparls_ctx {
   double *fs_x = nullptr;
   int32_t *seg_j = nullptr;
   int64_t nfib[kMaxModes] = {0};
+  uint32_t *deg[kMaxModes] = {nullptr};   // row degrees of each copy (single-sort build; else null)
 };
 
 struct cparls_comm {
@@ -242,9 +244,18 @@ Comm *make_comm(cparls_comm *cc, int rank) {
   return l;
 }
 
+// host wall time of a scope added to *acc (ms)
+struct WallAcc {
+  double *acc;
+  std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
+  explicit WallAcc(double *a) : acc(a) {}
+  ~WallAcc() { *acc += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count(); }
+};
+
 void *dalloc(cparls_ctx *c, size_t bytes) {
   void *p = nullptr;
   if (bytes == 0) bytes = 16;
+  WallAcc wa(&c->stats.build_ms[0]);
   cudaError_t e = cudaMalloc(&p, bytes);
   if (e != cudaSuccess) {
     cudaGetLastError();
@@ -257,6 +268,7 @@ void dfree(cparls_ctx *c, void *p) {
   if (!p) return;
   auto it = std::find(c->allocs.begin(), c->allocs.end(), p);
   if (it != c->allocs.end()) c->allocs.erase(it);
+  WallAcc wa(&c->stats.build_ms[0]);
   cudaFree(p);
 }
 
@@ -343,6 +355,7 @@ void rows_to_host(cparls_ctx *c, double *dst, const double *src, int64_t rows, i
     for (int b = 0; b < 2; ++b) {
       CK(cudaHostAlloc(&c->stage[b], kStageBytes, cudaHostAllocDefault));
       CK(cudaEventCreateWithFlags(&c->stage_ev[b], cudaEventDisableTiming));
+      c->stage_dev[b] = static_cast<double *>(dalloc(c, kStageBytes));
     }
   }
   const int64_t per = std::max<int64_t>(1, (int64_t)(kStageBytes / pitch_h));
@@ -369,7 +382,12 @@ void rows_to_host(cparls_ctx *c, double *dst, const double *src, int64_t rows, i
     const int b = (int)(i & 1);
     if (i >= 2) drain(i - 2);
     const int64_t r0 = i * per, nr = std::min(per, rows - r0);
-    CK(cudaMemcpy2DAsync(c->stage[b], pitch_h, src + r0 * ld, pitch_d, pitch_h, nr, cudaMemcpyDeviceToHost, c->st));
+    // rows packed on the device first: one contiguous copy instead of a
+    // 2D copy of nr r-wide rows (the copy engine moves those row by row)
+    k_pack_rows<<<(unsigned)std::min<int64_t>(1184, ceil_div(nr * r, 256)), 256, 0, c->st>>>(src + r0 * ld, ld, r, nr,
+                                                                                            c->stage_dev[b]);
+    CK_LAUNCH();
+    CK(cudaMemcpyAsync(c->stage[b], c->stage_dev[b], (size_t)nr * pitch_h, cudaMemcpyDeviceToHost, c->st));
     CK(cudaEventRecord(c->stage_ev[b], c->st));
   }
   for (int64_t i = std::max<int64_t>(0, nch - 2); i < nch; ++i) drain(i);
@@ -732,25 +750,20 @@ constexpr size_t kHotSmemBytes = 200 * 1024;
 
 int hot_capacity(int r) { return r > 32 ? 0 : (int)(kHotSmemBytes / (8 * (size_t)r)); }
 
-void build_hot_rows(cparls_ctx *c, int k) {
+// The H (< n_k) rows of mode k of largest degree in this rank's copy (ties:
+// lower row first) into rows_dst (device, H entries); returns the fraction of
+// the copy's nonzeros they hold.
+double top_rows_by_degree(cparls_ctx *c, int k, int64_t H, int32_t *rows_dst) {
   ModeIndex &ix = c->idx[k];
   const int64_t nk = c->dims[k];
-  const int req = c->opts.rhs_hot_rows;
-  int64_t H = std::min<int64_t>(hot_capacity(c->r), nk);
-  if (req > 0) H = std::min<int64_t>(H, req);
-  if (req == 0 || H <= 0 || ix.nnz == 0 || c->opts.rhs_path == 3) return;
   uint32_t *deg = dalloc_t<uint32_t>(c, nk);
-  CK(cudaMemsetAsync(deg, 0, sizeof(uint32_t) * nk, c->st));
-  k_row_degree<<<(unsigned)std::min<int64_t>(4096, ceil_div(ix.nnz, 256)), 256, 0, c->st>>>(ix.out, ix.nnz, deg);
-  CK_LAUNCH();
-  if (H == nk) {   // every row hot: slot = row
-    ix.hot_n = (int)H;
-    ix.hot_share = 1.0;
-    sync(c);
-    dfree(c, deg);
-    return;
+  if (c->deg[k]) {   // from the run boundaries of the neighbouring copy
+    CK(cudaMemcpyAsync(deg, c->deg[k], sizeof(uint32_t) * nk, cudaMemcpyDeviceToDevice, c->st));
+  } else {
+    CK(cudaMemsetAsync(deg, 0, sizeof(uint32_t) * nk, c->st));
+    k_row_degree<<<(unsigned)std::min<int64_t>(4096, ceil_div(ix.nnz, 256)), 256, 0, c->st>>>(ix.out, ix.nnz, deg);
+    CK_LAUNCH();
   }
-  // rows by degree, descending (stable: ties keep the lower row first)
   uint32_t *deg1 = dalloc_t<uint32_t>(c, nk);
   int32_t *rows0 = dalloc_t<int32_t>(c, nk), *rows1 = dalloc_t<int32_t>(c, nk);
   k_iota_u32<<<(unsigned)ceil_div(nk, 256), 256, 0, c->st>>>(reinterpret_cast<uint32_t *>(rows0), nk);
@@ -763,31 +776,52 @@ void build_hot_rows(cparls_ctx *c, int k) {
   CK(cub::DeviceRadixSort::SortPairsDescending(tmp, tb, kb, vb, nk, 0, 32, c->st));
   std::vector<uint32_t> top(H);
   CK(cudaMemcpyAsync(top.data(), kb.Current(), sizeof(uint32_t) * H, cudaMemcpyDeviceToHost, c->st));
+  CK(cudaMemcpyAsync(rows_dst, vb.Current(), sizeof(int32_t) * H, cudaMemcpyDeviceToDevice, c->st));
   sync(c);
   double hot = 0.0;
   for (uint32_t d : top) hot += d;
-  ix.hot_share = hot / (double)ix.nnz;
-  if (req > 0 || ix.hot_share >= 0.7) {
-    ix.hot_n = (int)H;
-    ix.hot_rows = dalloc_t<int32_t>(c, H);
-    CK(cudaMemcpyAsync(ix.hot_rows, vb.Current(), sizeof(int32_t) * H, cudaMemcpyDeviceToDevice, c->st));
-    ix.hot_slot = dalloc_t<int32_t>(c, nk);
-    CK(cudaMemsetAsync(ix.hot_slot, 0xff, sizeof(int32_t) * nk, c->st));
-    k_hot_slots<<<(unsigned)ceil_div(H, 256), 256, 0, c->st>>>(ix.hot_rows, (int)H, ix.hot_slot);
-    CK_LAUNCH();
-    sync(c);
-  }
   dfree(c, tmp);
   dfree(c, deg);
   dfree(c, deg1);
   dfree(c, rows0);
   dfree(c, rows1);
+  return ix.nnz > 0 ? hot / (double)ix.nnz : 0.0;
+}
+
+void build_hot_rows(cparls_ctx *c, int k) {
+  ModeIndex &ix = c->idx[k];
+  const int64_t nk = c->dims[k];
+  const int req = c->opts.rhs_hot_rows;
+  int64_t H = std::min<int64_t>(hot_capacity(c->r), nk);
+  if (req > 0) H = std::min<int64_t>(H, req);
+  if (req == 0 || H <= 0 || ix.nnz == 0 || c->opts.rhs_path == 3) return;
+  if (H == nk) {   // every row hot: slot = row
+    ix.hot_n = (int)H;
+    ix.hot_share = 1.0;
+    return;
+  }
+  int32_t *rows = dalloc_t<int32_t>(c, H);
+  ix.hot_share = top_rows_by_degree(c, k, H, rows);
+  if (req > 0 || ix.hot_share >= 0.7) {
+    ix.hot_n = (int)H;
+    ix.hot_rows = rows;
+    ix.hot_slot = dalloc_t<int32_t>(c, nk);
+    CK(cudaMemsetAsync(ix.hot_slot, 0xff, sizeof(int32_t) * nk, c->st));
+    k_hot_slots<<<(unsigned)ceil_div(H, 256), 256, 0, c->st>>>(ix.hot_rows, (int)H, ix.hot_slot);
+    CK_LAUNCH();
+    sync(c);
+  } else {
+    dfree(c, rows);
+  }
 }
 
 template <typename IT, typename VT>
 void build_index_mode(cparls_ctx *c, int k, const IT *coords, const VT *vals, int64_t nnz) {
   ModeIndex &ix = c->idx[k];
   ix.nnz = nnz;
+  sync(c);
+  const double b0 = c->stats.build_ms[0] + c->stats.build_ms[1] + c->stats.build_ms[3];
+  const auto tw0 = std::chrono::steady_clock::now();
   const unsigned g = (unsigned)std::max<int64_t>(1, ceil_div(nnz, 256));
   // pass 1: stable sort of nonzero ids by mode-k coordinate
   uint32_t *ok0 = dalloc_t<uint32_t>(c, nnz), *ok1 = dalloc_t<uint32_t>(c, nnz);
@@ -803,8 +837,12 @@ void build_index_mode(cparls_ctx *c, int k, const IT *coords, const VT *vals, in
   size_t tb = 0;
   CK(cub::DeviceRadixSort::SortPairs(nullptr, tb, kb, vb, nnz, 0, obits, c->st));
   void *tmp = dalloc(c, tb);
-  CK(cub::DeviceRadixSort::SortPairs(tmp, tb, kb, vb, nnz, 0, obits, c->st));
-  sync(c);
+  {
+    sync(c);
+    WallAcc ws(&c->stats.build_ms[1]);
+    CK(cub::DeviceRadixSort::SortPairs(tmp, tb, kb, vb, nnz, 0, obits, c->st));
+    sync(c);
+  }
   dfree(c, tmp);
   uint32_t *ids = vb.Current();
   dfree(c, kb.Current());
@@ -831,8 +869,12 @@ void build_index_mode(cparls_ctx *c, int k, const IT *coords, const VT *vals, in
   tb = 0;
   CK(cub::DeviceRadixSort::SortPairs(nullptr, tb, kb2, vb2, nnz, 0, kbits, c->st));
   tmp = dalloc(c, tb);
-  CK(cub::DeviceRadixSort::SortPairs(tmp, tb, kb2, vb2, nnz, 0, kbits, c->st));
-  sync(c);
+  {
+    sync(c);
+    WallAcc ws(&c->stats.build_ms[1]);
+    CK(cub::DeviceRadixSort::SortPairs(tmp, tb, kb2, vb2, nnz, 0, kbits, c->st));
+    sync(c);
+  }
   dfree(c, tmp);
   ix.key = kb2.Current();
   dfree(c, kb2.Alternate());
@@ -860,7 +902,12 @@ void build_index_mode(cparls_ctx *c, int k, const IT *coords, const VT *vals, in
     CK(cudaMemsetAsync(ix.dir, 0, sizeof(int64_t) * (ix.nbkt + 1), c->st));
   }
   sync(c);
-  build_hot_rows(c, k);
+  {
+    WallAcc wh(&c->stats.build_ms[3]);
+    build_hot_rows(c, k);
+  }
+  const double tot = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tw0).count();
+  c->stats.build_ms[2] += tot - (c->stats.build_ms[0] + c->stats.build_ms[1] + c->stats.build_ms[3] - b0);
 }
 
 // Row partition of mode k into world contiguous blocks balanced by nonzeros
@@ -993,6 +1040,133 @@ void route_and_build(cparls_ctx *c, int k, const IT *coords, const VT *vals) {
   dfree(c, rval);
 }
 
+// Single-sort build of the per-mode copies (world_size 1, prod_m n_m < 2^64):
+// scratch allocated once for all modes (cudaMalloc of tens of GB is slow, and
+// slower still right after large frees), one stable radix sort per mode of
+// the composite key with the value as payload (kernels.cuh k_make_comp), the
+// sorted composite split in place into (key, out).  The sorted key and value
+// buffers become the copy's; fresh scratch replaces them for the next mode.
+struct BuildArena {
+  uint64_t *comp[2] = {nullptr, nullptr};
+  void *val[2] = {nullptr, nullptr};
+  void *tmp = nullptr;
+  size_t tmp_bytes = 0;
+  int cbits = 64;
+};
+
+int key_bits(long double N) {   // bits of the largest value N - 1
+  int b = 1;
+  while (b < 64 && (long double)((unsigned long long)1 << b) < N) ++b;
+  return b;
+}
+
+template <typename VT>
+void arena_alloc(cparls_ctx *c, BuildArena &ar, int64_t nnz) {
+  for (int i = 0; i < 2; ++i) {
+    ar.comp[i] = dalloc_t<uint64_t>(c, nnz);
+    ar.val[i] = dalloc(c, sizeof(VT) * (size_t)std::max<int64_t>(nnz, 1));
+  }
+  cub::DoubleBuffer<uint64_t> kb(ar.comp[0], ar.comp[1]);
+  cub::DoubleBuffer<VT> vb((VT *)ar.val[0], (VT *)ar.val[1]);
+  CK(cub::DeviceRadixSort::SortPairs(nullptr, ar.tmp_bytes, kb, vb, nnz, 0, ar.cbits, c->st));
+  ar.tmp = dalloc(c, ar.tmp_bytes);
+}
+
+void build_directory(cparls_ctx *c, int k) {
+  ModeIndex &ix = c->idx[k];
+  const int64_t nnz = ix.nnz;
+  long double Nk = 1;
+  for (int m = 0; m < c->D; ++m)
+    if (m != k) Nk *= (long double)c->dims[m];
+  const int kbits = key_bits(Nk);
+  int dbits = 1;
+  while (dbits < 26 && (int64_t(1) << (dbits + 1)) <= std::max<int64_t>(nnz / 8, 2)) ++dbits;
+  ix.shift = std::max(0, kbits - dbits);
+  unsigned long long Nk1 = (unsigned long long)(Nk - 1);
+  ix.nbkt = (int64_t)(Nk1 >> ix.shift) + 1;
+  ix.dir = dalloc_t<int64_t>(c, ix.nbkt + 1);
+  if (nnz > 0) {
+    k_dir_fill<<<(unsigned)std::max<int64_t>(1, ceil_div(nnz, 256)), 256, 0, c->st>>>(ix.key, nnz, ix.shift, ix.dir,
+                                                                                     ix.nbkt);
+    CK_LAUNCH();
+  } else {
+    CK(cudaMemsetAsync(ix.dir, 0, sizeof(int64_t) * (ix.nbkt + 1), c->st));
+  }
+}
+
+template <typename IT, typename VT>
+void build_index_mode_comp(cparls_ctx *c, int k, const IT *coords, const VT *vals, int64_t nnz, BuildArena &ar,
+                           bool last) {
+  ModeIndex &ix = c->idx[k];
+  ix.nnz = nnz;
+  sync(c);
+  const double b0 = c->stats.build_ms[0] + c->stats.build_ms[1] + c->stats.build_ms[3];
+  const auto tw0 = std::chrono::steady_clock::now();
+  KeySpec ks{};
+  ks.D = c->D;
+  ks.k = k;
+  for (int m = 0; m < c->D; ++m) ks.dims[m] = c->dims[m];
+  copy_order(c, k, ix.order);
+  for (int j = 0; j < c->D - 1; ++j) ks.order[j] = ix.order[j];
+  const unsigned g = (unsigned)std::min<int64_t>(148 * 16, std::max<int64_t>(1, ceil_div(nnz, 256)));
+  if (nnz > 0) {
+    k_make_comp<IT, VT><<<g, 256, 0, c->st>>>(coords, vals, nnz, ks, ar.comp[0], (VT *)ar.val[0]);
+    CK_LAUNCH();
+  }
+  cub::DoubleBuffer<uint64_t> kb(ar.comp[0], ar.comp[1]);
+  cub::DoubleBuffer<VT> vb((VT *)ar.val[0], (VT *)ar.val[1]);
+  {
+    sync(c);
+    WallAcc ws(&c->stats.build_ms[1]);
+    CK(cub::DeviceRadixSort::SortPairs(ar.tmp, ar.tmp_bytes, kb, vb, nnz, 0, ar.cbits, c->st));
+    sync(c);
+  }
+  ix.out = dalloc_t<int32_t>(c, nnz);
+  if (nnz > 0) {
+    k_split_comp<<<g, 256, 0, c->st>>>(kb.Current(), nnz, make_fastdiv((uint64_t)c->dims[k]), ix.out);
+    CK_LAUNCH();
+  }
+  ix.key = kb.Current();
+  ix.val = vb.Current();
+  const int ci = kb.Current() == ar.comp[0] ? 0 : 1;
+  const int vi = (void *)vb.Current() == ar.val[0] ? 0 : 1;
+  ar.comp[ci] = last ? nullptr : dalloc_t<uint64_t>(c, nnz);
+  ar.val[vi] = last ? nullptr : dalloc(c, sizeof(VT) * (size_t)std::max<int64_t>(nnz, 1));
+  build_directory(c, k);
+  sync(c);
+  const double tot = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tw0).count();
+  c->stats.build_ms[2] += tot - (c->stats.build_ms[0] + c->stats.build_ms[1] + c->stats.build_ms[3] - b0);
+}
+
+// Row degrees of every mode from the copy whose slowest key mode it is
+// (copy_order: mode (k+1) mod D in copy k), then the RHS hot rows.
+void degrees_and_hot_rows(cparls_ctx *c) {
+  const int D = c->D;
+  for (int m = 0; m < D; ++m) {
+    const int k = (m - 1 + D) % D;
+    const ModeIndex &ix = c->idx[k];
+    const int64_t n = c->dims[m];
+    uint64_t stride = 1;
+    for (int j = 0; j + 1 < D - 1; ++j) stride *= (uint64_t)c->dims[ix.order[j]];
+    int64_t *beg = dalloc_t<int64_t>(c, n), *end = dalloc_t<int64_t>(c, n);
+    CK(cudaMemsetAsync(beg, 0, sizeof(int64_t) * n, c->st));
+    CK(cudaMemsetAsync(end, 0, sizeof(int64_t) * n, c->st));
+    if (ix.nnz > 0) {
+      k_slow_bounds<<<(unsigned)std::min<int64_t>(148 * 16, ceil_div(ix.nnz, 256)), 256, 0, c->st>>>(
+          ix.key, ix.nnz, make_fastdiv(stride), beg, end);
+      CK_LAUNCH();
+    }
+    c->deg[m] = dalloc_t<uint32_t>(c, n);
+    k_bounds_deg<<<(unsigned)std::min<int64_t>(148 * 16, ceil_div(n, 256)), 256, 0, c->st>>>(beg, end, n, c->deg[m]);
+    CK_LAUNCH();
+    sync(c);
+    dfree(c, beg);
+    dfree(c, end);
+  }
+  WallAcc wh(&c->stats.build_ms[3]);
+  for (int k = 0; k < D; ++k) build_hot_rows(c, k);
+}
+
 template <typename IT, typename VT>
 void build_all(cparls_ctx *c, const IT *coords, const VT *vals) {
   KeySpec ks{};
@@ -1015,6 +1189,26 @@ void build_all(cparls_ctx *c, const IT *coords, const VT *vals) {
     c->comm->allreduce_f64(&c->dv->maxabs, 1, c->st);   // sum of the ranks' maxima: a common upper bound
   }
   c->normX2 = read_dev(c, &c->dv->normX2);
+  long double Nall = 1;
+  for (int m = 0; m < c->D; ++m) Nall *= (long double)c->dims[m];
+  if (c->world == 1 && Nall <= 18446744073709551615.0L && c->D >= 2) {
+    BuildArena ar;
+    ar.cbits = key_bits(Nall);
+    arena_alloc<VT>(c, ar, c->nnz);
+    for (int k = 0; k < c->D; ++k) {
+      c->row_lo[k] = 0;
+      c->row_hi[k] = c->dims[k];
+      build_index_mode_comp<IT, VT>(c, k, coords, vals, c->nnz, ar, k == c->D - 1);
+    }
+    sync(c);
+    for (int i = 0; i < 2; ++i) {
+      dfree(c, ar.comp[i]);
+      dfree(c, ar.val[i]);
+    }
+    dfree(c, ar.tmp);
+    degrees_and_hot_rows(c);
+    return;
+  }
   for (int k = 0; k < c->D; ++k) {
     if (c->world == 1) {
       c->row_lo[k] = 0;
@@ -2955,6 +3149,7 @@ cparls_status cparls_reset_stats(cparls_ctx *c) {
     std::memcpy(c->stats.create_ms, keep.create_ms, sizeof(keep.create_ms));
     std::memcpy(c->stats.rhs_hot_rows, keep.rhs_hot_rows, sizeof(keep.rhs_hot_rows));
     std::memcpy(c->stats.rhs_hot_share, keep.rhs_hot_share, sizeof(keep.rhs_hot_share));
+    std::memcpy(c->stats.build_ms, keep.build_ms, sizeof(keep.build_ms));
     c->ctl_seen = *reinterpret_cast<const StepCtl *>(c->hctl);
   });
 }

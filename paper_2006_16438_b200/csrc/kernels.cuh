@@ -958,6 +958,62 @@ __global__ void k_make_keys(const IT *__restrict__ coords, int64_t nnz, KeySpec 
   keys[t] = key;
 }
 
+// rows x r block of a row-major (pitch ld) matrix into a dense rows x r buffer
+__global__ void k_pack_rows(const double *__restrict__ src, int ld, int r, int64_t rows, double *__restrict__ dst) {
+  const int64_t n = rows * r;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t row = i / r;
+    dst[i] = src[row * ld + (i - row * r)];
+  }
+}
+
+// Single-sort build (round 2): one composite key per nonzero, the copy's key
+// times n_k plus the mode-k coordinate, so one stable radix sort by it yields
+// (key, then out, then input order) -- the order of the two stable sorts (by
+// out, then by key) -- with the value as the sort's payload (no id gathers).
+template <typename IT, typename VT>
+__global__ void k_make_comp(const IT *__restrict__ coords, const VT *__restrict__ vals, int64_t nnz, KeySpec ks,
+                            uint64_t *__restrict__ comp, VT *__restrict__ v) {
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < nnz; e += (int64_t)gridDim.x * blockDim.x) {
+    uint64_t key = 0, mult = 1;
+    for (int j = 0; j < ks.D - 1; ++j) {
+      const int m = ks.order[j];
+      key += (uint64_t)coords[e * ks.D + m] * mult;
+      mult *= (uint64_t)ks.dims[m];
+    }
+    comp[e] = key * (uint64_t)ks.dims[ks.k] + (uint64_t)coords[e * ks.D + ks.k];
+    v[e] = vals[e];
+  }
+}
+
+// composite -> (key in place, out)
+__global__ void k_split_comp(uint64_t *__restrict__ comp, int64_t nnz, FastDiv nk, int32_t *__restrict__ out) {
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < nnz; e += (int64_t)gridDim.x * blockDim.x) {
+    uint64_t rem;
+    const uint64_t q = fastdivmod(comp[e], nk, rem);
+    comp[e] = q;
+    out[e] = (int32_t)rem;
+  }
+}
+
+// Row degrees of the slowest key mode of a sorted copy from its run
+// boundaries (no atomics: a Zipf head row would serialize them): beg[d] /
+// end[d] = first / one-past-last position whose key has slowest digit d.
+__global__ void k_slow_bounds(const uint64_t *__restrict__ keys, int64_t nnz, FastDiv stride, int64_t *__restrict__ beg,
+                              int64_t *__restrict__ end) {
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < nnz; e += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t d = fastdiv(keys[e], stride);
+    if (e == 0 || fastdiv(keys[e - 1], stride) != d) beg[d] = e;
+    if (e == nnz - 1 || fastdiv(keys[e + 1], stride) != d) end[d] = e + 1;
+  }
+}
+
+__global__ void k_bounds_deg(const int64_t *__restrict__ beg, const int64_t *__restrict__ end, int64_t n,
+                             uint32_t *__restrict__ deg) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    deg[i] = (uint32_t)(end[i] - beg[i]);
+}
+
 template <typename IT, typename VT>
 __global__ void k_gather_nz(const IT *__restrict__ coords, const VT *__restrict__ vals, int64_t nnz, int D, int k,
                             const uint32_t *__restrict__ ids, int32_t *__restrict__ out, VT *__restrict__ v) {

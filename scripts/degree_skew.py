@@ -10,6 +10,6 @@ for k in range(3):
     deg = torch.bincount(T.coords[:, k].long(), minlength=cfg.dims[k]).double()
     d, _ = torch.sort(deg, descending=True)
     cs = torch.cumsum(d, 0) / d.sum()
-    out[k] = {K: float(cs[min(K, len(cs)) - 1]) for K in (10_000, 50_000, 100_000, 200_000, 400_000, 800_000)}
+    out[k] = {K: float(cs[min(K, len(cs)) - 1]) for K in (256, 512, 1024, 2048, 4096, 10_000, 50_000, 100_000, 400_000)}
     out[k]["n"] = cfg.dims[k]
 print(json.dumps(out))

@@ -1,0 +1,10 @@
+mkdir -p gpurun_out
+python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/c39_smoke.log 2>&1; echo "rc=$?" >> gpurun_out/c39_smoke.log
+timeout 2400 python -m pytest tests -x -q -m gpu > gpurun_out/c39_pytest.log 2>&1
+echo "rc=$?" >> gpurun_out/c39_pytest.log
+timeout 900 python bench.py > gpurun_out/c39_bench_C4.json 2> gpurun_out/c39_bench_C4.err
+for C in C2 C3; do
+  timeout 600 python bench.py --config $C --steps 50 --warmup 5 > gpurun_out/c39_bench_$C.json 2> gpurun_out/c39_bench_$C.err
+done
+timeout 1200 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/c39_launches_C4.csv python bench.py --steps 5 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/c39_ncu_C4.log 2>&1
+echo done
