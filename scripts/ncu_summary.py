@@ -40,7 +40,7 @@ def launches(path, out, steps):
     first = rhs[3 * W]
     start = max(i for i in range(first) if base[i] == "k_lev_rows_w") + 1
     last = rhs[3 * W + 3 * steps - 1]
-    end = next(i for i in range(last, len(base)) if base[i] == "k_cand_count")
+    end = next(i for i in range(last, len(base)) if base[i] in ("k_cand_count", "k_cand_append"))
     tot, cnt = collections.Counter(), collections.Counter()
     peaks = {"k_peak_red", "k_peak_gather"}
     for i in range(start, end):

@@ -581,3 +581,23 @@ def test_higher_order_and_rank_boundaries(dims, r):
     vals = rng.uniform(0.5, 2.0, nnz)
     T = synth.Tensor(synth.CONFIGS["C1"], dims, torch.from_numpy(coords), torch.from_numpy(vals))
     lockstep(T, r, 2, 96, 13)
+
+
+@pytest.mark.parametrize("dims", [(4194301, 2097151, 2097143), (4194319, 2097169, 2097157)])
+def test_index_build_at_the_64_bit_composite_boundary(dims):
+    """The single-sort build (composite key key*n_k + out, prod n_m < 2^64) at
+    prod n_m just below 2^64 (cbits = 64) and the two-sort fallback just above
+    it: fibers, samples, solves and fit in lockstep with the oracle.  Rows of
+    the slow key modes come from small hot sets so fibers hold several
+    entries (row degrees from run boundaries, duplicates merged)."""
+    need_gpu()
+    assert (int(np.prod(dims, dtype=object)) < 2 ** 64) == (dims[0] < 2 ** 22)
+    rng = np.random.default_rng(dims[0])
+    nnz = 3000
+    hot = [rng.choice(n, 40, replace=False) for n in dims]
+    coords = np.stack([rng.integers(0, dims[0], nnz)] +
+                      [hot[m][rng.integers(0, 40, nnz)] for m in (1, 2)], 1)
+    coords = np.unique(coords, axis=0).astype(np.int32)
+    vals = rng.uniform(0.5, 2.0, len(coords))
+    T = synth.Tensor(synth.CONFIGS["C1"], dims, torch.from_numpy(coords), torch.from_numpy(vals))
+    lockstep(T, 3, 1, 128, 17)
