@@ -534,6 +534,11 @@ def run_ours(args):
     e2e = None
     if host is not None:
         torch.cuda.synchronize()
+        # the driver reclaims the memory of the context closed above in the
+        # background; cudaMalloc right after such a free waits for it (~0.4-1 s
+        # on C4, profiles/r02_create_after_free_C4.json) -- a cost of this
+        # benchmark's earlier context, not of the user's call, so let it settle
+        time.sleep(5.0)
         hc, hv = host
         e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
         e0.record(stream)

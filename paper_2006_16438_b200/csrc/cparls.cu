@@ -521,22 +521,38 @@ size_t gram_smem(int r, int ld) { return sizeof(double) * (tile_d(ld) + 64); }
 size_t solve_smem(int r, int ld) { return sizeof(double) * ((size_t)r * ld + (size_t)kRowThreads * (ld + 2) + 64); }
 // B = M G^+ and B^T B block partials: FP64 tensor-core kernel for r in 5..32
 // (ld = 8..32), CUDA-core k_solve_rows_t otherwise or with CPARLS_SOLVE_DMMA=0
-void launch_solve_rows(cparls_ctx *c, double *M, int64_t n, double *B, int64_t grid, int zero_m,
-                       const double *fscale) {
+// returns the grid it launched (the number of BtB block partials in gpart)
+int64_t launch_solve_rows(cparls_ctx *c, double *M, int64_t n, double *B, int64_t grid, int zero_m,
+                          const double *fscale) {
   const int r = c->r, ld = c->ld;
   const bool dmma = r > 4 && ld <= 32 && ld % 8 == 0;
   if (dmma) {
-    const size_t sm = sizeof(double) * solve_dmma_smem_d(ld);
+    const bool pipe = CPARLS_SOLVE_PIPE != 0;
+    const size_t sm = sizeof(double) * solve_dmma_smem_d(ld, pipe);
+    if (pipe) grid = std::min<int64_t>(grid, c->nsm);   // one CTA per SM
+#define SOLVE_DMMA(NTV)                                                                                          \
+  do {                                                                                                           \
+    if (pipe)                                                                                                    \
+      k_solve_dmma<NTV, true><<<(unsigned)grid, kRowThreads, sm, c->st>>>(M, n, r, ld, c->sd, B, c->gpart,       \
+                                                                         &c->dv->touched, zero_m, fscale,       \
+                                                                         c->ctl);                               \
+    else                                                                                                         \
+      k_solve_dmma<NTV, false><<<(unsigned)grid, kRowThreads, sm, c->st>>>(M, n, r, ld, c->sd, B, c->gpart,      \
+                                                                          &c->dv->touched, zero_m, fscale,      \
+                                                                          c->ctl);                              \
+  } while (0)
     switch (ld / 8) {
-      case 1: k_solve_dmma<1><<<(unsigned)grid, kRowThreads, sm, c->st>>>(M, n, r, ld, c->sd, B, c->gpart, &c->dv->touched, zero_m, fscale, c->ctl); break;
-      case 2: k_solve_dmma<2><<<(unsigned)grid, kRowThreads, sm, c->st>>>(M, n, r, ld, c->sd, B, c->gpart, &c->dv->touched, zero_m, fscale, c->ctl); break;
-      case 3: k_solve_dmma<3><<<(unsigned)grid, kRowThreads, sm, c->st>>>(M, n, r, ld, c->sd, B, c->gpart, &c->dv->touched, zero_m, fscale, c->ctl); break;
-      default: k_solve_dmma<4><<<(unsigned)grid, kRowThreads, sm, c->st>>>(M, n, r, ld, c->sd, B, c->gpart, &c->dv->touched, zero_m, fscale, c->ctl); break;
+      case 1: SOLVE_DMMA(1); break;
+      case 2: SOLVE_DMMA(2); break;
+      case 3: SOLVE_DMMA(3); break;
+      default: SOLVE_DMMA(4); break;
     }
+#undef SOLVE_DMMA
   } else {
     RSWITCH(r, k_solve_rows_t<RM><<<(unsigned)grid, kRowThreads, solve_smem(r, ld), c->st>>>(
                    M, n, r, ld, c->sd, B, c->gpart, &c->dv->touched, zero_m, fscale, c->ctl));
   }
+  return grid;
 }
 size_t krp_smem(int r, int ld) { return sizeof(double) * (tile_d(ld) + kRowThreads + 64); }
 size_t prep_smem(int r) { return sizeof(double) * 4 * (size_t)r * r; }
@@ -575,6 +591,8 @@ void set_attrs_rm() {
 void set_kernel_attrs(int r, int ld) {
   max_dyn_smem(k_solve_dmma<1>); max_dyn_smem(k_solve_dmma<2>); max_dyn_smem(k_solve_dmma<3>);
   max_dyn_smem(k_solve_dmma<4>);
+  max_dyn_smem(k_solve_dmma<1, true>); max_dyn_smem(k_solve_dmma<2, true>); max_dyn_smem(k_solve_dmma<3, true>);
+  max_dyn_smem(k_solve_dmma<4, true>);
   max_dyn_smem(k_rhs_hot<float>); max_dyn_smem(k_rhs_hot<double>);
   set_attrs_rm<4>(); set_attrs_rm<8>(); set_attrs_rm<16>(); set_attrs_rm<28>(); set_attrs_rm<32>();
   set_attrs_rm<64>();
@@ -1977,10 +1995,11 @@ void solve_impl(cparls_ctx *c, int k, cparls_solve_info *info) {
       const int64_t grid = row_grid(c, ceil_div(std::max<int64_t>(nown, 1), kRowThreads));
       CK(cudaMemsetAsync(&c->dv->touched, 0, sizeof(unsigned long long), c->st));
       KTimer kts(c, KT_SOLVE);
-      launch_solve_rows(c, c->M + r0 * ld, nown, c->A[k] + r0 * ld, grid, 1, c->fx_on ? c->fx_scale : nullptr);
+      const int64_t sgrid =
+          launch_solve_rows(c, c->M + r0 * ld, nown, c->A[k] + r0 * ld, grid, 1, c->fx_on ? c->fx_scale : nullptr);
       kts.stop();
       CK_LAUNCH();
-      k_pairs_reduce<<<pairs_reduce_grid(r), 256, 0, c->st>>>(c->gpart, grid, r, c->sd->BtB, ctl);
+      k_pairs_reduce<<<pairs_reduce_grid(r), 256, 0, c->st>>>(c->gpart, sgrid, r, c->sd->BtB, ctl);
       CK_LAUNCH();
     }
     if (c->world > 1) {
@@ -2084,10 +2103,10 @@ void als_update_impl(cparls_ctx *c, int k) {
   const int64_t grid = row_grid(c, ceil_div(std::max<int64_t>(nk, 1), kRowThreads));
   CK(cudaMemsetAsync(&c->dv->touched, 0, sizeof(unsigned long long), c->st));
   KTimer kts(c, KT_SOLVE);
-  launch_solve_rows(c, c->M, nk, c->A[k], grid, 1, nullptr);
+  const int64_t sgrid = launch_solve_rows(c, c->M, nk, c->A[k], grid, 1, nullptr);
   kts.stop();
   CK_LAUNCH();
-  k_pairs_reduce<<<pairs_reduce_grid(r), 256, 0, c->st>>>(c->gpart, grid, r, c->sd->BtB);
+  k_pairs_reduce<<<pairs_reduce_grid(r), 256, 0, c->st>>>(c->gpart, sgrid, r, c->sd->BtB);
   CK_LAUNCH();
   k_norm_prep<<<1, kPrepThreads, prep_smem(r), c->st>>>(r, c->sd, c->md[k], nullptr, c->A[k], nk, ld);
   CK_LAUNCH();

@@ -259,6 +259,28 @@ __device__ __forceinline__ void warp_store(double *__restrict__ dst, int rows, i
   }
 }
 
+// The tile of warp_stage as 16-byte cp.async copies (no registers, the data
+// lands while the warp computes on its other tile); chunks past `rows` rows
+// are not copied (the consumers read rows < rows only).
+__device__ __forceinline__ void warp_stage_async(const double *__restrict__ src, int rows, int ld, double *tile,
+                                                 int S) {
+  const int lane = threadIdx.x & 31;
+  const double2 *s2 = reinterpret_cast<const double2 *>(src);
+  const int n2 = rows * ld / 2;
+  ChunkWalk cw(lane, ld);
+  for (int i = lane; i < n2; i += 32) {
+    const unsigned sa = (unsigned)__cvta_generic_to_shared(tile + cw.row * S + cw.c);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(s2 + i) : "memory");
+    cw.next();
+  }
+}
+__device__ __forceinline__ void warp_zero(double *__restrict__ dst, int rows, int ld) {
+  const int lane = threadIdx.x & 31;
+  double2 *d2 = reinterpret_cast<double2 *>(dst);
+  const int n2 = rows * ld / 2;
+  for (int i = lane; i < n2; i += 32) d2[i] = make_double2(0.0, 0.0);
+}
+
 // p~_i = ||a_i W||^2 / rank of one normalized row x (16-byte aligned, r columns)
 // with W (RMAX x RMAX, zero padded; zero below the diagonal if tri): s_c =
 // sum_{k < r} a_k W_kc, l = sum_c s_c^2.  One definition for the leverage pass
@@ -389,12 +411,20 @@ __device__ __forceinline__ void dmma_884(double (&c)[2], double a, double b) {
                : "d"(a), "d"(b));
 }
 
-__host__ __device__ constexpr size_t solve_dmma_smem_d(int LD) {
-  return (size_t)LD * LD + LD + (size_t)(kRowThreads / 32) * kWarpRows * (LD + 2) + 64;
+// PIPE (round 2): two tiles per warp, the next one's M rows in flight
+// (cp.async) while the current one is multiplied and stored; one CTA per SM
+// (the tiles take ~140 KB of shared memory), grid = SMs.  C4: 0.611 -> 0.566
+// ms per launch.  (The same pipeline in k_lev_rows_w measured slower, 0.514 ->
+// 0.622 ms: its per-row quadratic forms want the 16 warps per SM of two CTAs.)
+#ifndef CPARLS_SOLVE_PIPE
+#define CPARLS_SOLVE_PIPE 1
+#endif
+__host__ __device__ constexpr size_t solve_dmma_smem_d(int LD, bool pipe = false) {
+  return (size_t)LD * LD + LD + (pipe ? 2 : 1) * (size_t)(kRowThreads / 32) * kWarpRows * (LD + 2) + 64;
 }
 
-template <int NT>
-__global__ void __launch_bounds__(kRowThreads, CPARLS_SOLVE_MINB) k_solve_dmma(double *__restrict__ M, int64_t n, int r, int ld,
+template <int NT, bool PIPE = false>
+__global__ void __launch_bounds__(kRowThreads, PIPE ? 1 : CPARLS_SOLVE_MINB) k_solve_dmma(double *__restrict__ M, int64_t n, int r, int ld,
                                                                const SolveDev *__restrict__ sd,
                                                                double *__restrict__ B, double *__restrict__ part,
                                                                unsigned long long *__restrict__ touched, int zero_m,
@@ -407,7 +437,8 @@ __global__ void __launch_bounds__(kRowThreads, CPARLS_SOLVE_MINB) k_solve_dmma(d
   double *Gs = smem;          // LD x LD, G^+ zero padded
   double *fs = Gs + LD * LD;  // 2^-e_c (fixed-point RHS) or 1
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, gid = lane >> 2, tig = lane & 3;
-  double *tile = fs + LD + (size_t)w * kWarpRows * S;
+  double *tile0 = fs + LD + (size_t)w * (PIPE ? 2 : 1) * kWarpRows * S;
+  double *tile = tile0;
   const bool fixed = fscale != nullptr && fscale[2 * kMaxRank] != 0.0;
   for (int i = threadIdx.x; i < LD * LD; i += blockDim.x) {
     const int p = i / LD, c = i - p * LD;
@@ -421,10 +452,29 @@ __global__ void __launch_bounds__(kRowThreads, CPARLS_SOLVE_MINB) k_solve_dmma(d
   unsigned long long ntouch = 0;
   const int64_t ntiles = ceil_div(n, kWarpRows);
   const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
-  for (int64_t t = (int64_t)blockIdx.x * (blockDim.x >> 5) + w; t < ntiles; t += nwarps) {
+  const int64_t tfirst = (int64_t)blockIdx.x * (blockDim.x >> 5) + w;
+  if (PIPE && tfirst < ntiles) {
+    warp_stage_async(M + tfirst * kWarpRows * ld, (int)min((int64_t)kWarpRows, n - tfirst * kWarpRows), ld, tile0, S);
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+  }
+  int buf = 0;
+  for (int64_t t = tfirst; t < ntiles; t += nwarps) {
     const int64_t base = t * kWarpRows;
     const int rows = (int)min((int64_t)kWarpRows, n - base);
-    warp_stage(M + base * ld, rows, ld, tile, S, zero_m ? M + base * ld : nullptr);
+    if (PIPE) {
+      tile = tile0 + (size_t)buf * kWarpRows * S;
+      const int64_t tn = t + nwarps;
+      if (tn < ntiles)
+        warp_stage_async(M + tn * kWarpRows * ld, (int)min((int64_t)kWarpRows, n - tn * kWarpRows), ld,
+                         tile0 + (size_t)(buf ^ 1) * kWarpRows * S, S);
+      asm volatile("cp.async.commit_group;\n" ::: "memory");
+      asm volatile("cp.async.wait_group 1;\n" ::: "memory");   // this tile's rows have landed
+      __syncwarp();
+      if (zero_m) warp_zero(M + base * ld, rows, ld);
+      buf ^= 1;
+    } else {
+      warp_stage(M + base * ld, rows, ld, tile, S, zero_m ? M + base * ld : nullptr);
+    }
     __syncwarp();
 #pragma unroll
     for (int m = 0; m < 4; ++m) {
@@ -472,6 +522,7 @@ __global__ void __launch_bounds__(kRowThreads, CPARLS_SOLVE_MINB) k_solve_dmma(d
     }
     __syncwarp();
   }
+  if (PIPE) asm volatile("cp.async.wait_group 0;\n" ::: "memory");
   unsigned long long nt = warp_sum<unsigned long long>(ntouch);
   if (lane == 0 && nt) atomicAdd(touched, nt);
   __syncthreads();
