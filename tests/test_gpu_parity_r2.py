@@ -307,3 +307,28 @@ def test_leverage_short_mode(dup):
         o.set_factor(m, g.get_factor(m)[0])
         o.set_ptilde(m, g.get_ptilde(m))
     _step_lockstep(g, o, 1, 256, -1.0, 3, 0)
+
+
+@pytest.mark.parametrize("name", ["C2", "C3"])
+def test_row_degrees_from_run_boundaries(name):
+    """The single-sort build takes each mode's row degrees from the run
+    boundaries of the copy whose slowest key mode it is (k_slow_bounds, no
+    atomics); the RHS hot rows are the top-H rows by those degrees.  With
+    H = 100 forced, the share of nonzeros the library reports for every mode
+    equals the top-100 share of torch.bincount of that mode's coordinates."""
+    need_gpu()
+    from paper_2006_16438_b200 import Cparls
+    T = synth.make(name, device="cuda")
+    cfg = T.cfg
+    g = Cparls(T.dims, T.coords, T.vals, cfg.rank, rhs_hot_rows=100)
+    st = g.stats()
+    nnz = T.coords.shape[0]
+    for m, n in enumerate(T.dims):
+        deg = torch.bincount(T.coords[:, m].long(), minlength=n)
+        H = min(100, n)
+        assert st["rhs_hot_rows"][m] == H
+        if H == n:
+            assert st["rhs_hot_share"][m] == 1.0
+        else:
+            top = int(torch.topk(deg, H).values.sum())
+            assert st["rhs_hot_share"][m] == top / nnz, (m, st["rhs_hot_share"][m], top / nnz)
