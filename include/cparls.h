@@ -174,8 +174,9 @@ cparls_status cparls_destroy(cparls_ctx *ctx);
  * leverage scores / CDF.  lambda is reset to ones. */
 cparls_status cparls_set_factor(cparls_ctx *ctx, int32_t mode, const double *A);
 /* Copy factor k (n_k x r row-major fp64) and the model weights lambda (r, may
- * be NULL) into caller memory: device, pinned host or pageable host (the
- * latter through a pinned double buffer the context owns).  Synchronous. */
+ * be NULL) into caller memory: device, pinned host (rows packed on the device,
+ * then contiguous DMA into A) or pageable host (through a pinned double buffer
+ * the context owns).  Synchronous. */
 cparls_status cparls_get_factor(cparls_ctx *ctx, int32_t mode, double *A, double *lambda);
 
 /* Leverage scores of A_k (Def. leverages_scores P:319-331 as l_i =

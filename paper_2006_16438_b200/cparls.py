@@ -220,9 +220,16 @@ class Cparls:
         assert A.shape == (self.dims[k], self.r)
         self._check(lib().cparls_set_factor(self._h, k, A.ctypes.data))
 
-    def get_factor(self, k):
-        A = np.zeros((self.dims[k], self.r))
-        lam = np.zeros(self.r)
+    def get_factor(self, k, out=None, lam_out=None):
+        """Factor k (n_k x r fp64) and lambda.  out / lam_out: optional caller
+        arrays (C-contiguous fp64; e.g. numpy views of pinned torch tensors,
+        which the library copies into without staging)."""
+        A = np.zeros((self.dims[k], self.r)) if out is None else out
+        lam = np.zeros(self.r) if lam_out is None else lam_out
+        if A.shape != (self.dims[k], self.r) or A.dtype != np.float64 or not A.flags.c_contiguous:
+            raise ValueError("out must be a C-contiguous float64 array of shape (n_k, r)")
+        if lam.shape != (self.r,) or lam.dtype != np.float64 or not lam.flags.c_contiguous:
+            raise ValueError("lam_out must be a C-contiguous float64 array of shape (r,)")
         self._check(lib().cparls_get_factor(self._h, k, A.ctypes.data, lam.ctypes.data))
         return A, lam
 

@@ -345,17 +345,34 @@ bool is_pinned_host(const void *p) {
 void rows_to_host(cparls_ctx *c, double *dst, const double *src, int64_t rows, int r, int ld) {
   if (rows <= 0) return;
   const size_t pitch_d = sizeof(double) * ld, pitch_h = sizeof(double) * r;
-  if (is_device_ptr(dst) || is_pinned_host(dst)) {
+  if (is_device_ptr(dst) || ld == r) {
     CK(cudaMemcpy2DAsync(dst, pitch_h, src, pitch_d, pitch_h, rows, cudaMemcpyDefault, c->st));
     sync(c);
     return;
   }
   constexpr size_t kStageBytes = size_t(32) << 20;
+  const bool pinned = is_pinned_host(dst);
+  if (pinned && !c->stage_dev[0]) {
+    for (int b = 0; b < 2; ++b) c->stage_dev[b] = static_cast<double *>(dalloc(c, kStageBytes));
+  }
+  if (pinned) {   // rows packed on the device, then contiguous D2H copies straight into dst
+    const int64_t per = std::max<int64_t>(1, (int64_t)(kStageBytes / pitch_h));
+    for (int64_t r0 = 0, i = 0; r0 < rows; r0 += per, ++i) {
+      const int b = (int)(i & 1);
+      const int64_t nr = std::min(per, rows - r0);
+      k_pack_rows<<<(unsigned)std::min<int64_t>(1184, ceil_div(nr * r, 256)), 256, 0, c->st>>>(
+          src + r0 * ld, ld, r, nr, c->stage_dev[b]);
+      CK_LAUNCH();
+      CK(cudaMemcpyAsync(dst + r0 * r, c->stage_dev[b], (size_t)nr * pitch_h, cudaMemcpyDeviceToHost, c->st));
+    }
+    sync(c);
+    return;
+  }
   if (!c->stage[0]) {
     for (int b = 0; b < 2; ++b) {
       CK(cudaHostAlloc(&c->stage[b], kStageBytes, cudaHostAllocDefault));
       CK(cudaEventCreateWithFlags(&c->stage_ev[b], cudaEventDisableTiming));
-      c->stage_dev[b] = static_cast<double *>(dalloc(c, kStageBytes));
+      if (!c->stage_dev[b]) c->stage_dev[b] = static_cast<double *>(dalloc(c, kStageBytes));
     }
   }
   const int64_t per = std::max<int64_t>(1, (int64_t)(kStageBytes / pitch_h));
@@ -1114,7 +1131,7 @@ void build_directory(cparls_ctx *c, int k) {
 
 template <typename IT, typename VT>
 void build_index_mode_comp(cparls_ctx *c, int k, const IT *coords, const VT *vals, int64_t nnz, BuildArena &ar,
-                           bool last) {
+                           bool last, bool comp_made = false) {
   ModeIndex &ix = c->idx[k];
   ix.nnz = nnz;
   sync(c);
@@ -1127,7 +1144,7 @@ void build_index_mode_comp(cparls_ctx *c, int k, const IT *coords, const VT *val
   copy_order(c, k, ix.order);
   for (int j = 0; j < c->D - 1; ++j) ks.order[j] = ix.order[j];
   const unsigned g = (unsigned)std::min<int64_t>(148 * 16, std::max<int64_t>(1, ceil_div(nnz, 256)));
-  if (nnz > 0) {
+  if (nnz > 0 && !comp_made) {
     k_make_comp<IT, VT><<<g, 256, 0, c->st>>>(coords, vals, nnz, ks, ar.comp[0], (VT *)ar.val[0]);
     CK_LAUNCH();
   }
@@ -1185,11 +1202,63 @@ void degrees_and_hot_rows(cparls_ctx *c) {
   for (int k = 0; k < D; ++k) build_hot_rows(c, k);
 }
 
+// Chunked host->device copy of the COO in flight on its own stream (cparls_create):
+// chunk i covers nonzeros [end[i-1], end[i]) and is resident once ev[i] fires.
+struct H2DChunks {
+  static constexpr int64_t kChunk = int64_t(1) << 26;
+  cudaStream_t cs = nullptr;
+  cudaEvent_t ev0 = nullptr;
+  std::vector<int64_t> end;
+  std::vector<cudaEvent_t> ev;
+  H2DChunks() { CK(cudaEventCreateWithFlags(&ev0, cudaEventDisableTiming)); }
+  ~H2DChunks() {   // every user of the chunks is ordered after them on c->st by then
+    if (cs) cudaStreamSynchronize(cs);
+    for (cudaEvent_t e : ev) cudaEventDestroy(e);
+    if (ev0) cudaEventDestroy(ev0);
+    if (cs) cudaStreamDestroy(cs);
+  }
+  H2DChunks(const H2DChunks &) = delete;
+  H2DChunks &operator=(const H2DChunks &) = delete;
+  void wait_all(cudaStream_t st) const {
+    if (!ev.empty()) CK(cudaStreamWaitEvent(st, ev.back(), 0));
+  }
+};
+
 template <typename IT, typename VT>
-void build_all(cparls_ctx *c, const IT *coords, const VT *vals) {
+void build_all(cparls_ctx *c, const IT *coords, const VT *vals, const H2DChunks *hc) {
   KeySpec ks{};
   ks.D = c->D;
   for (int m = 0; m < c->D; ++m) ks.dims[m] = c->dims[m];
+  long double Nall = 1;
+  for (int m = 0; m < c->D; ++m) Nall *= (long double)c->dims[m];
+  const bool single_sort = c->world == 1 && Nall <= 18446744073709551615.0L && c->D >= 2;
+  BuildArena ar;
+  bool comp0_made = false;
+  if (single_sort && hc && c->nnz > 0) {
+    // the arena is allocated and mode 0's composite keys are made chunk by
+    // chunk while the rest of the COO is still crossing PCIe
+    ar.cbits = key_bits(Nall);
+    arena_alloc<VT>(c, ar, c->nnz);
+    KeySpec k0{};
+    k0.D = c->D;
+    k0.k = 0;
+    for (int m = 0; m < c->D; ++m) k0.dims[m] = c->dims[m];
+    int ord[kMaxModes];
+    copy_order(c, 0, ord);
+    for (int j = 0; j < c->D - 1; ++j) k0.order[j] = ord[j];
+    int64_t e0 = 0;
+    for (size_t i = 0; i < hc->ev.size(); ++i) {
+      const int64_t n = hc->end[i] - e0;
+      CK(cudaStreamWaitEvent(c->st, hc->ev[i], 0));
+      const unsigned g = (unsigned)std::min<int64_t>(148 * 16, std::max<int64_t>(1, ceil_div(n, 256)));
+      k_make_comp<IT, VT><<<g, 256, 0, c->st>>>(coords + e0 * c->D, vals + e0, n, k0, ar.comp[0] + e0,
+                                                (VT *)ar.val[0] + e0);
+      CK_LAUNCH();
+      e0 = hc->end[i];
+    }
+    comp0_made = true;
+  }
+  if (hc) hc->wait_all(c->st);
   CK(cudaMemsetAsync(&c->dv->bad, 0, sizeof(unsigned long long), c->st));
   if (c->nnz > 0) {
     k_check_coords<IT><<<(unsigned)ceil_div(c->nnz, 256), 256, 0, c->st>>>(coords, c->nnz, ks, &c->dv->bad);
@@ -1207,16 +1276,15 @@ void build_all(cparls_ctx *c, const IT *coords, const VT *vals) {
     c->comm->allreduce_f64(&c->dv->maxabs, 1, c->st);   // sum of the ranks' maxima: a common upper bound
   }
   c->normX2 = read_dev(c, &c->dv->normX2);
-  long double Nall = 1;
-  for (int m = 0; m < c->D; ++m) Nall *= (long double)c->dims[m];
-  if (c->world == 1 && Nall <= 18446744073709551615.0L && c->D >= 2) {
-    BuildArena ar;
-    ar.cbits = key_bits(Nall);
-    arena_alloc<VT>(c, ar, c->nnz);
+  if (single_sort) {
+    if (!comp0_made) {
+      ar.cbits = key_bits(Nall);
+      arena_alloc<VT>(c, ar, c->nnz);
+    }
     for (int k = 0; k < c->D; ++k) {
       c->row_lo[k] = 0;
       c->row_hi[k] = c->dims[k];
-      build_index_mode_comp<IT, VT>(c, k, coords, vals, c->nnz, ar, k == c->D - 1);
+      build_index_mode_comp<IT, VT>(c, k, coords, vals, c->nnz, ar, k == c->D - 1, k == 0 && comp0_made);
     }
     sync(c);
     for (int i = 0; i < 2; ++i) {
@@ -2578,22 +2646,41 @@ cparls_status cparls_create(cparls_ctx **out, int32_t nmodes, const int64_t *dim
     const size_t isz = opts->index_dtype == 1 ? 8 : 4, vsz = c->vf32 ? 4 : 8;
     const void *dco = coords, *dva = vals;
     void *own_c = nullptr, *own_v = nullptr;
-    if (nnz_local > 0 && !is_device_ptr(coords)) {
-      own_c = dalloc(c, isz * nmodes * nnz_local);
-      CK(cudaMemcpyAsync(own_c, coords, isz * nmodes * nnz_local, cudaMemcpyHostToDevice, c->st));
-      dco = own_c;
+    // host COO: copied in chunks on a copy stream, each chunk's completion an
+    // event the build waits on, so the build's allocations and its first key
+    // pass run under the PCIe transfer (build_all)
+    H2DChunks hc;
+    const bool hc_c = nnz_local > 0 && !is_device_ptr(coords), hc_v = nnz_local > 0 && !is_device_ptr(vals);
+    if (hc_c) own_c = dalloc(c, isz * nmodes * nnz_local);
+    if (hc_v) own_v = dalloc(c, vsz * nnz_local);
+    if (hc_c || hc_v) {
+      CK(cudaStreamCreateWithFlags(&hc.cs, cudaStreamNonBlocking));
+      CK(cudaEventRecord(hc.ev0, c->st));   // after the context's own memsets
+      CK(cudaStreamWaitEvent(hc.cs, hc.ev0, 0));
+      const int64_t per = H2DChunks::kChunk;
+      for (int64_t e0 = 0; e0 < nnz_local; e0 += per) {
+        const int64_t n = std::min(per, nnz_local - e0);
+        if (hc_c)
+          CK(cudaMemcpyAsync((char *)own_c + isz * nmodes * e0, (const char *)coords + isz * nmodes * e0,
+                             isz * nmodes * n, cudaMemcpyHostToDevice, hc.cs));
+        if (hc_v)
+          CK(cudaMemcpyAsync((char *)own_v + vsz * e0, (const char *)vals + vsz * e0, vsz * n, cudaMemcpyHostToDevice,
+                             hc.cs));
+        cudaEvent_t ev;
+        CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+        CK(cudaEventRecord(ev, hc.cs));
+        hc.end.push_back(e0 + n);
+        hc.ev.push_back(ev);
+      }
+      if (hc_c) dco = own_c;
+      if (hc_v) dva = own_v;
     }
-    if (nnz_local > 0 && !is_device_ptr(vals)) {
-      own_v = dalloc(c, vsz * nnz_local);
-      CK(cudaMemcpyAsync(own_v, vals, vsz * nnz_local, cudaMemcpyHostToDevice, c->st));
-      dva = own_v;
-    }
-    sync(c);
+    const H2DChunks *hcp = hc.ev.empty() ? nullptr : &hc;
     t_h2d = since();
-    if (isz == 4 && vsz == 4) build_all<int32_t, float>(c, (const int32_t *)dco, (const float *)dva);
-    else if (isz == 4) build_all<int32_t, double>(c, (const int32_t *)dco, (const double *)dva);
-    else if (vsz == 4) build_all<int64_t, float>(c, (const int64_t *)dco, (const float *)dva);
-    else build_all<int64_t, double>(c, (const int64_t *)dco, (const double *)dva);
+    if (isz == 4 && vsz == 4) build_all<int32_t, float>(c, (const int32_t *)dco, (const float *)dva, hcp);
+    else if (isz == 4) build_all<int32_t, double>(c, (const int32_t *)dco, (const double *)dva, hcp);
+    else if (vsz == 4) build_all<int64_t, float>(c, (const int64_t *)dco, (const float *)dva, hcp);
+    else build_all<int64_t, double>(c, (const int64_t *)dco, (const double *)dva, hcp);
     sync(c);
     t_build = since();
     c->drow_lo = dalloc_t<int64_t>(c, kMaxModes);
