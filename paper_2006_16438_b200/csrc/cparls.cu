@@ -12,6 +12,8 @@
 #include <cstring>
 #include <thread>
 #include <cub/device/device_radix_sort.cuh>
+#include <thrust/execution_policy.h>
+#include <thrust/merge.h>
 #include <new>
 #include <numeric>
 #include <string>
@@ -1202,10 +1204,56 @@ void degrees_and_hot_rows(cparls_ctx *c) {
   for (int k = 0; k < D; ++k) build_hot_rows(c, k);
 }
 
+// Merge the sorted runs [rb[j], rb[j+1]) of (k, v) pairwise until one run is
+// left (stable: on equal keys the earlier run first, i.e. input order).  The
+// result ends in (k, v); (sk, sv) is scratch of the same size and the pointers
+// are swapped so the caller's (k, v) hold the result.
+template <typename VT>
+void merge_runs(cparls_ctx *c, const std::vector<int64_t> &rb0, uint64_t *&k, VT *&v, uint64_t *&sk, VT *&sv) {
+  std::vector<int64_t> rb = rb0;
+  auto pol = thrust::cuda::par_nosync.on(c->st);
+  while (rb.size() > 2) {
+    std::vector<int64_t> nb{0};
+    for (size_t j = 0; j + 1 < rb.size(); j += 2) {
+      if (j + 2 < rb.size()) {
+        thrust::merge_by_key(pol, k + rb[j], k + rb[j + 1], k + rb[j + 1], k + rb[j + 2], v + rb[j], v + rb[j + 1],
+                             sk + rb[j], sv + rb[j]);
+        nb.push_back(rb[j + 2]);
+      } else {
+        const int64_t n = rb[j + 1] - rb[j];
+        CK(cudaMemcpyAsync(sk + rb[j], k + rb[j], sizeof(uint64_t) * n, cudaMemcpyDeviceToDevice, c->st));
+        CK(cudaMemcpyAsync(sv + rb[j], v + rb[j], sizeof(VT) * n, cudaMemcpyDeviceToDevice, c->st));
+        nb.push_back(rb[j + 1]);
+      }
+    }
+    CK(cudaGetLastError());
+    std::swap(k, sk);
+    std::swap(v, sv);
+    rb.swap(nb);
+  }
+}
+
+// Copy k from composite keys already sorted (merge_runs): split, directory.
+void finish_mode_presorted(cparls_ctx *c, int k, int64_t nnz, uint64_t *comp, void *val) {
+  ModeIndex &ix = c->idx[k];
+  ix.nnz = nnz;
+  copy_order(c, k, ix.order);
+  const unsigned g = (unsigned)std::min<int64_t>(148 * 16, std::max<int64_t>(1, ceil_div(nnz, 256)));
+  ix.out = dalloc_t<int32_t>(c, nnz);
+  if (nnz > 0) {
+    k_split_comp<<<g, 256, 0, c->st>>>(comp, nnz, make_fastdiv((uint64_t)c->dims[k]), ix.out);
+    CK_LAUNCH();
+  }
+  ix.key = comp;
+  ix.val = val;
+  build_directory(c, k);
+  sync(c);
+}
+
 // Chunked host->device copy of the COO in flight on its own stream (cparls_create):
 // chunk i covers nonzeros [end[i-1], end[i]) and is resident once ev[i] fires.
 struct H2DChunks {
-  static constexpr int64_t kChunk = int64_t(1) << 26;
+  static constexpr int64_t kChunk = int64_t(1) << 27;
   cudaStream_t cs = nullptr;
   cudaEvent_t ev0 = nullptr;
   std::vector<int64_t> end;
@@ -1234,29 +1282,65 @@ void build_all(cparls_ctx *c, const IT *coords, const VT *vals, const H2DChunks 
   const bool single_sort = c->world == 1 && Nall <= 18446744073709551615.0L && c->D >= 2;
   BuildArena ar;
   bool comp0_made = false;
-  if (single_sort && hc && c->nnz > 0) {
-    // the arena is allocated and mode 0's composite keys are made chunk by
-    // chunk while the rest of the COO is still crossing PCIe
-    ar.cbits = key_bits(Nall);
-    arena_alloc<VT>(c, ar, c->nnz);
-    KeySpec k0{};
-    k0.D = c->D;
-    k0.k = 0;
-    for (int m = 0; m < c->D; ++m) k0.dims[m] = c->dims[m];
-    int ord[kMaxModes];
-    copy_order(c, 0, ord);
-    for (int j = 0; j < c->D - 1; ++j) k0.order[j] = ord[j];
-    int64_t e0 = 0;
-    for (size_t i = 0; i < hc->ev.size(); ++i) {
-      const int64_t n = hc->end[i] - e0;
-      CK(cudaStreamWaitEvent(c->st, hc->ev[i], 0));
-      const unsigned g = (unsigned)std::min<int64_t>(148 * 16, std::max<int64_t>(1, ceil_div(n, 256)));
-      k_make_comp<IT, VT><<<g, 256, 0, c->st>>>(coords + e0 * c->D, vals + e0, n, k0, ar.comp[0] + e0,
-                                                (VT *)ar.val[0] + e0);
-      CK_LAUNCH();
-      e0 = hc->end[i];
+  // create from host: every mode's composite keys of chunk i are made and
+  // sorted while chunks > i are still crossing PCIe (sorted runs, one per
+  // chunk and mode); the runs are merged once the input is complete
+  // (merge_runs).  Stable throughout, so the copies equal those of the
+  // single full sort bit for bit.
+  std::vector<uint64_t *> rk;
+  std::vector<VT *> rv;
+  std::vector<int64_t> rb;
+  if (single_sort && hc && c->nnz > 0 && hc->ev.size() > 1) {
+    const int D = c->D;
+    const int64_t nnz = c->nnz;
+    const size_t pair = sizeof(uint64_t) + sizeof(VT);
+    size_t fr = 0, tot = 0;
+    CK(cudaMemGetInfo(&fr, &tot));
+    const int64_t cmax = hc->end[0];
+    const size_t need = pair * (size_t)nnz * (D + 1) + sizeof(int32_t) * (size_t)nnz * D + pair * (size_t)cmax * 2 +
+                        (size_t(6) << 30);
+    if (need < fr) {
+      ar.cbits = key_bits(Nall);
+      rk.resize(D);
+      rv.resize(D);
+      for (int k = 0; k < D; ++k) {
+        rk[k] = dalloc_t<uint64_t>(c, nnz);
+        rv[k] = (VT *)dalloc(c, sizeof(VT) * (size_t)nnz);
+      }
+      uint64_t *ck = dalloc_t<uint64_t>(c, cmax);
+      VT *cv = (VT *)dalloc(c, sizeof(VT) * (size_t)cmax);
+      size_t tb = 0;
+      CK(cub::DeviceRadixSort::SortPairs(nullptr, tb, ck, rk[0], cv, rv[0], cmax, 0, ar.cbits, c->st));
+      void *tmp = dalloc(c, tb);
+      KeySpec km[kMaxModes];
+      for (int k = 0; k < D; ++k) {
+        km[k] = KeySpec{};
+        km[k].D = D;
+        km[k].k = k;
+        for (int m = 0; m < D; ++m) km[k].dims[m] = c->dims[m];
+        int ord[kMaxModes];
+        copy_order(c, k, ord);
+        for (int j = 0; j < D - 1; ++j) km[k].order[j] = ord[j];
+      }
+      rb.push_back(0);
+      int64_t e0 = 0;
+      for (size_t i = 0; i < hc->ev.size(); ++i) {
+        const int64_t n = hc->end[i] - e0;
+        CK(cudaStreamWaitEvent(c->st, hc->ev[i], 0));
+        const unsigned g = (unsigned)std::min<int64_t>(148 * 16, std::max<int64_t>(1, ceil_div(n, 256)));
+        for (int k = 0; k < D; ++k) {
+          k_make_comp<IT, VT><<<g, 256, 0, c->st>>>(coords + e0 * D, vals + e0, n, km[k], ck, cv);
+          CK_LAUNCH();
+          CK(cub::DeviceRadixSort::SortPairs(tmp, tb, ck, rk[k] + e0, cv, rv[k] + e0, n, 0, ar.cbits, c->st));
+        }
+        e0 = hc->end[i];
+        rb.push_back(e0);
+      }
+      sync(c);
+      dfree(c, tmp);
+      dfree(c, ck);
+      dfree(c, cv);
     }
-    comp0_made = true;
   }
   if (hc) hc->wait_all(c->st);
   CK(cudaMemsetAsync(&c->dv->bad, 0, sizeof(unsigned long long), c->st));
@@ -1276,6 +1360,26 @@ void build_all(cparls_ctx *c, const IT *coords, const VT *vals, const H2DChunks 
     c->comm->allreduce_f64(&c->dv->maxabs, 1, c->st);   // sum of the ranks' maxima: a common upper bound
   }
   c->normX2 = read_dev(c, &c->dv->normX2);
+  if (single_sort && !rk.empty()) {
+    // merge each mode's runs (the spare pair of buffers passes from mode to mode)
+    uint64_t *sk = dalloc_t<uint64_t>(c, c->nnz);
+    VT *sv = (VT *)dalloc(c, sizeof(VT) * (size_t)c->nnz);
+    for (int k = 0; k < c->D; ++k) {
+      c->row_lo[k] = 0;
+      c->row_hi[k] = c->dims[k];
+      {
+        WallAcc ws(&c->stats.build_ms[1]);
+        merge_runs<VT>(c, rb, rk[k], rv[k], sk, sv);
+        sync(c);
+      }
+      finish_mode_presorted(c, k, c->nnz, rk[k], rv[k]);
+    }
+    sync(c);
+    dfree(c, sk);
+    dfree(c, sv);
+    degrees_and_hot_rows(c);
+    return;
+  }
   if (single_sort) {
     if (!comp0_made) {
       ar.cbits = key_bits(Nall);

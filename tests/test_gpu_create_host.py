@@ -1,10 +1,13 @@
-"""cparls_create from host COO: the chunked host->device copy (64M nonzeros per
-chunk on a copy stream, mode 0's composite keys made per chunk while later
-chunks are in flight) must give the same context as a create from device
-memory -- identical sorted copies, hence identical samples, factors and fits,
-bit for bit.  A C4-shaped tensor of 150M nonzeros spans three chunks, the last
-one ragged.  Also: factors read back into pinned and pageable host buffers and
-into device memory agree exactly."""
+"""cparls_create from host COO: the chunked host->device copy (2^27 nonzeros per
+chunk on a copy stream; every mode's composite keys of a chunk made and sorted
+while later chunks are in flight, the sorted runs merged at the end) must give
+the same context as a create from device memory (one full stable sort per
+mode) -- identical sorted copies, hence identical samples, factors and fits,
+bit for bit.  A C4-shaped tensor of 150M nonzeros plus 1M duplicated
+coordinates (copies of chunk-0 nonzeros with other values, placed in the last
+chunk: the merge must keep input order among equal keys) spans two chunks, the
+last one ragged.  Also: factors read back into pinned and pageable host
+buffers agree exactly."""
 import dataclasses
 
 import numpy as np
@@ -15,7 +18,8 @@ import synth
 
 pytestmark = pytest.mark.gpu
 
-NNZ = 150_000_123          # 2 full 2^26-nonzero chunks + a ragged third
+NNZ = 150_000_123          # one full 2^27-nonzero chunk + a ragged second
+NDUP = 1_000_000
 
 
 def need_gpu():
@@ -29,15 +33,18 @@ def test_create_from_host_chunks_equals_device():
     cfg = dataclasses.replace(synth.CONFIGS["C4"], nnz=NNZ)
     dev = torch.device("cuda", 0)
     T = synth.make(cfg, device=dev, index_dtype=torch.int32)
-    hc = torch.empty(T.coords.shape, dtype=T.coords.dtype, pin_memory=True)
-    hv = torch.empty(T.vals.shape, dtype=T.vals.dtype, pin_memory=True)
-    hc.copy_(T.coords)
-    hv.copy_(T.vals)
+    dc = torch.cat([T.coords, T.coords[:NDUP]])
+    dv = torch.cat([T.vals, T.vals[:NDUP] * 2 + 1])
+    del T
+    hc = torch.empty(dc.shape, dtype=dc.dtype, pin_memory=True)
+    hv = torch.empty(dv.shape, dtype=dv.dtype, pin_memory=True)
+    hc.copy_(dc)
+    hv.copy_(dv)
     torch.cuda.synchronize()
     traces, facs = [], []
     for src in ("device", "pinned", "pageable"):
         if src == "device":
-            c, v = T.coords, T.vals
+            c, v = dc, dv
         elif src == "pinned":
             c, v = hc.numpy(), hv.numpy()
         else:
@@ -66,7 +73,7 @@ def test_create_from_host_rejects_bad_coordinate_in_last_chunk():
     need_gpu()
     from paper_2006_16438_b200 import Cparls
     dims = (1000, 900, 800)
-    n = (1 << 26) + 5
+    n = (1 << 27) + 5
     rng = np.random.default_rng(0)
     coords = np.stack([rng.integers(0, d, n, dtype=np.int32) for d in dims], axis=1)
     vals = rng.random(n, dtype=np.float32)
