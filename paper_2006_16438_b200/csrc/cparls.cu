@@ -1253,7 +1253,16 @@ void finish_mode_presorted(cparls_ctx *c, int k, int64_t nnz, uint64_t *comp, vo
 // Chunked host->device copy of the COO in flight on its own stream (cparls_create):
 // chunk i covers nonzeros [end[i-1], end[i]) and is resident once ev[i] fires.
 struct H2DChunks {
-  static constexpr int64_t kChunk = int64_t(1) << 27;
+  static constexpr int64_t kMinSplit = int64_t(1) << 27;
+  // chunk ends: 4 chunks of 40/30/20/10% above kMinSplit nonzeros (each chunk's
+  // sorts take about as long as the next chunk's transfer, the last chunk is
+  // small -- little left to sort after the transfer -- and 4 runs merge in 2
+  // rounds); one chunk below
+  static std::vector<int64_t> plan(int64_t nnz) {
+    if (nnz < kMinSplit) return {nnz};
+    const int64_t a = nnz / 10 * 4, b = a + nnz / 10 * 3, c = b + nnz / 10 * 2;
+    return {a, b, c, nnz};
+  }
   cudaStream_t cs = nullptr;
   cudaEvent_t ev0 = nullptr;
   std::vector<int64_t> end;
@@ -2761,9 +2770,9 @@ cparls_status cparls_create(cparls_ctx **out, int32_t nmodes, const int64_t *dim
       CK(cudaStreamCreateWithFlags(&hc.cs, cudaStreamNonBlocking));
       CK(cudaEventRecord(hc.ev0, c->st));   // after the context's own memsets
       CK(cudaStreamWaitEvent(hc.cs, hc.ev0, 0));
-      const int64_t per = H2DChunks::kChunk;
-      for (int64_t e0 = 0; e0 < nnz_local; e0 += per) {
-        const int64_t n = std::min(per, nnz_local - e0);
+      const std::vector<int64_t> ends = H2DChunks::plan(nnz_local);
+      for (size_t i = 0, e0 = 0; i < ends.size(); e0 = ends[i++]) {
+        const int64_t n = ends[i] - (int64_t)e0;
         if (hc_c)
           CK(cudaMemcpyAsync((char *)own_c + isz * nmodes * e0, (const char *)coords + isz * nmodes * e0,
                              isz * nmodes * n, cudaMemcpyHostToDevice, hc.cs));

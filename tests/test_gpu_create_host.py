@@ -1,12 +1,11 @@
-"""cparls_create from host COO: the chunked host->device copy (2^27 nonzeros per
-chunk on a copy stream; every mode's composite keys of a chunk made and sorted
+"""cparls_create from host COO: the chunked host->device copy (above 2^27
+nonzeros: 4 chunks of 40/30/20/10% on a copy stream; every mode's composite keys of a chunk made and sorted
 while later chunks are in flight, the sorted runs merged at the end) must give
 the same context as a create from device memory (one full stable sort per
 mode) -- identical sorted copies, hence identical samples, factors and fits,
 bit for bit.  A C4-shaped tensor of 150M nonzeros plus 1M duplicated
 coordinates (copies of chunk-0 nonzeros with other values, placed in the last
-chunk: the merge must keep input order among equal keys) spans two chunks, the
-last one ragged.  Also: factors read back into pinned and pageable host
+chunk: the merge must keep input order among equal keys) spans four chunks.  Also: factors read back into pinned and pageable host
 buffers agree exactly."""
 import dataclasses
 
@@ -18,7 +17,7 @@ import synth
 
 pytestmark = pytest.mark.gpu
 
-NNZ = 150_000_123          # one full 2^27-nonzero chunk + a ragged second
+NNZ = 150_000_123          # > 2^27: four chunks
 NDUP = 1_000_000
 
 
@@ -77,6 +76,6 @@ def test_create_from_host_rejects_bad_coordinate_in_last_chunk():
     rng = np.random.default_rng(0)
     coords = np.stack([rng.integers(0, d, n, dtype=np.int32) for d in dims], axis=1)
     vals = rng.random(n, dtype=np.float32)
-    coords[-1, 2] = dims[2]          # out of range, in the second chunk
+    coords[-1, 2] = dims[2]          # out of range, in the last chunk
     with pytest.raises(Exception):
         Cparls(dims, coords, vals, 5, tau=-1.0, init_seed=1)
